@@ -1,0 +1,135 @@
+/*
+ * btp.h — C-ABI of the B200-native Bottleneck-aware Tensor Parallelism (BTP) block step.
+ *
+ * Plain pointers and sizes only: every pointer is a DEVICE pointer owned by the caller
+ * (kernels never allocate), every call is asynchronous on the caller's cudaStream_t
+ * (passed as void*), and every entry point returns a btp_status.
+ *
+ * The reference (`btpsim`, pure Python/NumPy) has no FFI; each entry point below replaces
+ * one compute site of its executor. The replaced reference symbol is cited per function
+ * (paths relative to the reference package root `pkg/src/btpsim/`).
+ *
+ * Precision: bf16 storage for activations and GEMM operands, fp32 accumulation (TMEM),
+ * fp32 for every per-row statistic (sum of squares, local/global RMS), fp32 weight grads.
+ */
+#ifndef BTP_H_
+#define BTP_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum btp_status {
+  BTP_OK = 0,
+  BTP_ERR_DIM = 1,          /* shapes do not conform (reference DimensionError / PlanError) */
+  BTP_ERR_DIVISIBILITY = 2, /* dimension not divisible as required (reference DivisibilityError) */
+  BTP_ERR_ALIGNMENT = 3,    /* TMA/vector alignment violated (row stride or width not a multiple of 8) */
+  BTP_ERR_CUDA = 4          /* CUDA launch/runtime failure */
+} btp_status;
+
+/* One GEMM problem  C[M,N] = alpha * rowscale[m] * colscale[n] * sum_k A[m,k] B[n,k]  (+ resid[m,n]).
+ *   A: a_mn == 0 -> row-major [M, K] (ld = lda);  a_mn == 1 -> row-major [K, M] (A transposed in memory)
+ *   B: b_mn == 0 -> row-major [N, K] (ld = ldb);  b_mn == 1 -> row-major [K, N]
+ *   C: bf16 (c_fp32 == 0) or fp32 (c_fp32 == 1) row-major [M, N] with ld = ldc.
+ *   splits > 1: split-K; split s writes fp32 partial C + s*split_stride (reduce with btp_reduce_rows).
+ * Replaces: tensor.py:71-83 `mm_values` (every GEMM), simulator.py:198-205 `_gemm_ranks`. */
+typedef struct btp_gemm_problem {
+  const void* a;
+  long long lda;
+  int a_mn;
+  const void* b;
+  long long ldb;
+  int b_mn;
+  void* c;
+  long long ldc;
+  int c_fp32;
+  int M, N, K;
+  const float* row_scale; /* [M] or NULL */
+  const float* col_scale; /* [N] or NULL */
+  const void* resid;      /* bf16 [M, ld_resid] or NULL (bf16 output only) */
+  long long ld_resid;
+  int splits;
+  long long split_stride;
+  float alpha; /* 0 is read as 1 */
+} btp_gemm_problem;
+
+/* Grouped/batched tcgen05 GEMM: n (1..4) independent problems in ONE persistent launch.
+ * All problems share (a_mn, b_mn). bn_hint: 0 = auto, 128 or 256 = N tile.
+ * Replaces: simulator.py:208-218 `_gemm_ranks_batched`, tensor.py:97-112 `batched_matmul`
+ * (grouped up-projections q|k|v and gate|up, simulator.py:655-668). */
+int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream);
+
+/* Online RMSNorm (local form) fused with the residual add, one row per warp.
+ *   v = x (+ branch); if x_out: x_out = bf16(v); stats use the rounded v
+ *   ss[t] = sum_k v^2 ; rms_loc[t] = sqrt(ss/width + eps) ; n = v * gamma / rms_loc
+ * n_out may be NULL (stat-only pass of the sync form). width <= 8192, width % 8 == 0.
+ * Replaces: simulator.py:574-590 `norm_local` (online branch), norms.py:38-44 `local_sumsq`/
+ * `local_rms`, residual adds simulator.py:687 / :706, norms.py:33-35 `rmsnorm_values` (width = d). */
+int btp_rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
+                         long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
+                         float* rms_loc_out, int rows, int width, float eps, void* stream);
+
+/* Sync-form RMSNorm apply: n = x * gamma / sqrt(ss_total/d + eps); rms_out[t] = that sqrt.
+ * Replaces: simulator.py:585-590 (sync branch of `norm_local`), norms.py:47-64 `sync_rmsnorm`. */
+int btp_rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d,
+                      float eps, void* n_out, long long ldn, float* rms_out, int rows, int width,
+                      void* stream);
+
+/* Post-all-reduce fix-up and rank-r activation for one chunk boundary.
+ *   if ss_total: s = sqrt(ss_total/d + eps) (written to s_out if non-NULL), z = P / s
+ *   else       : z = P
+ *   z_out = bf16(z) (skipped if z_out == P and no division);  a_out = sigma(z_out)
+ *   sigma: variant 0 (svd) identity (a_out may be NULL); variant 1 (cola) crossgate per projection:
+ *          [silu(u)*v, silu(v)*u] with u = z[:, p*r : p*r + r/2], v = z[:, p*r + r/2 : (p+1)*r]
+ * Replaces: simulator.py:599-602 `correct`, :636 `/ rms_g`, :247-265 `_variant_a_input`,
+ * model.py:189-196 `lowrank_crossgate_values`. */
+int btp_fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                    void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj,
+                    int variant, void* stream);
+
+/* SwiGLU forward act = silu(g) * u.  Replaces tensor.py:131-132 `swiglu_values` (simulator.py:699). */
+int btp_swiglu(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda,
+               int rows, int cols, void* stream);
+
+/* SwiGLU backward: dg = dact * u * silu'(g), du = dact * silu(g). */
+int btp_swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, const void* dact,
+                   long long ldda, void* dg, long long lddg, void* du, long long lddu, int rows, int cols,
+                   void* stream);
+
+/* Backward of `btp_fixup_sigma` for one chunk (sigma-bwd + normalisation-bwd, no collective):
+ *   dz = sigma'(z) . da       (crossgate-bwd for variant 1, identity for 0)
+ *   if s: dP = dz / s ;  dss[t] = -<dz_t, z_t> / (2 s^2 d)      else dP = dz
+ * dP may alias da. Replaces the (absent) backward of simulator.py:592-653. */
+int btp_fixup_sigma_bwd(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d,
+                        void* dP, long long lddp, float* dss, int rows, int r, int nproj, int variant,
+                        void* stream);
+
+/* Online/sync RMSNorm backward, rank-local (needs no collective):
+ *   dx = dres + dh * gamma + 2 * x * dss[t]          (bf16 out; dres may be NULL)
+ *   dgamma_partial[blk, k] = sum_{t in blk} dh[t,k] * x[t,k]   (fp32, nblk partial rows)
+ * nblk partial rows are reduced by btp_reduce_rows. Returns the number of blocks used via *nblk. */
+int btp_rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma,
+                    const float* dss, const void* dres, long long ldr, void* dx, long long lddx,
+                    float* dgamma_partial, int max_blocks, int* nblk, int rows, int width, void* stream);
+
+/* out[r, c] = (accumulate ? out : 0) + colscale[c] * sum_{s<splits} in[s*split_stride + r*ldi + c]
+ * Deterministic (ascending split order) split-K / partial-sum reduction, fp32. */
+int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
+                    const float* col_scale, float* out, long long ldo, int accumulate, void* stream);
+
+/* out = a + b (bf16, elementwise over rows x cols). Replicated residual adds of the baselines
+ * (simulator.py:367, :395, :523, :540). */
+int btp_add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows,
+            int cols, void* stream);
+
+/* Number of SMs the library sizes persistent grids for (device 0 of the current context). */
+int btp_num_sms(void);
+
+/* Library version string. */
+const char* btp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BTP_H_ */

@@ -1,0 +1,75 @@
+"""TP communicator: the collective sub-boundary of the reference (`SimGroup`,
+simulator.py:123-186) over torch.distributed — NCCL over NVLink/NVSwitch on the GPU box,
+gloo for the multi-process CPU tests.
+
+* `all_reduce`            — in-place sum of one buffer (chunk boundary [T, k*r]).
+* `all_reduce_coalesced`  — the BTP online-norm rider: the bf16 [T, k*r] partial and the fp32
+                            [T] sum-of-squares reduced under ONE record, issued inside one NCCL
+                            group (one launch), so the statistic never costs its own collective.
+* `all_gather`            — model-tail gather of the d-sharded residual along the feature axis.
+
+At tp == 1 nothing is sent, but the record is still written, exactly like the reference's
+single-rank group. Every call records into a `Trace` with the current pass tag.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .trace import Trace
+
+
+class TPComm:
+    def __init__(self, tp: int = 1, rank: int = 0, group=None, trace: Trace | None = None):
+        self.tp = tp
+        self.rank = rank
+        self.group = group
+        self.trace = trace if trace is not None else Trace()
+        self.pass_tag = "forward"
+        if tp > 1 and not dist.is_initialized():
+            raise RuntimeError("tp > 1 needs an initialised torch.distributed process group")
+
+    @classmethod
+    def from_env(cls, tp: int | None = None, trace: Trace | None = None) -> "TPComm":
+        if not dist.is_initialized():
+            return cls(1, 0, None, trace)
+        world = dist.get_world_size()
+        tp = world if tp is None else tp
+        if tp != world:
+            raise ValueError(f"tp={tp} must equal the process-group size {world} (one TP group per job)")
+        return cls(tp, dist.get_rank(), None, trace)
+
+    # ------------------------------------------------------------------ collectives
+    def all_reduce(self, buf: torch.Tensor, chunk_id: str, tag: str = "block") -> torch.Tensor:
+        if self.tp > 1:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+        self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
+        return buf
+
+    def all_reduce_coalesced(self, main: torch.Tensor, stat: torch.Tensor, chunk_id: str,
+                             tag: str = "block", stat_tag: str = "fused-stat"):
+        if self.tp > 1:
+            if dist.get_backend(self.group) == "nccl":
+                # one ncclGroupStart/End: both reductions ride one launch
+                with dist._coalescing_manager(group=self.group, device=main.device):
+                    dist.all_reduce(main, group=self.group)
+                    dist.all_reduce(stat, group=self.group)
+            else:
+                dist.all_reduce(main, group=self.group)
+                dist.all_reduce(stat, group=self.group)
+        self.trace.emit("all-reduce-coalesced", chunk_id, tag, main.numel(), self.pass_tag,
+                        extras=((stat_tag, stat.numel()),))
+        return main, stat
+
+    def all_gather_cols(self, shard: torch.Tensor, chunk_id: str, tag: str = "boundary") -> torch.Tensor:
+        """Gather [rows, w] shards along the feature axis into [rows, tp*w]."""
+        rows, w = shard.shape
+        if self.tp > 1:
+            stacked = torch.empty((self.tp, rows, w), dtype=shard.dtype, device=shard.device)
+            dist.all_gather_into_tensor(stacked, shard.contiguous(), group=self.group)
+            out = stacked.permute(1, 0, 2).reshape(rows, self.tp * w)
+        else:
+            out = shard
+        self.trace.emit("all-gather", chunk_id, tag, out.numel(), self.pass_tag)
+        return out

@@ -1,0 +1,389 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+//   C[M,N] = epilogue( sum_k A[m,k] * B[n,k] )
+//
+// One launch serves up to kMaxProblems independent problems (the grouped / batched
+// GEMMs of the BTP chunks: q|k|v or gate|up up-projections, reference
+// simulator.py:655-668 `up_gemms`, tensor.py:97-112 `batched_matmul`) and optional
+// split-K (weight gradients, whose reduction runs over the T tokens).
+//
+// Operands are staged by TMA into 128B-swizzled shared memory; either operand may be
+// K-major (row-major [rows, K]) or MN-major (row-major [K, rows]); the UMMA descriptor
+// "major" bits absorb the transpose so dgrad/wgrad never materialise a transposed copy.
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4..w7 epilogue (TMEM lane quarter = warp % 4). The accumulator is double-buffered in
+// TMEM (2 x BN columns) so the epilogue of tile i overlaps the mainloop of tile i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "btp_internal.h"
+#include "ptx.cuh"
+
+namespace btp {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kMaxProblems = 4;
+constexpr int kThreads = 256;
+
+struct alignas(64) DevProblem {
+  CUtensorMap tma_a;
+  CUtensorMap tma_b;
+  void* c;
+  const float* row_scale;
+  const float* col_scale;
+  const __nv_bfloat16* resid;
+  long long ldc;
+  long long ld_resid;
+  long long split_stride;
+  int M, N, K;
+  int m_tiles, n_tiles, splits, kb_per_split, k_blocks;
+  int tile_start;
+  int out_fp32;
+  float alpha;
+};
+
+struct DevParams {
+  DevProblem prob[kMaxProblems];
+  int num_problems;
+  int total_tiles;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kBarrierBytes = 256;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBarrierBytes;
+};
+
+struct TileCoord {
+  int p, split, m_blk, n_blk;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const DevParams& P, int tile) {
+  int p = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxProblems; ++i)
+    if (i < P.num_problems && tile >= P.prob[i].tile_start) p = i;
+  const DevProblem& pr = P.prob[p];
+  int local = tile - pr.tile_start;
+  const int per_split = pr.m_tiles * pr.n_tiles;
+  TileCoord t;
+  t.p = p;
+  t.split = local / per_split;
+  local -= t.split * per_split;
+  t.m_blk = local / pr.n_tiles;
+  t.n_blk = local - t.m_blk * pr.n_tiles;
+  return t;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ DevParams P) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < P.num_problems; ++i) {
+      tma_prefetch_desc(&P.prob[i].tma_a);
+      tma_prefetch_desc(&P.prob[i].tma_b);
+    }
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
+        const TileCoord tc = decode_tile(P, tile);
+        const DevProblem& pr = P.prob[tc.p];
+        const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
+        const int kb0 = tc.split * pr.kb_per_split;
+        const int kb1 = min(kb0 + pr.kb_per_split, pr.k_blocks);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+          const int k0 = kb * kBK;
+          if (!A_MN) {
+            tma_load_2d(a_dst, &pr.tma_a, &full_bar[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < kBM / 64; ++c)
+              tma_load_2d(a_dst + c * 64 * kBK * 2, &pr.tma_a, &full_bar[stage], m0 + c * 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_dst, &pr.tma_b, &full_bar[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d(b_dst + c * 64 * kBK * 2, &pr.tma_b, &full_bar[stage], n0 + c * 64, k0);
+          }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
+      const TileCoord tc = decode_tile(P, tile);
+      const DevProblem& pr = P.prob[tc.p];
+      const int kb0 = tc.split * pr.kb_per_split;
+      const int kb1 = min(kb0 + pr.kb_per_split, pr.k_blocks);
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            uint64_t a_desc, b_desc;
+            if (!A_MN) a_desc = make_sw128_desc(a_base + k * 32, 16, 1024);
+            else       a_desc = make_sw128_desc(a_base + k * 16 * 128, 64 * kBK * 2, 1024);
+            if (!B_MN) b_desc = make_sw128_desc(b_base + k * 32, 16, 1024);
+            else       b_desc = make_sw128_desc(b_base + k * 16 * 128, 64 * kBK * 2, 1024);
+            umma_bf16(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[buf]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp & 3;  // TMEM lane quarter
+    int it = 0;
+    for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
+      const TileCoord tc = decode_tile(P, tile);
+      const DevProblem& pr = P.prob[tc.p];
+      const int buf = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull_bar[buf], acc_phase);
+      tc_fence_after();
+      const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < pr.M;
+      float rscale = pr.alpha;
+      if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
+      const int n_valid = min(BN, pr.N - n0);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (c0 >= n_valid) break;  // warp-uniform
+        uint32_t r[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + buf * BN + c0, r);
+        tmem_ld_wait();
+        if (row_ok) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rscale;
+        const int col = n0 + c0;
+        const int ncols = min(32, n_valid - c0);  // multiple of 8 (host guarantees N % 8 == 0)
+        if (pr.col_scale != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) v[j] *= __ldg(pr.col_scale + col + j);
+        }
+        if (pr.resid != nullptr) {
+          const uint4* rp = reinterpret_cast<const uint4*>(pr.resid + (long long)row * pr.ld_resid + col);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (g * 8 < ncols) {
+              const uint4 rv = __ldg(rp + g);
+              const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                v[g * 8 + 2 * h] += bf16_lo(w[h]);
+                v[g * 8 + 2 * h + 1] += bf16_hi(w[h]);
+              }
+            }
+          }
+        }
+        if (pr.out_fp32) {
+          float* cp = reinterpret_cast<float*>(pr.c) + (long long)tc.split * pr.split_stride +
+                      (long long)row * pr.ldc + col;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (g * 4 < ncols)
+              reinterpret_cast<float4*>(cp)[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+        } else {
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(pr.c) + (long long)row * pr.ldc + col;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (g * 8 < ncols)
+              reinterpret_cast<uint4*>(cp)[g] =
+                  make_uint4(pack_bf16(v[8 * g], v[8 * g + 1]), pack_bf16(v[8 * g + 2], v[8 * g + 3]),
+                             pack_bf16(v[8 * g + 4], v[8 * g + 5]), pack_bf16(v[8 * g + 6], v[8 * g + 7]));
+        }
+        }  // row_ok
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[buf]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+// ============================================================================ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 row-major tensor [outer, inner] with row stride `ld` elements, 128B swizzle.
+static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                     uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode_fn();
+  if (!enc) return BTP_ERR_CUDA;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch(const DevParams& P, int grid, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes) != cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::kSmemBytes, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream) {
+  if (n <= 0 || n > kMaxProblems) return BTP_ERR_DIM;
+  const int a_mn = probs[0].a_mn, b_mn = probs[0].b_mn;
+  int maxN = 0;
+  for (int i = 0; i < n; ++i) {
+    const btp_gemm_problem& q = probs[i];
+    if (q.a_mn != a_mn || q.b_mn != b_mn) return BTP_ERR_DIM;
+    if (q.M <= 0 || q.N <= 0 || q.K <= 0) return BTP_ERR_DIM;
+    if (q.N % 8 != 0 || q.K % 8 != 0) return BTP_ERR_ALIGNMENT;
+    if (q.splits < 1) return BTP_ERR_DIM;
+    if (q.splits > 1 && !q.c_fp32) return BTP_ERR_DIM;
+    if (q.resid && q.c_fp32) return BTP_ERR_DIM;
+    maxN = maxN > q.N ? maxN : q.N;
+  }
+  const int BN = (bn_hint == 128 || bn_hint == 256) ? bn_hint : (maxN >= 256 ? 256 : 128);
+  DevParams P;
+  memset(&P, 0, sizeof(P));
+  int tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    const btp_gemm_problem& q = probs[i];
+    DevProblem& d = P.prob[i];
+    int rc;
+    if (!a_mn) rc = make_tmap(&d.tma_a, q.a, q.K, q.M, q.lda, kBK, kBM);
+    else       rc = make_tmap(&d.tma_a, q.a, q.M, q.K, q.lda, 64, kBK);
+    if (rc) return rc;
+    if (!b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN);
+    else       rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
+    if (rc) return rc;
+    d.c = q.c;
+    d.row_scale = q.row_scale;
+    d.col_scale = q.col_scale;
+    d.resid = reinterpret_cast<const __nv_bfloat16*>(q.resid);
+    d.ldc = q.ldc;
+    d.ld_resid = q.ld_resid;
+    d.split_stride = q.split_stride;
+    d.M = q.M; d.N = q.N; d.K = q.K;
+    d.m_tiles = (q.M + kBM - 1) / kBM;
+    d.n_tiles = (q.N + BN - 1) / BN;
+    d.k_blocks = (q.K + kBK - 1) / kBK;
+    d.splits = q.splits;
+    d.kb_per_split = (d.k_blocks + q.splits - 1) / q.splits;
+    d.out_fp32 = q.c_fp32;
+    d.alpha = q.alpha == 0.0f ? 1.0f : q.alpha;
+    d.tile_start = tiles;
+    tiles += d.m_tiles * d.n_tiles * q.splits;
+  }
+  P.num_problems = n;
+  P.total_tiles = tiles;
+  int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (BN == 256) {
+    if (!a_mn && !b_mn) return launch<256, false, false>(P, grid, stream);
+    if (!a_mn && b_mn) return launch<256, false, true>(P, grid, stream);
+    if (a_mn && b_mn) return launch<256, true, true>(P, grid, stream);
+    return launch<256, true, false>(P, grid, stream);
+  } else {
+    if (!a_mn && !b_mn) return launch<128, false, false>(P, grid, stream);
+    if (!a_mn && b_mn) return launch<128, false, true>(P, grid, stream);
+    if (a_mn && b_mn) return launch<128, true, true>(P, grid, stream);
+    return launch<128, true, false>(P, grid, stream);
+  }
+}
+
+}  // namespace btp

@@ -1,0 +1,553 @@
+// HBM-bound row/elementwise kernels of the BTP block: online RMSNorm + residual (K3),
+// post-all-reduce fix-up + crossgate sigma (K4), SwiGLU (K5), and their backward passes.
+//
+// All loads/stores are 128-bit (8 x bf16); statistics and math are fp32. Row reductions
+// use one warp per row with shuffle reductions (no shared memory, no atomics), so every
+// result is deterministic.
+#include <cuda_runtime.h>
+
+#include "btp_internal.h"
+#include "ptx.cuh"
+
+namespace btp {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ void unpack8(const uint4& w, float (&f)[8]) {
+  f[0] = bf16_lo(w.x); f[1] = bf16_hi(w.x);
+  f[2] = bf16_lo(w.y); f[3] = bf16_hi(w.y);
+  f[4] = bf16_lo(w.z); f[5] = bf16_hi(w.z);
+  f[6] = bf16_lo(w.w); f[7] = bf16_hi(w.w);
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float silu_f(float x) { return x * sigmoidf_safe(x); }
+
+// ----------------------------------------------------------------------------- K3 forward
+// One warp per row; NCH = max 8-element chunks per lane held in registers.
+template <int NCH>
+__global__ void __launch_bounds__(256) rmsnorm_residual_kernel(
+    const bf16* __restrict__ x, long long ldx, const bf16* __restrict__ branch, long long ldb,
+    bf16* __restrict__ x_out, long long ldo, const float* __restrict__ gamma, bf16* __restrict__ n_out,
+    long long ldn, float* __restrict__ ss_out, float* __restrict__ rl_out, int rows, int width, float eps) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nch = width >> 3;
+  uint4 keep[NCH];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      uint4 w = *reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8);
+      if (branch != nullptr) {
+        const uint4 b = *reinterpret_cast<const uint4*>(branch + (long long)row * ldb + c * 8);
+        float fx[8], fb[8];
+        unpack8(w, fx);
+        unpack8(b, fb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) fx[j] += fb[j];
+        w = pack8(fx);
+        if (x_out != nullptr) *reinterpret_cast<uint4*>(x_out + (long long)row * ldo + c * 8) = w;
+      }
+      keep[i] = w;
+      float f[8];
+      unpack8(w, f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss = fmaf(f[j], f[j], ss);
+    }
+  }
+  ss = warp_sum(ss);
+  const float rl = sqrtf(ss / (float)width + eps);
+  if (lane == 0) {
+    if (ss_out) ss_out[row] = ss;
+    if (rl_out) rl_out[row] = rl;
+  }
+  if (n_out == nullptr) return;
+  const float inv = 1.0f / rl;
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nch) {
+      float f[8];
+      unpack8(keep[i], f);
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
+      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = f[j] * g[j] * inv;
+      *reinterpret_cast<uint4*>(n_out + (long long)row * ldn + c * 8) = pack8(f);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_apply_kernel(const bf16* __restrict__ x, long long ldx,
+                                                            const float* __restrict__ gamma,
+                                                            const float* __restrict__ ss_total, int d, float eps,
+                                                            bf16* __restrict__ n_out, long long ldn,
+                                                            float* __restrict__ rms_out, int rows, int width) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float s = sqrtf(ss_total[row] / (float)d + eps);
+  if (lane == 0 && rms_out) rms_out[row] = s;
+  const float inv = 1.0f / s;
+  for (int c = lane; c < (width >> 3); c += 32) {
+    float f[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), f);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * g[j] * inv;
+    *reinterpret_cast<uint4*>(n_out + (long long)row * ldn + c * 8) = pack8(f);
+  }
+}
+
+// ----------------------------------------------------------------------------- K4 forward
+// Work item = (row, projection, group of 8 columns of the u half) for cola,
+//             (row, projection, group of 8 columns) for svd.
+__global__ void __launch_bounds__(256) fixup_sigma_kernel(const bf16* __restrict__ P, long long ldp,
+                                                          const float* __restrict__ ss_total, int d, float eps,
+                                                          float* __restrict__ s_out, bf16* __restrict__ z_out,
+                                                          long long ldz, bf16* __restrict__ a_out, long long lda,
+                                                          int rows, int r, int nproj, int variant) {
+  const int per_proj = variant == 1 ? (r >> 4) : (r >> 3);
+  const long long per_row = (long long)per_proj * nproj;
+  const long long total = per_row * rows;
+  const bool write_z = (z_out != nullptr) && (ss_total != nullptr || (const void*)z_out != (const void*)P);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int rem = (int)(idx - (long long)row * per_row);
+    const int p = rem / per_proj;
+    const int g = rem - p * per_proj;
+    float inv = 1.0f;
+    if (ss_total != nullptr) {
+      const float s = sqrtf(ss_total[row] / (float)d + eps);
+      inv = 1.0f / s;
+      if (s_out != nullptr && p == 0 && g == 0) s_out[row] = s;
+    }
+    if (variant == 1) {
+      const int cu = p * r + g * 8, cv = cu + (r >> 1);
+      float u[8], v[8];
+      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + cu), u);
+      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + cv), v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { u[j] *= inv; v[j] *= inv; }
+      const uint4 zu = pack8(u), zv = pack8(v);
+      if (write_z) {
+        *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + cu) = zu;
+        *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + cv) = zv;
+      }
+      // sigma acts on the stored (rounded) z so a checkpointed recompute is bit-identical
+      unpack8(zu, u);
+      unpack8(zv, v);
+      float au[8], av[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        au[j] = silu_f(u[j]) * v[j];
+        av[j] = silu_f(v[j]) * u[j];
+      }
+      *reinterpret_cast<uint4*>(a_out + (long long)row * lda + cu) = pack8(au);
+      *reinterpret_cast<uint4*>(a_out + (long long)row * lda + cv) = pack8(av);
+    } else {
+      const int c = p * r + g * 8;
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + c), f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] *= inv;
+      const uint4 zz = pack8(f);
+      if (write_z) *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + c) = zz;
+      if (a_out != nullptr) *reinterpret_cast<uint4*>(a_out + (long long)row * lda + c) = zz;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- K4 backward
+// One warp per row: sigma-bwd, then dP = dz / s and dss = -<dz, z> / (2 s^2 d).
+__global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const bf16* __restrict__ z, long long ldz,
+                                                              const bf16* da, long long ldda,
+                                                              const float* __restrict__ s_in, int d, bf16* dP,
+                                                              long long lddp, float* __restrict__ dss, int rows,
+                                                              int r, int nproj, int variant) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float s = s_in ? s_in[row] : 1.0f;
+  const float inv = 1.0f / s;
+  const int per_proj = variant == 1 ? (r >> 4) : (r >> 3);
+  const int groups = per_proj * nproj;
+  float dot = 0.f;
+  for (int gi = lane; gi < groups; gi += 32) {
+    const int p = gi / per_proj;
+    const int g = gi - p * per_proj;
+    if (variant == 1) {
+      const int cu = p * r + g * 8, cv = cu + (r >> 1);
+      float u[8], v[8], du_[8], dv_[8];
+      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + cu), u);
+      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + cv), v);
+      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + cu), du_);
+      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + cv), dv_);
+      float gu[8], gv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float su = sigmoidf_safe(u[j]), sv = sigmoidf_safe(v[j]);
+        const float silu_u = u[j] * su, silu_v = v[j] * sv;
+        const float dsilu_u = su * (1.0f + u[j] * (1.0f - su));
+        const float dsilu_v = sv * (1.0f + v[j] * (1.0f - sv));
+        // a_u = silu(u) v ; a_v = silu(v) u
+        gu[j] = du_[j] * dsilu_u * v[j] + dv_[j] * silu_v;
+        gv[j] = du_[j] * silu_u + dv_[j] * dsilu_v * u[j];
+        dot = fmaf(gu[j], u[j], dot);
+        dot = fmaf(gv[j], v[j], dot);
+        gu[j] *= inv;
+        gv[j] *= inv;
+      }
+      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + cu) = pack8(gu);
+      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + cv) = pack8(gv);
+    } else {
+      const int c = p * r + g * 8;
+      float zz[8], dd[8];
+      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + c), zz);
+      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + c), dd);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        dot = fmaf(dd[j], zz[j], dot);
+        dd[j] *= inv;
+      }
+      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + c) = pack8(dd);
+    }
+  }
+  dot = warp_sum(dot);
+  if (lane == 0 && dss != nullptr && s_in != nullptr) dss[row] = -dot / (2.0f * s * s * (float)d);
+}
+
+// ----------------------------------------------------------------------------- K5
+__global__ void __launch_bounds__(256) swiglu_kernel(const bf16* __restrict__ g, long long ldg,
+                                                     const bf16* __restrict__ u, long long ldu,
+                                                     bf16* __restrict__ act, long long lda, int rows, int cols) {
+  const int per_row = cols >> 3;
+  const long long total = (long long)per_row * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 8;
+    float fg[8], fu[8];
+    unpack8(*reinterpret_cast<const uint4*>(g + (long long)row * ldg + c), fg);
+    unpack8(*reinterpret_cast<const uint4*>(u + (long long)row * ldu + c), fu);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fg[j] = silu_f(fg[j]) * fu[j];
+    *reinterpret_cast<uint4*>(act + (long long)row * lda + c) = pack8(fg);
+  }
+}
+
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const bf16* __restrict__ g, long long ldg,
+                                                         const bf16* __restrict__ u, long long ldu,
+                                                         const bf16* __restrict__ dact, long long ldda,
+                                                         bf16* __restrict__ dg, long long lddg,
+                                                         bf16* __restrict__ du, long long lddu, int rows,
+                                                         int cols) {
+  const int per_row = cols >> 3;
+  const long long total = (long long)per_row * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 8;
+    float fg[8], fu[8], fd[8], og[8], ou[8];
+    unpack8(*reinterpret_cast<const uint4*>(g + (long long)row * ldg + c), fg);
+    unpack8(*reinterpret_cast<const uint4*>(u + (long long)row * ldu + c), fu);
+    unpack8(*reinterpret_cast<const uint4*>(dact + (long long)row * ldda + c), fd);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float sg = sigmoidf_safe(fg[j]);
+      const float silu_g = fg[j] * sg;
+      og[j] = fd[j] * fu[j] * sg * (1.0f + fg[j] * (1.0f - sg));
+      ou[j] = fd[j] * silu_g;
+    }
+    *reinterpret_cast<uint4*>(dg + (long long)row * lddg + c) = pack8(og);
+    *reinterpret_cast<uint4*>(du + (long long)row * lddu + c) = pack8(ou);
+  }
+}
+
+// ----------------------------------------------------------------------------- K3 backward
+// Block of 256 threads: tpr threads per row (8 columns each, looping over column groups),
+// 256/tpr rows in flight. dgamma partial per block, combined across row slots in smem.
+constexpr int kNormBwdMaxGroups = 4;  // width <= 256 * 8 * 4 = 8192
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const bf16* __restrict__ dh, long long lddh,
+                                                          const bf16* __restrict__ x, long long ldx,
+                                                          const float* __restrict__ gamma,
+                                                          const float* __restrict__ dss,
+                                                          const bf16* __restrict__ dres, long long ldr,
+                                                          bf16* __restrict__ dx, long long lddx,
+                                                          float* __restrict__ dgamma_partial, int rows, int width,
+                                                          int tpr, int rows_per_block) {
+  extern __shared__ float red[];  // [256/tpr][width] when rows in flight > 1
+  const int nch = width >> 3;
+  const int slot = threadIdx.x / tpr;
+  const int cg = threadIdx.x - slot * tpr;
+  const int slots = blockDim.x / tpr;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  float acc[kNormBwdMaxGroups][8];
+#pragma unroll
+  for (int q = 0; q < kNormBwdMaxGroups; ++q)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
+  for (int row = r0 + slot; row < r1; row += slots) {
+    const float two_dss = 2.0f * dss[row];
+#pragma unroll
+    for (int q = 0; q < kNormBwdMaxGroups; ++q) {
+      const int c = cg + q * tpr;
+      if (c < nch) {
+        float fh[8], fx[8], fr[8];
+        unpack8(*reinterpret_cast<const uint4*>(dh + (long long)row * lddh + c * 8), fh);
+        unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), fx);
+        if (dres != nullptr) unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * ldr + c * 8), fr);
+        else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fr[j] = 0.f;
+        }
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          o[j] = fr[j] + fh[j] * g[j] + two_dss * fx[j];
+          acc[q][j] = fmaf(fh[j], fx[j], acc[q][j]);
+        }
+        *reinterpret_cast<uint4*>(dx + (long long)row * lddx + c * 8) = pack8(o);
+      }
+    }
+  }
+  // combine the row slots, ascending slot order
+  if (slots == 1) {
+#pragma unroll
+    for (int q = 0; q < kNormBwdMaxGroups; ++q) {
+      const int c = cg + q * tpr;
+      if (c < nch) {
+        float* out = dgamma_partial + (long long)blockIdx.x * width + c * 8;
+        reinterpret_cast<float4*>(out)[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+        reinterpret_cast<float4*>(out)[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < kNormBwdMaxGroups; ++q) {
+    const int c = cg + q * tpr;
+    if (c < nch)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) red[slot * width + c * 8 + j] = acc[q][j];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < width; col += blockDim.x) {
+    float s = 0.f;
+    for (int sl = 0; sl < slots; ++sl) s += red[sl * width + col];
+    dgamma_partial[(long long)blockIdx.x * width + col] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------- reductions
+__global__ void __launch_bounds__(256) reduce_rows_kernel(const float* __restrict__ in, int splits,
+                                                          long long split_stride, long long ldi, int rows,
+                                                          int cols, const float* __restrict__ col_scale,
+                                                          float* __restrict__ out, long long ldo, int accumulate) {
+  const int per_row = cols >> 2;
+  const long long total = (long long)per_row * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 4;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < splits; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(in + k * split_stride + (long long)row * ldi + c);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    if (col_scale != nullptr) {
+      const float4 cs = *reinterpret_cast<const float4*>(col_scale + c);
+      s.x *= cs.x; s.y *= cs.y; s.z *= cs.z; s.w *= cs.w;
+    }
+    float4* o = reinterpret_cast<float4*>(out + (long long)row * ldo + c);
+    if (accumulate) {
+      const float4 p = *o;
+      s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+    }
+    *o = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) add_kernel(const bf16* __restrict__ a, long long lda,
+                                                  const bf16* __restrict__ b, long long ldb, bf16* __restrict__ out,
+                                                  long long ldo, int rows, int cols) {
+  const int per_row = cols >> 3;
+  const long long total = (long long)per_row * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 8;
+    float fa[8], fb[8];
+    unpack8(*reinterpret_cast<const uint4*>(a + (long long)row * lda + c), fa);
+    unpack8(*reinterpret_cast<const uint4*>(b + (long long)row * ldb + c), fb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] += fb[j];
+    *reinterpret_cast<uint4*>(out + (long long)row * ldo + c) = pack8(fa);
+  }
+}
+
+// ============================================================================= launchers
+static inline int grid_for(long long items, int threads = 256) {
+  const long long want = (items + threads - 1) / threads;
+  const long long cap = (long long)num_sms_cached() * 16;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+#define BTP_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA
+
+int rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out, long long ldo,
+                     const float* gamma, void* n_out, long long ldn, float* ss_out, float* rl_out, int rows,
+                     int width, float eps, cudaStream_t st) {
+  if (rows <= 0 || width <= 0) return BTP_ERR_DIM;
+  if (width % 8 || width > 8192 || ldx % 8 || (branch && ldb % 8) || (x_out && ldo % 8) || (n_out && ldn % 8))
+    return BTP_ERR_ALIGNMENT;
+  if (!al16(x) || (branch && !al16(branch)) || (x_out && !al16(x_out)) || (n_out && !al16(n_out)) ||
+      (n_out && !al16(gamma)))
+    return BTP_ERR_ALIGNMENT;
+  const int blocks = (rows + 7) / 8;
+  const int nch = width / 8;
+  const bf16* xb = static_cast<const bf16*>(x);
+  const bf16* bb = static_cast<const bf16*>(branch);
+  bf16* xo = static_cast<bf16*>(x_out);
+  bf16* no = static_cast<bf16*>(n_out);
+  if (nch <= 32 * 4)
+    rmsnorm_residual_kernel<4><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows,
+                                                       width, eps);
+  else if (nch <= 32 * 8)
+    rmsnorm_residual_kernel<8><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows,
+                                                       width, eps);
+  else if (nch <= 32 * 16)
+    rmsnorm_residual_kernel<16><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                        rows, width, eps);
+  else
+    rmsnorm_residual_kernel<32><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                        rows, width, eps);
+  BTP_CHECK_LAUNCH();
+}
+
+int rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps,
+                  void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st) {
+  if (rows <= 0 || width <= 0 || d <= 0) return BTP_ERR_DIM;
+  if (width % 8 || ldx % 8 || ldn % 8 || !al16(x) || !al16(n_out) || !al16(gamma)) return BTP_ERR_ALIGNMENT;
+  rmsnorm_apply_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(x), ldx, gamma, ss_total, d, eps,
+                                                       static_cast<bf16*>(n_out), ldn, rms_out, rows, width);
+  BTP_CHECK_LAUNCH();
+}
+
+int fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out, void* z_out,
+                long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant,
+                cudaStream_t st) {
+  if (rows <= 0 || r <= 0 || nproj <= 0) return BTP_ERR_DIM;
+  if (variant != 0 && variant != 1) return BTP_ERR_DIM;
+  if (variant == 1 && (r % 16)) return BTP_ERR_DIVISIBILITY;
+  if (r % 8 || ldp % 8 || (z_out && ldz % 8) || (a_out && lda % 8)) return BTP_ERR_ALIGNMENT;
+  if (variant == 1 && a_out == nullptr) return BTP_ERR_DIM;
+  if (!al16(P) || (z_out && !al16(z_out)) || (a_out && !al16(a_out))) return BTP_ERR_ALIGNMENT;
+  const long long items = (long long)rows * nproj * (variant == 1 ? r / 16 : r / 8);
+  fixup_sigma_kernel<<<grid_for(items), 256, 0, st>>>(static_cast<const bf16*>(P), ldp, ss_total, d, eps, s_out,
+                                                      static_cast<bf16*>(z_out), ldz, static_cast<bf16*>(a_out), lda,
+                                                      rows, r, nproj, variant);
+  BTP_CHECK_LAUNCH();
+}
+
+int fixup_sigma_bwd(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d, void* dP,
+                    long long lddp, float* dss, int rows, int r, int nproj, int variant, cudaStream_t st) {
+  if (rows <= 0 || r <= 0 || nproj <= 0) return BTP_ERR_DIM;
+  if (variant != 0 && variant != 1) return BTP_ERR_DIM;
+  if (variant == 1 && (r % 16)) return BTP_ERR_DIVISIBILITY;
+  if (r % 8 || ldz % 8 || ldda % 8 || lddp % 8) return BTP_ERR_ALIGNMENT;
+  if (!al16(z) || !al16(da) || !al16(dP)) return BTP_ERR_ALIGNMENT;
+  fixup_sigma_bwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(z), ldz,
+                                                         static_cast<const bf16*>(da), ldda, s, d,
+                                                         static_cast<bf16*>(dP), lddp, dss, rows, r, nproj, variant);
+  BTP_CHECK_LAUNCH();
+}
+
+int swiglu(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows, int cols,
+           cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
+  if (cols % 8 || ldg % 8 || ldu % 8 || lda % 8 || !al16(g) || !al16(u) || !al16(act)) return BTP_ERR_ALIGNMENT;
+  swiglu_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(
+      static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu, static_cast<bf16*>(act), lda, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+int swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, const void* dact, long long ldda,
+               void* dg, long long lddg, void* du, long long lddu, int rows, int cols, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
+  if (cols % 8 || ldg % 8 || ldu % 8 || ldda % 8 || lddg % 8 || lddu % 8) return BTP_ERR_ALIGNMENT;
+  if (!al16(g) || !al16(u) || !al16(dact) || !al16(dg) || !al16(du)) return BTP_ERR_ALIGNMENT;
+  swiglu_bwd_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(
+      static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu, static_cast<const bf16*>(dact), ldda,
+      static_cast<bf16*>(dg), lddg, static_cast<bf16*>(du), lddu, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma, const float* dss,
+                const void* dres, long long ldr, void* dx, long long lddx, float* dgamma_partial, int max_blocks,
+                int* nblk_out, int rows, int width, cudaStream_t st) {
+  if (rows <= 0 || width <= 0 || max_blocks <= 0) return BTP_ERR_DIM;
+  if (width % 8 || width > 8192 || lddh % 8 || ldx % 8 || lddx % 8 || (dres && ldr % 8)) return BTP_ERR_ALIGNMENT;
+  if (!al16(dh) || !al16(x) || !al16(dx) || !al16(gamma) || (dres && !al16(dres))) return BTP_ERR_ALIGNMENT;
+  const int nch = width / 8;
+  int tpr = 256;
+  while (tpr > 32 && tpr / 2 >= nch) tpr /= 2;
+  if (nch > tpr * kNormBwdMaxGroups) return BTP_ERR_DIM;
+  const int slots = 256 / tpr;
+  int nblk = max_blocks;
+  int rows_per_block = (rows + nblk - 1) / nblk;
+  nblk = (rows + rows_per_block - 1) / rows_per_block;
+  const size_t smem = slots > 1 ? (size_t)slots * width * sizeof(float) : 0;
+  if (smem > 48 * 1024) return BTP_ERR_DIM;
+  rmsnorm_bwd_kernel<<<nblk, 256, smem, st>>>(static_cast<const bf16*>(dh), lddh, static_cast<const bf16*>(x), ldx,
+                                              gamma, dss, static_cast<const bf16*>(dres), ldr, static_cast<bf16*>(dx),
+                                              lddx, dgamma_partial, rows, width, tpr, rows_per_block);
+  if (nblk_out) *nblk_out = nblk;
+  BTP_CHECK_LAUNCH();
+}
+
+int reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
+                const float* col_scale, float* out, long long ldo, int accumulate, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || splits <= 0) return BTP_ERR_DIM;
+  if (cols % 4 || ldi % 4 || ldo % 4 || split_stride % 4) return BTP_ERR_ALIGNMENT;
+  reduce_rows_kernel<<<grid_for((long long)rows * cols / 4), 256, 0, st>>>(in, splits, split_stride, ldi, rows, cols,
+                                                                          col_scale, out, ldo, accumulate);
+  BTP_CHECK_LAUNCH();
+}
+
+int add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows, int cols,
+        cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
+  if (cols % 8 || lda % 8 || ldb % 8 || ldo % 8 || !al16(a) || !al16(b) || !al16(out)) return BTP_ERR_ALIGNMENT;
+  add_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(static_cast<const bf16*>(a), lda,
+                                                                   static_cast<const bf16*>(b), ldb,
+                                                                   static_cast<bf16*>(out), ldo, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+}  // namespace btp

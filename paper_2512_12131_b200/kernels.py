@@ -1,0 +1,173 @@
+"""Torch-tensor front end of the C-ABI kernels (device memory and streams come from torch;
+all arithmetic runs in libbtp.so).
+
+Every wrapper takes 2-D row-major views (last stride 1), forwards data pointers, leading
+dimensions and the current CUDA stream, and raises on a non-zero btp_status.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from ._native import GemmProblem
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+def _p(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _ld(t: torch.Tensor | None) -> int:
+    if t is None:
+        return 0
+    if t.dim() == 1:
+        return t.shape[0]
+    if t.stride(-1) != 1:
+        raise ValueError(f"tensor must be row-major in its last dim, strides {t.stride()}")
+    return t.stride(-2)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check(t: torch.Tensor, dtype, name: str):
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
+@dataclass
+class Gemm:
+    """One problem of a (grouped) GEMM launch.
+
+    a: [M, K] (a_mn False) or [K, M] (a_mn True);  b: [N, K] (b_mn False) or [K, N] (b_mn True)
+    c: [M, N] bf16/fp32, or [splits, M, N] fp32 partials when splits > 1.
+    """
+
+    a: torch.Tensor
+    b: torch.Tensor
+    c: torch.Tensor
+    a_mn: bool = False
+    b_mn: bool = False
+    row_scale: torch.Tensor | None = None
+    col_scale: torch.Tensor | None = None
+    resid: torch.Tensor | None = None
+    splits: int = 1
+    alpha: float = 1.0
+
+    def to_c(self) -> GemmProblem:
+        _check(self.a, BF16, "A")
+        _check(self.b, BF16, "B")
+        M, K = (self.a.shape[1], self.a.shape[0]) if self.a_mn else (self.a.shape[0], self.a.shape[1])
+        if self.b_mn:
+            Kb, N = self.b.shape
+        else:
+            N, Kb = self.b.shape
+        if Kb != K:
+            raise ValueError(f"GEMM inner dims disagree: A {tuple(self.a.shape)} B {tuple(self.b.shape)}")
+        c2 = self.c[0] if self.splits > 1 else self.c
+        if tuple(c2.shape) != (M, N):
+            raise ValueError(f"GEMM output {tuple(c2.shape)} != ({M}, {N})")
+        c_fp32 = self.c.dtype == F32
+        split_stride = self.c.stride(0) if self.splits > 1 else 0
+        return GemmProblem(
+            a=self.a.data_ptr(), lda=_ld(self.a), a_mn=int(self.a_mn),
+            b=self.b.data_ptr(), ldb=_ld(self.b), b_mn=int(self.b_mn),
+            c=self.c.data_ptr(), ldc=_ld(c2), c_fp32=int(c_fp32),
+            M=M, N=N, K=K,
+            row_scale=None if self.row_scale is None else self.row_scale.data_ptr(),
+            col_scale=None if self.col_scale is None else self.col_scale.data_ptr(),
+            resid=None if self.resid is None else self.resid.data_ptr(),
+            ld_resid=_ld(self.resid),
+            splits=self.splits, split_stride=split_stride, alpha=float(self.alpha),
+        )
+
+
+def gemm(*problems: Gemm, bn: int = 0) -> None:
+    """One launch of the persistent tcgen05 GEMM over 1..4 problems."""
+    arr = (GemmProblem * len(problems))(*[p.to_c() for p in problems])
+    _native.call("btp_gemm", arr, len(problems), bn, _stream())
+
+
+def rmsnorm_residual(x, gamma, *, branch=None, x_out=None, n_out=None, ss_out=None, rl_out=None, eps=1e-6):
+    rows, width = x.shape
+    _native.call(
+        "btp_rmsnorm_residual", _p(x), _ld(x), _p(branch), _ld(branch), _p(x_out), _ld(x_out), _p(gamma),
+        _p(n_out), _ld(n_out), _p(ss_out), _p(rl_out), rows, width, ctypes.c_float(eps), _stream(),
+    )
+
+
+def rmsnorm_apply(x, gamma, ss_total, d, n_out, *, rms_out=None, eps=1e-6):
+    rows, width = x.shape
+    _native.call(
+        "btp_rmsnorm_apply", _p(x), _ld(x), _p(gamma), _p(ss_total), d, ctypes.c_float(eps), _p(n_out),
+        _ld(n_out), _p(rms_out), rows, width, _stream(),
+    )
+
+
+def fixup_sigma(P, *, r, nproj, variant, z_out=None, a_out=None, ss_total=None, d=1, s_out=None, eps=1e-6):
+    rows = P.shape[0]
+    _native.call(
+        "btp_fixup_sigma", _p(P), _ld(P), _p(ss_total), d, ctypes.c_float(eps), _p(s_out), _p(z_out),
+        _ld(z_out), _p(a_out), _ld(a_out), rows, r, nproj, variant, _stream(),
+    )
+
+
+def fixup_sigma_bwd(z, da, dP, *, r, nproj, variant, s=None, d=1, dss=None):
+    rows = z.shape[0]
+    _native.call(
+        "btp_fixup_sigma_bwd", _p(z), _ld(z), _p(da), _ld(da), _p(s), d, _p(dP), _ld(dP), _p(dss), rows, r,
+        nproj, variant, _stream(),
+    )
+
+
+def swiglu(g, u, act):
+    rows, cols = g.shape
+    _native.call("btp_swiglu", _p(g), _ld(g), _p(u), _ld(u), _p(act), _ld(act), rows, cols, _stream())
+
+
+def swiglu_bwd(g, u, dact, dg, du):
+    rows, cols = g.shape
+    _native.call(
+        "btp_swiglu_bwd", _p(g), _ld(g), _p(u), _ld(u), _p(dact), _ld(dact), _p(dg), _ld(dg), _p(du), _ld(du),
+        rows, cols, _stream(),
+    )
+
+
+def rmsnorm_bwd(dh, x, gamma, dss, dx, dgamma_partial, *, dres=None) -> int:
+    """dgamma_partial: fp32 [max_blocks, width]; returns the number of partial rows written."""
+    rows, width = x.shape
+    nblk = ctypes.c_int(0)
+    _native.call(
+        "btp_rmsnorm_bwd", _p(dh), _ld(dh), _p(x), _ld(x), _p(gamma), _p(dss), _p(dres), _ld(dres), _p(dx),
+        _ld(dx), _p(dgamma_partial), dgamma_partial.shape[0], ctypes.byref(nblk), rows, width, _stream(),
+    )
+    return nblk.value
+
+
+def reduce_rows(parts, out, *, splits=None, col_scale=None, accumulate=False):
+    """out[r, c] = sum_s parts[s, r, c] (* col_scale[c]) (+ out); parts is [S, rows, cols] fp32."""
+    S = parts.shape[0] if splits is None else splits
+    rows, cols = out.shape if out.dim() == 2 else (1, out.shape[0])
+    ldi = parts.stride(1) if parts.dim() == 3 else cols
+    _native.call(
+        "btp_reduce_rows", _p(parts), S, parts.stride(0), ldi, rows, cols, _p(col_scale), _p(out),
+        _ld(out) if out.dim() == 2 else cols, int(accumulate), _stream(),
+    )
+
+
+def add(a, b, out):
+    rows, cols = a.shape
+    _native.call("btp_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), rows, cols, _stream())
+
+
+def num_sms() -> int:
+    return _native.load().btp_num_sms()
