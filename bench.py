@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark: train tokens/s (fwd+bwd) of one CoLA decoder block under BTP, TP = number of GPUs.
+
+Workload (BASELINE.json configs[1]): CoLA-1B block (d=2048, d_ff=5472, r=512, 32 heads),
+b=4, s=4096 (T=16384 tokens per step, counted once per TP group), BTP + online RMSNorm +
+grouped GEMMs, cola crossgate, bf16 storage / fp32 accumulation, synthetic seeded inputs and
+fan-in-scaled random-init weights. One step = forward + loss + backward (all weight grads).
+
+    python bench.py [--gpus N --steps K --warmup W]           # our arm (TP = N)
+    python bench.py --impl reference [...]                     # CPU reference arm (oracle port)
+    torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: one rank per GPU, NCCL
+
+Timing: W warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
+launching stream, max over ranks. Working set (~1.3 GB of activations) >> L2 (126 MB), so no
+L2 flush is needed. Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "train tokens/s (fwd+bwd) for CoLA block at TP 1/2/4/8; % of bf16 tensor peak"
+UNIT = "tokens/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), d.get("hbm_gbs", 6650.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def flops_per_step(cfg, b, s, lowrank=True):
+    """Algorithmic FLOPs of one block fwd+bwd: 3*[2T(11dr+3d_ff r) + 4 b s^2 d]."""
+    T = b * s
+    lin = 2 * T * (11 * cfg.d * cfg.r + 3 * cfg.d_ff * cfg.r) if lowrank else 2 * T * (4 * cfg.d**2 + 3 * cfg.d * cfg.d_ff)
+    return 3 * (lin + 4 * b * s * s * cfg.d)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------- CPU arm
+def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True):
+    """Oracle port (float64 NumPy, BLAS) fwd+bwd on a bounded sample: ONE sequence (b=1) of the
+    workload's length s. Returns (tokens_per_s, per-step seconds list, threads)."""
+    from oracle import btp_oracle as O
+
+    blk = O.build_block(cfg.d, cfg.d_ff, cfg.r, "cola", 0, scale_fan_in=3.0)
+    x = O.seeded_fill((s, cfg.d), 10000)
+    G = O.loss_projection((s, cfg.d), 30000)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        y, cache = O.block_forward(blk, x, 1, s, cfg.heads, lean=lean)
+        O.block_backward(blk, cache, G, 1, s, cfg.heads)
+        times.append(time.perf_counter() - t0)
+        if max_steps is not None and len(times) >= max_steps:
+            break
+        if max_steps is None and time.perf_counter() - t_start > seconds_budget:
+            break
+    threads = _blas_threads()
+    return s / statistics.median(times), times, threads
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    # W untimed + K timed steps of the bounded sample (1 sequence of s tokens, fwd+bwd)
+    from oracle import btp_oracle as O  # noqa: F401
+
+    cpu_oracle_rate(cfg, args.s, max_steps=max(args.warmup, 1))
+    rate, times, threads = cpu_oracle_rate(cfg, args.s, max_steps=args.steps)
+    ms = statistics.mean(times) * 1e3
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"CoLA-{args.config} block fwd+bwd, BTP math, b={args.b} s={args.s}",
+                   "sample": f"1 sequence x {args.s} tokens per step (b=1 of {args.b})"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"b=1 s={args.s} CoLA-{args.config} block fwd+bwd per step, float64 NumPy/BLAS "
+                                   "restatement of btpsim (reference itself is forward-only)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------- GPU arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2512_12131_b200.api import BlockTrainer
+    from paper_2512_12131_b200.model import RunShape, Variant, build_block, fan_in_scaled
+    from paper_2512_12131_b200.plan import Strategy, plan
+    from paper_2512_12131_b200.tensor import seeded_fill
+
+    b, s, tp = args.b, args.s, world
+    shape = RunShape(b, s, tp)
+    strategy = Strategy(args.strategy)
+    variant = Variant.FULL_RANK if strategy is Strategy.FULL_RANK else Variant.COLA
+    pl = plan(strategy, cfg, shape, None if variant is Variant.FULL_RANK else variant,
+              online_norm=strategy is Strategy.BOTTLENECK, grouping=not args.no_grouping,
+              lowrank_ckpt=args.ckpt)
+    blk = fan_in_scaled(build_block(cfg, variant, 0))
+    x = seeded_fill((b, s, cfg.d), 10000).values
+    G = seeded_fill((b, s, cfg.d), 30000).values
+    trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph)
+    x_dev, g_dev = trainer.device_inputs(x, G)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        trainer.step_device(x_dev, g_dev)
+    barrier()
+    launches0 = trainer.kernel_launches
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            trainer.step_device(x_dev, g_dev)
+        e1.record(st)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = (trainer.kernel_launches - launches0)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = b * s / (ms / 1e3)
+
+    # ---- end to end through the public API: pinned host inputs -> H2D -> step -> loss D2H
+    xh, gh = trainer.pinned_host_inputs(x, G)
+    for _ in range(2):
+        trainer.step(xh, gh)
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    for _ in range(args.steps):
+        loss = trainer.step(xh, gh)
+    e3.record(st)
+    barrier()
+    ms_e2e = e2.elapsed_time(e3) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    e2e = {"value": b * s / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * 2 + gh.numel() * 2),
+           "d2h_bytes_per_step": 4, "loss": loss}
+
+    # ---- roofline of the dominant kernel (the tcgen05 GEMM family), timed live per launch
+    gemm = trainer.time_gemms(x_dev, g_dev)
+    peak_burst, peak_sus, hbm, peak_kind = _peaks()
+    flops = flops_per_step(cfg, b, s, lowrank=variant is not Variant.FULL_RANK) / tp
+    roof = {"bound": "tensor", "kernel": "btp gemm_kernel (all tcgen05 GEMM launches of one step)",
+            "achieved": gemm["tflops"], "peak": peak_sus, "unit": "TFLOP/s", "frac": gemm["tflops"] / peak_sus,
+            "traffic": None, "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
+            "gemm_share_of_step": gemm["ms"] / ms, "gemm_launches_per_step": gemm["launches"],
+            "step_frac_of_peak": flops / (ms / 1e3) / 1e12 / peak_sus}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform inputs, fan-in-scaled random init)",
+        "config": {"workload": f"CoLA-{args.config} decoder block fwd+bwd, {strategy.value} "
+                               f"{'grouped ' if pl.grouping else ''}{'online-RMSNorm ' if pl.norm_mode.value == 'online' else ''}"
+                               f"TP={tp}{' lowrank-ckpt' if pl.lowrank_ckpt else ''}",
+                   "d": cfg.d, "d_ff": cfg.d_ff, "r": cfg.r, "heads": cfg.heads, "global_batch": b, "seq_len": s,
+                   "tokens_per_step": b * s, "parallelism": f"tp{tp}", "l2": "inputs larger than L2 (no flush)",
+                   "cuda_graph": trainer.graphed, "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roof,
+        "algorithmic_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, times, threads = cpu_oracle_rate(cfg, s, seconds_budget=args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"b=1 s={s} (1 of {b} sequences) CoLA-{args.config} block fwd+bwd, float64 "
+                                          f"NumPy/BLAS oracle, {len(times)} steps"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="1b")
+    ap.add_argument("--b", type=int, default=4)
+    ap.add_argument("--s", type=int, default=4096)
+    ap.add_argument("--strategy", default="btp", choices=["btp", "vanilla", "full-rank"])
+    ap.add_argument("--ckpt", action="store_true")
+    ap.add_argument("--no-grouping", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args(argv)
+    from paper_2512_12131_b200.model import COLA_60M, preset
+
+    cfg = COLA_60M if args.config == "60m" else preset(args.config)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -122,6 +122,12 @@ int btp_reduce_rows(const float* in, int splits, long long split_stride, long lo
 int btp_add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows,
             int cols, void* stream);
 
+/* partial[blk] = sum over a block's share of rows of <a_row, b_row> (bf16 in, fp32 out), for the
+ * builder-defined loss L = sum(y * G) (the reference has no loss). Reduce the *nblk partials with
+ * btp_reduce_rows; deterministic. */
+int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
+            int max_blocks, int* nblk, void* stream);
+
 /* Number of SMs the library sizes persistent grids for (device 0 of the current context). */
 int btp_num_sms(void);
 

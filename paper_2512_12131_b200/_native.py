@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "btp_rmsnorm_bwd",
     "btp_reduce_rows",
     "btp_add",
+    "btp_dot",
     "btp_num_sms",
     "btp_version",
 )
@@ -93,6 +94,7 @@ _SIGNATURES = {
     "btp_rmsnorm_bwd": [_P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _I, ctypes.POINTER(_I), _I, _I, _P],
     "btp_reduce_rows": [_P, _I, _LL, _LL, _I, _I, _P, _P, _LL, _I, _P],
     "btp_add": [_P, _LL, _P, _LL, _P, _LL, _I, _I, _P],
+    "btp_dot": [_P, _LL, _P, _LL, _I, _I, _P, _I, ctypes.POINTER(_I), _P],
     "btp_num_sms": [],
     "btp_version": [],
 }

@@ -1,0 +1,236 @@
+"""Public entry points, drop-in for the reference's `execute_forward` (simulator.py:268-316)
+plus the training step the reference does not have.
+
+Process model: one process per GPU. At tp == 1 no process group is needed. At tp > 1 the
+caller runs one process per TP rank with torch.distributed initialised (NCCL on the box); each
+rank calls the same function with the same logical inputs, exactly like the reference's SPMD
+ranks, and gets back the same gathered logical output.
+
+Input/output convention matches the reference: x is a host `Tensor` [b, s, d] (float64 values),
+y is returned as a host float64 `Tensor` [b, s, d]. Arithmetic runs in bf16/fp32 on the GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+from .comm import TPComm
+from .executor import BTPBlockExecutor
+from .model import EPS_DEFAULT, DecoderBlockWeights, Variant
+from .plan import PlanError, ShardPlan, Strategy
+from .tensor import Tensor
+from .trace import Trace
+
+BF16 = torch.bfloat16
+
+
+@dataclass
+class SimResult:
+    """Same fields as the reference's SimResult (simulator.py:189-195). `workspaces` holds only
+    THIS rank's dict (index rank) — other ranks live in other processes — and is filled only
+    when capture_workspaces=True."""
+
+    y: Tensor
+    h_cur: dict | None
+    trace: Trace
+    workspaces: list
+    plan: ShardPlan
+
+
+@dataclass
+class StepResult:
+    y: Tensor
+    loss: float
+    dx: np.ndarray            # this rank's [T, d/tp] input-gradient shard (float64 host copy)
+    grads: dict               # this rank's weight grads keyed like the reference block
+    trace: Trace
+    plan: ShardPlan
+    executor: object
+
+
+def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
+    if block.variant is not pl.variant:
+        raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
+    xv = x.values if isinstance(x, Tensor) else np.asarray(x)
+    if xv.ndim != 3 or xv.shape[2] != pl.cfg.d:
+        raise PlanError(f"x must be [b, s, d={pl.cfg.d}], got {tuple(xv.shape)}")
+    if (xv.shape[0], xv.shape[1]) != (pl.shape.b, pl.shape.s):
+        raise PlanError(f"x batch/seq {tuple(xv.shape[:2])} disagrees with plan shape")
+    return xv
+
+
+def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
+                  device=None, attn_backend: str = "auto"):
+    """Build this rank's executor for the plan's strategy."""
+    comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if pl.strategy is Strategy.BOTTLENECK:
+        return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend)
+    from .baselines import FullRankExecutor, VanillaExecutor
+
+    cls = VanillaExecutor if pl.strategy is Strategy.VANILLA else FullRankExecutor
+    return cls(pl, block, comm, dev, eps, attn_backend)
+
+
+def shard_input(ex, xv: np.ndarray) -> torch.Tensor:
+    """This rank's slice of the logical input as a device bf16 [T, width] tensor."""
+    T = xv.shape[0] * xv.shape[1]
+    x2 = xv.reshape(T, -1)
+    if getattr(ex, "residual_sharded", True):
+        lo = ex.rank * ex.dl
+        x2 = x2[:, lo:lo + ex.dl]
+    return torch.from_numpy(np.ascontiguousarray(x2)).to(ex.dev, BF16)
+
+
+def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
+    if not getattr(ex, "residual_sharded", True):
+        return y_sh
+    if model_tail:
+        return ex.comm.all_gather_cols(y_sh, "final-gather", tag="boundary")
+    if ex.tp == 1:
+        return y_sh
+    # host-side result assembly (the reference concatenates without a record, simulator.py:713)
+    parts = [torch.empty_like(y_sh) for _ in range(ex.tp)]
+    dist.all_gather(parts, y_sh.contiguous())
+    return torch.cat(parts, dim=1)
+
+
+def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *, eps: float = EPS_DEFAULT,
+                    model_tail: bool = False, trace: Trace | None = None, capture_workspaces: bool = False,
+                    attn_backend: str = "auto") -> SimResult:
+    """Run one block forward under the plan on the GPU; returns the gathered logical y."""
+    if h_prev is not None and block.variant is Variant.LAX:
+        raise PlanError("the lax variant is outside the device path (SURVEY §2.1: out of scope)")
+    xv = _check_inputs(pl, block, x)
+    ex = make_executor(pl, block, eps=eps, trace=trace, attn_backend=attn_backend)
+    x_sh = shard_input(ex, xv)
+    y_sh = ex.forward(x_sh)
+    y = _gather_y(ex, y_sh, model_tail)
+    ws = [dict() for _ in range(pl.shape.tp)]
+    if capture_workspaces:
+        ws[ex.rank] = ex.capture_workspaces()
+    b, s, d = xv.shape
+    y_host = y.double().cpu().numpy().reshape(b, s, d)
+    eb = x.element_bytes if isinstance(x, Tensor) else 2
+    return SimResult(Tensor(y_host, eb), None, ex.comm.trace, ws, pl)
+
+
+def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: float = EPS_DEFAULT,
+               attn_backend: str = "auto", executor=None) -> StepResult:
+    """Forward + backward of the block for the builder-defined loss L = sum(y * G) (dL/dy = G).
+
+    G defaults to the loss projection seeded_fill((b, s, d), 30000)."""
+    from .tensor import seeded_fill
+
+    xv = _check_inputs(pl, block, x)
+    b, s, d = xv.shape
+    if G is None:
+        G = seeded_fill((b, s, d), 30000).values
+    Gv = G.values if isinstance(G, Tensor) else np.asarray(G)
+    ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend)
+    x_sh = shard_input(ex, xv)
+    g_sh = shard_input(ex, Gv)
+    y_sh = ex.forward(x_sh)
+    loss = ex.loss(y_sh, g_sh)
+    dx = ex.backward(g_sh)
+    y = _gather_y(ex, y_sh, False)
+    return StepResult(
+        y=Tensor(y.double().cpu().numpy().reshape(b, s, d)),
+        loss=loss,
+        dx=dx.double().cpu().numpy(),
+        grads=ex.weight_grads_by_name(),
+        trace=ex.comm.trace,
+        plan=pl,
+        executor=ex,
+    )
+
+
+class BlockTrainer:
+    """Persistent block training step on this rank: weights, activations and workspaces stay
+    resident in HBM; one step = forward + loss + backward. At tp == 1 the whole step is captured
+    once into a CUDA graph and replayed (the step is ~60 kernel launches).
+
+    step_device(x, G): device-resident inputs, no host sync (the bench's `value`).
+    step(x_host, G_host): the user-facing call — H2D copy of this step's pinned-host inputs,
+    the step, and a D2H read of the loss (the bench's `e2e`)."""
+
+    def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
+                 attn_backend: str = "auto", use_graph: bool = True):
+        self.pl = pl
+        self.ex = make_executor(pl, block, eps=eps, attn_backend=attn_backend)
+        self.use_graph = use_graph and pl.shape.tp == 1
+        self.graph = None
+        self.graphed = False
+        self._per_step_launches = 0
+        self._replays = 0
+        self._x = self._g = None
+        self.loss_buf = None
+
+    @property
+    def kernel_launches(self) -> int:
+        return self.ex.stats.kernel_launches + self._replays * self._per_step_launches
+
+    def device_inputs(self, x: np.ndarray, G: np.ndarray):
+        self._x, self._g = shard_input(self.ex, np.asarray(x)), shard_input(self.ex, np.asarray(G))
+        return self._x, self._g
+
+    def pinned_host_inputs(self, x: np.ndarray, G: np.ndarray):
+        xs, gs = shard_input(self.ex, np.asarray(x)).cpu(), shard_input(self.ex, np.asarray(G)).cpu()
+        return xs.pin_memory(), gs.pin_memory()
+
+    def _eager(self, x, g):
+        y = self.ex.forward(x)
+        self.loss_buf = self.ex.loss_device(y, g)
+        self.ex.backward(g)
+
+    def step_device(self, x: torch.Tensor, g: torch.Tensor) -> None:
+        if not self.use_graph:
+            self._eager(x, g)
+            return
+        if self._x is None or x.data_ptr() != self._x.data_ptr() or g.data_ptr() != self._g.data_ptr():
+            self._x, self._g = x, g
+            self.graph = None
+        if self.graph is None:
+            # eager warm-up allocates every buffer, then capture one step into a graph
+            before = self.ex.stats.kernel_launches
+            self._eager(x, g)
+            self._per_step_launches = self.ex.stats.kernel_launches - before
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                saved = self.ex.stats.kernel_launches
+                with torch.cuda.graph(graph, stream=side):
+                    self._eager(x, g)
+                self.ex.stats.kernel_launches = saved
+            torch.cuda.current_stream().wait_stream(side)
+            self.graph, self.graphed = graph, True
+        self.graph.replay()
+        self._replays += 1
+
+    def step(self, x_host: torch.Tensor, g_host: torch.Tensor) -> float:
+        if self._x is None:
+            self._x = torch.empty(x_host.shape, dtype=x_host.dtype, device=self.ex.dev)
+            self._g = torch.empty(g_host.shape, dtype=g_host.dtype, device=self.ex.dev)
+        self._x.copy_(x_host, non_blocking=True)
+        self._g.copy_(g_host, non_blocking=True)
+        self.step_device(self._x, self._g)
+        return float(self.loss_buf.item())
+
+    def time_gemms(self, x: torch.Tensor, g: torch.Tensor) -> dict:
+        """One eager step with every GEMM launch bracketed by CUDA events on its stream."""
+        self.ex.gemm_timer = []
+        self._eager(x, g)
+        torch.cuda.synchronize()
+        rec, self.ex.gemm_timer = self.ex.gemm_timer, None
+        ms = sum(a.elapsed_time(b) for a, b, _ in rec)
+        fl = sum(f for _, _, f in rec)
+        per = [(a.elapsed_time(b), f) for a, b, f in rec]
+        return {"ms": ms, "flops": fl, "tflops": fl / (ms / 1e3) / 1e12 if ms else 0.0, "launches": len(rec),
+                "per_launch": per}

@@ -66,9 +66,9 @@ class TPComm:
         """Gather [rows, w] shards along the feature axis into [rows, tp*w]."""
         rows, w = shard.shape
         if self.tp > 1:
-            stacked = torch.empty((self.tp, rows, w), dtype=shard.dtype, device=shard.device)
+            stacked = torch.empty((self.tp * rows, w), dtype=shard.dtype, device=shard.device)
             dist.all_gather_into_tensor(stacked, shard.contiguous(), group=self.group)
-            out = stacked.permute(1, 0, 2).reshape(rows, self.tp * w)
+            out = stacked.view(self.tp, rows, w).permute(1, 0, 2).reshape(rows, self.tp * w)
         else:
             out = shard
         self.trace.emit("all-gather", chunk_id, tag, out.numel(), self.pass_tag)

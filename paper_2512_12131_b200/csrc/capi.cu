@@ -76,6 +76,11 @@ int btp_add(const void* a, long long lda, const void* b, long long ldb, void* ou
   return btp::add(a, lda, b, ldb, out, ldo, rows, cols, ST(stream));
 }
 
+int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
+            int max_blocks, int* nblk, void* stream) {
+  return btp::dot(a, lda, b, ldb, rows, cols, partial, max_blocks, nblk, ST(stream));
+}
+
 int btp_num_sms(void) { return btp::num_sms_cached(); }
 
 const char* btp_version(void) { return "btp-b200 0.1.0 (sm_100a)"; }

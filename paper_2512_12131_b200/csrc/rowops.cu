@@ -409,6 +409,36 @@ __global__ void __launch_bounds__(256) add_kernel(const bf16* __restrict__ a, lo
   }
 }
 
+
+// ----------------------------------------------------------------------------- loss dot
+// partial[blk] = sum over this block's rows of <a_row, b_row>; fixed block/thread order.
+__global__ void __launch_bounds__(256) dot_kernel(const bf16* __restrict__ a, long long lda,
+                                                  const bf16* __restrict__ b, long long ldb, int rows, int cols,
+                                                  float* __restrict__ partial) {
+  __shared__ float red[8];
+  const int per_row = cols >> 3;
+  const long long total = (long long)per_row * rows;
+  float acc = 0.f;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 8;
+    float fa[8], fb[8];
+    unpack8(*reinterpret_cast<const uint4*>(a + (long long)row * lda + c), fa);
+    unpack8(*reinterpret_cast<const uint4*>(b + (long long)row * ldb + c), fb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = fmaf(fa[j], fb[j], acc);
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    partial[blockIdx.x] = s;
+  }
+}
+
 // ============================================================================= launchers
 static inline int grid_for(long long items, int threads = 256) {
   const long long want = (items + threads - 1) / threads;
@@ -531,10 +561,32 @@ int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, co
   BTP_CHECK_LAUNCH();
 }
 
+__global__ void __launch_bounds__(256) reduce_rows_scalar_kernel(const float* __restrict__ in, int splits,
+                                                                 long long split_stride, long long ldi, int rows,
+                                                                 int cols, const float* __restrict__ col_scale,
+                                                                 float* __restrict__ out, long long ldo,
+                                                                 int accumulate) {
+  const long long total = (long long)rows * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / cols);
+    const int c = (int)(idx - (long long)row * cols);
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += in[k * split_stride + (long long)row * ldi + c];
+    if (col_scale != nullptr) s *= col_scale[c];
+    float* o = out + (long long)row * ldo + c;
+    *o = accumulate ? *o + s : s;
+  }
+}
+
 int reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
                 const float* col_scale, float* out, long long ldo, int accumulate, cudaStream_t st) {
   if (rows <= 0 || cols <= 0 || splits <= 0) return BTP_ERR_DIM;
-  if (cols % 4 || ldi % 4 || ldo % 4 || split_stride % 4) return BTP_ERR_ALIGNMENT;
+  if (cols % 4 || ldi % 4 || ldo % 4 || split_stride % 4 || !al16(in) || !al16(out) || (col_scale && !al16(col_scale))) {
+    reduce_rows_scalar_kernel<<<grid_for((long long)rows * cols), 256, 0, st>>>(in, splits, split_stride, ldi, rows,
+                                                                             cols, col_scale, out, ldo, accumulate);
+    BTP_CHECK_LAUNCH();
+  }
   reduce_rows_kernel<<<grid_for((long long)rows * cols / 4), 256, 0, st>>>(in, splits, split_stride, ldi, rows, cols,
                                                                           col_scale, out, ldo, accumulate);
   BTP_CHECK_LAUNCH();
@@ -547,6 +599,18 @@ int add(const void* a, long long lda, const void* b, long long ldb, void* out, l
   add_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(static_cast<const bf16*>(a), lda,
                                                                    static_cast<const bf16*>(b), ldb,
                                                                    static_cast<bf16*>(out), ldo, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+int dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
+        int max_blocks, int* nblk_out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || max_blocks <= 0) return BTP_ERR_DIM;
+  if (cols % 8 || lda % 8 || ldb % 8 || !al16(a) || !al16(b)) return BTP_ERR_ALIGNMENT;
+  int nblk = grid_for((long long)rows * cols / 8);
+  if (nblk > max_blocks) nblk = max_blocks;
+  dot_kernel<<<nblk, 256, 0, st>>>(static_cast<const bf16*>(a), lda, static_cast<const bf16*>(b), ldb, rows, cols,
+                                   partial);
+  if (nblk_out) *nblk_out = nblk;
   BTP_CHECK_LAUNCH();
 }
 

@@ -1,0 +1,541 @@
+"""Device executor of one decoder block under a BTP plan, forward + backward, on one TP rank.
+
+Follows the reference's BTP chunk orchestration (`_forward_btp`, simulator.py:550-714) with
+every compute site on libbtp.so kernels and every boundary on `TPComm` (NCCL on the box):
+
+  attention half  K3 norm1(x) -> K1 down qkv (x rms_loc) -> AR [T,3r]+rider -> K4 fix-up+sigma
+                  -> K2 batched up q|k|v -> SDPA -> K1 down o -> AR [T,r] -> K4 sigma
+                  -> K2 up o (+x residual in the epilogue) = x_mid
+  mlp half        K3 norm2(x_mid) -> K1 down gate|up -> AR [T,2r]+rider -> K4 -> K2 batched up
+                  gate|up -> K5 swiglu -> K1 down -> AR [T,r] -> K4 -> K2 up down (+x_mid) = y
+
+Backward mirrors it (the reference has none): each up-projection's input gradient is the
+only collective ([T,k*r] all-reduce), sigma-bwd and the online-norm backward are rank-local
+(dP = dz/s, dss = -<dz,z>/(2 s^2 d), dx = dh*gamma + 2 x dss), and every weight gradient is
+a local split-K tcgen05 GEMM in fp32. The down-factor gradient uses dB_i = (dP^T x_i) * gamma_i
+(column scale), so the normalised activations never need to be kept.
+
+Low-rank activation checkpointing (plan.lowrank_ckpt, reference simulator.py:720-921): the
+forward keeps only x, the seven rank-r z's and the per-row global RMS; backward recomputes
+sigma, the up-projections, attention and swiglu with ZERO collectives.
+
+Layouts (per rank, dl = d/tp, fl = d_ff/tp): activations row-major bf16 [T, width]; the
+grouped down weight [k*r, dl] (K-major, so the forward GEMM reads it directly and dgrad reads
+it MN-major); up weights [d_out/tp, r]; all weight grads fp32.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .attention import Attention
+from .comm import TPComm
+from .model import DecoderBlockWeights, Variant
+from .plan import NormMode, PlanError, ShardPlan, Strategy
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+_VAR = {Variant.SVD: 0, Variant.COLA: 1}
+
+
+def _pick_splits(tiles: int, k_blocks: int, sms: int) -> int:
+    """Split-K factor for a weight-gradient GEMM: fill >= ~90% of the SM waves while keeping
+    >= 8 k-blocks (512 tokens) per split."""
+    best, best_eff = 1, 0.0
+    for s in range(1, 17):
+        if k_blocks // s < 8:
+            break
+        waves = math.ceil(tiles * s / sms)
+        eff = tiles * s / (waves * sms)
+        if eff >= 0.9:
+            return s
+        if eff > best_eff + 1e-9:
+            best, best_eff = s, eff
+    return best
+
+
+@dataclass
+class StepStats:
+    gemm_launches: int = 0
+    kernel_launches: int = 0
+    gemm_flops: int = 0
+
+
+class BTPBlockExecutor:
+    """One rank's shard of a low-rank (svd/cola) block under a BTP plan."""
+
+    def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None,
+                 device: torch.device | str = "cuda", eps: float = 1e-6, attn_backend: str = "auto"):
+        if pl.strategy is not Strategy.BOTTLENECK:
+            raise PlanError(f"BTPBlockExecutor needs a btp plan, got {pl.strategy.value}")
+        if block.variant is not pl.variant:
+            raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
+        if pl.variant not in _VAR:
+            raise PlanError(f"variant {pl.variant.value} is not supported on the device path (svd, cola)")
+        self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
+        self.comm = comm if comm is not None else TPComm(1, 0)
+        if self.comm.tp != pl.shape.tp:
+            raise PlanError(f"communicator size {self.comm.tp} != plan tp {pl.shape.tp}")
+        self.dev = torch.device(device)
+        self.eps = eps
+        self.var = _VAR[pl.variant]
+        self.online = pl.norm_mode is NormMode.ONLINE
+        self.grouping = pl.grouping
+        self.ckpt = pl.lowrank_ckpt
+        cfg, tp, rank = self.cfg, pl.shape.tp, self.comm.rank
+        self.tp, self.rank = tp, rank
+        self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
+        self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
+        self.T = pl.shape.tokens
+        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim, attn_backend)
+        self.sms = K.num_sms()
+        self._load_weights(block)
+        self.stats = StepStats()
+        self._buf: dict[str, torch.Tensor] = {}
+        self.saved: dict[str, torch.Tensor] = {}
+
+    # ------------------------------------------------------------------ weights
+    def _load_weights(self, block: DecoderBlockWeights) -> None:
+        sl = slice(self.rank * self.dl, (self.rank + 1) * self.dl)
+        fsl = slice(self.rank * self.fl, (self.rank + 1) * self.fl)
+        B = {n: t.values for n, t in block.down_factors.items()}
+        A = {n: t.values for n, t in block.up_factors.items()}
+
+        def dev(a, dtype=BF16):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype)
+
+        self.W = {
+            "d_qkv": dev(np.concatenate([B[n][:, sl] for n in ("q", "k", "v")], axis=0)),   # [3r, dl]
+            "u_qkv": dev(np.stack([A[n][sl, :] for n in ("q", "k", "v")])),                 # [3, dl, r]
+            "d_o": dev(B["o"][:, sl]),                                                       # [r, dl]
+            "u_o": dev(A["o"][sl, :]),                                                       # [dl, r]
+            "d_gu": dev(np.concatenate([B[n][:, sl] for n in ("gate", "up")], axis=0)),     # [2r, dl]
+            "u_gu": dev(np.stack([A[n][fsl, :] for n in ("gate", "up")])),                  # [2, fl, r]
+            "d_d": dev(B["down"][:, fsl]),                                                   # [r, fl]
+            "u_d": dev(A["down"][sl, :]),                                                    # [dl, r]
+        }
+        self.gamma1 = dev(block.gamma1.values[sl], F32)
+        self.gamma2 = dev(block.gamma2.values[sl], F32)
+        self.grad = {k: torch.zeros(v.shape, device=self.dev, dtype=F32) for k, v in self.W.items()}
+        self.grad["gamma1"] = torch.zeros(self.dl, device=self.dev, dtype=F32)
+        self.grad["gamma2"] = torch.zeros(self.dl, device=self.dev, dtype=F32)
+
+    def weight_grads_by_name(self) -> dict[str, dict[str, np.ndarray]]:
+        """Rank-local gradients keyed like the reference block: {'A': {name: [d_out/tp, r]},
+        'B': {name: [r, d_in/tp]}, 'gamma1': [dl], 'gamma2': [dl]} (float64 host copies)."""
+        g = {k: v.double().cpu().numpy() for k, v in self.grad.items()}
+        r = self.r
+        out = {"A": {}, "B": {}, "gamma1": g["gamma1"], "gamma2": g["gamma2"]}
+        for i, n in enumerate(("q", "k", "v")):
+            out["B"][n] = g["d_qkv"][i * r:(i + 1) * r]
+            out["A"][n] = g["u_qkv"][i]
+        for i, n in enumerate(("gate", "up")):
+            out["B"][n] = g["d_gu"][i * r:(i + 1) * r]
+            out["A"][n] = g["u_gu"][i]
+        out["B"]["o"], out["A"]["o"] = g["d_o"], g["u_o"]
+        out["B"]["down"], out["A"]["down"] = g["d_d"], g["u_d"]
+        return out
+
+    # ------------------------------------------------------------------ buffers
+    def buf(self, name: str, shape, dtype=BF16) -> torch.Tensor:
+        t = self._buf.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, device=self.dev, dtype=dtype)
+            self._buf[name] = t
+        return t
+
+    def _wgrad_parts(self, n_elems: int) -> torch.Tensor:
+        t = self._buf.get("_wg_parts")
+        if t is None or t.numel() < n_elems:
+            t = torch.empty(n_elems, device=self.dev, dtype=F32)
+            self._buf["_wg_parts"] = t
+        return t
+
+    # ------------------------------------------------------------------ GEMM helpers
+    gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
+
+    def _gemm(self, *probs: K.Gemm) -> None:
+        flops = 0
+        for p in probs:
+            M = p.a.shape[1] if p.a_mn else p.a.shape[0]
+            Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
+            N = p.b.shape[1] if p.b_mn else p.b.shape[0]
+            flops += 2 * M * N * Kd
+        if self.gemm_timer is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            K.gemm(*probs)
+            e1.record()
+            self.gemm_timer.append((e0, e1, flops))
+        else:
+            K.gemm(*probs)
+        self.stats.gemm_launches += 1
+        self.stats.kernel_launches += 1
+        self.stats.gemm_flops += flops
+
+    def _wgrad(self, pairs, col_scale=None):
+        """pairs: list of (dY [T, M] (MN-major A), X [T, N] (MN-major B), out fp32 [M, N]).
+        out = (dY^T X) (* col_scale) via split-K and a deterministic reduction."""
+        T = pairs[0][0].shape[0]
+        kb = (T + 63) // 64
+        tiles = sum(math.ceil(dy.shape[1] / 128) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
+        splits = _pick_splits(tiles, kb, self.sms)
+        if splits == 1 and col_scale is None:
+            self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True) for dy, x, o in pairs])
+            return
+        sizes = [splits * o.numel() for _, _, o in pairs]
+        flat = self._wgrad_parts(sum(sizes))
+        probs, views, off = [], [], 0
+        for (dy, x, o), n in zip(pairs, sizes):
+            part = flat[off:off + n].view(splits, *o.shape)
+            off += n
+            probs.append(K.Gemm(dy, x, part, a_mn=True, b_mn=True, splits=splits))
+            views.append((part, o))
+        self._gemm(*probs)
+        for part, o in views:
+            K.reduce_rows(part, o, col_scale=col_scale)
+            self.stats.kernel_launches += 1
+
+    # ------------------------------------------------------------------ forward pieces
+    def _norm(self, x, gamma, tag):
+        """Online: n = x*gamma/rms_loc, ss -> rider. Sync: stat AR then global normalisation."""
+        T, dl = self.T, self.dl
+        n = self.buf(f"n{tag}", (T, dl))
+        ss = self.buf(f"ss{tag}", (T,), F32)
+        if self.online:
+            rl = self.buf(f"rl{tag}", (T,), F32)
+            K.rmsnorm_residual(x, gamma, n_out=n, ss_out=ss, rl_out=rl, eps=self.eps)
+            self.stats.kernel_launches += 1
+            return n, ss, rl, None
+        K.rmsnorm_residual(x, gamma, ss_out=ss, eps=self.eps)
+        self.comm.all_reduce(ss, f"norm{tag}-stat", tag="block")
+        s = self.buf(f"s{tag}", (T,), F32)
+        K.rmsnorm_apply(x, gamma, ss, self.d, n, rms_out=s, eps=self.eps)
+        self.stats.kernel_launches += 2
+        return n, ss, None, s
+
+    def _down_boundary(self, names, n_in, W, ss, rl, s_tag, norm_chunk: bool):
+        """Row-parallel down GEMM(s) -> all-reduce(s) -> fix-up + sigma.
+        Returns (z views, a views, P storage); z aliases the all-reduce buffer."""
+        T, r, k = self.T, self.r, len(names)
+        row_scale = rl if (norm_chunk and self.online) else None
+        ss_total = ss if (norm_chunk and self.online) else None
+        s_out = self.buf(f"s{s_tag}", (T,), F32) if (norm_chunk and self.online) else None
+        a_store = self.buf(f"a_{'_'.join(names)}", (T, k * r)) if self.var == 1 else None
+        if self.grouping or k == 1:
+            P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
+            self._gemm(K.Gemm(n_in, W, P, row_scale=row_scale))
+            if ss_total is not None:
+                self.comm.all_reduce_coalesced(P, ss, names[0] if k == 1 else self._gid(names))
+            else:
+                self.comm.all_reduce(P, names[0] if k == 1 else self._gid(names))
+            if self.var == 1 or ss_total is not None:
+                K.fixup_sigma(P, r=r, nproj=k, variant=self.var, z_out=P, a_out=a_store, ss_total=ss_total,
+                              d=self.d, s_out=s_out, eps=self.eps)
+                self.stats.kernel_launches += 1
+            z = [P[:, i * r:(i + 1) * r] for i in range(k)]
+            a = [a_store[:, i * r:(i + 1) * r] for i in range(k)] if a_store is not None else z
+            return z, a, P
+        # ungrouped: one GEMM + one collective per projection (reference simulator.py:623-639)
+        P3 = self.buf(f"P3_{'_'.join(names)}", (k, T, r))
+        z, a = [], []
+        for i, nm in enumerate(names):
+            self._gemm(K.Gemm(n_in, W[i * r:(i + 1) * r], P3[i], row_scale=row_scale))
+            if ss_total is not None and i == 0:
+                self.comm.all_reduce_coalesced(P3[i], ss, nm)
+            else:
+                self.comm.all_reduce(P3[i], nm)
+            if self.var == 1 or ss_total is not None:
+                a_i = a_store[:, i * r:(i + 1) * r] if a_store is not None else None
+                K.fixup_sigma(P3[i], r=r, nproj=1, variant=self.var, z_out=P3[i], a_out=a_i, ss_total=ss_total,
+                              d=self.d, s_out=s_out if i == 0 else None, eps=self.eps)
+                self.stats.kernel_launches += 1
+            z.append(P3[i])
+            a.append(a_store[:, i * r:(i + 1) * r] if a_store is not None else P3[i])
+        return z, a, P3
+
+    @staticmethod
+    def _gid(names) -> str:
+        return {("q", "k", "v"): "qkv", ("gate", "up"): "gate_up"}[tuple(names)]
+
+    def _sigma_only(self, z_views, names, out_name):
+        """a = sigma(z) for stored z (checkpoint recompute); svd: a = z."""
+        if self.var == 0:
+            return z_views
+        T, r, k = self.T, self.r, len(z_views)
+        a_store = self.buf(out_name, (T, k * r))
+        for i, z in enumerate(z_views):
+            K.fixup_sigma(z, r=r, nproj=1, variant=1, z_out=z, a_out=a_store[:, i * r:(i + 1) * r])
+            self.stats.kernel_launches += 1
+        return [a_store[:, i * r:(i + 1) * r] for i in range(k)]
+
+    def _up(self, a_list, W_list, outs, resid=None):
+        probs = [K.Gemm(a, w, o, resid=resid) for a, w, o in zip(a_list, W_list, outs)]
+        if self.grouping:
+            self._gemm(*probs)
+        else:
+            for p in probs:
+                self._gemm(p)
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x: this rank's residual shard [T, d/tp] bf16. Returns y shard [T, d/tp] bf16."""
+        T, dl, fl, r = self.T, self.dl, self.fl, self.r
+        if tuple(x.shape) != (T, dl) or x.dtype != BF16:
+            raise PlanError(f"x shard must be bf16 [{T}, {dl}], got {x.dtype} {tuple(x.shape)}")
+        self.comm.pass_tag = "forward"
+        W = self.W
+        S = {"x": x}
+        # ---- attention half
+        n1, ss1, rl1, s1 = self._norm(x, self.gamma1, 1)
+        z_qkv, a_qkv, P_qkv = self._down_boundary(("q", "k", "v"), n1, W["d_qkv"], ss1, rl1, 1, True)
+        S["s1"] = s1 if s1 is not None else self._buf["s1"]
+        qkv = self.buf("qkv", (3, T, dl))
+        self._up(a_qkv, [W["u_qkv"][i] for i in range(3)], [qkv[i] for i in range(3)])
+        attn, actx = self.attn.forward(qkv[0], qkv[1], qkv[2])
+        self._buf["attn"] = attn
+        z_o, a_o, P_o = self._down_boundary(("o",), attn, W["d_o"], None, None, 0, False)
+        x_mid = self.buf("x_mid", (T, dl))
+        self._up(a_o, [W["u_o"]], [x_mid], resid=x)
+        # ---- mlp half
+        n2, ss2, rl2, s2 = self._norm(x_mid, self.gamma2, 2)
+        z_gu, a_gu, P_gu = self._down_boundary(("gate", "up"), n2, W["d_gu"], ss2, rl2, 2, True)
+        S["s2"] = s2 if s2 is not None else self._buf["s2"]
+        gu = self.buf("gu", (2, T, fl))
+        self._up(a_gu, [W["u_gu"][0], W["u_gu"][1]], [gu[0], gu[1]])
+        act = self.buf("act", (T, fl))
+        K.swiglu(gu[0], gu[1], act)
+        self.stats.kernel_launches += 1
+        z_d, a_d, P_d = self._down_boundary(("down",), act, W["d_d"], None, None, 0, False)
+        y = self.buf("y", (T, dl))
+        self._up(a_d, [W["u_d"]], [y], resid=x_mid)
+        # ---- what backward keeps
+        S.update(P_qkv=P_qkv, z_qkv=z_qkv, P_o=P_o, z_o=z_o, P_gu=P_gu, z_gu=z_gu, P_d=P_d, z_d=z_d)
+        if not self.ckpt:
+            S.update(a_qkv=a_qkv, qkv=qkv, attn=attn, actx=actx, a_o=a_o, x_mid=x_mid, a_gu=a_gu, gu=gu, act=act,
+                     a_d=a_d)
+        self.saved = S
+        return y
+
+    residual_sharded = True
+
+    def loss_device(self, y: torch.Tensor, G: torch.Tensor) -> torch.Tensor:
+        """L = sum(y * G) over the logical [T, d] (builder-defined; the reference has no loss).
+        Device dot product + deterministic reduction into a 1-element fp32 buffer (no sync)."""
+        part = self.buf("loss_parts", (4 * self.sms,), F32)
+        nb = K.dot(y, G, part)
+        out = self.buf("loss", (1,), F32)
+        K.reduce_rows(part[:nb].view(nb, 1, 1), out.view(1, 1))
+        self.stats.kernel_launches += 2
+        if self.tp > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(out)  # loss assembly across d-shards (outside the block's collective log)
+        return out
+
+    def loss(self, y: torch.Tensor, G: torch.Tensor) -> float:
+        return float(self.loss_device(y, G).item())
+
+    def capture_workspaces(self) -> dict[str, np.ndarray]:
+        """This rank's intermediates under the reference's workspace names (simulator.py:561-708),
+        as float64 host arrays. `o` and `mlp` are fused into the residual epilogue on the hot path,
+        so they are recomputed here by one extra (unfused) GEMM each, for parity checks only."""
+        S, T, r = self.saved, self.T, self.r
+        names3, names2 = ("q", "k", "v"), ("gate", "up")
+        ws = {"x": S["x"]}
+        ws["n1"], ws["n2"] = self._buf["n1"], self._buf["n2"]
+        qkv, gu = self._buf["qkv"], self._buf["gu"]
+        for i, n in enumerate(names3):
+            ws[n] = qkv[i]
+        ws["gate"], ws["up"] = gu[0], gu[1]
+        ws["attn"] = S.get("attn", self._buf.get("attn"))
+        ws["x_mid"], ws["act"], ws["y"] = self._buf["x_mid"], self._buf["act"], self._buf["y"]
+        zs = {n: S["z_qkv"][i] for i, n in enumerate(names3)}
+        zs.update({n: S["z_gu"][i] for i, n in enumerate(names2)})
+        zs["o"], zs["down"] = S["z_o"][0], S["z_d"][0]
+        for n, z in zs.items():
+            ws[f"z_{n}"] = z
+        if self.var == 1:
+            for key, names in (("a_q_k_v", names3), ("a_gate_up", names2), ("a_o", ("o",)), ("a_down", ("down",))):
+                a = self._buf[key]
+                for i, n in enumerate(names):
+                    ws[f"a_in_{n}"] = a[:, i * r:(i + 1) * r]
+        if not self.online:
+            ws["norm1-rms"], ws["norm2-rms"] = S["s1"].view(T, 1), S["s2"].view(T, 1)
+        a_o = ws.get("a_in_o", zs["o"])
+        a_d = ws.get("a_in_down", zs["down"])
+        o = torch.empty(T, self.dl, device=self.dev, dtype=BF16)
+        mlp = torch.empty(T, self.dl, device=self.dev, dtype=BF16)
+        K.gemm(K.Gemm(a_o, self.W["u_o"], o))
+        K.gemm(K.Gemm(a_d, self.W["u_d"], mlp))
+        ws["o"], ws["mlp"] = o, mlp
+        torch.cuda.synchronize(self.dev)
+        return {k: v.double().cpu().numpy() for k, v in ws.items() if v is not None}
+
+    def saved_activation_bytes(self) -> int:
+        """Bytes of activations held between forward and backward (distinct storages)."""
+        seen, total = set(), 0
+        for v in self.saved.values():
+            ts = v if isinstance(v, (list, tuple)) else [v]
+            for t in ts:
+                if isinstance(t, torch.Tensor):
+                    key = t.untyped_storage().data_ptr()
+                    if key not in seen:
+                        seen.add(key)
+                        total += t.untyped_storage().nbytes()
+        return total
+
+    # ------------------------------------------------------------------ recompute (ckpt)
+    def _recompute_mlp_inputs(self):
+        """Rebuild x_mid, a_gu, gate/up, act, a_d from x and the stored z's; no collective."""
+        S, W, T, dl, fl = self.saved, self.W, self.T, self.dl, self.fl
+        self.comm.pass_tag = "reforward"
+        a_o = self._sigma_only(S["z_o"], ("o",), "a_o_rc")
+        x_mid = self.buf("x_mid", (T, dl))
+        self._up(a_o, [W["u_o"]], [x_mid], resid=S["x"])
+        a_gu = self._sigma_only(S["z_gu"], ("gate", "up"), "a_gu_rc")
+        gu = self.buf("gu", (2, T, fl))
+        self._up(a_gu, [W["u_gu"][0], W["u_gu"][1]], [gu[0], gu[1]])
+        act = self.buf("act", (T, fl))
+        K.swiglu(gu[0], gu[1], act)
+        self.stats.kernel_launches += 1
+        a_d = self._sigma_only(S["z_d"], ("down",), "a_d_rc")
+        S.update(a_o=a_o, x_mid=x_mid, a_gu=a_gu, gu=gu, act=act, a_d=a_d)
+
+    def _recompute_attn_inputs(self):
+        S, W, T, dl = self.saved, self.W, self.T, self.dl
+        self.comm.pass_tag = "reforward"
+        a_qkv = self._sigma_only(S["z_qkv"], ("q", "k", "v"), "a_qkv_rc")
+        qkv = self.buf("qkv", (3, T, dl))
+        self._up(a_qkv, [W["u_qkv"][i] for i in range(3)], [qkv[i] for i in range(3)])
+        attn, actx = self.attn.forward(qkv[0], qkv[1], qkv[2])
+        S.update(a_qkv=a_qkv, qkv=qkv, attn=attn, actx=actx)
+
+    # ------------------------------------------------------------------ backward pieces
+    def _boundary_bwd(self, names, da_P, zP, s, dss_name):
+        """AR of the up-projection input grads, then sigma-bwd (+ norm-bwd prologue) in place.
+        zP is the stored z (= all-reduce buffer of the forward): [T, k*r] grouped, [k, T, r] not."""
+        k, r, T = len(names), self.r, self.T
+        if self.grouping or k == 1:
+            self.comm.all_reduce(da_P, names[0] if k == 1 else self._gid(names))
+            dss = self.buf(dss_name, (T,), F32) if s is not None else None
+            K.fixup_sigma_bwd(zP, da_P, da_P, r=r, nproj=k, variant=self.var, s=s, d=self.d, dss=dss)
+            self.stats.kernel_launches += 1
+            return da_P, dss
+        # ungrouped: one AR per projection; the norm statistic gradient sums over projections
+        parts = self.buf(f"{dss_name}_parts", (k, 1, T), F32) if s is not None else None
+        for i, nm in enumerate(names):
+            self.comm.all_reduce(da_P[i], nm)
+            K.fixup_sigma_bwd(zP[i], da_P[i], da_P[i], r=r, nproj=1, variant=self.var, s=s, d=self.d,
+                              dss=None if parts is None else parts[i, 0])
+            self.stats.kernel_launches += 1
+        if s is None:
+            return da_P, None
+        dss = self.buf(dss_name, (T,), F32)
+        K.reduce_rows(parts, dss.view(1, T))
+        self.stats.kernel_launches += 1
+        return da_P, dss
+
+    def _da_buffer(self, names):
+        T, r, k = self.T, self.r, len(names)
+        if self.grouping or k == 1:
+            return self.buf(f"dA_{'_'.join(names)}", (T, k * r))
+        return self.buf(f"dA3_{'_'.join(names)}", (k, T, r))
+
+    def _da_views(self, names, da):
+        r = self.r
+        if self.grouping or len(names) == 1:
+            return [da[:, i * r:(i + 1) * r] for i in range(len(names))]
+        return [da[i] for i in range(len(names))]
+
+    def _down_bwd(self, names, dP, W, x_res, gamma, dres, dx_out, dss, grad_key, gamma_key):
+        """dh = dP @ W (dgrad) ; dW = (dP^T x) * gamma (wgrad) ; dx = dres + dh*gamma + 2 x dss."""
+        T, dl, r, k = self.T, self.dl, self.r, len(names)
+        dh = self.buf("dh", (T, dl))
+        if self.grouping or k == 1:
+            self._gemm(K.Gemm(dP, W, dh, b_mn=True))
+            self._wgrad([(dP, x_res, self.grad[grad_key])], col_scale=gamma)
+        else:
+            # dh = sum_i dP_i @ W_i, accumulated through the residual epilogue (one launch each,
+            # like the reference's per-projection GEMMs)
+            for i in range(k):
+                self._gemm(K.Gemm(dP[i], W[i * r:(i + 1) * r], dh, b_mn=True, resid=dh if i else None))
+            g = self.grad[grad_key]
+            self._wgrad([(dP[i], x_res, g[i * r:(i + 1) * r]) for i in range(k)], col_scale=gamma)
+        gparts = self.buf("gparts", (2 * self.sms, dl), F32)
+        nb = K.rmsnorm_bwd(dh, x_res, gamma, dss, dx_out, gparts, dres=dres)
+        K.reduce_rows(gparts[:nb].view(nb, 1, dl), self.grad[gamma_key].view(1, dl))
+        self.stats.kernel_launches += 2
+
+    # ------------------------------------------------------------------ backward
+    def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        """dy: upstream gradient of this rank's y shard [T, d/tp] bf16. Returns dx shard and fills
+        self.grad (fp32) for every local weight."""
+        S, W, T, dl, fl, r = self.saved, self.W, self.T, self.dl, self.fl, self.r
+        if not S:
+            raise RuntimeError("backward called before forward")
+        if self.ckpt:
+            self._recompute_mlp_inputs()
+        self.comm.pass_tag = "backward"
+        G = self.grad
+        # ---------------- mlp down chunk: y = x_mid + a_d @ Wu_d^T
+        names = ("down",)
+        da = self._da_buffer(names)
+        self._gemm(K.Gemm(dy, W["u_d"], da, b_mn=True))                       # da_d = dy @ Wu_d
+        self._wgrad([(dy, S["a_d"][0], G["u_d"])])                             # dWu_d = dy^T a_d
+        dP, _ = self._boundary_bwd(names, da, S["P_d"], None, "dss_d")
+        dact = self.buf("dact", (T, fl))
+        self._gemm(K.Gemm(dP, W["d_d"], dact, b_mn=True))                     # dact = dz_d @ Wd_d
+        self._wgrad([(dP, S["act"], G["d_d"])])                                # dWd_d = dz_d^T act
+        gu = S["gu"]
+        dgu = self.buf("dgu", (2, T, fl))
+        K.swiglu_bwd(gu[0], gu[1], dact, dgu[0], dgu[1])
+        self.stats.kernel_launches += 1
+        # ---------------- gate|up chunk
+        names = ("gate", "up")
+        da = self._da_buffer(names)
+        dav = self._da_views(names, da)
+        probs = [K.Gemm(dgu[i], W["u_gu"][i], dav[i], b_mn=True) for i in range(2)]
+        if self.grouping:
+            self._gemm(*probs)
+        else:
+            for p in probs:
+                self._gemm(p)
+        self._wgrad([(dgu[i], S["a_gu"][i], G["u_gu"][i]) for i in range(2)])
+        dP, dss2 = self._boundary_bwd(names, da, S["P_gu"], S["s2"], "dss2")
+        dx_mid = self.buf("dx_mid", (T, dl))
+        self._down_bwd(names, dP, W["d_gu"], S["x_mid"], self.gamma2, dy, dx_mid, dss2, "d_gu", "gamma2")
+        # ---------------- attention o chunk: x_mid = x + a_o @ Wu_o^T
+        if self.ckpt:
+            self._recompute_attn_inputs()
+            self.comm.pass_tag = "backward"
+        names = ("o",)
+        da = self._da_buffer(names)
+        self._gemm(K.Gemm(dx_mid, W["u_o"], da, b_mn=True))
+        self._wgrad([(dx_mid, S["a_o"][0], G["u_o"])])
+        dP, _ = self._boundary_bwd(names, da, S["P_o"], None, "dss_o")
+        dattn = self.buf("dattn", (T, dl))
+        self._gemm(K.Gemm(dP, W["d_o"], dattn, b_mn=True))
+        self._wgrad([(dP, S["attn"], G["d_o"])])
+        dq, dk, dv = self.attn.backward(dattn, S["actx"])
+        # ---------------- q|k|v chunk
+        names = ("q", "k", "v")
+        da = self._da_buffer(names)
+        dav = self._da_views(names, da)
+        dqkv = (dq, dk, dv)
+        probs = [K.Gemm(dqkv[i], W["u_qkv"][i], dav[i], b_mn=True) for i in range(3)]
+        if self.grouping:
+            self._gemm(*probs)
+        else:
+            for p in probs:
+                self._gemm(p)
+        self._wgrad([(dqkv[i], S["a_qkv"][i], G["u_qkv"][i]) for i in range(3)])
+        dP, dss1 = self._boundary_bwd(names, da, S["P_qkv"], S["s1"], "dss1")
+        dx = self.buf("dx", (T, dl))
+        self._down_bwd(names, dP, W["d_qkv"], S["x"], self.gamma1, dx_mid, dx, dss1, "d_qkv", "gamma1")
+        return dx

@@ -73,11 +73,13 @@ class Gemm:
             N, Kb = self.b.shape
         if Kb != K:
             raise ValueError(f"GEMM inner dims disagree: A {tuple(self.a.shape)} B {tuple(self.b.shape)}")
-        c2 = self.c[0] if self.splits > 1 else self.c
+        c2 = self.c[0] if self.c.dim() == 3 else self.c
         if tuple(c2.shape) != (M, N):
             raise ValueError(f"GEMM output {tuple(c2.shape)} != ({M}, {N})")
+        if self.c.dim() == 3 and self.c.shape[0] < self.splits:
+            raise ValueError(f"split-K output has {self.c.shape[0]} slabs < splits={self.splits}")
         c_fp32 = self.c.dtype == F32
-        split_stride = self.c.stride(0) if self.splits > 1 else 0
+        split_stride = self.c.stride(0) if self.c.dim() == 3 else 0
         return GemmProblem(
             a=self.a.data_ptr(), lda=_ld(self.a), a_mn=int(self.a_mn),
             b=self.b.data_ptr(), ldb=_ld(self.b), b_mn=int(self.b_mn),
@@ -167,6 +169,15 @@ def reduce_rows(parts, out, *, splits=None, col_scale=None, accumulate=False):
 def add(a, b, out):
     rows, cols = a.shape
     _native.call("btp_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), rows, cols, _stream())
+
+
+def dot(a, b, partial) -> int:
+    """partial: fp32 [max_blocks]; returns the number of partials written (sum them with reduce_rows)."""
+    rows, cols = a.shape
+    nblk = ctypes.c_int(0)
+    _native.call("btp_dot", _p(a), _ld(a), _p(b), _ld(b), rows, cols, _p(partial), partial.shape[0],
+                 ctypes.byref(nblk), _stream())
+    return nblk.value
 
 
 def num_sms() -> int:
