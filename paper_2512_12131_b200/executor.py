@@ -66,7 +66,121 @@ class StepStats:
     gemm_flops: int = 0
 
 
-class BTPBlockExecutor:
+class ExecutorBase:
+    """Buffers, GEMM dispatch (+ optional per-launch timing), split-K weight gradients and the
+    loss, shared by the BTP executor and the naive-TP / full-rank baselines (baselines.py)."""
+
+    residual_sharded = True
+    gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
+
+    def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float):
+        self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
+        self.comm = comm if comm is not None else TPComm(1, 0)
+        if self.comm.tp != pl.shape.tp:
+            raise PlanError(f"communicator size {self.comm.tp} != plan tp {pl.shape.tp}")
+        self.dev = torch.device(device)
+        self.eps = eps
+        self.tp, self.rank = pl.shape.tp, self.comm.rank
+        self.T = pl.shape.tokens
+        self.sms = K.num_sms()
+        self.stats = StepStats()
+        self._buf: dict[str, torch.Tensor] = {}
+        self.saved: dict = {}
+
+    def _dev(self, a, dtype=BF16) -> torch.Tensor:
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype)
+
+    # ------------------------------------------------------------------ buffers
+    def buf(self, name: str, shape, dtype=BF16) -> torch.Tensor:
+        t = self._buf.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            t = torch.empty(shape, device=self.dev, dtype=dtype)
+            self._buf[name] = t
+        return t
+
+    def _wgrad_parts(self, n_elems: int) -> torch.Tensor:
+        t = self._buf.get("_wg_parts")
+        if t is None or t.numel() < n_elems:
+            t = torch.empty(n_elems, device=self.dev, dtype=F32)
+            self._buf["_wg_parts"] = t
+        return t
+
+    # ------------------------------------------------------------------ GEMM helpers
+    def _gemm(self, *probs: K.Gemm) -> None:
+        flops = 0
+        for p in probs:
+            M = p.a.shape[1] if p.a_mn else p.a.shape[0]
+            Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
+            N = p.b.shape[1] if p.b_mn else p.b.shape[0]
+            flops += 2 * M * N * Kd
+        if self.gemm_timer is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            K.gemm(*probs)
+            e1.record()
+            self.gemm_timer.append((e0, e1, flops))
+        else:
+            K.gemm(*probs)
+        self.stats.gemm_launches += 1
+        self.stats.kernel_launches += 1
+        self.stats.gemm_flops += flops
+
+    def _wgrad(self, pairs, col_scale=None):
+        """pairs: list of (dY [T, M] (MN-major A), X [T, N] (MN-major B), out fp32 [M, N]).
+        out = (dY^T X) (* col_scale) via split-K and a deterministic reduction."""
+        T = pairs[0][0].shape[0]
+        kb = (T + 63) // 64
+        tiles = sum(math.ceil(dy.shape[1] / 128) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
+        splits = _pick_splits(tiles, kb, self.sms)
+        if splits == 1 and col_scale is None:
+            self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True) for dy, x, o in pairs])
+            return
+        sizes = [splits * o.numel() for _, _, o in pairs]
+        flat = self._wgrad_parts(sum(sizes))
+        probs, views, off = [], [], 0
+        for (dy, x, o), n in zip(pairs, sizes):
+            part = flat[off:off + n].view(splits, *o.shape)
+            off += n
+            probs.append(K.Gemm(dy, x, part, a_mn=True, b_mn=True, splits=splits))
+            views.append((part, o))
+        self._gemm(*probs)
+        for part, o in views:
+            K.reduce_rows(part, o, col_scale=col_scale)
+            self.stats.kernel_launches += 1
+
+    # ------------------------------------------------------------------ loss / accounting
+    def loss_device(self, y: torch.Tensor, G: torch.Tensor) -> torch.Tensor:
+        """L = sum(y * G) over the logical [T, d] (builder-defined; the reference has no loss).
+        Device dot product + deterministic reduction into a 1-element fp32 buffer (no sync)."""
+        part = self.buf("loss_parts", (4 * self.sms,), F32)
+        nb = K.dot(y, G, part)
+        out = self.buf("loss", (1,), F32)
+        K.reduce_rows(part[:nb].view(nb, 1, 1), out.view(1, 1))
+        self.stats.kernel_launches += 2
+        if self.tp > 1 and self.residual_sharded:
+            import torch.distributed as dist
+
+            dist.all_reduce(out)  # loss assembly across d-shards (outside the block's collective log)
+        return out
+
+    def loss(self, y: torch.Tensor, G: torch.Tensor) -> float:
+        return float(self.loss_device(y, G).item())
+
+    def saved_activation_bytes(self) -> int:
+        """Bytes of activations held between forward and backward (distinct storages)."""
+        seen, total = set(), 0
+        for v in self.saved.values():
+            ts = v if isinstance(v, (list, tuple)) else [v]
+            for t in ts:
+                if isinstance(t, torch.Tensor):
+                    key = t.untyped_storage().data_ptr()
+                    if key not in seen:
+                        seen.add(key)
+                        total += t.untyped_storage().nbytes()
+        return total
+
+
+class BTPBlockExecutor(ExecutorBase):
     """One rank's shard of a low-rank (svd/cola) block under a BTP plan."""
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None,
@@ -77,27 +191,16 @@ class BTPBlockExecutor:
             raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
         if pl.variant not in _VAR:
             raise PlanError(f"variant {pl.variant.value} is not supported on the device path (svd, cola)")
-        self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
-        self.comm = comm if comm is not None else TPComm(1, 0)
-        if self.comm.tp != pl.shape.tp:
-            raise PlanError(f"communicator size {self.comm.tp} != plan tp {pl.shape.tp}")
-        self.dev = torch.device(device)
-        self.eps = eps
+        self._setup(pl, comm, device, eps)
         self.var = _VAR[pl.variant]
         self.online = pl.norm_mode is NormMode.ONLINE
         self.grouping = pl.grouping
         self.ckpt = pl.lowrank_ckpt
-        cfg, tp, rank = self.cfg, pl.shape.tp, self.comm.rank
-        self.tp, self.rank = tp, rank
+        cfg, tp = self.cfg, self.tp
         self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
         self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
-        self.T = pl.shape.tokens
         self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim, attn_backend)
-        self.sms = K.num_sms()
         self._load_weights(block)
-        self.stats = StepStats()
-        self._buf: dict[str, torch.Tensor] = {}
-        self.saved: dict[str, torch.Tensor] = {}
 
     # ------------------------------------------------------------------ weights
     def _load_weights(self, block: DecoderBlockWeights) -> None:
@@ -140,66 +243,6 @@ class BTPBlockExecutor:
         out["B"]["o"], out["A"]["o"] = g["d_o"], g["u_o"]
         out["B"]["down"], out["A"]["down"] = g["d_d"], g["u_d"]
         return out
-
-    # ------------------------------------------------------------------ buffers
-    def buf(self, name: str, shape, dtype=BF16) -> torch.Tensor:
-        t = self._buf.get(name)
-        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
-            t = torch.empty(shape, device=self.dev, dtype=dtype)
-            self._buf[name] = t
-        return t
-
-    def _wgrad_parts(self, n_elems: int) -> torch.Tensor:
-        t = self._buf.get("_wg_parts")
-        if t is None or t.numel() < n_elems:
-            t = torch.empty(n_elems, device=self.dev, dtype=F32)
-            self._buf["_wg_parts"] = t
-        return t
-
-    # ------------------------------------------------------------------ GEMM helpers
-    gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
-
-    def _gemm(self, *probs: K.Gemm) -> None:
-        flops = 0
-        for p in probs:
-            M = p.a.shape[1] if p.a_mn else p.a.shape[0]
-            Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
-            N = p.b.shape[1] if p.b_mn else p.b.shape[0]
-            flops += 2 * M * N * Kd
-        if self.gemm_timer is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            K.gemm(*probs)
-            e1.record()
-            self.gemm_timer.append((e0, e1, flops))
-        else:
-            K.gemm(*probs)
-        self.stats.gemm_launches += 1
-        self.stats.kernel_launches += 1
-        self.stats.gemm_flops += flops
-
-    def _wgrad(self, pairs, col_scale=None):
-        """pairs: list of (dY [T, M] (MN-major A), X [T, N] (MN-major B), out fp32 [M, N]).
-        out = (dY^T X) (* col_scale) via split-K and a deterministic reduction."""
-        T = pairs[0][0].shape[0]
-        kb = (T + 63) // 64
-        tiles = sum(math.ceil(dy.shape[1] / 128) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
-        splits = _pick_splits(tiles, kb, self.sms)
-        if splits == 1 and col_scale is None:
-            self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True) for dy, x, o in pairs])
-            return
-        sizes = [splits * o.numel() for _, _, o in pairs]
-        flat = self._wgrad_parts(sum(sizes))
-        probs, views, off = [], [], 0
-        for (dy, x, o), n in zip(pairs, sizes):
-            part = flat[off:off + n].view(splits, *o.shape)
-            off += n
-            probs.append(K.Gemm(dy, x, part, a_mn=True, b_mn=True, splits=splits))
-            views.append((part, o))
-        self._gemm(*probs)
-        for part, o in views:
-            K.reduce_rows(part, o, col_scale=col_scale)
-            self.stats.kernel_launches += 1
 
     # ------------------------------------------------------------------ forward pieces
     def _norm(self, x, gamma, tag):
@@ -322,25 +365,6 @@ class BTPBlockExecutor:
         self.saved = S
         return y
 
-    residual_sharded = True
-
-    def loss_device(self, y: torch.Tensor, G: torch.Tensor) -> torch.Tensor:
-        """L = sum(y * G) over the logical [T, d] (builder-defined; the reference has no loss).
-        Device dot product + deterministic reduction into a 1-element fp32 buffer (no sync)."""
-        part = self.buf("loss_parts", (4 * self.sms,), F32)
-        nb = K.dot(y, G, part)
-        out = self.buf("loss", (1,), F32)
-        K.reduce_rows(part[:nb].view(nb, 1, 1), out.view(1, 1))
-        self.stats.kernel_launches += 2
-        if self.tp > 1:
-            import torch.distributed as dist
-
-            dist.all_reduce(out)  # loss assembly across d-shards (outside the block's collective log)
-        return out
-
-    def loss(self, y: torch.Tensor, G: torch.Tensor) -> float:
-        return float(self.loss_device(y, G).item())
-
     def capture_workspaces(self) -> dict[str, np.ndarray]:
         """This rank's intermediates under the reference's workspace names (simulator.py:561-708),
         as float64 host arrays. `o` and `mlp` are fused into the residual epilogue on the hot path,
@@ -376,19 +400,6 @@ class BTPBlockExecutor:
         ws["o"], ws["mlp"] = o, mlp
         torch.cuda.synchronize(self.dev)
         return {k: v.double().cpu().numpy() for k, v in ws.items() if v is not None}
-
-    def saved_activation_bytes(self) -> int:
-        """Bytes of activations held between forward and backward (distinct storages)."""
-        seen, total = set(), 0
-        for v in self.saved.values():
-            ts = v if isinstance(v, (list, tuple)) else [v]
-            for t in ts:
-                if isinstance(t, torch.Tensor):
-                    key = t.untyped_storage().data_ptr()
-                    if key not in seen:
-                        seen.add(key)
-                        total += t.untyped_storage().nbytes()
-        return total
 
     # ------------------------------------------------------------------ recompute (ckpt)
     def _recompute_mlp_inputs(self):
