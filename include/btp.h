@@ -51,6 +51,11 @@ typedef struct btp_gemm_problem {
   int splits;
   long long split_stride;
   float alpha; /* 0 is read as 1 */
+  /* reduce_add: the epilogue adds its (scaled) tile into C with the TMA reduce-add (fp32 add
+   * performed in L2) instead of storing it. Required for splits > 1 (split-K over the T tokens of
+   * a weight gradient): C must be fp32 and zero-initialised (btp_zero); summation order across
+   * splits is not fixed (fp32 round-off only). split_stride is unused. */
+  int reduce_add;
 } btp_gemm_problem;
 
 /* Grouped/batched tcgen05 GEMM: n (1..4) independent problems in ONE persistent launch.
@@ -112,6 +117,14 @@ int btp_rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx
                     const float* dss, const void* dres, long long ldr, void* dx, long long lddx,
                     float* dgamma_partial, int max_blocks, int* nblk, int rows, int width, void* stream);
 
+/* Replicated (full-width) RMSNorm backward prologue for the naive-TP / full-rank baselines,
+ * n = x*gamma/s with s = sqrt(mean(x^2)+eps) saved by the forward:
+ *   dh = dn / s (dh may alias dn),  dss[t] = -<dn_t, gamma*x_t> / (2 s^3 width)
+ * then btp_rmsnorm_bwd(dh, x, gamma, dss, ...) yields dx and dgamma.
+ * Replaces the (absent) backward of norms.py:27-35 `rmsnorm_reference`. */
+int btp_rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                         const float* s, void* dh, long long lddh, float* dss, int rows, int width, void* stream);
+
 /* out[r, c] = (accumulate ? out : 0) + colscale[c] * sum_{s<splits} in[s*split_stride + r*ldi + c]
  * Deterministic (ascending split order) split-K / partial-sum reduction, fp32. */
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
@@ -127,6 +140,9 @@ int btp_add(const void* a, long long lda, const void* b, long long ldb, void* ou
  * btp_reduce_rows; deterministic. */
 int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
             int max_blocks, int* nblk, void* stream);
+
+/* Zero `bytes` bytes of device memory on the stream (split-K reduce-add targets). */
+int btp_zero(void* ptr, long long bytes, void* stream);
 
 /* Number of SMs the library sizes persistent grids for (device 0 of the current context). */
 int btp_num_sms(void);

@@ -38,7 +38,9 @@ EXPORTED_SYMBOLS = (
     "btp_rmsnorm_bwd",
     "btp_reduce_rows",
     "btp_add",
+    "btp_rmsnorm_bwd_prep",
     "btp_dot",
+    "btp_zero",
     "btp_num_sms",
     "btp_version",
 )
@@ -75,6 +77,7 @@ class GemmProblem(ctypes.Structure):
         ("splits", ctypes.c_int),
         ("split_stride", ctypes.c_longlong),
         ("alpha", ctypes.c_float),
+        ("reduce_add", ctypes.c_int),
     ]
 
 
@@ -94,7 +97,9 @@ _SIGNATURES = {
     "btp_rmsnorm_bwd": [_P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _I, ctypes.POINTER(_I), _I, _I, _P],
     "btp_reduce_rows": [_P, _I, _LL, _LL, _I, _I, _P, _P, _LL, _I, _P],
     "btp_add": [_P, _LL, _P, _LL, _P, _LL, _I, _I, _P],
+    "btp_rmsnorm_bwd_prep": [_P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _I, _I, _P],
     "btp_dot": [_P, _LL, _P, _LL, _I, _I, _P, _I, ctypes.POINTER(_I), _P],
+    "btp_zero": [_P, _LL, _P],
     "btp_num_sms": [],
     "btp_version": [],
 }

@@ -1,0 +1,322 @@
+"""The two comparison points of the metric, on the SAME kernels as BTP:
+
+* VanillaExecutor  — naive low-rank TP (reference `_forward_vanilla`, simulator.py:412-543):
+  factor pairs sharded along r (cola keeps each crossgate pair rank-local via
+  `cola_pair_indices`, plan.py:419-428), sigma fused per rank, the up-projection produces a
+  full-width PARTIAL [T, d_out] that is all-reduced; residual, norms and attention are
+  replicated on every rank (the reference's semantics, :518-520).
+* FullRankExecutor — Megatron column->row TP of the full-rank block (reference
+  `_forward_full_rank`, simulator.py:323-398): 2 all-reduces of [T, d] per pass.
+
+Both run forward + backward (the backward all-reduces the input gradient of every
+row-split boundary) and report the same collective log schema as the BTP executor.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .attention import Attention
+from .comm import TPComm
+from .executor import BF16, F32, ExecutorBase
+from .model import DecoderBlockWeights, Variant
+from .plan import PlanError, ShardPlan, Strategy, cola_pair_indices, col_shard_bounds
+
+_VAR = {Variant.SVD: 0, Variant.COLA: 1}
+
+
+class _ReplicatedNormMixin:
+    """Full-width RMSNorm forward/backward for the replicated-residual strategies."""
+
+    def _rnorm(self, x, gamma, tag, branch=None, x_out=None):
+        T, d = self.T, self.d
+        n = self.buf(f"n{tag}", (T, d))
+        s = self.buf(f"s{tag}", (T,), F32)
+        K.rmsnorm_residual(x, gamma, branch=branch, x_out=x_out, n_out=n, rl_out=s, eps=self.eps)
+        self.stats.kernel_launches += 1
+        return n, s
+
+    def _rnorm_bwd(self, dn, x, gamma, s, dres, dx_out, gkey):
+        T, d = self.T, self.d
+        dss = self.buf("dss_r", (T,), F32)
+        K.rmsnorm_bwd_prep(dn, x, gamma, s, dn, dss)
+        gparts = self.buf("gparts", (2 * self.sms, d), F32)
+        nb = K.rmsnorm_bwd(dn, x, gamma, dss, dx_out, gparts, dres=dres)
+        K.reduce_rows(gparts[:nb].view(nb, 1, d), self.grad[gkey].view(1, d))
+        self.stats.kernel_launches += 3
+
+
+class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
+    residual_sharded = False
+
+    def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None, device="cuda",
+                 eps: float = 1e-6, attn_backend: str = "auto"):
+        if pl.strategy is not Strategy.VANILLA:
+            raise PlanError(f"VanillaExecutor needs a vanilla plan, got {pl.strategy.value}")
+        if block.variant is not pl.variant or pl.variant not in _VAR:
+            raise PlanError(f"vanilla device path supports svd/cola blocks matching the plan")
+        self._setup(pl, comm, device, eps)
+        cfg = self.cfg
+        self.var = _VAR[pl.variant]
+        self.grouping = pl.grouping
+        self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
+        self.rl = cfg.r // self.tp
+        self.dl = cfg.d  # replicated residual
+        self.attn = Attention(pl.shape.b, pl.shape.s, cfg.heads, cfg.head_dim, attn_backend)
+        if pl.variant is Variant.COLA:
+            idx = cola_pair_indices(cfg.r, self.tp, self.rank)
+        else:
+            idx = np.arange(*col_shard_bounds(cfg.r, self.tp, self.rank))
+        B = {n: t.values[idx, :] for n, t in block.down_factors.items()}     # [r/tp, d_in]
+        A = {n: t.values[:, idx] for n, t in block.up_factors.items()}       # [d_out, r/tp]
+        self.W = {
+            "d_qkv": self._dev(np.concatenate([B[n] for n in "qkv"])),      # [3rl, d]
+            "u_qkv": [self._dev(A[n]) for n in "qkv"],                         # [d, rl] x3
+            "d_o": self._dev(B["o"]), "u_o": self._dev(A["o"]),
+            "d_gu": self._dev(np.concatenate([B["gate"], B["up"]])),           # [2rl, d]
+            "u_gu": [self._dev(A["gate"]), self._dev(A["up"])],                # [d_ff, rl] x2
+            "d_d": self._dev(B["down"]), "u_d": self._dev(A["down"]),          # [rl, d_ff], [d, rl]
+        }
+        self.gamma1 = self._dev(block.gamma1.values, F32)
+        self.gamma2 = self._dev(block.gamma2.values, F32)
+        self.grad = {
+            k: ([torch.zeros(t.shape, device=self.dev, dtype=F32) for t in v] if isinstance(v, list)
+                else torch.zeros(v.shape, device=self.dev, dtype=F32))
+            for k, v in self.W.items()
+        }
+        self.grad["gamma1"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+        self.grad["gamma2"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+
+    # ------------------------------------------------------------------ one vanilla chunk group
+    def _pair(self, names, inp, Wd, Wu, out_full, chunk_id):
+        """down (col-parallel over r) -> local sigma -> up (row-parallel over r) -> AR of the
+        full-width partial. Grouped: one down GEMM, one batched up launch, one AR."""
+        T, rl, k = self.T, self.rl, len(names)
+        z = self.buf(f"z_{chunk_id}", (T, k * rl))
+        self._gemm(K.Gemm(inp, Wd, z))
+        if self.var == 1:
+            a = self.buf(f"a_{chunk_id}", (T, k * rl))
+            K.fixup_sigma(z, r=rl, nproj=k, variant=1, z_out=z, a_out=a)
+            self.stats.kernel_launches += 1
+        else:
+            a = z
+        widths = [w.shape[0] for w in Wu]
+        offs = np.cumsum([0] + widths)
+        probs = [K.Gemm(a[:, i * rl:(i + 1) * rl], Wu[i], out_full[:, offs[i]:offs[i + 1]]) for i in range(k)]
+        if self.grouping or k == 1:
+            self._gemm(*probs)
+            self.comm.all_reduce(out_full, chunk_id)
+        else:
+            raise AssertionError("ungrouped path handled by caller")
+        return z, a
+
+    def _pairs(self, names, inp, Wd_all, Wu_list, chunk_grouped, widths):
+        """Grouped: one chunk. Ungrouped: one chunk per projection (separate buffers + ARs)."""
+        T, rl = self.T, self.rl
+        if self.grouping:
+            full = self.buf(f"F_{chunk_grouped}", (T, sum(widths)))
+            z, a = self._pair(names, inp, Wd_all, Wu_list, full, chunk_grouped)
+            offs = np.cumsum([0] + widths)
+            return [full[:, offs[i]:offs[i + 1]] for i in range(len(names))], [z], [a]
+        outs, zs, as_ = [], [], []
+        for i, n in enumerate(names):
+            full = self.buf(f"F_{n}", (T, widths[i]))
+            z, a = self._pair((n,), inp, Wd_all[i * rl:(i + 1) * rl], [Wu_list[i]], full, n)
+            outs.append(full)
+            zs.append(z)
+            as_.append(a)
+        return outs, zs, as_
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        T, d, f = self.T, self.d, self.d_ff
+        self.comm.pass_tag = "forward"
+        W = self.W
+        n1, s1 = self._rnorm(x, self.gamma1, 1)
+        (q, k, v), z_qkv, a_qkv = self._pairs(("q", "k", "v"), n1, W["d_qkv"], W["u_qkv"], "qkv", [d, d, d])
+        attn, actx = self.attn.forward(q, k, v)
+        o_full = self.buf("F_o", (T, d))
+        z_o, a_o = self._pair(("o",), attn, W["d_o"], [W["u_o"]], o_full, "o")
+        x_mid = self.buf("x_mid", (T, d))
+        n2, s2 = self._rnorm(x, self.gamma2, 2, branch=o_full, x_out=x_mid)
+        (g, u), z_gu, a_gu = self._pairs(("gate", "up"), n2, W["d_gu"], W["u_gu"], "gate_up", [f, f])
+        act = self.buf("act", (T, f))
+        K.swiglu(g, u, act)
+        mlp = self.buf("F_down", (T, d))
+        z_d, a_d = self._pair(("down",), act, W["d_d"], [W["u_d"]], mlp, "down")
+        y = self.buf("y", (T, d))
+        K.add(x_mid, mlp, y)
+        self.stats.kernel_launches += 2
+        self.saved = dict(x=x, n1=n1, s1=s1, z_qkv=z_qkv, a_qkv=a_qkv, q=q, k=k, v=v, attn=attn, actx=actx, z_o=[z_o],
+                          a_o=[a_o], x_mid=x_mid, n2=n2, s2=s2, z_gu=z_gu, a_gu=a_gu, g=g, u=u, act=act, z_d=[z_d],
+                          a_d=[a_d])
+        return y
+
+    # ------------------------------------------------------------------ backward
+    def _pair_bwd(self, names, dout_list, zs, as_, Wd_all, Wu_list, inp, gkey_d, gkey_u, din_full, chunk_ids):
+        """Backward of one vanilla chunk group. dout: grads of the full-width outputs (replicated).
+        da = dout @ Wu (local, no AR); sigma-bwd; dWd = dz^T inp; din partial = dz @ Wd -> AR."""
+        T, rl, k = self.T, self.rl, len(names)
+        G = self.grad
+        dz = self.buf(f"dz_{'_'.join(names)}", (T, k * rl))
+        probs = [K.Gemm(dout_list[i], Wu_list[i], dz[:, i * rl:(i + 1) * rl], b_mn=True) for i in range(k)]
+        self._gemm(*probs)
+        z_all = zs[0] if len(zs) == 1 else None
+        for i in range(k):
+            a_i = (as_[0] if len(as_) == 1 else as_[i])
+            a_i = a_i[:, i * rl:(i + 1) * rl] if len(as_) == 1 else a_i
+            gu = G[gkey_u][i] if isinstance(G[gkey_u], list) else G[gkey_u]
+            self._wgrad([(dout_list[i], a_i, gu)])
+        if self.var == 1:
+            if z_all is not None:
+                K.fixup_sigma_bwd(z_all, dz, dz, r=rl, nproj=k, variant=1)
+            else:
+                for i in range(k):
+                    K.fixup_sigma_bwd(zs[i], dz[:, i * rl:(i + 1) * rl], dz[:, i * rl:(i + 1) * rl], r=rl, nproj=1,
+                                      variant=1)
+            self.stats.kernel_launches += 1
+        self._wgrad([(dz, inp, G[gkey_d])])
+        self._gemm(K.Gemm(dz, Wd_all, din_full, b_mn=True))
+        self.comm.all_reduce(din_full, chunk_ids[0])
+
+    def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        S, W, T, d, f = self.saved, self.W, self.T, self.d, self.d_ff
+        self.comm.pass_tag = "backward"
+        dact = self.buf("dact", (T, f))
+        self._pair_bwd(("down",), [dy], S["z_d"], S["a_d"], W["d_d"], [W["u_d"]], S["act"], "d_d", "u_d", dact,
+                       ["down"])
+        dgu = self.buf("dgu", (T, 2 * f))
+        K.swiglu_bwd(S["g"], S["u"], dact, dgu[:, :f], dgu[:, f:])
+        self.stats.kernel_launches += 1
+        dn2 = self.buf("dn2", (T, d))
+        self._pair_bwd(("gate", "up"), [dgu[:, :f], dgu[:, f:]], S["z_gu"], S["a_gu"], W["d_gu"], W["u_gu"], S["n2"],
+                       "d_gu", "u_gu", dn2, ["gate_up"])
+        dx_mid = self.buf("dx_mid", (T, d))
+        self._rnorm_bwd(dn2, S["x_mid"], self.gamma2, S["s2"], dy, dx_mid, "gamma2")
+        dattn = self.buf("dattn", (T, d))
+        self._pair_bwd(("o",), [dx_mid], S["z_o"], S["a_o"], W["d_o"], [W["u_o"]], S["attn"], "d_o", "u_o", dattn,
+                       ["o"])
+        dq, dk, dv = self.attn.backward(dattn, S["actx"])
+        dn1 = self.buf("dn1", (T, d))
+        self._pair_bwd(("q", "k", "v"), [dq, dk, dv], S["z_qkv"], S["a_qkv"], W["d_qkv"], W["u_qkv"], S["n1"],
+                       "d_qkv", "u_qkv", dn1, ["qkv"])
+        dx = self.buf("dx", (T, d))
+        self._rnorm_bwd(dn1, S["x"], self.gamma1, S["s1"], dx_mid, dx, "gamma1")
+        return dx
+
+    def weight_grads_by_name(self):
+        g = {k: ([t.double().cpu().numpy() for t in v] if isinstance(v, list) else v.double().cpu().numpy())
+             for k, v in self.grad.items()}
+        rl = self.rl
+        out = {"A": {}, "B": {}, "gamma1": g["gamma1"], "gamma2": g["gamma2"]}
+        for i, n in enumerate("qkv"):
+            out["B"][n] = g["d_qkv"][i * rl:(i + 1) * rl]
+            out["A"][n] = g["u_qkv"][i]
+        for i, n in enumerate(("gate", "up")):
+            out["B"][n] = g["d_gu"][i * rl:(i + 1) * rl]
+            out["A"][n] = g["u_gu"][i]
+        out["B"]["o"], out["A"]["o"] = g["d_o"], g["u_o"]
+        out["B"]["down"], out["A"]["down"] = g["d_d"], g["u_d"]
+        return out
+
+
+class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
+    residual_sharded = False
+
+    def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None, device="cuda",
+                 eps: float = 1e-6, attn_backend: str = "auto"):
+        if pl.strategy is not Strategy.FULL_RANK or block.variant is not Variant.FULL_RANK:
+            raise PlanError("FullRankExecutor needs a full-rank plan and block")
+        self._setup(pl, comm, device, eps)
+        cfg, tp, rk = self.cfg, self.tp, self.rank
+        self.grouping = pl.grouping
+        self.d, self.d_ff = cfg.d, cfg.d_ff
+        self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
+        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim, attn_backend)
+        sl, fsl = slice(rk * self.dl, (rk + 1) * self.dl), slice(rk * self.fl, (rk + 1) * self.fl)
+        Wf = {n: t.values for n, t in block.full.items()}
+        self.W = {
+            "qkv": self._dev(np.concatenate([Wf[n][sl, :] for n in "qkv"])),          # [3dl, d] col-parallel
+            "o": self._dev(Wf["o"][:, sl]),                                            # [d, dl]  row-parallel
+            "gu": self._dev(np.concatenate([Wf["gate"][fsl, :], Wf["up"][fsl, :]])),  # [2fl, d]
+            "down": self._dev(Wf["down"][:, fsl]),                                     # [d, fl]
+        }
+        self.gamma1 = self._dev(block.gamma1.values, F32)
+        self.gamma2 = self._dev(block.gamma2.values, F32)
+        self.grad = {k: torch.zeros(v.shape, device=self.dev, dtype=F32) for k, v in self.W.items()}
+        self.grad["gamma1"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+        self.grad["gamma2"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+
+    def _col(self, inp, Wcat, out, k):
+        """Column-parallel GEMM(s): grouped = one launch over the concatenated weight."""
+        n = Wcat.shape[0] // k
+        if self.grouping:
+            self._gemm(K.Gemm(inp, Wcat, out))
+        else:
+            for i in range(k):
+                self._gemm(K.Gemm(inp, Wcat[i * n:(i + 1) * n], out[:, i * n:(i + 1) * n]))
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        T, d, dl, fl = self.T, self.d, self.dl, self.fl
+        self.comm.pass_tag = "forward"
+        W = self.W
+        n1, s1 = self._rnorm(x, self.gamma1, 1)
+        qkv = self.buf("qkv", (T, 3 * dl))
+        self._col(n1, W["qkv"], qkv, 3)
+        attn, actx = self.attn.forward(qkv[:, :dl], qkv[:, dl:2 * dl], qkv[:, 2 * dl:])
+        o = self.buf("o", (T, d))
+        self._gemm(K.Gemm(attn, W["o"], o))
+        self.comm.all_reduce(o, "attn")
+        x_mid = self.buf("x_mid", (T, d))
+        n2, s2 = self._rnorm(x, self.gamma2, 2, branch=o, x_out=x_mid)
+        gu = self.buf("gu", (T, 2 * fl))
+        self._col(n2, W["gu"], gu, 2)
+        act = self.buf("act", (T, fl))
+        K.swiglu(gu[:, :fl], gu[:, fl:], act)
+        mlp = self.buf("mlp", (T, d))
+        self._gemm(K.Gemm(act, W["down"], mlp))
+        self.comm.all_reduce(mlp, "mlp")
+        y = self.buf("y", (T, d))
+        K.add(x_mid, mlp, y)
+        self.stats.kernel_launches += 2
+        self.saved = dict(x=x, n1=n1, s1=s1, qkv=qkv, attn=attn, actx=actx, x_mid=x_mid, n2=n2, s2=s2, gu=gu, act=act)
+        return y
+
+    def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        S, W, G, T, d, dl, fl = self.saved, self.W, self.grad, self.T, self.d, self.dl, self.fl
+        self.comm.pass_tag = "backward"
+        dact = self.buf("dact", (T, fl))
+        self._gemm(K.Gemm(dy, W["down"], dact, b_mn=True))
+        self._wgrad([(dy, S["act"], G["down"])])
+        dgu = self.buf("dgu", (T, 2 * fl))
+        K.swiglu_bwd(S["gu"][:, :fl], S["gu"][:, fl:], dact, dgu[:, :fl], dgu[:, fl:])
+        self.stats.kernel_launches += 1
+        self._wgrad([(dgu, S["n2"], G["gu"])])
+        dn2 = self.buf("dn2", (T, d))
+        self._gemm(K.Gemm(dgu, W["gu"], dn2, b_mn=True))
+        self.comm.all_reduce(dn2, "mlp")
+        dx_mid = self.buf("dx_mid", (T, d))
+        self._rnorm_bwd(dn2, S["x_mid"], self.gamma2, S["s2"], dy, dx_mid, "gamma2")
+        dattn = self.buf("dattn", (T, dl))
+        self._gemm(K.Gemm(dx_mid, W["o"], dattn, b_mn=True))
+        self._wgrad([(dx_mid, S["attn"], G["o"])])
+        dq, dk, dv = self.attn.backward(dattn, S["actx"])
+        gq = G["qkv"]
+        self._wgrad([(dq, S["n1"], gq[:dl]), (dk, S["n1"], gq[dl:2 * dl]), (dv, S["n1"], gq[2 * dl:])])
+        dn1 = self.buf("dn1", (T, d))
+        Wq = W["qkv"]
+        self._gemm(K.Gemm(dq, Wq[:dl], dn1, b_mn=True))
+        self._gemm(K.Gemm(dk, Wq[dl:2 * dl], dn1, b_mn=True, resid=dn1))
+        self._gemm(K.Gemm(dv, Wq[2 * dl:], dn1, b_mn=True, resid=dn1))
+        self.comm.all_reduce(dn1, "attn")
+        dx = self.buf("dx", (T, d))
+        self._rnorm_bwd(dn1, S["x"], self.gamma1, S["s1"], dx_mid, dx, "gamma1")
+        return dx
+
+    def weight_grads_by_name(self):
+        g = {k: v.double().cpu().numpy() for k, v in self.grad.items()}
+        dl, fl = self.dl, self.fl
+        W = {"q": g["qkv"][:dl], "k": g["qkv"][dl:2 * dl], "v": g["qkv"][2 * dl:], "o": g["o"],
+             "gate": g["gu"][:fl], "up": g["gu"][fl:], "down": g["down"]}
+        return {"W": W, "gamma1": g["gamma1"], "gamma2": g["gamma2"]}

@@ -26,6 +26,8 @@ int reduce_rows(const float* in, int splits, long long split_stride, long long l
                 const float* col_scale, float* out, long long ldo, int accumulate, cudaStream_t st);
 int add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows, int cols,
         cudaStream_t st);
+int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                     const float* s, void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st);
 int dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
         int max_blocks, int* nblk_out, cudaStream_t st);
 }  // namespace btp

@@ -76,9 +76,20 @@ int btp_add(const void* a, long long lda, const void* b, long long ldb, void* ou
   return btp::add(a, lda, b, ldb, out, ldo, rows, cols, ST(stream));
 }
 
+int btp_rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                         const float* s, void* dh, long long lddh, float* dss, int rows, int width, void* stream) {
+  return btp::rmsnorm_bwd_prep(dn, lddn, x, ldx, gamma, s, dh, lddh, dss, rows, width, ST(stream));
+}
+
 int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
             int max_blocks, int* nblk, void* stream) {
   return btp::dot(a, lda, b, ldb, rows, cols, partial, max_blocks, nblk, ST(stream));
+}
+
+int btp_zero(void* ptr, long long bytes, void* stream) {
+  if (bytes < 0) return BTP_ERR_DIM;
+  if (bytes == 0) return BTP_OK;
+  return cudaMemsetAsync(ptr, 0, (size_t)bytes, ST(stream)) == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
 int btp_num_sms(void) { return btp::num_sms_cached(); }

@@ -14,11 +14,17 @@
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
 // w4..w7 epilogue (TMEM lane quarter = warp % 4). The accumulator is double-buffered in
 // TMEM (2 x BN columns) so the epilogue of tile i overlaps the mainloop of tile i+1.
+//
+// Epilogue: TMEM -> registers (scale / residual / convert) -> 128B-swizzled smem staging
+// (32 rows x 128 B per warp, double-buffered) -> TMA bulk tensor store. Split-K partials use
+// the TMA reduce-add form (fp32 add performed in L2) into a zero-initialised fp32 output, so
+// there are no partial slabs and no separate reduction pass.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "btp_internal.h"
@@ -30,21 +36,22 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kMaxProblems = 4;
 constexpr int kThreads = 256;
+constexpr int kEpiStageBytes = 32 * 128;              // one warp's 32 rows x 128 B chunk
+constexpr int kEpiBytes = 4 * 2 * kEpiStageBytes;     // 4 epilogue warps, double-buffered
 
 struct alignas(64) DevProblem {
   CUtensorMap tma_a;
   CUtensorMap tma_b;
-  void* c;
+  CUtensorMap tma_c;
   const float* row_scale;
   const float* col_scale;
   const __nv_bfloat16* resid;
-  long long ldc;
   long long ld_resid;
-  long long split_stride;
   int M, N, K;
   int m_tiles, n_tiles, splits, kb_per_split, k_blocks;
   int tile_start;
   int out_fp32;
+  int reduce_add;   // split-K: TMA reduce-add into the fp32 output
   float alpha;
 };
 
@@ -62,7 +69,7 @@ struct Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr int kBarrierBytes = 256;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBarrierBytes;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarrierBytes;
 };
 
 struct TileCoord {
@@ -93,7 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* sEpi = smem + C::kStages * C::kStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -106,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int i = 0; i < P.num_problems; ++i) {
       tma_prefetch_desc(&P.prob[i].tma_a);
       tma_prefetch_desc(&P.prob[i].tma_b);
+      tma_prefetch_desc(&P.prob[i].tma_c);
     }
   }
   if (warp == 1 && lane == 0) {
@@ -201,8 +210,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const uint32_t q = warp & 3;  // TMEM lane quarter
+    const uint32_t q = warp & 3;  // TMEM lane quarter == rows [32q, 32q+32) of the tile
+    const uint32_t stage0 = smem_u32(sEpi + q * 2 * kEpiStageBytes);
+    const uint32_t row_sw = lane & 7;  // 128B swizzle: 16B chunk j of row i lives at chunk j ^ (i % 8)
     int it = 0;
+    int chunk_seq = 0;  // running chunk counter -> staging buffer parity
     for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
       const TileCoord tc = decode_tile(P, tile);
       const DevProblem& pr = P.prob[tc.p];
@@ -216,29 +228,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       float rscale = pr.alpha;
       if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
       const int n_valid = min(BN, pr.N - n0);
+      const int cols_per_chunk = pr.out_fp32 ? 32 : 64;  // 128 bytes of output per row
+      const int out_row0 = m0 + q * 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        if (c0 >= n_valid) break;  // warp-uniform
-        uint32_t r[32];
+      for (int c0 = 0; c0 < n_valid; c0 += cols_per_chunk, ++chunk_seq) {
+        const uint32_t stage = stage0 + (chunk_seq & 1) * kEpiStageBytes;
+        // the TMA store issued two chunks ago used this staging buffer: it must have read it
+        if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
+        float v[64];
+        uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + buf * BN + c0, r);
         tmem_ld_wait();
-        if (row_ok) {
-        float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rscale;
-        const int col = n0 + c0;
-        const int ncols = min(32, n_valid - c0);  // multiple of 8 (host guarantees N % 8 == 0)
-        if (pr.col_scale != nullptr) {
+        if (!pr.out_fp32) {
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + buf * BN + c0 + 32, r);
+          tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) v[j] *= __ldg(pr.col_scale + col + j);
+          for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r[j]) * rscale;
         }
-        if (pr.resid != nullptr) {
+        const int col = n0 + c0;
+        if (pr.col_scale != nullptr) {
+          const int lim = min(cols_per_chunk, n_valid - c0);
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < lim) v[j] *= __ldg(pr.col_scale + col + j);
+        }
+        if (pr.resid != nullptr && row_ok) {
+          const int lim = min(cols_per_chunk, n_valid - c0);
           const uint4* rp = reinterpret_cast<const uint4*>(pr.resid + (long long)row * pr.ld_resid + col);
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            if (g * 8 < ncols) {
+          for (int g = 0; g < 8; ++g) {
+            if (g * 8 < lim) {
               const uint4 rv = __ldg(rp + g);
               const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
@@ -249,27 +271,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
         }
+        const uint32_t row_addr = stage + lane * 128;
         if (pr.out_fp32) {
-          float* cp = reinterpret_cast<float*>(pr.c) + (long long)tc.split * pr.split_stride +
-                      (long long)row * pr.ldc + col;
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            if (g * 4 < ncols)
-              reinterpret_cast<float4*>(cp)[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(row_addr + ((j ^ row_sw) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
         } else {
-          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(pr.c) + (long long)row * pr.ldc + col;
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            if (g * 8 < ncols)
-              reinterpret_cast<uint4*>(cp)[g] =
-                  make_uint4(pack_bf16(v[8 * g], v[8 * g + 1]), pack_bf16(v[8 * g + 2], v[8 * g + 3]),
-                             pack_bf16(v[8 * g + 4], v[8 * g + 5]), pack_bf16(v[8 * g + 6], v[8 * g + 7]));
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(row_addr + ((j ^ row_sw) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
+                         pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
         }
-        }  // row_ok
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          // out-of-range rows / columns of the box are clipped by the TMA unit
+          if (pr.reduce_add) tma_reduce_add_2d(&pr.tma_c, sEpi + (stage - smem_u32(sEpi)), col, out_row0);
+          else               tma_store_2d(&pr.tma_c, sEpi + (stage - smem_u32(sEpi)), col, out_row0);
+          bulk_commit();
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   __syncthreads();
@@ -294,18 +321,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// 2-D bf16 row-major tensor [outer, inner] with row stride `ld` elements, 128B swizzle.
+// 2-D row-major tensor [outer, inner] with row stride `ld` elements, 128B swizzle.
 static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer, bool fp32 = false) {
   auto enc = get_encode_fn();
   if (!enc) return BTP_ERR_CUDA;
+  const uint64_t esz = fp32 ? 4 : 2;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
+  cuuint64_t strides[1] = {ld * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
@@ -331,10 +359,12 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     const btp_gemm_problem& q = probs[i];
     if (q.a_mn != a_mn || q.b_mn != b_mn) return BTP_ERR_DIM;
     if (q.M <= 0 || q.N <= 0 || q.K <= 0) return BTP_ERR_DIM;
-    if (q.N % 8 != 0 || q.K % 8 != 0) return BTP_ERR_ALIGNMENT;
+    if (q.N % 8 != 0 || q.K % 8 != 0 || q.ldc % 8 != 0) return BTP_ERR_ALIGNMENT;
     if (q.splits < 1) return BTP_ERR_DIM;
     if (q.splits > 1 && !q.c_fp32) return BTP_ERR_DIM;
-    if (q.resid && q.c_fp32) return BTP_ERR_DIM;
+    if (q.resid && (q.c_fp32 || q.ld_resid % 8)) return BTP_ERR_DIM;
+    // split-K accumulates through TMA reduce-add into a zero-initialised fp32 output
+    if (q.splits > 1 && !q.reduce_add) return BTP_ERR_DIM;
     maxN = maxN > q.N ? maxN : q.N;
   }
   const int BN = (bn_hint == 128 || bn_hint == 256) ? bn_hint : (maxN >= 256 ? 256 : 128);
@@ -351,13 +381,12 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     if (!b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN);
     else       rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
     if (rc) return rc;
-    d.c = q.c;
+    rc = make_tmap(&d.tma_c, q.c, q.N, q.M, q.ldc, q.c_fp32 ? 32 : 64, 32, q.c_fp32 != 0);
+    if (rc) return rc;
     d.row_scale = q.row_scale;
     d.col_scale = q.col_scale;
     d.resid = reinterpret_cast<const __nv_bfloat16*>(q.resid);
-    d.ldc = q.ldc;
     d.ld_resid = q.ld_resid;
-    d.split_stride = q.split_stride;
     d.M = q.M; d.N = q.N; d.K = q.K;
     d.m_tiles = (q.M + kBM - 1) / kBM;
     d.n_tiles = (q.N + BN - 1) / BN;
@@ -365,6 +394,7 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     d.splits = q.splits;
     d.kb_per_split = (d.k_blocks + q.splits - 1) / q.splits;
     d.out_fp32 = q.c_fp32;
+    d.reduce_add = q.reduce_add;
     d.alpha = q.alpha == 0.0f ? 1.0f : q.alpha;
     d.tile_start = tiles;
     tiles += d.m_tiles * d.n_tiles * q.splits;

@@ -410,6 +410,40 @@ __global__ void __launch_bounds__(256) add_kernel(const bf16* __restrict__ a, lo
 }
 
 
+// ----------------------------------------------------------------------------- replicated norm bwd prologue
+// Full-width RMSNorm n = x*gamma/s (baselines): dn -> dh = dn / s (in place allowed) and
+// dss = -<dn, gamma*x> / (2 s^3 d), so btp_rmsnorm_bwd finishes dx and dgamma.
+__global__ void __launch_bounds__(256) rmsnorm_bwd_prep_kernel(const bf16* dn, long long lddn,
+                                                               const bf16* __restrict__ x, long long ldx,
+                                                               const float* __restrict__ gamma,
+                                                               const float* __restrict__ s_in, bf16* dh,
+                                                               long long lddh, float* __restrict__ dss, int rows,
+                                                               int width) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float s = s_in[row];
+  const float inv = 1.0f / s;
+  float dot = 0.f;
+  for (int c = lane; c < (width >> 3); c += 32) {
+    float fd[8], fx[8];
+    unpack8(*reinterpret_cast<const uint4*>(dn + (long long)row * lddn + c * 8), fd);
+    unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), fx);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      dot = fmaf(fd[j], g[j] * fx[j], dot);
+      fd[j] *= inv;
+    }
+    *reinterpret_cast<uint4*>(dh + (long long)row * lddh + c * 8) = pack8(fd);
+  }
+  dot = warp_sum(dot);
+  if (lane == 0) dss[row] = -dot / (2.0f * s * s * s * (float)width);
+}
+
 // ----------------------------------------------------------------------------- loss dot
 // partial[blk] = sum over this block's rows of <a_row, b_row>; fixed block/thread order.
 __global__ void __launch_bounds__(256) dot_kernel(const bf16* __restrict__ a, long long lda,
@@ -599,6 +633,17 @@ int add(const void* a, long long lda, const void* b, long long ldb, void* out, l
   add_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(static_cast<const bf16*>(a), lda,
                                                                    static_cast<const bf16*>(b), ldb,
                                                                    static_cast<bf16*>(out), ldo, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                     const float* s, void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st) {
+  if (rows <= 0 || width <= 0) return BTP_ERR_DIM;
+  if (width % 8 || lddn % 8 || ldx % 8 || lddh % 8 || !al16(dn) || !al16(x) || !al16(dh) || !al16(gamma))
+    return BTP_ERR_ALIGNMENT;
+  rmsnorm_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(dn), lddn,
+                                                          static_cast<const bf16*>(x), ldx, gamma, s,
+                                                          static_cast<bf16*>(dh), lddh, dss, rows, width);
   BTP_CHECK_LAUNCH();
 }
 

@@ -132,21 +132,14 @@ class ExecutorBase:
         kb = (T + 63) // 64
         tiles = sum(math.ceil(dy.shape[1] / 128) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
         splits = _pick_splits(tiles, kb, self.sms)
-        if splits == 1 and col_scale is None:
-            self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True) for dy, x, o in pairs])
+        if splits == 1:
+            self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True, col_scale=col_scale) for dy, x, o in pairs])
             return
-        sizes = [splits * o.numel() for _, _, o in pairs]
-        flat = self._wgrad_parts(sum(sizes))
-        probs, views, off = [], [], 0
-        for (dy, x, o), n in zip(pairs, sizes):
-            part = flat[off:off + n].view(splits, *o.shape)
-            off += n
-            probs.append(K.Gemm(dy, x, part, a_mn=True, b_mn=True, splits=splits))
-            views.append((part, o))
-        self._gemm(*probs)
-        for part, o in views:
-            K.reduce_rows(part, o, col_scale=col_scale)
-            self.stats.kernel_launches += 1
+        # split-K: every split adds its fp32 tile into the zeroed gradient with the TMA reduce-add
+        for _, _, o in pairs:
+            K.zero(o)
+        self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True, splits=splits, col_scale=col_scale)
+                     for dy, x, o in pairs])
 
     # ------------------------------------------------------------------ loss / accounting
     def loss_device(self, y: torch.Tensor, G: torch.Tensor) -> torch.Tensor:

@@ -62,6 +62,7 @@ class Gemm:
     resid: torch.Tensor | None = None
     splits: int = 1
     alpha: float = 1.0
+    reduce_add: bool = False                # add into C (fp32, zeroed) via TMA reduce; needed for splits > 1
 
     def to_c(self) -> GemmProblem:
         _check(self.a, BF16, "A")
@@ -73,23 +74,23 @@ class Gemm:
             N, Kb = self.b.shape
         if Kb != K:
             raise ValueError(f"GEMM inner dims disagree: A {tuple(self.a.shape)} B {tuple(self.b.shape)}")
-        c2 = self.c[0] if self.c.dim() == 3 else self.c
-        if tuple(c2.shape) != (M, N):
-            raise ValueError(f"GEMM output {tuple(c2.shape)} != ({M}, {N})")
-        if self.c.dim() == 3 and self.c.shape[0] < self.splits:
-            raise ValueError(f"split-K output has {self.c.shape[0]} slabs < splits={self.splits}")
+        if tuple(self.c.shape) != (M, N):
+            raise ValueError(f"GEMM output {tuple(self.c.shape)} != ({M}, {N})")
         c_fp32 = self.c.dtype == F32
-        split_stride = self.c.stride(0) if self.c.dim() == 3 else 0
+        if (self.splits > 1 or self.reduce_add) and not c_fp32:
+            raise ValueError("split-K / reduce-add GEMMs need an fp32 output")
+        split_stride = 0
         return GemmProblem(
             a=self.a.data_ptr(), lda=_ld(self.a), a_mn=int(self.a_mn),
             b=self.b.data_ptr(), ldb=_ld(self.b), b_mn=int(self.b_mn),
-            c=self.c.data_ptr(), ldc=_ld(c2), c_fp32=int(c_fp32),
+            c=self.c.data_ptr(), ldc=_ld(self.c), c_fp32=int(c_fp32),
             M=M, N=N, K=K,
             row_scale=None if self.row_scale is None else self.row_scale.data_ptr(),
             col_scale=None if self.col_scale is None else self.col_scale.data_ptr(),
             resid=None if self.resid is None else self.resid.data_ptr(),
             ld_resid=_ld(self.resid),
             splits=self.splits, split_stride=split_stride, alpha=float(self.alpha),
+            reduce_add=int(self.reduce_add or self.splits > 1),
         )
 
 
@@ -97,6 +98,10 @@ def gemm(*problems: Gemm, bn: int = 0) -> None:
     """One launch of the persistent tcgen05 GEMM over 1..4 problems."""
     arr = (GemmProblem * len(problems))(*[p.to_c() for p in problems])
     _native.call("btp_gemm", arr, len(problems), bn, _stream())
+
+
+def zero(t: torch.Tensor) -> None:
+    _native.call("btp_zero", _p(t), t.numel() * t.element_size(), _stream())
 
 
 def rmsnorm_residual(x, gamma, *, branch=None, x_out=None, n_out=None, ss_out=None, rl_out=None, eps=1e-6):
@@ -169,6 +174,12 @@ def reduce_rows(parts, out, *, splits=None, col_scale=None, accumulate=False):
 def add(a, b, out):
     rows, cols = a.shape
     _native.call("btp_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), rows, cols, _stream())
+
+
+def rmsnorm_bwd_prep(dn, x, gamma, s, dh, dss):
+    rows, width = x.shape
+    _native.call("btp_rmsnorm_bwd_prep", _p(dn), _ld(dn), _p(x), _ld(x), _p(gamma), _p(s), _p(dh), _ld(dh),
+                 _p(dss), rows, width, _stream())
 
 
 def dot(a, b, partial) -> int:

@@ -21,9 +21,10 @@ def run(M, N, Kd, a_mn, b_mn, bn=0, out=torch.bfloat16, splits=1, rs=False, cs=F
     if col is not None: ref = ref * col[None, :]
     if R is not None: ref = ref + R.float()
     if splits > 1:
-        C = torch.zeros(splits, M, N, device=dev)
+        C = torch.empty(M, N, device=dev)
+        K.zero(C)
         K.gemm(K.Gemm(a_arg, b_arg, C, a_mn=a_mn, b_mn=b_mn, row_scale=row, col_scale=col, splits=splits), bn=bn)
-        Cs = C.sum(0)
+        Cs = C
     else:
         C = torch.zeros(M, N, device=dev, dtype=out)
         K.gemm(K.Gemm(a_arg, b_arg, C, a_mn=a_mn, b_mn=b_mn, row_scale=row, col_scale=col, resid=R), bn=bn)

@@ -25,12 +25,12 @@ def inputs(cfg, variant, b, s, seed=0):
     return blk, x, G, oblk
 
 
-def oracle_step(oblk, x, G, cfg, b, s, tp=1, online=True):
+def oracle_step(oblk, x, G, cfg, b, s, tp=1, online=True, sharded=True):
     T = b * s
     x2 = x.values.reshape(T, cfg.d)
     G2 = G.values.reshape(T, cfg.d)
     y, cache = O.block_forward(oblk, x2, b, s, cfg.heads)
     grads = O.block_backward(oblk, cache, G2, b, s, cfg.heads)
-    _, ws = O.btp_forward_sharded(oblk, x2, b, s, cfg.heads, tp, online=online)
+    ws = O.btp_forward_sharded(oblk, x2, b, s, cfg.heads, tp, online=online)[1] if sharded else None
     loss = float(np.sum(y * G2))
     return y, grads, ws, loss

@@ -87,3 +87,18 @@ def test_c60m_block_step():
         assert rel(st.grads["A"][n], g_ref["A"][n]) < BF16_TOL, n
         assert rel(st.grads["B"][n], g_ref["B"][n]) < BF16_TOL, n
     assert rel(st.dx, g_ref["dx"]) < BF16_TOL
+
+
+def test_run_with_ckpt_bitwise_and_collective_free():
+    """Reference contract (test_ckpt.py:79-87): the BTP re-forward from the checkpoint set has
+    zero collectives and reproduces the forward bitwise; it frees memory."""
+    from paper_2512_12131_b200.checkpointing import CkptPolicy, eff_ckpt, run_with_ckpt
+
+    b, s = 2, 64
+    blk, x, G, oblk = inputs(SMALL, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    run = run_with_ckpt(pl, blk, x, CkptPolicy.LOWRANK_BOUNDARY)
+    assert run.recompute_bitwise_ok, run.recompute_checks
+    assert run.report.reforward_collectives == 0
+    assert run.report.delta_mem_bytes > 0
+    assert eff_ckpt(run.report) > 0
