@@ -1,2 +1,39 @@
-"""B200-native Bottleneck-aware Tensor Parallelism (BTP) for CoLA low-rank decoder blocks."""
+"""B200-native Bottleneck-aware Tensor Parallelism (BTP) for CoLA low-rank decoder blocks.
+
+Drop-in for the BTP path of the reference package `btpsim` (pkg/src/btpsim/__init__.py:9-42):
+the same config / plan / execution names, with the block computed on sm_100a tensor cores
+through libbtp.so (include/btp.h) and the TP collectives on NCCL. Additions the reference does
+not have: `train_step` (forward + backward), `BlockTrainer` (resident, CUDA-graph replayed
+training step), and the naive-TP / full-rank executors on the same kernels.
+"""
+
+from .tensor import DimensionError, DivisibilityError, Tensor, seeded_fill, tensor, zeros
+from .model import (
+    COLA_60M,
+    PRESETS,
+    DecoderBlockWeights,
+    ModelConfig,
+    RunShape,
+    Variant,
+    build_block,
+    fan_in_scaled,
+    preset,
+    projection_dims,
+)
+from .plan import NormMode, PlanError, ShardPlan, Strategy, apply_grouping, describe, enumerate_collectives, plan
+from .trace import CollectiveRecord, Trace, ring_transfer_elements, trace_volume
+from .api import BlockTrainer, SimResult, StepResult, execute_forward, make_executor, train_step
+from .checkpointing import CkptPolicy, CkptReport, eff_ckpt, run_with_ckpt
+
+__all__ = [
+    "Tensor", "tensor", "zeros", "seeded_fill", "DimensionError", "DivisibilityError",
+    "ModelConfig", "RunShape", "Variant", "PRESETS", "COLA_60M", "preset", "projection_dims",
+    "DecoderBlockWeights", "build_block", "fan_in_scaled",
+    "Strategy", "NormMode", "ShardPlan", "PlanError", "plan", "apply_grouping", "describe",
+    "enumerate_collectives",
+    "CollectiveRecord", "Trace", "trace_volume", "ring_transfer_elements",
+    "execute_forward", "train_step", "make_executor", "BlockTrainer", "SimResult", "StepResult",
+    "CkptPolicy", "CkptReport", "eff_ckpt", "run_with_ckpt",
+]
+
 __version__ = "0.1.0"

@@ -1,0 +1,122 @@
+"""TP = 2 end to end on ONE GPU: two processes (one per TP rank) share cuda:0 and talk over the
+gloo backend (the box has a single GPU; NCCL refuses two ranks on one device). Every compute
+site runs in libbtp.so on each rank's shard; the all-reduces / rider / gather go through the
+same TPComm code the NCCL path uses. Outputs, the loss, per-rank dx shards and per-rank weight
+gradient shards are compared with the float64 oracle sliced to each rank."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q):
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        import datetime
+
+        dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=180))
+        from tests.gpu_util import SMALL, inputs
+        from paper_2512_12131_b200.api import train_step
+        from paper_2512_12131_b200.model import RunShape, Variant
+        from paper_2512_12131_b200.plan import Strategy, plan
+
+        b, s = 2, 64
+        variant = Variant.COLA
+        blk, x, G, _ = inputs(SMALL, variant, b, s)
+        pl = plan(Strategy(strategy), SMALL, RunShape(b, s, world), variant, online_norm=online, grouping=grouping,
+                  lowrank_ckpt=ckpt)
+        st = train_step(pl, blk, x, G)
+        q.put((rank, st.y.values, st.loss, st.dx, st.grads, st.trace.record_tuples("forward"),
+               st.trace.record_tuples("backward"), st.trace.record_tuples("reforward"), None))
+        dist.destroy_process_group()
+    except Exception as exc:  # surface the failure to the parent instead of hanging it
+        import traceback
+
+        q.put((rank, None, None, None, None, None, None, None, traceback.format_exc()))
+
+
+def _run_tp2(strategy, grouping, online, ckpt):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, strategy, grouping, online, ckpt, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in procs:
+            item = q.get(timeout=600)
+            res[item[0]] = item
+            assert item[-1] is None, f"rank {item[0]} failed:\n{item[-1]}"  # fail fast; peers are killed below
+    finally:
+        for p in procs:
+            p.join(timeout=60 if len(res) == len(procs) else 1)
+            if p.is_alive():
+                p.kill()
+    return res
+
+
+@pytest.mark.parametrize("grouping,online,ckpt", [(True, True, False), (False, True, False), (True, False, True)])
+def test_btp_tp2_matches_oracle(grouping, online, ckpt):
+    from tests.gpu_util import BF16_TOL, SMALL, inputs, oracle_step, rel
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, enumerate_collectives, plan
+
+    b, s = 2, 64
+    res = _run_tp2("btp", grouping, online, ckpt)
+    blk, x, G, oblk = inputs(SMALL, Variant.COLA, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, tp=2, online=online)
+    pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 2), Variant.COLA, online_norm=online, grouping=grouping)
+    pred = [(p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
+    for rank, (_, y, loss, dx, grads, fwd, bwd, refwd, _) in res.items():
+        assert rel(y.reshape(-1, SMALL.d), y_ref) < BF16_TOL
+        assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
+        gr = O.grads_for_rank(g_ref, 2, rank, SMALL.d, SMALL.d_ff)
+        assert rel(dx, gr["dx"]) < BF16_TOL
+        for n in O.PROJECTIONS:
+            assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
+            assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
+        assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
+        assert fwd == pred                      # real collectives == the plan's prediction
+        assert sum(rec[3] for rec in bwd) == 7 * b * s * SMALL.r  # backward moves only rank-r tensors
+        assert refwd == []                      # checkpoint recompute is collective-free
+
+
+@pytest.mark.parametrize("strategy", ["vanilla"])
+def test_vanilla_tp2_matches_oracle(strategy):
+    from tests.gpu_util import BF16_TOL, SMALL, inputs, oracle_step, rel
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import Variant
+    from paper_2512_12131_b200.plan import cola_pair_indices
+
+    b, s = 2, 64
+    res = _run_tp2(strategy, True, False, False)
+    blk, x, G, oblk = inputs(SMALL, Variant.COLA, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, sharded=False)
+    for rank, (_, y, loss, dx, grads, *_rest) in res.items():
+        assert rel(y.reshape(-1, SMALL.d), y_ref) < BF16_TOL
+        assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
+        assert rel(dx, g_ref["dx"]) < BF16_TOL
+        idx = cola_pair_indices(SMALL.r, 2, rank)
+        for n in O.PROJECTIONS:
+            assert rel(grads["B"][n], g_ref["B"][n][idx, :]) < BF16_TOL, (rank, "B", n)
+            assert rel(grads["A"][n], g_ref["A"][n][:, idx]) < BF16_TOL, (rank, "A", n)
