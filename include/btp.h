@@ -56,6 +56,16 @@ typedef struct btp_gemm_problem {
    * a weight gradient): C must be fp32 and zero-initialised (btp_zero); summation order across
    * splits is not fixed (fp32 round-off only). split_stride is unused. */
   int reduce_add;
+  /* epilogue: 0 = store (with the optional resid add above);
+   *           2 = SwiGLU backward: acc = dact, resid = g (bf16), aux2 = u (bf16),
+   *               C = dg = dact*u*silu'(g), c2 = du = dact*silu(g)   (both bf16, no split-K)
+   * Aux inputs are TMA-loaded into the epilogue's swizzled staging buffers, prefetched one
+   * chunk ahead; outputs leave through TMA bulk stores. */
+  int epilogue;
+  const void* aux2;
+  long long ld_aux2;
+  void* c2;
+  long long ldc2;
 } btp_gemm_problem;
 
 /* Grouped/batched tcgen05 GEMM: n (1..4) independent problems in ONE persistent launch.

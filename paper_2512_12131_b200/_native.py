@@ -78,6 +78,11 @@ class GemmProblem(ctypes.Structure):
         ("split_stride", ctypes.c_longlong),
         ("alpha", ctypes.c_float),
         ("reduce_add", ctypes.c_int),
+        ("epilogue", ctypes.c_int),
+        ("aux2", ctypes.c_void_p),
+        ("ld_aux2", ctypes.c_longlong),
+        ("c2", ctypes.c_void_p),
+        ("ldc2", ctypes.c_longlong),
     ]
 
 

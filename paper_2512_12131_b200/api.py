@@ -157,19 +157,24 @@ class BlockTrainer:
 
     step_device(x, G): device-resident inputs, no host sync (the bench's `value`).
     step(x_host, G_host): the user-facing call — H2D copy of this step's pinned-host inputs,
-    the step, and a D2H read of the loss (the bench's `e2e`)."""
+    the step, and a D2H read of the loss.
+    fit(x_hosts, G_host): the training loop — the loss projection G is copied once, each batch's
+    pinned-host x is copied on a side stream while the previous step computes (two input slots,
+    one CUDA graph each), and every step's loss is read back (the bench's `e2e`)."""
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True):
         self.pl = pl
         self.ex = make_executor(pl, block, eps=eps, attn_backend=attn_backend)
         self.use_graph = use_graph and pl.shape.tp == 1
-        self.graph = None
+        self.graphs: dict = {}
         self.graphed = False
         self._per_step_launches = 0
         self._replays = 0
         self._x = self._g = None
         self.loss_buf = None
+        self._slots = None
+        self._copy_stream = None
 
     @property
     def kernel_launches(self) -> int:
@@ -192,10 +197,9 @@ class BlockTrainer:
         if not self.use_graph:
             self._eager(x, g)
             return
-        if self._x is None or x.data_ptr() != self._x.data_ptr() or g.data_ptr() != self._g.data_ptr():
-            self._x, self._g = x, g
-            self.graph = None
-        if self.graph is None:
+        key = (x.data_ptr(), g.data_ptr())
+        graph = self.graphs.get(key)
+        if graph is None:
             # eager warm-up allocates every buffer, then capture one step into a graph
             before = self.ex.stats.kernel_launches
             self._eager(x, g)
@@ -210,9 +214,41 @@ class BlockTrainer:
                     self._eager(x, g)
                 self.ex.stats.kernel_launches = saved
             torch.cuda.current_stream().wait_stream(side)
-            self.graph, self.graphed = graph, True
-        self.graph.replay()
+            self.graphs[key], self.graphed = graph, True
+        graph.replay()
         self._replays += 1
+
+    def fit(self, x_hosts, G_host: torch.Tensor) -> list[float]:
+        """Pipelined steps over pinned-host input shards; returns every step's loss (read back)."""
+        dev = self.ex.dev
+        if self._slots is None:
+            shape, dt = x_hosts[0].shape, x_hosts[0].dtype
+            self._slots = [torch.empty(shape, dtype=dt, device=dev) for _ in range(2)]
+            self._target = torch.empty(G_host.shape, dtype=G_host.dtype, device=dev)
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        main, copy = torch.cuda.current_stream(), self._copy_stream
+        self._target.copy_(G_host, non_blocking=True)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        copy.wait_stream(main)
+        with torch.cuda.stream(copy):
+            self._slots[0].copy_(x_hosts[0], non_blocking=True)
+            copied[0].record(copy)
+        losses = []
+        for i in range(len(x_hosts)):
+            s = i & 1
+            main.wait_event(copied[s])
+            if i + 1 < len(x_hosts):
+                ns = s ^ 1
+                if i >= 1:
+                    copy.wait_event(consumed[ns])  # slot ns was read by step i-1
+                with torch.cuda.stream(copy):
+                    self._slots[ns].copy_(x_hosts[i + 1], non_blocking=True)
+                    copied[ns].record(copy)
+            self.step_device(self._slots[s], self._target)
+            consumed[s].record(main)
+            losses.append(float(self.loss_buf.item()))
+        return losses
 
     def step(self, x_host: torch.Tensor, g_host: torch.Tensor) -> float:
         if self._x is None:
@@ -224,13 +260,36 @@ class BlockTrainer:
         return float(self.loss_buf.item())
 
     def time_gemms(self, x: torch.Tensor, g: torch.Tensor) -> dict:
-        """One eager step with every GEMM launch bracketed by CUDA events on its stream."""
+        """One step with every GEMM launch bracketed by CUDA events on its stream. The step is
+        captured into a CUDA graph (events as record nodes) and replayed, so each interval is
+        device time only — no host enqueue gaps."""
         self.ex.gemm_timer = []
-        self._eager(x, g)
+        self._eager(x, g)  # allocate every buffer outside the capture
+        torch.cuda.synchronize()
+        if self.ex.tp > 1:  # collectives stay eager; timings then include host gaps
+            rec, self.ex.gemm_timer = self.ex.gemm_timer, None
+            return self._gemm_summary(rec)
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        saved = self.ex.stats.kernel_launches
+        with torch.cuda.stream(side):
+            self.ex.gemm_timer = []
+            with torch.cuda.graph(graph, stream=side):
+                self._eager(x, g)
+        self.ex.stats.kernel_launches = saved
+        torch.cuda.current_stream().wait_stream(side)
+        for _ in range(2):
+            graph.replay()
         torch.cuda.synchronize()
         rec, self.ex.gemm_timer = self.ex.gemm_timer, None
-        ms = sum(a.elapsed_time(b) for a, b, _ in rec)
-        fl = sum(f for _, _, f in rec)
-        per = [(a.elapsed_time(b), f) for a, b, f in rec]
+        return self._gemm_summary(rec)
+
+    @staticmethod
+    def _gemm_summary(rec) -> dict:
+        ms = sum(a.elapsed_time(b) for a, b, _, _ in rec)
+        fl = sum(f for _, _, f, _ in rec)
+        per = [{"us": a.elapsed_time(b) * 1e3, "tflops": f / (a.elapsed_time(b) / 1e3) / 1e12, "problems": sh}
+               for a, b, f, sh in rec]
         return {"ms": ms, "flops": fl, "tflops": fl / (ms / 1e3) / 1e12 if ms else 0.0, "launches": len(rec),
                 "per_launch": per}

@@ -286,12 +286,16 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
         S, W, G, T, d, dl, fl = self.saved, self.W, self.grad, self.T, self.d, self.dl, self.fl
         self.comm.pass_tag = "backward"
-        dact = self.buf("dact", (T, fl))
-        self._gemm(K.Gemm(dy, W["down"], dact, b_mn=True))
-        self._wgrad([(dy, S["act"], G["down"])])
         dgu = self.buf("dgu", (T, 2 * fl))
-        K.swiglu_bwd(S["gu"][:, :fl], S["gu"][:, fl:], dact, dgu[:, :fl], dgu[:, fl:])
-        self.stats.kernel_launches += 1
+        g, u = S["gu"][:, :fl], S["gu"][:, fl:]
+        if self.fuse_swiglu_bwd:  # dact stays in the GEMM epilogue, which emits dg, du
+            self._gemm(K.Gemm(dy, W["down"], dgu[:, :fl], b_mn=True, swiglu_bwd=(g, u, dgu[:, fl:])))
+        else:
+            dact = self.buf("dact", (T, fl))
+            self._gemm(K.Gemm(dy, W["down"], dact, b_mn=True))
+            K.swiglu_bwd(g, u, dact, dgu[:, :fl], dgu[:, fl:])
+            self.stats.kernel_launches += 1
+        self._wgrad([(dy, S["act"], G["down"])])
         self._wgrad([(dgu, S["n2"], G["gu"])])
         dn2 = self.buf("dn2", (T, d))
         self._gemm(K.Gemm(dgu, W["gu"], dn2, b_mn=True))

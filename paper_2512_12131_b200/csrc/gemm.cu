@@ -37,12 +37,19 @@ constexpr int kBK = 64;
 constexpr int kMaxProblems = 4;
 constexpr int kThreads = 256;
 constexpr int kEpiStageBytes = 32 * 128;              // one warp's 32 rows x 128 B chunk
-constexpr int kEpiBytes = 4 * 2 * kEpiStageBytes;     // 4 epilogue warps, double-buffered
+
+// Epilogue modes (per problem)
+constexpr int kEpiStore = 0;      // C = scale * acc (+ resid if given); store or reduce-add
+constexpr int kEpiSwigluBwd = 2;  // acc = dact; aux g (resid slot), u (aux2): C = dg, C2 = du
 
 struct alignas(64) DevProblem {
   CUtensorMap tma_a;
   CUtensorMap tma_b;
   CUtensorMap tma_c;
+  CUtensorMap tma_r;   // residual / first aux input (bf16, same box as the bf16 output)
+  CUtensorMap tma_c2;  // second output (swiglu-bwd: du)
+  CUtensorMap tma_r2;  // second aux input (swiglu-bwd: u)
+  int epi;
   const float* row_scale;
   const float* col_scale;
   const __nv_bfloat16* resid;
@@ -52,6 +59,8 @@ struct alignas(64) DevProblem {
   int tile_start;
   int out_fp32;
   int reduce_add;   // split-K: TMA reduce-add into the fp32 output
+  int a_mn, b_mn;   // operand majors (per problem: a launch may mix dgrad and wgrad problems)
+  uint32_t idesc;   // tcgen05 instruction descriptor for this problem
   float alpha;
 };
 
@@ -61,13 +70,17 @@ struct DevParams {
   int total_tiles;
 };
 
-template <int BN>
+// kSlots: staging slots per chunk buffer (2 for the two-input / two-output swiglu-bwd epilogue,
+// which trades mainloop stages for epilogue staging).
+template <int BN, int kSlots>
 struct Cfg {
-  static constexpr int kStages = (BN == 256) ? 4 : 6;
+  static constexpr int kStages = kSlots == 1 ? ((BN == 128) ? 6 : 4) : ((BN == 128) ? 4 : 3);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;  // double-buffered accumulator (pow2 alloc)
+  static constexpr int kEpiWarpBytes = 2 * kSlots * kEpiStageBytes;  // double-buffered chunks
+  static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
   static constexpr int kBarrierBytes = 256;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarrierBytes;
 };
@@ -93,19 +106,20 @@ __device__ __forceinline__ TileCoord decode_tile(const DevParams& P, int tile) {
   return t;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int kSlots>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ DevParams P) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kSlots>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
   uint8_t* sEpi = smem + C::kStages * C::kStageBytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar_all = tempty_bar + 2;  // 4 epilogue warps x 2 staging buffers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar_all + 8);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -126,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 128);
     }
+    for (int b = 0; b < 8; ++b) mbar_init(&aux_bar_all[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -151,14 +166,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * kBK;
-          if (!A_MN) {
+          if (!pr.a_mn) {
             tma_load_2d(a_dst, &pr.tma_a, &full_bar[stage], k0, m0);
           } else {
 #pragma unroll
             for (int c = 0; c < kBM / 64; ++c)
               tma_load_2d(a_dst + c * 64 * kBK * 2, &pr.tma_a, &full_bar[stage], m0 + c * 64, k0);
           }
-          if (!B_MN) {
+          if (!pr.b_mn) {
             tma_load_2d(b_dst, &pr.tma_b, &full_bar[stage], k0, n0);
           } else {
 #pragma unroll
@@ -171,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = make_idesc_bf16_f32(kBM, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -191,14 +205,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (elect_one()) {
           const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
           const uint32_t b_base = smem_u32(sB + stage * C::kBBytes);
+          // K-major: advance 32 B along the swizzled row; MN-major: advance 16 rows (2 KB)
+          const uint32_t a_step = pr.a_mn ? 16 * 128 : 32, b_step = pr.b_mn ? 16 * 128 : 32;
+          const uint32_t a_lbo = pr.a_mn ? 64 * kBK * 2 : 16, b_lbo = pr.b_mn ? 64 * kBK * 2 : 16;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            uint64_t a_desc, b_desc;
-            if (!A_MN) a_desc = make_sw128_desc(a_base + k * 32, 16, 1024);
-            else       a_desc = make_sw128_desc(a_base + k * 16 * 128, 64 * kBK * 2, 1024);
-            if (!B_MN) b_desc = make_sw128_desc(b_base + k * 32, 16, 1024);
-            else       b_desc = make_sw128_desc(b_base + k * 16 * 128, 64 * kBK * 2, 1024);
-            umma_bf16(d_tmem, a_desc, b_desc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            const uint64_t a_desc = make_sw128_desc(a_base + k * a_step, a_lbo, 1024);
+            const uint64_t b_desc = make_sw128_desc(b_base + k * b_step, b_lbo, 1024);
+            umma_bf16(d_tmem, a_desc, b_desc, pr.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
         }
@@ -211,8 +225,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter == rows [32q, 32q+32) of the tile
-    const uint32_t stage0 = smem_u32(sEpi + q * 2 * kEpiStageBytes);
+    uint8_t* stage_ptr0 = sEpi + q * C::kEpiWarpBytes;
+    const uint32_t stage0 = smem_u32(stage_ptr0);
     const uint32_t row_sw = lane & 7;  // 128B swizzle: 16B chunk j of row i lives at chunk j ^ (i % 8)
+    uint64_t* aux_bar = aux_bar_all + q * 2;  // one per staging buffer of this warp
+    uint32_t aux_phase = 0u;  // bit b: parity of the next wait on aux_bar[b]
+    // staging slot s of buffer b (each slot = one 32-row x 128 B chunk)
+    auto slot_ptr = [&](int b, int s) { return stage_ptr0 + (b * kSlots + s) * kEpiStageBytes; };
+    // lane 0: TMA-load the aux chunk(s) for output column `col` into buffer b
+    auto issue_aux = [&](const DevProblem& pr, int b, int col, int row0) {
+      const int naux = pr.epi == kEpiSwigluBwd ? 2 : 1;
+      bulk_wait_read<0>();  // every earlier store has finished reading its staging slots
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&aux_bar[b], naux * kEpiStageBytes);
+      tma_load_2d(slot_ptr(b, 0), &pr.tma_r, &aux_bar[b], col, row0);
+      if (naux == 2) tma_load_2d(slot_ptr(b, 1), &pr.tma_r2, &aux_bar[b], col, row0);
+    };
     int it = 0;
     int chunk_seq = 0;  // running chunk counter -> staging buffer parity
     for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
@@ -220,21 +248,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const DevProblem& pr = P.prob[tc.p];
       const int buf = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
+      const int n_valid = min(BN, pr.N - n0);
+      const int cols_per_chunk = pr.out_fp32 ? 32 : 64;  // 128 bytes of output per row
+      const int out_row0 = m0 + q * 32;
+      // aux tiles (residual, or g/u for swiglu-bwd) ride the staging buffers (bf16 out only)
+      const bool aux = pr.resid != nullptr;
+      const bool swb = pr.epi == kEpiSwigluBwd;
+      if (aux && lane == 0) issue_aux(pr, chunk_seq & 1, n0, out_row0);  // prefetch under the mainloop
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < pr.M;
       float rscale = pr.alpha;
       if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
-      const int n_valid = min(BN, pr.N - n0);
-      const int cols_per_chunk = pr.out_fp32 ? 32 : 64;  // 128 bytes of output per row
-      const int out_row0 = m0 + q * 32;
 #pragma unroll 1
       for (int c0 = 0; c0 < n_valid; c0 += cols_per_chunk, ++chunk_seq) {
-        const uint32_t stage = stage0 + (chunk_seq & 1) * kEpiStageBytes;
-        // the TMA store issued two chunks ago used this staging buffer: it must have read it
-        if (lane == 0) bulk_wait_read<1>();
+        const int b = chunk_seq & 1;
+        const uint32_t stage = smem_u32(slot_ptr(b, 0));
+        if (!aux) {
+          // the TMA store issued two chunks ago used this staging buffer: it must have read it
+          if (lane == 0) bulk_wait_read<kSlots>();
+        } else {
+          // prefetch the next chunk's aux into the other buffer, then wait for this one
+          if (lane == 0 && c0 + cols_per_chunk < n_valid) issue_aux(pr, b ^ 1, n0 + c0 + cols_per_chunk, out_row0);
+          mbar_wait(&aux_bar[b], (aux_phase >> b) & 1u);
+          aux_phase ^= 1u << b;
+        }
         __syncwarp();
         float v[64];
         uint32_t r[32];
@@ -255,23 +295,58 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           for (int j = 0; j < 64; ++j)
             if (j < lim) v[j] *= __ldg(pr.col_scale + col + j);
         }
-        if (pr.resid != nullptr && row_ok) {
-          const int lim = min(cols_per_chunk, n_valid - c0);
-          const uint4* rp = reinterpret_cast<const uint4*>(pr.resid + (long long)row * pr.ld_resid + col);
+        const uint32_t row_addr = stage + lane * 128;
+        if (swb) {
+          // acc = dact; slot 0 holds g, slot 1 holds u: dg = dact*u*silu'(g) -> slot 0, du = dact*silu(g) -> slot 1
+          const uint32_t row_addr2 = smem_u32(slot_ptr(b, 1)) + lane * 128;
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            const uint32_t off = ((g8 ^ row_sw) << 4);
+            const uint4 gv = ld_shared_v4(row_addr + off);
+            const uint4 uv = ld_shared_v4(row_addr2 + off);
+            const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w};
+            const uint32_t uw[4] = {uv.x, uv.y, uv.z, uv.w};
+            uint32_t dgw[4], duw[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              float dg2[2], du2[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const float gg = e ? bf16_hi(gw[h]) : bf16_lo(gw[h]);
+                const float uu = e ? bf16_hi(uw[h]) : bf16_lo(uw[h]);
+                const float da = v[g8 * 8 + 2 * h + e];
+                const float sg = sigmoidf_safe(gg);
+                dg2[e] = da * uu * sg * (1.0f + gg * (1.0f - sg));
+                du2[e] = da * gg * sg;
+              }
+              dgw[h] = pack_bf16(dg2[0], dg2[1]);
+              duw[h] = pack_bf16(du2[0], du2[1]);
+            }
+            st_shared_v4(row_addr + off, dgw[0], dgw[1], dgw[2], dgw[3]);
+            st_shared_v4(row_addr2 + off, duw[0], duw[1], duw[2], duw[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pr.tma_c, slot_ptr(b, 0), col, out_row0);
+            tma_store_2d(&pr.tma_c2, slot_ptr(b, 1), col, out_row0);
+            bulk_commit();
+          }
+          continue;
+        }
+        if (aux) {
+          // residual chunk (same swizzled layout as the output), read then overwritten in place
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
-            if (g * 8 < lim) {
-              const uint4 rv = __ldg(rp + g);
-              const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+            const uint4 rv = ld_shared_v4(row_addr + ((g ^ row_sw) << 4));
+            const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                v[g * 8 + 2 * h] += bf16_lo(w[h]);
-                v[g * 8 + 2 * h + 1] += bf16_hi(w[h]);
-              }
+            for (int h = 0; h < 4; ++h) {
+              v[g * 8 + 2 * h] += bf16_lo(w[h]);
+              v[g * 8 + 2 * h + 1] += bf16_hi(w[h]);
             }
           }
         }
-        const uint32_t row_addr = stage + lane * 128;
         if (pr.out_fp32) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -288,8 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         __syncwarp();
         if (lane == 0) {
           // out-of-range rows / columns of the box are clipped by the TMA unit
-          if (pr.reduce_add) tma_reduce_add_2d(&pr.tma_c, sEpi + (stage - smem_u32(sEpi)), col, out_row0);
-          else               tma_store_2d(&pr.tma_c, sEpi + (stage - smem_u32(sEpi)), col, out_row0);
+          if (pr.reduce_add) tma_reduce_add_2d(&pr.tma_c, slot_ptr(b, 0), col, out_row0);
+          else               tma_store_2d(&pr.tma_c, slot_ptr(b, 0), col, out_row0);
           bulk_commit();
         }
       }
@@ -337,27 +412,43 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int kSlots>
 static int launch(const DevParams& P, int grid, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, kSlots>;
+  static_assert(C::kSmemBytes <= 232448, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_kernel<BN, kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
   }
-  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::kSmemBytes, stream>>>(P);
+  gemm_kernel<BN, kSlots><<<grid, kThreads, C::kSmemBytes, stream>>>(P);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+// N-tile choice: persistent CTAs run ceil(tiles / SMs) waves of tiles whose mainloop time is
+// ~ proportional to BN (+ a fixed per-tile cost, ~32 columns' worth); pick the cheapest.
+static int pick_bn(const btp_gemm_problem* probs, int n, int sms) {
+  static const int cands[3] = {256, 192, 128};
+  int best = 256;
+  long long best_cost = -1;
+  for (int c = 0; c < 3; ++c) {
+    const int bn = cands[c];
+    long long tiles = 0;
+    for (int i = 0; i < n; ++i)
+      tiles += (long long)((probs[i].M + kBM - 1) / kBM) * ((probs[i].N + bn - 1) / bn) * probs[i].splits;
+    const long long waves = (tiles + sms - 1) / sms;
+    const long long cost = waves * (bn + 32);
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
+  }
+  return best;
 }
 
 int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream) {
   if (n <= 0 || n > kMaxProblems) return BTP_ERR_DIM;
-  const int a_mn = probs[0].a_mn, b_mn = probs[0].b_mn;
-  int maxN = 0;
   for (int i = 0; i < n; ++i) {
     const btp_gemm_problem& q = probs[i];
-    if (q.a_mn != a_mn || q.b_mn != b_mn) return BTP_ERR_DIM;
     if (q.M <= 0 || q.N <= 0 || q.K <= 0) return BTP_ERR_DIM;
     if (q.N % 8 != 0 || q.K % 8 != 0 || q.ldc % 8 != 0) return BTP_ERR_ALIGNMENT;
     if (q.splits < 1) return BTP_ERR_DIM;
@@ -365,9 +456,14 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     if (q.resid && (q.c_fp32 || q.ld_resid % 8)) return BTP_ERR_DIM;
     // split-K accumulates through TMA reduce-add into a zero-initialised fp32 output
     if (q.splits > 1 && !q.reduce_add) return BTP_ERR_DIM;
-    maxN = maxN > q.N ? maxN : q.N;
+    if (q.epilogue != kEpiStore && q.epilogue != kEpiSwigluBwd) return BTP_ERR_DIM;
+    if (q.epilogue == kEpiSwigluBwd &&
+        (!q.resid || !q.aux2 || !q.c2 || q.c_fp32 || q.splits > 1 || q.reduce_add || q.ld_aux2 % 8 || q.ldc2 % 8))
+      return BTP_ERR_DIM;
   }
-  const int BN = (bn_hint == 128 || bn_hint == 256) ? bn_hint : (maxN >= 256 ? 256 : 128);
+  int slots = 1;
+  for (int i = 0; i < n; ++i) slots = probs[i].epilogue == kEpiSwigluBwd ? 2 : slots;
+  const int BN = (bn_hint == 128 || bn_hint == 192 || bn_hint == 256) ? bn_hint : pick_bn(probs, n, num_sms_cached());
   DevParams P;
   memset(&P, 0, sizeof(P));
   int tiles = 0;
@@ -375,14 +471,28 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     const btp_gemm_problem& q = probs[i];
     DevProblem& d = P.prob[i];
     int rc;
-    if (!a_mn) rc = make_tmap(&d.tma_a, q.a, q.K, q.M, q.lda, kBK, kBM);
-    else       rc = make_tmap(&d.tma_a, q.a, q.M, q.K, q.lda, 64, kBK);
+    if (!q.a_mn) rc = make_tmap(&d.tma_a, q.a, q.K, q.M, q.lda, kBK, kBM);
+    else         rc = make_tmap(&d.tma_a, q.a, q.M, q.K, q.lda, 64, kBK);
     if (rc) return rc;
-    if (!b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN);
-    else       rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
+    if (!q.b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN);
+    else         rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
     if (rc) return rc;
+    d.a_mn = q.a_mn != 0;
+    d.b_mn = q.b_mn != 0;
+    d.idesc = make_idesc_bf16_f32(kBM, BN, d.a_mn, d.b_mn);
     rc = make_tmap(&d.tma_c, q.c, q.N, q.M, q.ldc, q.c_fp32 ? 32 : 64, 32, q.c_fp32 != 0);
     if (rc) return rc;
+    if (q.resid) {
+      rc = make_tmap(&d.tma_r, q.resid, q.N, q.M, q.ld_resid, 64, 32);
+      if (rc) return rc;
+    }
+    d.epi = q.epilogue;
+    if (q.epilogue == kEpiSwigluBwd) {
+      rc = make_tmap(&d.tma_r2, q.aux2, q.N, q.M, q.ld_aux2, 64, 32);
+      if (rc) return rc;
+      rc = make_tmap(&d.tma_c2, q.c2, q.N, q.M, q.ldc2, 64, 32);
+      if (rc) return rc;
+    }
     d.row_scale = q.row_scale;
     d.col_scale = q.col_scale;
     d.resid = reinterpret_cast<const __nv_bfloat16*>(q.resid);
@@ -403,17 +513,14 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
   P.total_tiles = tiles;
   int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (BN == 256) {
-    if (!a_mn && !b_mn) return launch<256, false, false>(P, grid, stream);
-    if (!a_mn && b_mn) return launch<256, false, true>(P, grid, stream);
-    if (a_mn && b_mn) return launch<256, true, true>(P, grid, stream);
-    return launch<256, true, false>(P, grid, stream);
-  } else {
-    if (!a_mn && !b_mn) return launch<128, false, false>(P, grid, stream);
-    if (!a_mn && b_mn) return launch<128, false, true>(P, grid, stream);
-    if (a_mn && b_mn) return launch<128, true, true>(P, grid, stream);
-    return launch<128, true, false>(P, grid, stream);
+  if (slots == 2) {
+    if (BN == 256) return launch<256, 2>(P, grid, stream);
+    if (BN == 192) return launch<192, 2>(P, grid, stream);
+    return launch<128, 2>(P, grid, stream);
   }
+  if (BN == 256) return launch<256, 1>(P, grid, stream);
+  if (BN == 192) return launch<192, 1>(P, grid, stream);
+  return launch<128, 1>(P, grid, stream);
 }
 
 }  // namespace btp

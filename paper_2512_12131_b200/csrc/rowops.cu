@@ -444,6 +444,31 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_prep_kernel(const bf16* dn, l
   if (lane == 0) dss[row] = -dot / (2.0f * s * s * s * (float)width);
 }
 
+// ----------------------------------------------------------------------------- column sums
+// out[c] (+)= scale[c] * sum_{s<S} in[s*lds + c]: 32 columns x 32 row-groups per block, rows
+// strided by 32, then a fixed-order tree over the row-groups in smem (deterministic).
+__global__ void __launch_bounds__(1024) colsum_kernel(const float* __restrict__ in, int S, long long lds, int C,
+                                                      const float* __restrict__ scale, float* __restrict__ out,
+                                                      int accumulate) {
+  __shared__ float red[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  float s = 0.f;
+  if (c < C)
+    for (int r = ty; r < S; r += 32) s += in[(long long)r * lds + c];
+  red[ty][tx] = s;
+  __syncthreads();
+  for (int w = 16; w > 0; w >>= 1) {
+    if (ty < w) red[ty][tx] += red[ty + w][tx];
+    __syncthreads();
+  }
+  if (ty == 0 && c < C) {
+    float v = red[0][tx];
+    if (scale) v *= scale[c];
+    out[c] = accumulate ? out[c] + v : v;
+  }
+}
+
 // ----------------------------------------------------------------------------- loss dot
 // partial[blk] = sum over this block's rows of <a_row, b_row>; fixed block/thread order.
 __global__ void __launch_bounds__(256) dot_kernel(const bf16* __restrict__ a, long long lda,
@@ -616,6 +641,10 @@ __global__ void __launch_bounds__(256) reduce_rows_scalar_kernel(const float* __
 int reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
                 const float* col_scale, float* out, long long ldo, int accumulate, cudaStream_t st) {
   if (rows <= 0 || cols <= 0 || splits <= 0) return BTP_ERR_DIM;
+  if (rows == 1 && splits >= 32) {  // many partial rows of one vector: parallel column sums
+    colsum_kernel<<<(cols + 31) / 32, 1024, 0, st>>>(in, splits, split_stride, cols, col_scale, out, accumulate);
+    BTP_CHECK_LAUNCH();
+  }
   if (cols % 4 || ldi % 4 || ldo % 4 || split_stride % 4 || !al16(in) || !al16(out) || (col_scale && !al16(col_scale))) {
     reduce_rows_scalar_kernel<<<grid_for((long long)rows * cols), 256, 0, st>>>(in, splits, split_stride, ldi, rows,
                                                                              cols, col_scale, out, ldo, accumulate);

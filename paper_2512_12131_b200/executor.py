@@ -72,6 +72,7 @@ class ExecutorBase:
 
     residual_sharded = True
     gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
+    fuse_swiglu_bwd = True          # SwiGLU backward in the dgrad GEMM epilogue (False: separate kernel)
 
     def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float):
         self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
@@ -108,17 +109,22 @@ class ExecutorBase:
     # ------------------------------------------------------------------ GEMM helpers
     def _gemm(self, *probs: K.Gemm) -> None:
         flops = 0
+        shapes = []
         for p in probs:
             M = p.a.shape[1] if p.a_mn else p.a.shape[0]
             Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
             N = p.b.shape[1] if p.b_mn else p.b.shape[0]
             flops += 2 * M * N * Kd
+            shapes.append((M, N, Kd, int(p.a_mn), int(p.b_mn), p.splits))
         if self.gemm_timer is not None:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # external=True: inside a CUDA-graph capture these become event-record nodes, so the
+            # timings are pure device time (no host launch gaps)
+            e0 = torch.cuda.Event(enable_timing=True, external=True)
+            e1 = torch.cuda.Event(enable_timing=True, external=True)
             e0.record()
             K.gemm(*probs)
             e1.record()
-            self.gemm_timer.append((e0, e1, flops))
+            self.gemm_timer.append((e0, e1, flops, shapes))
         else:
             K.gemm(*probs)
         self.stats.gemm_launches += 1
@@ -493,13 +499,17 @@ class BTPBlockExecutor(ExecutorBase):
         self._gemm(K.Gemm(dy, W["u_d"], da, b_mn=True))                       # da_d = dy @ Wu_d
         self._wgrad([(dy, S["a_d"][0], G["u_d"])])                             # dWu_d = dy^T a_d
         dP, _ = self._boundary_bwd(names, da, S["P_d"], None, "dss_d")
-        dact = self.buf("dact", (T, fl))
-        self._gemm(K.Gemm(dP, W["d_d"], dact, b_mn=True))                     # dact = dz_d @ Wd_d
-        self._wgrad([(dP, S["act"], G["d_d"])])                                # dWd_d = dz_d^T act
         gu = S["gu"]
         dgu = self.buf("dgu", (2, T, fl))
-        K.swiglu_bwd(gu[0], gu[1], dact, dgu[0], dgu[1])
-        self.stats.kernel_launches += 1
+        if self.fuse_swiglu_bwd:
+            # dact = dz_d @ Wd_d never leaves the GEMM: its epilogue emits dg and du directly
+            self._gemm(K.Gemm(dP, W["d_d"], dgu[0], b_mn=True, swiglu_bwd=(gu[0], gu[1], dgu[1])))
+        else:
+            dact = self.buf("dact", (T, fl))
+            self._gemm(K.Gemm(dP, W["d_d"], dact, b_mn=True))                 # dact = dz_d @ Wd_d
+            K.swiglu_bwd(gu[0], gu[1], dact, dgu[0], dgu[1])
+            self.stats.kernel_launches += 1
+        self._wgrad([(dP, S["act"], G["d_d"])])                                # dWd_d = dz_d^T act
         # ---------------- gate|up chunk
         names = ("gate", "up")
         da = self._da_buffer(names)

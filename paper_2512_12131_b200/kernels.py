@@ -63,6 +63,7 @@ class Gemm:
     splits: int = 1
     alpha: float = 1.0
     reduce_add: bool = False                # add into C (fp32, zeroed) via TMA reduce; needed for splits > 1
+    swiglu_bwd: tuple | None = None         # (g, u, du): acc = dact -> C = dg, du written too
 
     def to_c(self) -> GemmProblem:
         _check(self.a, BF16, "A")
@@ -80,6 +81,14 @@ class Gemm:
         if (self.splits > 1 or self.reduce_add) and not c_fp32:
             raise ValueError("split-K / reduce-add GEMMs need an fp32 output")
         split_stride = 0
+        resid, epilogue, aux2, c2 = self.resid, 0, None, None
+        if self.swiglu_bwd is not None:
+            g, u, du = self.swiglu_bwd
+            for t, nm in ((g, "g"), (u, "u"), (du, "du")):
+                _check(t, BF16, nm)
+                if tuple(t.shape) != (M, N):
+                    raise ValueError(f"swiglu-bwd operand {nm} {tuple(t.shape)} != ({M}, {N})")
+            resid, epilogue, aux2, c2 = g, 2, u, du
         return GemmProblem(
             a=self.a.data_ptr(), lda=_ld(self.a), a_mn=int(self.a_mn),
             b=self.b.data_ptr(), ldb=_ld(self.b), b_mn=int(self.b_mn),
@@ -87,10 +96,13 @@ class Gemm:
             M=M, N=N, K=K,
             row_scale=None if self.row_scale is None else self.row_scale.data_ptr(),
             col_scale=None if self.col_scale is None else self.col_scale.data_ptr(),
-            resid=None if self.resid is None else self.resid.data_ptr(),
-            ld_resid=_ld(self.resid),
+            resid=None if resid is None else resid.data_ptr(),
+            ld_resid=_ld(resid),
             splits=self.splits, split_stride=split_stride, alpha=float(self.alpha),
             reduce_add=int(self.reduce_add or self.splits > 1),
+            epilogue=epilogue,
+            aux2=None if aux2 is None else aux2.data_ptr(), ld_aux2=_ld(aux2),
+            c2=None if c2 is None else c2.data_ptr(), ldc2=_ld(c2),
         )
 
 

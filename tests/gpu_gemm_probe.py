@@ -37,7 +37,7 @@ def run(M, N, Kd, a_mn, b_mn, bn=0, out=torch.bfloat16, splits=1, rs=False, cs=F
 bad = 0
 for (M, N, Kd) in [(128, 128, 64), (256, 256, 128), (296, 200, 72), (1024, 512, 512), (2048, 1536, 2048)]:
     for a_mn, b_mn in [(False, False), (False, True), (True, True), (True, False)]:
-        for bn in (128, 256):
+        for bn in (128, 192, 256):
             e = run(M, N, Kd, a_mn, b_mn, bn)
             bad += e > 1e-2
 e = run(1000, 640, 512, False, False, 0, out=torch.float32, rs=True, cs=True); bad += e > 1e-2
@@ -51,6 +51,16 @@ K.gemm(*[K.Gemm(a, b, c) for a, b, c in zip(A, B, C)])
 torch.cuda.synchronize()
 for a, b, c in zip(A, B, C):
     e = rel(c, a.float() @ b.float().t()); print("grouped", e); bad += e > 1e-2
+# mixed majors in one launch: a dgrad-like (K, MN) problem + a split-K wgrad-like (MN, MN) problem
+dY = torch.randn(4096, 1024, device=dev).bfloat16()
+W = torch.randn(1024, 512, device=dev).bfloat16()      # [K=1024, N=512] -> MN-major B
+X = torch.randn(4096, 512, device=dev).bfloat16()
+dA = torch.empty(4096, 512, device=dev).bfloat16()
+dW = torch.empty(1024, 512, device=dev); K.zero(dW)
+K.gemm(K.Gemm(dY, W, dA, b_mn=True), K.Gemm(dY, X, dW, a_mn=True, b_mn=True, splits=4))
+torch.cuda.synchronize()
+e1 = rel(dA, dY.float() @ W.float()); e2 = rel(dW, dY.float().t() @ X.float())
+print("mixed-major dgrad", e1, "wgrad", e2); bad += (e1 > 1e-2) + (e2 > 1e-2)
 # timing
 for (M, N, Kd) in [(16384, 2048, 512), (16384, 1536, 2048), (8192, 8192, 8192)]:
     A = torch.randn(M, Kd, device=dev).bfloat16(); B = torch.randn(N, Kd, device=dev).bfloat16()

@@ -1,0 +1,97 @@
+"""tcgen05 GEMM kernel (libbtp.so `btp_gemm`) against a torch fp32 reference of the same op:
+every operand-major combination and N tile, grouped launches, mixed majors in one launch,
+split-K via TMA reduce-add, row/col scales, the TMA residual epilogue and the fused SwiGLU
+backward epilogue. bf16 inputs, fp32 accumulation: tolerance 1e-2 relative Frobenius."""
+
+import pytest
+import torch
+
+from paper_2512_12131_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+def rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+def _mk(*shape):
+    return torch.randn(*shape, device="cuda").bfloat16()
+
+
+@pytest.mark.parametrize("M,N,Kd", [(128, 128, 64), (296, 200, 72), (1024, 512, 512), (2048, 1536, 2048)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
+@pytest.mark.parametrize("bn", [128, 192, 256])
+def test_layouts(M, N, Kd, a_mn, b_mn, bn):
+    A, B = _mk(M, Kd), _mk(N, Kd)
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(K.Gemm(A.t().contiguous() if a_mn else A, B.t().contiguous() if b_mn else B, C, a_mn=a_mn, b_mn=b_mn),
+           bn=bn)
+    assert rel(C, A.float() @ B.float().t()) < TOL
+
+
+def test_scales_fp32_out_and_residual():
+    A, B = _mk(1000, 512), _mk(640, 512)
+    row = torch.rand(1000, device="cuda") + 0.5
+    col = torch.rand(640, device="cuda") + 0.5
+    C = torch.empty(1000, 640, device="cuda")
+    K.gemm(K.Gemm(A, B, C, row_scale=row, col_scale=col))
+    assert rel(C, (A.float() @ B.float().t()) * row[:, None] * col[None, :]) < 1e-5
+    R = _mk(1000, 640)
+    Cb = torch.empty(1000, 640, device="cuda", dtype=torch.bfloat16)
+    K.gemm(K.Gemm(A, B, Cb, resid=R))
+    assert rel(Cb, A.float() @ B.float().t() + R.float()) < TOL
+    # residual aliasing the output (in-place accumulate, used by chained dgrads)
+    K.gemm(K.Gemm(A, B, Cb, resid=Cb))
+    assert rel(Cb, 2 * (A.float() @ B.float().t()) + R.float()) < TOL
+
+
+@pytest.mark.parametrize("splits", [2, 4, 9])
+def test_split_k_reduce_add(splits):
+    dY, X = _mk(4096, 512), _mk(4096, 2048)
+    dW = torch.empty(512, 2048, device="cuda")
+    K.zero(dW)
+    cs = torch.rand(2048, device="cuda") + 0.5
+    K.gemm(K.Gemm(dY, X, dW, a_mn=True, b_mn=True, splits=splits, col_scale=cs))
+    assert rel(dW, (dY.float().t() @ X.float()) * cs[None, :]) < 1e-5
+
+
+def test_grouped_and_mixed_majors():
+    A = [_mk(2048, 512) for _ in range(3)]
+    B = [_mk(768, 512) for _ in range(3)]
+    C = [torch.empty(2048, 768, device="cuda", dtype=torch.bfloat16) for _ in range(3)]
+    K.gemm(*[K.Gemm(a, b, c) for a, b, c in zip(A, B, C)])
+    for a, b, c in zip(A, B, C):
+        assert rel(c, a.float() @ b.float().t()) < TOL
+    dY, W, X = _mk(4096, 1024), _mk(1024, 512), _mk(4096, 512)
+    dA = torch.empty(4096, 512, device="cuda", dtype=torch.bfloat16)
+    dW = torch.empty(1024, 512, device="cuda")
+    K.zero(dW)
+    K.gemm(K.Gemm(dY, W, dA, b_mn=True), K.Gemm(dY, X, dW, a_mn=True, b_mn=True, splits=4))
+    assert rel(dA, dY.float() @ W.float()) < TOL
+    assert rel(dW, dY.float().t() @ X.float()) < 1e-5
+
+
+@pytest.mark.parametrize("N", [640, 5472])
+def test_swiglu_bwd_epilogue(N):
+    T, r = 1024, 512
+    dP, Wd = _mk(T, r), _mk(r, N)          # dact = dP @ Wd  (B operand MN-major)
+    g, u = _mk(T, N), _mk(T, N)
+    dg = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+    du = torch.empty_like(dg)
+    K.gemm(K.Gemm(dP, Wd, dg, b_mn=True, swiglu_bwd=(g, u, du)))
+    dact = dP.float() @ Wd.float()
+    gf, uf = g.float(), u.float()
+    sg = torch.sigmoid(gf)
+    assert rel(dg, dact * uf * sg * (1 + gf * (1 - sg))) < TOL
+    assert rel(du, dact * gf * sg) < TOL
+
+
+def test_rejects_misaligned():
+    A, B = _mk(64, 60), _mk(64, 60)
+    C = torch.empty(64, 64, device="cuda", dtype=torch.bfloat16)
+    from paper_2512_12131_b200._native import NativeError
+
+    with pytest.raises(NativeError):
+        K.gemm(K.Gemm(A, B, C))
