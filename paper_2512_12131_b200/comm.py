@@ -47,6 +47,19 @@ class TPComm:
         self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
         return buf
 
+    def all_reduce_start(self, buf: torch.Tensor, chunk_id: str, tag: str = "block"):
+        """Asynchronous in-place all-reduce: NCCL runs on its own stream (ordered after the work
+        already queued on the current stream) while the caller keeps launching independent
+        kernels; `wait(handle)` orders the current stream after the reduction."""
+        work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True) if self.tp > 1 else None
+        self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
+        return work
+
+    @staticmethod
+    def wait(handle) -> None:
+        if handle is not None:
+            handle.wait()
+
     def all_reduce_coalesced(self, main: torch.Tensor, stat: torch.Tensor, chunk_id: str,
                              tag: str = "block", stat_tag: str = "fused-stat"):
         if self.tp > 1:

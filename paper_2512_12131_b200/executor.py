@@ -72,7 +72,7 @@ class ExecutorBase:
 
     residual_sharded = True
     gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
-    fuse_swiglu_bwd = True          # SwiGLU backward in the dgrad GEMM epilogue (False: separate kernel)
+    fuse_swiglu_bwd = False         # SwiGLU backward in the dgrad GEMM epilogue (False: separate kernel)
 
     def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float):
         self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
@@ -427,20 +427,36 @@ class BTPBlockExecutor(ExecutorBase):
         S.update(a_qkv=a_qkv, qkv=qkv, attn=attn, actx=actx)
 
     # ------------------------------------------------------------------ backward pieces
-    def _boundary_bwd(self, names, da_P, zP, s, dss_name):
-        """AR of the up-projection input grads, then sigma-bwd (+ norm-bwd prologue) in place.
+    def _up_bwd(self, names, dgrad_probs, wgrad_pairs, da_P, zP, s, dss_name):
+        """Backward of one chunk boundary: dgrad of the up-projection(s) into da_P, then the rank-r
+        all-reduce of da_P started asynchronously (NCCL's stream) while the independent weight
+        gradient GEMM runs, then sigma-bwd (+ norm-bwd prologue) in place once the sum landed.
         zP is the stored z (= all-reduce buffer of the forward): [T, k*r] grouped, [k, T, r] not."""
+        if self.grouping or len(dgrad_probs) == 1:
+            self._gemm(*dgrad_probs)
+        else:
+            for p in dgrad_probs:
+                self._gemm(p)
+        k = len(names)
+        if self.grouping or k == 1:
+            handles = [self.comm.all_reduce_start(da_P, names[0] if k == 1 else self._gid(names))]
+        else:
+            handles = [self.comm.all_reduce_start(da_P[i], nm) for i, nm in enumerate(names)]
+        self._wgrad(wgrad_pairs)
+        for h in handles:
+            self.comm.wait(h)
+        return self._sigma_bwd(names, da_P, zP, s, dss_name)
+
+    def _sigma_bwd(self, names, da_P, zP, s, dss_name):
         k, r, T = len(names), self.r, self.T
         if self.grouping or k == 1:
-            self.comm.all_reduce(da_P, names[0] if k == 1 else self._gid(names))
             dss = self.buf(dss_name, (T,), F32) if s is not None else None
             K.fixup_sigma_bwd(zP, da_P, da_P, r=r, nproj=k, variant=self.var, s=s, d=self.d, dss=dss)
             self.stats.kernel_launches += 1
             return da_P, dss
-        # ungrouped: one AR per projection; the norm statistic gradient sums over projections
+        # ungrouped: the norm statistic gradient sums over the projections
         parts = self.buf(f"{dss_name}_parts", (k, 1, T), F32) if s is not None else None
-        for i, nm in enumerate(names):
-            self.comm.all_reduce(da_P[i], nm)
+        for i in range(k):
             K.fixup_sigma_bwd(zP[i], da_P[i], da_P[i], r=r, nproj=1, variant=self.var, s=s, d=self.d,
                               dss=None if parts is None else parts[i, 0])
             self.stats.kernel_launches += 1
@@ -496,9 +512,9 @@ class BTPBlockExecutor(ExecutorBase):
         # ---------------- mlp down chunk: y = x_mid + a_d @ Wu_d^T
         names = ("down",)
         da = self._da_buffer(names)
-        self._gemm(K.Gemm(dy, W["u_d"], da, b_mn=True))                       # da_d = dy @ Wu_d
-        self._wgrad([(dy, S["a_d"][0], G["u_d"])])                             # dWu_d = dy^T a_d
-        dP, _ = self._boundary_bwd(names, da, S["P_d"], None, "dss_d")
+        dP, _ = self._up_bwd(names, [K.Gemm(dy, W["u_d"], da, b_mn=True)],    # da_d = dy @ Wu_d
+                             [(dy, S["a_d"][0], G["u_d"])],                     # dWu_d = dy^T a_d
+                             da, S["P_d"], None, "dss_d")
         gu = S["gu"]
         dgu = self.buf("dgu", (2, T, fl))
         if self.fuse_swiglu_bwd:
@@ -514,14 +530,9 @@ class BTPBlockExecutor(ExecutorBase):
         names = ("gate", "up")
         da = self._da_buffer(names)
         dav = self._da_views(names, da)
-        probs = [K.Gemm(dgu[i], W["u_gu"][i], dav[i], b_mn=True) for i in range(2)]
-        if self.grouping:
-            self._gemm(*probs)
-        else:
-            for p in probs:
-                self._gemm(p)
-        self._wgrad([(dgu[i], S["a_gu"][i], G["u_gu"][i]) for i in range(2)])
-        dP, dss2 = self._boundary_bwd(names, da, S["P_gu"], S["s2"], "dss2")
+        dP, dss2 = self._up_bwd(names, [K.Gemm(dgu[i], W["u_gu"][i], dav[i], b_mn=True) for i in range(2)],
+                                [(dgu[i], S["a_gu"][i], G["u_gu"][i]) for i in range(2)],
+                                da, S["P_gu"], S["s2"], "dss2")
         dx_mid = self.buf("dx_mid", (T, dl))
         self._down_bwd(names, dP, W["d_gu"], S["x_mid"], self.gamma2, dy, dx_mid, dss2, "d_gu", "gamma2")
         # ---------------- attention o chunk: x_mid = x + a_o @ Wu_o^T
@@ -530,9 +541,8 @@ class BTPBlockExecutor(ExecutorBase):
             self.comm.pass_tag = "backward"
         names = ("o",)
         da = self._da_buffer(names)
-        self._gemm(K.Gemm(dx_mid, W["u_o"], da, b_mn=True))
-        self._wgrad([(dx_mid, S["a_o"][0], G["u_o"])])
-        dP, _ = self._boundary_bwd(names, da, S["P_o"], None, "dss_o")
+        dP, _ = self._up_bwd(names, [K.Gemm(dx_mid, W["u_o"], da, b_mn=True)], [(dx_mid, S["a_o"][0], G["u_o"])],
+                             da, S["P_o"], None, "dss_o")
         dattn = self.buf("dattn", (T, dl))
         self._gemm(K.Gemm(dP, W["d_o"], dattn, b_mn=True))
         self._wgrad([(dP, S["attn"], G["d_o"])])
@@ -542,14 +552,9 @@ class BTPBlockExecutor(ExecutorBase):
         da = self._da_buffer(names)
         dav = self._da_views(names, da)
         dqkv = (dq, dk, dv)
-        probs = [K.Gemm(dqkv[i], W["u_qkv"][i], dav[i], b_mn=True) for i in range(3)]
-        if self.grouping:
-            self._gemm(*probs)
-        else:
-            for p in probs:
-                self._gemm(p)
-        self._wgrad([(dqkv[i], S["a_qkv"][i], G["u_qkv"][i]) for i in range(3)])
-        dP, dss1 = self._boundary_bwd(names, da, S["P_qkv"], S["s1"], "dss1")
+        dP, dss1 = self._up_bwd(names, [K.Gemm(dqkv[i], W["u_qkv"][i], dav[i], b_mn=True) for i in range(3)],
+                                [(dqkv[i], S["a_qkv"][i], G["u_qkv"][i]) for i in range(3)],
+                                da, S["P_qkv"], S["s1"], "dss1")
         dx = self.buf("dx", (T, dl))
         self._down_bwd(names, dP, W["d_qkv"], S["x"], self.gamma1, dx_mid, dx, dss1, "d_qkv", "gamma1")
         return dx
