@@ -151,6 +151,39 @@ int btp_add(const void* a, long long lda, const void* b, long long ldb, void* ou
 int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
             int max_blocks, int* nblk, void* stream);
 
+/* ---- fp32 parity mode ------------------------------------------------------------------
+ * The north_star's fp32 tolerance (1e-4 relative) cannot be met with single-pass TF32, so the
+ * fp32 mode runs exact-fp32 CUDA kernels: a SIMT FFMA GEMM over the same problem descriptor
+ * (A/B/C/resid fp32; epilogue 0 only; split-K computed in one pass, reduce_add honoured) and
+ * fp32-activation twins of every row kernel (same arguments, T = float instead of bf16). */
+int btp_gemm_f32(const btp_gemm_problem* problems, int n, void* stream);
+int btp_rmsnorm_residual_f32(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
+                             long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
+                             float* rms_loc_out, int rows, int width, float eps, void* stream);
+int btp_rmsnorm_apply_f32(const void* x, long long ldx, const float* gamma, const float* ss_total, int d,
+                          float eps, void* n_out, long long ldn, float* rms_out, int rows, int width, void* stream);
+int btp_fixup_sigma_f32(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                        void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj,
+                        int variant, void* stream);
+int btp_swiglu_f32(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows,
+                   int cols, void* stream);
+int btp_swiglu_bwd_f32(const void* g, long long ldg, const void* u, long long ldu, const void* dact,
+                       long long ldda, void* dg, long long lddg, void* du, long long lddu, int rows, int cols,
+                       void* stream);
+int btp_fixup_sigma_bwd_f32(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d,
+                            void* dP, long long lddp, float* dss, int rows, int r, int nproj, int variant,
+                            void* stream);
+int btp_rmsnorm_bwd_f32(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma,
+                        const float* dss, const void* dres, long long ldr, void* dx, long long lddx,
+                        float* dgamma_partial, int max_blocks, int* nblk, int rows, int width, void* stream);
+int btp_rmsnorm_bwd_prep_f32(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                             const float* s, void* dh, long long lddh, float* dss, int rows, int width,
+                             void* stream);
+int btp_add_f32(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows,
+                int cols, void* stream);
+int btp_dot_f32(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
+                int max_blocks, int* nblk, void* stream);
+
 /* Zero `bytes` bytes of device memory on the stream (split-K reduce-add targets). */
 int btp_zero(void* ptr, long long bytes, void* stream);
 

@@ -43,6 +43,18 @@ EXPORTED_SYMBOLS = (
     "btp_zero",
     "btp_num_sms",
     "btp_version",
+    # fp32 parity-mode twins
+    "btp_gemm_f32",
+    "btp_rmsnorm_residual_f32",
+    "btp_rmsnorm_apply_f32",
+    "btp_fixup_sigma_f32",
+    "btp_swiglu_f32",
+    "btp_swiglu_bwd_f32",
+    "btp_fixup_sigma_bwd_f32",
+    "btp_rmsnorm_bwd_f32",
+    "btp_rmsnorm_bwd_prep_f32",
+    "btp_add_f32",
+    "btp_dot_f32",
 )
 
 
@@ -107,7 +119,11 @@ _SIGNATURES = {
     "btp_zero": [_P, _LL, _P],
     "btp_num_sms": [],
     "btp_version": [],
+    "btp_gemm_f32": [ctypes.POINTER(GemmProblem), _I, _P],
 }
+for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
+              "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot"):
+    _SIGNATURES[_name + "_f32"] = _SIGNATURES[_name]
 
 _lib = None
 _lock = threading.Lock()

@@ -65,16 +65,16 @@ def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
 
 
 def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
-                  device=None, attn_backend: str = "auto"):
+                  device=None, attn_backend: str = "auto", precision: str = "bf16"):
     """Build this rank's executor for the plan's strategy."""
     comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:
-        return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend)
+        return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)
     from .baselines import FullRankExecutor, VanillaExecutor
 
     cls = VanillaExecutor if pl.strategy is Strategy.VANILLA else FullRankExecutor
-    return cls(pl, block, comm, dev, eps, attn_backend)
+    return cls(pl, block, comm, dev, eps, attn_backend, precision)
 
 
 def shard_input(ex, xv: np.ndarray) -> torch.Tensor:
@@ -84,7 +84,7 @@ def shard_input(ex, xv: np.ndarray) -> torch.Tensor:
     if getattr(ex, "residual_sharded", True):
         lo = ex.rank * ex.dl
         x2 = x2[:, lo:lo + ex.dl]
-    return torch.from_numpy(np.ascontiguousarray(x2)).to(ex.dev, BF16)
+    return torch.from_numpy(np.ascontiguousarray(x2)).to(ex.dev, ex.act)
 
 
 def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
@@ -102,12 +102,12 @@ def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
 
 def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *, eps: float = EPS_DEFAULT,
                     model_tail: bool = False, trace: Trace | None = None, capture_workspaces: bool = False,
-                    attn_backend: str = "auto") -> SimResult:
+                    attn_backend: str = "auto", precision: str = "bf16") -> SimResult:
     """Run one block forward under the plan on the GPU; returns the gathered logical y."""
     if h_prev is not None and block.variant is Variant.LAX:
         raise PlanError("the lax variant is outside the device path (SURVEY §2.1: out of scope)")
     xv = _check_inputs(pl, block, x)
-    ex = make_executor(pl, block, eps=eps, trace=trace, attn_backend=attn_backend)
+    ex = make_executor(pl, block, eps=eps, trace=trace, attn_backend=attn_backend, precision=precision)
     x_sh = shard_input(ex, xv)
     y_sh = ex.forward(x_sh)
     y = _gather_y(ex, y_sh, model_tail)
@@ -121,7 +121,7 @@ def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *
 
 
 def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: float = EPS_DEFAULT,
-               attn_backend: str = "auto", executor=None) -> StepResult:
+               attn_backend: str = "auto", executor=None, precision: str = "bf16") -> StepResult:
     """Forward + backward of the block for the builder-defined loss L = sum(y * G) (dL/dy = G).
 
     G defaults to the loss projection seeded_fill((b, s, d), 30000)."""
@@ -132,7 +132,8 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
     if G is None:
         G = seeded_fill((b, s, d), 30000).values
     Gv = G.values if isinstance(G, Tensor) else np.asarray(G)
-    ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend)
+    ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
+                                                             precision=precision)
     x_sh = shard_input(ex, xv)
     g_sh = shard_input(ex, Gv)
     y_sh = ex.forward(x_sh)

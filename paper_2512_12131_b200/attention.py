@@ -19,6 +19,8 @@ _BACKENDS = {
     "auto": [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION],
     "cudnn": [SDPBackend.CUDNN_ATTENTION],
     "flash": [SDPBackend.FLASH_ATTENTION],
+    # parity mode: fp32 q/k/v (cuDNN / flash are 16-bit only); exact fp32 GEMM softmax path
+    "fp32": [SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH],
 }
 
 

@@ -52,19 +52,20 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
     residual_sharded = False
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None, device="cuda",
-                 eps: float = 1e-6, attn_backend: str = "auto"):
+                 eps: float = 1e-6, attn_backend: str = "auto", precision: str = "bf16"):
         if pl.strategy is not Strategy.VANILLA:
             raise PlanError(f"VanillaExecutor needs a vanilla plan, got {pl.strategy.value}")
         if block.variant is not pl.variant or pl.variant not in _VAR:
             raise PlanError(f"vanilla device path supports svd/cola blocks matching the plan")
-        self._setup(pl, comm, device, eps)
+        self._setup(pl, comm, device, eps, precision)
         cfg = self.cfg
         self.var = _VAR[pl.variant]
         self.grouping = pl.grouping
         self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
         self.rl = cfg.r // self.tp
         self.dl = cfg.d  # replicated residual
-        self.attn = Attention(pl.shape.b, pl.shape.s, cfg.heads, cfg.head_dim, attn_backend)
+        self.attn = Attention(pl.shape.b, pl.shape.s, cfg.heads, cfg.head_dim,
+                              "fp32" if precision == "fp32" else attn_backend)
         if pl.variant is Variant.COLA:
             idx = cola_pair_indices(cfg.r, self.tp, self.rank)
         else:
@@ -225,15 +226,16 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
     residual_sharded = False
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None, device="cuda",
-                 eps: float = 1e-6, attn_backend: str = "auto"):
+                 eps: float = 1e-6, attn_backend: str = "auto", precision: str = "bf16"):
         if pl.strategy is not Strategy.FULL_RANK or block.variant is not Variant.FULL_RANK:
             raise PlanError("FullRankExecutor needs a full-rank plan and block")
-        self._setup(pl, comm, device, eps)
+        self._setup(pl, comm, device, eps, precision)
         cfg, tp, rk = self.cfg, self.tp, self.rank
         self.grouping = pl.grouping
         self.d, self.d_ff = cfg.d, cfg.d_ff
         self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
-        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim, attn_backend)
+        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
+                              "fp32" if precision == "fp32" else attn_backend)
         sl, fsl = slice(rk * self.dl, (rk + 1) * self.dl), slice(rk * self.fl, (rk + 1) * self.fl)
         Wf = {n: t.values for n, t in block.full.items()}
         self.W = {

@@ -6,28 +6,32 @@
 namespace btp {
 int num_sms_cached();
 int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream);
+int gemm_f32_launch(const btp_gemm_problem* probs, int n, cudaStream_t stream);
+// f32 = false: bf16 activations (training path); true: fp32 activations (parity mode)
 int rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out, long long ldo,
                      const float* gamma, void* n_out, long long ldn, float* ss_out, float* rl_out, int rows,
-                     int width, float eps, cudaStream_t st);
+                     int width, float eps, cudaStream_t st, bool f32);
 int rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps,
-                  void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st);
+                  void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st, bool f32);
 int fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out, void* z_out,
-                long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, cudaStream_t st);
+                long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, cudaStream_t st,
+                bool f32);
 int fixup_sigma_bwd(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d, void* dP,
-                    long long lddp, float* dss, int rows, int r, int nproj, int variant, cudaStream_t st);
+                    long long lddp, float* dss, int rows, int r, int nproj, int variant, cudaStream_t st, bool f32);
 int swiglu(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows, int cols,
-           cudaStream_t st);
+           cudaStream_t st, bool f32);
 int swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, const void* dact, long long ldda,
-               void* dg, long long lddg, void* du, long long lddu, int rows, int cols, cudaStream_t st);
+               void* dg, long long lddg, void* du, long long lddu, int rows, int cols, cudaStream_t st, bool f32);
 int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma, const float* dss,
                 const void* dres, long long ldr, void* dx, long long lddx, float* dgamma_partial, int max_blocks,
-                int* nblk_out, int rows, int width, cudaStream_t st);
+                int* nblk_out, int rows, int width, cudaStream_t st, bool f32);
+int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
+                     const float* s, void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st,
+                     bool f32);
 int reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
                 const float* col_scale, float* out, long long ldo, int accumulate, cudaStream_t st);
 int add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows, int cols,
-        cudaStream_t st);
-int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
-                     const float* s, void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st);
+        cudaStream_t st, bool f32);
 int dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
-        int max_blocks, int* nblk_out, cudaStream_t st);
+        int max_blocks, int* nblk_out, cudaStream_t st, bool f32);
 }  // namespace btp

@@ -1,5 +1,6 @@
 // extern "C" boundary of libbtp.so: argument marshalling only; every entry point forwards
-// to the kernels in gemm.cu / rowops.cu on the caller's stream. See include/btp.h.
+// to the kernels in gemm.cu / gemm_f32.cu / rowops.cu on the caller's stream. See include/btp.h.
+// The *_f32 twins take fp32 activations (parity mode); everything else is bf16.
 #include <cuda_runtime.h>
 
 #include "btp_internal.h"
@@ -18,72 +19,88 @@ int num_sms_cached() {
 
 #define ST(s) static_cast<cudaStream_t>(s)
 
+// Defines NAME (bf16) and NAME_f32 (fp32) for a row kernel whose last two internal args are (stream, f32).
+#define BTP_PAIR(NAME, IMPL, PARAMS, ARGS)                                             \
+  int NAME PARAMS { return btp::IMPL ARGS(false); }                                    \
+  int NAME##_f32 PARAMS { return btp::IMPL ARGS(true); }
+
 extern "C" {
 
 int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream) {
   return btp::gemm_launch(problems, n, bn_hint, 0, ST(stream));
 }
 
-int btp_rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
-                         long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
-                         float* rms_loc_out, int rows, int width, float eps, void* stream) {
-  return btp::rmsnorm_residual(x, ldx, branch, ldb, x_out, ldo, gamma, n_out, ldn, ss_out, rms_loc_out, rows, width,
-                               eps, ST(stream));
+int btp_gemm_f32(const btp_gemm_problem* problems, int n, void* stream) {
+  return btp::gemm_f32_launch(problems, n, ST(stream));
 }
 
-int btp_rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps,
-                      void* n_out, long long ldn, float* rms_out, int rows, int width, void* stream) {
-  return btp::rmsnorm_apply(x, ldx, gamma, ss_total, d, eps, n_out, ldn, rms_out, rows, width, ST(stream));
-}
+#define A_RMSNORM_RESIDUAL(f32) \
+  (x, ldx, branch, ldb, x_out, ldo, gamma, n_out, ldn, ss_out, rms_loc_out, rows, width, eps, ST(stream), f32)
+BTP_PAIR(btp_rmsnorm_residual, rmsnorm_residual,
+         (const void* x, long long ldx, const void* branch, long long ldb, void* x_out, long long ldo,
+          const float* gamma, void* n_out, long long ldn, float* ss_out, float* rms_loc_out, int rows, int width,
+          float eps, void* stream),
+         A_RMSNORM_RESIDUAL)
 
-int btp_fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
-                    void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj,
-                    int variant, void* stream) {
-  return btp::fixup_sigma(P, ldp, ss_total, d, eps, s_out, z_out, ldz, a_out, lda, rows, r, nproj, variant,
-                          ST(stream));
-}
+#define A_RMSNORM_APPLY(f32) (x, ldx, gamma, ss_total, d, eps, n_out, ldn, rms_out, rows, width, ST(stream), f32)
+BTP_PAIR(btp_rmsnorm_apply, rmsnorm_apply,
+         (const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps, void* n_out,
+          long long ldn, float* rms_out, int rows, int width, void* stream),
+         A_RMSNORM_APPLY)
 
-int btp_swiglu(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows,
-               int cols, void* stream) {
-  return btp::swiglu(g, ldg, u, ldu, act, lda, rows, cols, ST(stream));
-}
+#define A_FIXUP(f32) (P, ldp, ss_total, d, eps, s_out, z_out, ldz, a_out, lda, rows, r, nproj, variant, ST(stream), f32)
+BTP_PAIR(btp_fixup_sigma, fixup_sigma,
+         (const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out, void* z_out,
+          long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, void* stream),
+         A_FIXUP)
 
-int btp_swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, const void* dact, long long ldda,
-                   void* dg, long long lddg, void* du, long long lddu, int rows, int cols, void* stream) {
-  return btp::swiglu_bwd(g, ldg, u, ldu, dact, ldda, dg, lddg, du, lddu, rows, cols, ST(stream));
-}
+#define A_SWIGLU(f32) (g, ldg, u, ldu, act, lda, rows, cols, ST(stream), f32)
+BTP_PAIR(btp_swiglu, swiglu,
+         (const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows, int cols,
+          void* stream),
+         A_SWIGLU)
 
-int btp_fixup_sigma_bwd(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d,
-                        void* dP, long long lddp, float* dss, int rows, int r, int nproj, int variant,
-                        void* stream) {
-  return btp::fixup_sigma_bwd(z, ldz, da, ldda, s, d, dP, lddp, dss, rows, r, nproj, variant, ST(stream));
-}
+#define A_SWIGLU_BWD(f32) (g, ldg, u, ldu, dact, ldda, dg, lddg, du, lddu, rows, cols, ST(stream), f32)
+BTP_PAIR(btp_swiglu_bwd, swiglu_bwd,
+         (const void* g, long long ldg, const void* u, long long ldu, const void* dact, long long ldda, void* dg,
+          long long lddg, void* du, long long lddu, int rows, int cols, void* stream),
+         A_SWIGLU_BWD)
 
-int btp_rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma,
-                    const float* dss, const void* dres, long long ldr, void* dx, long long lddx,
-                    float* dgamma_partial, int max_blocks, int* nblk, int rows, int width, void* stream) {
-  return btp::rmsnorm_bwd(dh, lddh, x, ldx, gamma, dss, dres, ldr, dx, lddx, dgamma_partial, max_blocks, nblk, rows,
-                          width, ST(stream));
-}
+#define A_FIXUP_BWD(f32) (z, ldz, da, ldda, s, d, dP, lddp, dss, rows, r, nproj, variant, ST(stream), f32)
+BTP_PAIR(btp_fixup_sigma_bwd, fixup_sigma_bwd,
+         (const void* z, long long ldz, const void* da, long long ldda, const float* s, int d, void* dP,
+          long long lddp, float* dss, int rows, int r, int nproj, int variant, void* stream),
+         A_FIXUP_BWD)
+
+#define A_NORM_BWD(f32) \
+  (dh, lddh, x, ldx, gamma, dss, dres, ldr, dx, lddx, dgamma_partial, max_blocks, nblk, rows, width, ST(stream), f32)
+BTP_PAIR(btp_rmsnorm_bwd, rmsnorm_bwd,
+         (const void* dh, long long lddh, const void* x, long long ldx, const float* gamma, const float* dss,
+          const void* dres, long long ldr, void* dx, long long lddx, float* dgamma_partial, int max_blocks, int* nblk,
+          int rows, int width, void* stream),
+         A_NORM_BWD)
+
+#define A_NORM_PREP(f32) (dn, lddn, x, ldx, gamma, s, dh, lddh, dss, rows, width, ST(stream), f32)
+BTP_PAIR(btp_rmsnorm_bwd_prep, rmsnorm_bwd_prep,
+         (const void* dn, long long lddn, const void* x, long long ldx, const float* gamma, const float* s, void* dh,
+          long long lddh, float* dss, int rows, int width, void* stream),
+         A_NORM_PREP)
+
+#define A_ADD(f32) (a, lda, b, ldb, out, ldo, rows, cols, ST(stream), f32)
+BTP_PAIR(btp_add, add,
+         (const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows, int cols,
+          void* stream),
+         A_ADD)
+
+#define A_DOT(f32) (a, lda, b, ldb, rows, cols, partial, max_blocks, nblk, ST(stream), f32)
+BTP_PAIR(btp_dot, dot,
+         (const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
+          int max_blocks, int* nblk, void* stream),
+         A_DOT)
 
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
                     const float* col_scale, float* out, long long ldo, int accumulate, void* stream) {
   return btp::reduce_rows(in, splits, split_stride, ldi, rows, cols, col_scale, out, ldo, accumulate, ST(stream));
-}
-
-int btp_add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows,
-            int cols, void* stream) {
-  return btp::add(a, lda, b, ldb, out, ldo, rows, cols, ST(stream));
-}
-
-int btp_rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
-                         const float* s, void* dh, long long lddh, float* dss, int rows, int width, void* stream) {
-  return btp::rmsnorm_bwd_prep(dn, lddn, x, ldx, gamma, s, dh, lddh, dss, rows, width, ST(stream));
-}
-
-int btp_dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
-            int max_blocks, int* nblk, void* stream) {
-  return btp::dot(a, lda, b, ldb, rows, cols, partial, max_blocks, nblk, ST(stream));
 }
 
 int btp_zero(void* ptr, long long bytes, void* stream) {

@@ -1,9 +1,10 @@
 // HBM-bound row/elementwise kernels of the BTP block: online RMSNorm + residual (K3),
 // post-all-reduce fix-up + crossgate sigma (K4), SwiGLU (K5), and their backward passes.
 //
-// All loads/stores are 128-bit (8 x bf16); statistics and math are fp32. Row reductions
-// use one warp per row with shuffle reductions (no shared memory, no atomics), so every
-// result is deterministic.
+// Every kernel is templated on the activation element type T: bf16 (the training path,
+// 128-bit accesses of 8 elements) or fp32 (the parity mode, two 128-bit accesses per 8
+// elements). Statistics and math are always fp32. Row reductions use one warp per row with
+// shuffle reductions (no atomics), so every result is deterministic.
 #include <cuda_runtime.h>
 
 #include "btp_internal.h"
@@ -13,15 +14,62 @@ namespace btp {
 
 using bf16 = __nv_bfloat16;
 
-__device__ __forceinline__ void unpack8(const uint4& w, float (&f)[8]) {
-  f[0] = bf16_lo(w.x); f[1] = bf16_hi(w.x);
-  f[2] = bf16_lo(w.y); f[3] = bf16_hi(w.y);
-  f[4] = bf16_lo(w.z); f[5] = bf16_hi(w.z);
-  f[6] = bf16_lo(w.w); f[7] = bf16_hi(w.w);
+// ----------------------------------------------------------------------------- 8-wide access
+template <typename T>
+struct Vec8;
+
+template <>
+struct Vec8<bf16> {
+  using Raw = uint4;
+  __device__ static __forceinline__ Raw ld(const bf16* p) { return *reinterpret_cast<const uint4*>(p); }
+  __device__ static __forceinline__ void st(bf16* p, const Raw& r) { *reinterpret_cast<uint4*>(p) = r; }
+  __device__ static __forceinline__ void unpack(const Raw& w, float (&f)[8]) {
+    f[0] = bf16_lo(w.x); f[1] = bf16_hi(w.x);
+    f[2] = bf16_lo(w.y); f[3] = bf16_hi(w.y);
+    f[4] = bf16_lo(w.z); f[5] = bf16_hi(w.z);
+    f[6] = bf16_lo(w.w); f[7] = bf16_hi(w.w);
+  }
+  __device__ static __forceinline__ Raw pack(const float (&f)[8]) {
+    return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+  }
+};
+
+template <>
+struct Vec8<float> {
+  struct Raw {
+    float4 a, b;
+  };
+  __device__ static __forceinline__ Raw ld(const float* p) {
+    return Raw{reinterpret_cast<const float4*>(p)[0], reinterpret_cast<const float4*>(p)[1]};
+  }
+  __device__ static __forceinline__ void st(float* p, const Raw& r) {
+    reinterpret_cast<float4*>(p)[0] = r.a;
+    reinterpret_cast<float4*>(p)[1] = r.b;
+  }
+  __device__ static __forceinline__ void unpack(const Raw& w, float (&f)[8]) {
+    f[0] = w.a.x; f[1] = w.a.y; f[2] = w.a.z; f[3] = w.a.w;
+    f[4] = w.b.x; f[5] = w.b.y; f[6] = w.b.z; f[7] = w.b.w;
+  }
+  __device__ static __forceinline__ Raw pack(const float (&f)[8]) {
+    return Raw{make_float4(f[0], f[1], f[2], f[3]), make_float4(f[4], f[5], f[6], f[7])};
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&f)[8]) {
+  Vec8<T>::unpack(Vec8<T>::ld(p), f);
 }
 
-__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
-  return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+template <typename T>
+__device__ __forceinline__ void store8(T* p, const float (&f)[8]) {
+  Vec8<T>::st(p, Vec8<T>::pack(f));
+}
+
+__device__ __forceinline__ void load_gamma8(const float* g, float (&f)[8]) {
+  const float4 g0 = __ldg(reinterpret_cast<const float4*>(g));
+  const float4 g1 = __ldg(reinterpret_cast<const float4*>(g + 4));
+  f[0] = g0.x; f[1] = g0.y; f[2] = g0.z; f[3] = g0.w;
+  f[4] = g1.x; f[5] = g1.y; f[6] = g1.z; f[7] = g1.w;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -34,36 +82,39 @@ __device__ __forceinline__ float silu_f(float x) { return x * sigmoidf_safe(x); 
 
 // ----------------------------------------------------------------------------- K3 forward
 // One warp per row; NCH = max 8-element chunks per lane held in registers.
-template <int NCH>
-__global__ void __launch_bounds__(256) rmsnorm_residual_kernel(
-    const bf16* __restrict__ x, long long ldx, const bf16* __restrict__ branch, long long ldb,
-    bf16* __restrict__ x_out, long long ldo, const float* __restrict__ gamma, bf16* __restrict__ n_out,
-    long long ldn, float* __restrict__ ss_out, float* __restrict__ rl_out, int rows, int width, float eps) {
+template <typename T, int NCH>
+__global__ void __launch_bounds__(256) rmsnorm_residual_kernel(const T* __restrict__ x, long long ldx,
+                                                               const T* __restrict__ branch, long long ldb,
+                                                               T* __restrict__ x_out, long long ldo,
+                                                               const float* __restrict__ gamma, T* __restrict__ n_out,
+                                                               long long ldn, float* __restrict__ ss_out,
+                                                               float* __restrict__ rl_out, int rows, int width,
+                                                               float eps) {
+  using V = Vec8<T>;
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const int nch = width >> 3;
-  uint4 keep[NCH];
+  typename V::Raw keep[NCH];
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < NCH; ++i) {
     const int c = lane + 32 * i;
     if (c < nch) {
-      uint4 w = *reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8);
+      typename V::Raw w = V::ld(x + (long long)row * ldx + c * 8);
       if (branch != nullptr) {
-        const uint4 b = *reinterpret_cast<const uint4*>(branch + (long long)row * ldb + c * 8);
         float fx[8], fb[8];
-        unpack8(w, fx);
-        unpack8(b, fb);
+        V::unpack(w, fx);
+        load8(branch + (long long)row * ldb + c * 8, fb);
 #pragma unroll
         for (int j = 0; j < 8; ++j) fx[j] += fb[j];
-        w = pack8(fx);
-        if (x_out != nullptr) *reinterpret_cast<uint4*>(x_out + (long long)row * ldo + c * 8) = w;
+        w = V::pack(fx);
+        if (x_out != nullptr) V::st(x_out + (long long)row * ldo + c * 8, w);
       }
       keep[i] = w;
       float f[8];
-      unpack8(w, f);
+      V::unpack(w, f);  // statistics of the stored (rounded) value
 #pragma unroll
       for (int j = 0; j < 8; ++j) ss = fmaf(f[j], f[j], ss);
     }
@@ -80,22 +131,21 @@ __global__ void __launch_bounds__(256) rmsnorm_residual_kernel(
   for (int i = 0; i < NCH; ++i) {
     const int c = lane + 32 * i;
     if (c < nch) {
-      float f[8];
-      unpack8(keep[i], f);
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
-      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
-      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float f[8], g[8];
+      V::unpack(keep[i], f);
+      load_gamma8(gamma + c * 8, g);
 #pragma unroll
       for (int j = 0; j < 8; ++j) f[j] = f[j] * g[j] * inv;
-      *reinterpret_cast<uint4*>(n_out + (long long)row * ldn + c * 8) = pack8(f);
+      store8(n_out + (long long)row * ldn + c * 8, f);
     }
   }
 }
 
-__global__ void __launch_bounds__(256) rmsnorm_apply_kernel(const bf16* __restrict__ x, long long ldx,
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_apply_kernel(const T* __restrict__ x, long long ldx,
                                                             const float* __restrict__ gamma,
                                                             const float* __restrict__ ss_total, int d, float eps,
-                                                            bf16* __restrict__ n_out, long long ldn,
+                                                            T* __restrict__ n_out, long long ldn,
                                                             float* __restrict__ rms_out, int rows, int width) {
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
@@ -105,25 +155,24 @@ __global__ void __launch_bounds__(256) rmsnorm_apply_kernel(const bf16* __restri
   if (lane == 0 && rms_out) rms_out[row] = s;
   const float inv = 1.0f / s;
   for (int c = lane; c < (width >> 3); c += 32) {
-    float f[8];
-    unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), f);
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
-    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    float f[8], g[8];
+    load8(x + (long long)row * ldx + c * 8, f);
+    load_gamma8(gamma + c * 8, g);
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[j] = f[j] * g[j] * inv;
-    *reinterpret_cast<uint4*>(n_out + (long long)row * ldn + c * 8) = pack8(f);
+    store8(n_out + (long long)row * ldn + c * 8, f);
   }
 }
 
 // ----------------------------------------------------------------------------- K4 forward
 // Work item = (row, projection, group of 8 columns of the u half) for cola,
 //             (row, projection, group of 8 columns) for svd.
-__global__ void __launch_bounds__(256) fixup_sigma_kernel(const bf16* __restrict__ P, long long ldp,
-                                                          const float* __restrict__ ss_total, int d, float eps,
-                                                          float* __restrict__ s_out, bf16* __restrict__ z_out,
-                                                          long long ldz, bf16* __restrict__ a_out, long long lda,
+template <typename T>
+__global__ void __launch_bounds__(256) fixup_sigma_kernel(const T* P, long long ldp, const float* __restrict__ ss_total,
+                                                          int d, float eps, float* __restrict__ s_out, T* z_out,
+                                                          long long ldz, T* __restrict__ a_out, long long lda,
                                                           int rows, int r, int nproj, int variant) {
+  using V = Vec8<T>;
   const int per_proj = variant == 1 ? (r >> 4) : (r >> 3);
   const long long per_row = (long long)per_proj * nproj;
   const long long total = per_row * rows;
@@ -143,45 +192,45 @@ __global__ void __launch_bounds__(256) fixup_sigma_kernel(const bf16* __restrict
     if (variant == 1) {
       const int cu = p * r + g * 8, cv = cu + (r >> 1);
       float u[8], v[8];
-      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + cu), u);
-      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + cv), v);
+      load8(P + (long long)row * ldp + cu, u);
+      load8(P + (long long)row * ldp + cv, v);
 #pragma unroll
       for (int j = 0; j < 8; ++j) { u[j] *= inv; v[j] *= inv; }
-      const uint4 zu = pack8(u), zv = pack8(v);
+      const typename V::Raw zu = V::pack(u), zv = V::pack(v);
       if (write_z) {
-        *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + cu) = zu;
-        *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + cv) = zv;
+        V::st(z_out + (long long)row * ldz + cu, zu);
+        V::st(z_out + (long long)row * ldz + cv, zv);
       }
       // sigma acts on the stored (rounded) z so a checkpointed recompute is bit-identical
-      unpack8(zu, u);
-      unpack8(zv, v);
+      V::unpack(zu, u);
+      V::unpack(zv, v);
       float au[8], av[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         au[j] = silu_f(u[j]) * v[j];
         av[j] = silu_f(v[j]) * u[j];
       }
-      *reinterpret_cast<uint4*>(a_out + (long long)row * lda + cu) = pack8(au);
-      *reinterpret_cast<uint4*>(a_out + (long long)row * lda + cv) = pack8(av);
+      store8(a_out + (long long)row * lda + cu, au);
+      store8(a_out + (long long)row * lda + cv, av);
     } else {
       const int c = p * r + g * 8;
       float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(P + (long long)row * ldp + c), f);
+      load8(P + (long long)row * ldp + c, f);
 #pragma unroll
       for (int j = 0; j < 8; ++j) f[j] *= inv;
-      const uint4 zz = pack8(f);
-      if (write_z) *reinterpret_cast<uint4*>(z_out + (long long)row * ldz + c) = zz;
-      if (a_out != nullptr) *reinterpret_cast<uint4*>(a_out + (long long)row * lda + c) = zz;
+      const typename V::Raw zz = V::pack(f);
+      if (write_z) V::st(z_out + (long long)row * ldz + c, zz);
+      if (a_out != nullptr) V::st(a_out + (long long)row * lda + c, zz);
     }
   }
 }
 
 // ----------------------------------------------------------------------------- K4 backward
 // One warp per row: sigma-bwd, then dP = dz / s and dss = -<dz, z> / (2 s^2 d).
-__global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const bf16* __restrict__ z, long long ldz,
-                                                              const bf16* da, long long ldda,
-                                                              const float* __restrict__ s_in, int d, bf16* dP,
-                                                              long long lddp, float* __restrict__ dss, int rows,
+template <typename T>
+__global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const T* __restrict__ z, long long ldz, const T* da,
+                                                              long long ldda, const float* __restrict__ s_in, int d,
+                                                              T* dP, long long lddp, float* __restrict__ dss, int rows,
                                                               int r, int nproj, int variant) {
   const int warps = blockDim.x >> 5;
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
@@ -198,10 +247,10 @@ __global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const bf16* __rest
     if (variant == 1) {
       const int cu = p * r + g * 8, cv = cu + (r >> 1);
       float u[8], v[8], du_[8], dv_[8];
-      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + cu), u);
-      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + cv), v);
-      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + cu), du_);
-      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + cv), dv_);
+      load8(z + (long long)row * ldz + cu, u);
+      load8(z + (long long)row * ldz + cv, v);
+      load8(da + (long long)row * ldda + cu, du_);
+      load8(da + (long long)row * ldda + cv, dv_);
       float gu[8], gv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -217,19 +266,19 @@ __global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const bf16* __rest
         gu[j] *= inv;
         gv[j] *= inv;
       }
-      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + cu) = pack8(gu);
-      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + cv) = pack8(gv);
+      store8(dP + (long long)row * lddp + cu, gu);
+      store8(dP + (long long)row * lddp + cv, gv);
     } else {
       const int c = p * r + g * 8;
       float zz[8], dd[8];
-      unpack8(*reinterpret_cast<const uint4*>(z + (long long)row * ldz + c), zz);
-      unpack8(*reinterpret_cast<const uint4*>(da + (long long)row * ldda + c), dd);
+      load8(z + (long long)row * ldz + c, zz);
+      load8(da + (long long)row * ldda + c, dd);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         dot = fmaf(dd[j], zz[j], dot);
         dd[j] *= inv;
       }
-      *reinterpret_cast<uint4*>(dP + (long long)row * lddp + c) = pack8(dd);
+      store8(dP + (long long)row * lddp + c, dd);
     }
   }
   dot = warp_sum(dot);
@@ -237,9 +286,10 @@ __global__ void __launch_bounds__(256) fixup_sigma_bwd_kernel(const bf16* __rest
 }
 
 // ----------------------------------------------------------------------------- K5
-__global__ void __launch_bounds__(256) swiglu_kernel(const bf16* __restrict__ g, long long ldg,
-                                                     const bf16* __restrict__ u, long long ldu,
-                                                     bf16* __restrict__ act, long long lda, int rows, int cols) {
+template <typename T>
+__global__ void __launch_bounds__(256) swiglu_kernel(const T* __restrict__ g, long long ldg, const T* __restrict__ u,
+                                                     long long ldu, T* __restrict__ act, long long lda, int rows,
+                                                     int cols) {
   const int per_row = cols >> 3;
   const long long total = (long long)per_row * rows;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -247,20 +297,20 @@ __global__ void __launch_bounds__(256) swiglu_kernel(const bf16* __restrict__ g,
     const int row = (int)(idx / per_row);
     const int c = (int)(idx - (long long)row * per_row) * 8;
     float fg[8], fu[8];
-    unpack8(*reinterpret_cast<const uint4*>(g + (long long)row * ldg + c), fg);
-    unpack8(*reinterpret_cast<const uint4*>(u + (long long)row * ldu + c), fu);
+    load8(g + (long long)row * ldg + c, fg);
+    load8(u + (long long)row * ldu + c, fu);
 #pragma unroll
     for (int j = 0; j < 8; ++j) fg[j] = silu_f(fg[j]) * fu[j];
-    *reinterpret_cast<uint4*>(act + (long long)row * lda + c) = pack8(fg);
+    store8(act + (long long)row * lda + c, fg);
   }
 }
 
-__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const bf16* __restrict__ g, long long ldg,
-                                                         const bf16* __restrict__ u, long long ldu,
-                                                         const bf16* __restrict__ dact, long long ldda,
-                                                         bf16* __restrict__ dg, long long lddg,
-                                                         bf16* __restrict__ du, long long lddu, int rows,
-                                                         int cols) {
+template <typename T>
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const T* __restrict__ g, long long ldg,
+                                                         const T* __restrict__ u, long long ldu,
+                                                         const T* __restrict__ dact, long long ldda,
+                                                         T* __restrict__ dg, long long lddg, T* __restrict__ du,
+                                                         long long lddu, int rows, int cols) {
   const int per_row = cols >> 3;
   const long long total = (long long)per_row * rows;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -268,9 +318,9 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const bf16* __restrict_
     const int row = (int)(idx / per_row);
     const int c = (int)(idx - (long long)row * per_row) * 8;
     float fg[8], fu[8], fd[8], og[8], ou[8];
-    unpack8(*reinterpret_cast<const uint4*>(g + (long long)row * ldg + c), fg);
-    unpack8(*reinterpret_cast<const uint4*>(u + (long long)row * ldu + c), fu);
-    unpack8(*reinterpret_cast<const uint4*>(dact + (long long)row * ldda + c), fd);
+    load8(g + (long long)row * ldg + c, fg);
+    load8(u + (long long)row * ldu + c, fu);
+    load8(dact + (long long)row * ldda + c, fd);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float sg = sigmoidf_safe(fg[j]);
@@ -278,8 +328,8 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const bf16* __restrict_
       og[j] = fd[j] * fu[j] * sg * (1.0f + fg[j] * (1.0f - sg));
       ou[j] = fd[j] * silu_g;
     }
-    *reinterpret_cast<uint4*>(dg + (long long)row * lddg + c) = pack8(og);
-    *reinterpret_cast<uint4*>(du + (long long)row * lddu + c) = pack8(ou);
+    store8(dg + (long long)row * lddg + c, og);
+    store8(du + (long long)row * lddu + c, ou);
   }
 }
 
@@ -287,12 +337,12 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const bf16* __restrict_
 // Block of 256 threads: tpr threads per row (8 columns each, looping over column groups),
 // 256/tpr rows in flight. dgamma partial per block, combined across row slots in smem.
 constexpr int kNormBwdMaxGroups = 4;  // width <= 256 * 8 * 4 = 8192
-__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const bf16* __restrict__ dh, long long lddh,
-                                                          const bf16* __restrict__ x, long long ldx,
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const T* __restrict__ dh, long long lddh,
+                                                          const T* __restrict__ x, long long ldx,
                                                           const float* __restrict__ gamma,
-                                                          const float* __restrict__ dss,
-                                                          const bf16* __restrict__ dres, long long ldr,
-                                                          bf16* __restrict__ dx, long long lddx,
+                                                          const float* __restrict__ dss, const T* __restrict__ dres,
+                                                          long long ldr, T* __restrict__ dx, long long lddx,
                                                           float* __restrict__ dgamma_partial, int rows, int width,
                                                           int tpr, int rows_per_block) {
   extern __shared__ float red[];  // [256/tpr][width] when rows in flight > 1
@@ -313,24 +363,23 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const bf16* __restrict
     for (int q = 0; q < kNormBwdMaxGroups; ++q) {
       const int c = cg + q * tpr;
       if (c < nch) {
-        float fh[8], fx[8], fr[8];
-        unpack8(*reinterpret_cast<const uint4*>(dh + (long long)row * lddh + c * 8), fh);
-        unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), fx);
-        if (dres != nullptr) unpack8(*reinterpret_cast<const uint4*>(dres + (long long)row * ldr + c * 8), fr);
-        else {
+        float fh[8], fx[8], fr[8], g[8];
+        load8(dh + (long long)row * lddh + c * 8, fh);
+        load8(x + (long long)row * ldx + c * 8, fx);
+        if (dres != nullptr) {
+          load8(dres + (long long)row * ldr + c * 8, fr);
+        } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) fr[j] = 0.f;
         }
-        const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
-        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        load_gamma8(gamma + c * 8, g);
         float o[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           o[j] = fr[j] + fh[j] * g[j] + two_dss * fx[j];
           acc[q][j] = fmaf(fh[j], fx[j], acc[q][j]);
         }
-        *reinterpret_cast<uint4*>(dx + (long long)row * lddx + c * 8) = pack8(o);
+        store8(dx + (long long)row * lddx + c * 8, o);
       }
     }
   }
@@ -362,11 +411,41 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const bf16* __restrict
   }
 }
 
+// Full-width RMSNorm n = x*gamma/s (baselines): dn -> dh = dn / s (in place allowed) and
+// dss = -<dn, gamma*x> / (2 s^3 d), so rmsnorm_bwd finishes dx and dgamma.
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_bwd_prep_kernel(const T* dn, long long lddn, const T* __restrict__ x,
+                                                               long long ldx, const float* __restrict__ gamma,
+                                                               const float* __restrict__ s_in, T* dh, long long lddh,
+                                                               float* __restrict__ dss, int rows, int width) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float s = s_in[row];
+  const float inv = 1.0f / s;
+  float dot = 0.f;
+  for (int c = lane; c < (width >> 3); c += 32) {
+    float fd[8], fx[8], g[8];
+    load8(dn + (long long)row * lddn + c * 8, fd);
+    load8(x + (long long)row * ldx + c * 8, fx);
+    load_gamma8(gamma + c * 8, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      dot = fmaf(fd[j], g[j] * fx[j], dot);
+      fd[j] *= inv;
+    }
+    store8(dh + (long long)row * lddh + c * 8, fd);
+  }
+  dot = warp_sum(dot);
+  if (lane == 0) dss[row] = -dot / (2.0f * s * s * s * (float)width);
+}
+
 // ----------------------------------------------------------------------------- reductions
 __global__ void __launch_bounds__(256) reduce_rows_kernel(const float* __restrict__ in, int splits,
-                                                          long long split_stride, long long ldi, int rows,
-                                                          int cols, const float* __restrict__ col_scale,
-                                                          float* __restrict__ out, long long ldo, int accumulate) {
+                                                          long long split_stride, long long ldi, int rows, int cols,
+                                                          const float* __restrict__ col_scale, float* __restrict__ out,
+                                                          long long ldo, int accumulate) {
   const int per_row = cols >> 2;
   const long long total = (long long)per_row * rows;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -391,60 +470,24 @@ __global__ void __launch_bounds__(256) reduce_rows_kernel(const float* __restric
   }
 }
 
-__global__ void __launch_bounds__(256) add_kernel(const bf16* __restrict__ a, long long lda,
-                                                  const bf16* __restrict__ b, long long ldb, bf16* __restrict__ out,
-                                                  long long ldo, int rows, int cols) {
-  const int per_row = cols >> 3;
-  const long long total = (long long)per_row * rows;
+__global__ void __launch_bounds__(256) reduce_rows_scalar_kernel(const float* __restrict__ in, int splits,
+                                                                 long long split_stride, long long ldi, int rows,
+                                                                 int cols, const float* __restrict__ col_scale,
+                                                                 float* __restrict__ out, long long ldo,
+                                                                 int accumulate) {
+  const long long total = (long long)rows * cols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(idx / per_row);
-    const int c = (int)(idx - (long long)row * per_row) * 8;
-    float fa[8], fb[8];
-    unpack8(*reinterpret_cast<const uint4*>(a + (long long)row * lda + c), fa);
-    unpack8(*reinterpret_cast<const uint4*>(b + (long long)row * ldb + c), fb);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) fa[j] += fb[j];
-    *reinterpret_cast<uint4*>(out + (long long)row * ldo + c) = pack8(fa);
+    const int row = (int)(idx / cols);
+    const int c = (int)(idx - (long long)row * cols);
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += in[k * split_stride + (long long)row * ldi + c];
+    if (col_scale != nullptr) s *= col_scale[c];
+    float* o = out + (long long)row * ldo + c;
+    *o = accumulate ? *o + s : s;
   }
 }
 
-
-// ----------------------------------------------------------------------------- replicated norm bwd prologue
-// Full-width RMSNorm n = x*gamma/s (baselines): dn -> dh = dn / s (in place allowed) and
-// dss = -<dn, gamma*x> / (2 s^3 d), so btp_rmsnorm_bwd finishes dx and dgamma.
-__global__ void __launch_bounds__(256) rmsnorm_bwd_prep_kernel(const bf16* dn, long long lddn,
-                                                               const bf16* __restrict__ x, long long ldx,
-                                                               const float* __restrict__ gamma,
-                                                               const float* __restrict__ s_in, bf16* dh,
-                                                               long long lddh, float* __restrict__ dss, int rows,
-                                                               int width) {
-  const int warps = blockDim.x >> 5;
-  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const float s = s_in[row];
-  const float inv = 1.0f / s;
-  float dot = 0.f;
-  for (int c = lane; c < (width >> 3); c += 32) {
-    float fd[8], fx[8];
-    unpack8(*reinterpret_cast<const uint4*>(dn + (long long)row * lddn + c * 8), fd);
-    unpack8(*reinterpret_cast<const uint4*>(x + (long long)row * ldx + c * 8), fx);
-    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8));
-    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c * 8 + 4));
-    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      dot = fmaf(fd[j], g[j] * fx[j], dot);
-      fd[j] *= inv;
-    }
-    *reinterpret_cast<uint4*>(dh + (long long)row * lddh + c * 8) = pack8(fd);
-  }
-  dot = warp_sum(dot);
-  if (lane == 0) dss[row] = -dot / (2.0f * s * s * s * (float)width);
-}
-
-// ----------------------------------------------------------------------------- column sums
 // out[c] (+)= scale[c] * sum_{s<S} in[s*lds + c]: 32 columns x 32 row-groups per block, rows
 // strided by 32, then a fixed-order tree over the row-groups in smem (deterministic).
 __global__ void __launch_bounds__(1024) colsum_kernel(const float* __restrict__ in, int S, long long lds, int C,
@@ -469,11 +512,29 @@ __global__ void __launch_bounds__(1024) colsum_kernel(const float* __restrict__ 
   }
 }
 
-// ----------------------------------------------------------------------------- loss dot
+template <typename T>
+__global__ void __launch_bounds__(256) add_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ b,
+                                                  long long ldb, T* __restrict__ out, long long ldo, int rows,
+                                                  int cols) {
+  const int per_row = cols >> 3;
+  const long long total = (long long)per_row * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(idx / per_row);
+    const int c = (int)(idx - (long long)row * per_row) * 8;
+    float fa[8], fb[8];
+    load8(a + (long long)row * lda + c, fa);
+    load8(b + (long long)row * ldb + c, fb);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) fa[j] += fb[j];
+    store8(out + (long long)row * ldo + c, fa);
+  }
+}
+
 // partial[blk] = sum over this block's rows of <a_row, b_row>; fixed block/thread order.
-__global__ void __launch_bounds__(256) dot_kernel(const bf16* __restrict__ a, long long lda,
-                                                  const bf16* __restrict__ b, long long ldb, int rows, int cols,
-                                                  float* __restrict__ partial) {
+template <typename T>
+__global__ void __launch_bounds__(256) dot_kernel(const T* __restrict__ a, long long lda, const T* __restrict__ b,
+                                                  long long ldb, int rows, int cols, float* __restrict__ partial) {
   __shared__ float red[8];
   const int per_row = cols >> 3;
   const long long total = (long long)per_row * rows;
@@ -483,8 +544,8 @@ __global__ void __launch_bounds__(256) dot_kernel(const bf16* __restrict__ a, lo
     const int row = (int)(idx / per_row);
     const int c = (int)(idx - (long long)row * per_row) * 8;
     float fa[8], fb[8];
-    unpack8(*reinterpret_cast<const uint4*>(a + (long long)row * lda + c), fa);
-    unpack8(*reinterpret_cast<const uint4*>(b + (long long)row * ldb + c), fb);
+    load8(a + (long long)row * lda + c, fa);
+    load8(b + (long long)row * ldb + c, fb);
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc = fmaf(fa[j], fb[j], acc);
   }
@@ -509,48 +570,63 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 
 #define BTP_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA
 
+template <typename T>
+static int rmsnorm_residual_t(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
+                              long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
+                              float* rl_out, int rows, int width, float eps, cudaStream_t st) {
+  const int blocks = (rows + 7) / 8;
+  const int nch = width / 8;
+  const T* xb = static_cast<const T*>(x);
+  const T* bb = static_cast<const T*>(branch);
+  T* xo = static_cast<T*>(x_out);
+  T* no = static_cast<T*>(n_out);
+  if (nch <= 32 * 4)
+    rmsnorm_residual_kernel<T, 4><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                          rows, width, eps);
+  else if (nch <= 32 * 8)
+    rmsnorm_residual_kernel<T, 8><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                          rows, width, eps);
+  else if (nch <= 32 * 16)
+    rmsnorm_residual_kernel<T, 16><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                           rows, width, eps);
+  else
+    rmsnorm_residual_kernel<T, 32><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
+                                                           rows, width, eps);
+  BTP_CHECK_LAUNCH();
+}
+
 int rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out, long long ldo,
                      const float* gamma, void* n_out, long long ldn, float* ss_out, float* rl_out, int rows,
-                     int width, float eps, cudaStream_t st) {
+                     int width, float eps, cudaStream_t st, bool f32) {
   if (rows <= 0 || width <= 0) return BTP_ERR_DIM;
   if (width % 8 || width > 8192 || ldx % 8 || (branch && ldb % 8) || (x_out && ldo % 8) || (n_out && ldn % 8))
     return BTP_ERR_ALIGNMENT;
   if (!al16(x) || (branch && !al16(branch)) || (x_out && !al16(x_out)) || (n_out && !al16(n_out)) ||
       (n_out && !al16(gamma)))
     return BTP_ERR_ALIGNMENT;
-  const int blocks = (rows + 7) / 8;
-  const int nch = width / 8;
-  const bf16* xb = static_cast<const bf16*>(x);
-  const bf16* bb = static_cast<const bf16*>(branch);
-  bf16* xo = static_cast<bf16*>(x_out);
-  bf16* no = static_cast<bf16*>(n_out);
-  if (nch <= 32 * 4)
-    rmsnorm_residual_kernel<4><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows,
-                                                       width, eps);
-  else if (nch <= 32 * 8)
-    rmsnorm_residual_kernel<8><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows,
-                                                       width, eps);
-  else if (nch <= 32 * 16)
-    rmsnorm_residual_kernel<16><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
-                                                        rows, width, eps);
-  else
-    rmsnorm_residual_kernel<32><<<blocks, 256, 0, st>>>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out,
-                                                        rows, width, eps);
-  BTP_CHECK_LAUNCH();
+  if (f32) return rmsnorm_residual_t<float>(x, ldx, branch, ldb, x_out, ldo, gamma, n_out, ldn, ss_out, rl_out, rows,
+                                            width, eps, st);
+  return rmsnorm_residual_t<bf16>(x, ldx, branch, ldb, x_out, ldo, gamma, n_out, ldn, ss_out, rl_out, rows, width,
+                                  eps, st);
 }
 
 int rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps,
-                  void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st) {
+                  void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st, bool f32) {
   if (rows <= 0 || width <= 0 || d <= 0) return BTP_ERR_DIM;
   if (width % 8 || ldx % 8 || ldn % 8 || !al16(x) || !al16(n_out) || !al16(gamma)) return BTP_ERR_ALIGNMENT;
-  rmsnorm_apply_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(x), ldx, gamma, ss_total, d, eps,
-                                                       static_cast<bf16*>(n_out), ldn, rms_out, rows, width);
+  if (f32)
+    rmsnorm_apply_kernel<float><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const float*>(x), ldx, gamma, ss_total, d,
+                                                               eps, static_cast<float*>(n_out), ldn, rms_out, rows,
+                                                               width);
+  else
+    rmsnorm_apply_kernel<bf16><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(x), ldx, gamma, ss_total, d,
+                                                              eps, static_cast<bf16*>(n_out), ldn, rms_out, rows, width);
   BTP_CHECK_LAUNCH();
 }
 
 int fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out, void* z_out,
-                long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant,
-                cudaStream_t st) {
+                long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, cudaStream_t st,
+                bool f32) {
   if (rows <= 0 || r <= 0 || nproj <= 0) return BTP_ERR_DIM;
   if (variant != 0 && variant != 1) return BTP_ERR_DIM;
   if (variant == 1 && (r % 16)) return BTP_ERR_DIVISIBILITY;
@@ -558,48 +634,73 @@ int fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, floa
   if (variant == 1 && a_out == nullptr) return BTP_ERR_DIM;
   if (!al16(P) || (z_out && !al16(z_out)) || (a_out && !al16(a_out))) return BTP_ERR_ALIGNMENT;
   const long long items = (long long)rows * nproj * (variant == 1 ? r / 16 : r / 8);
-  fixup_sigma_kernel<<<grid_for(items), 256, 0, st>>>(static_cast<const bf16*>(P), ldp, ss_total, d, eps, s_out,
-                                                      static_cast<bf16*>(z_out), ldz, static_cast<bf16*>(a_out), lda,
-                                                      rows, r, nproj, variant);
+  if (f32)
+    fixup_sigma_kernel<float><<<grid_for(items), 256, 0, st>>>(static_cast<const float*>(P), ldp, ss_total, d, eps,
+                                                               s_out, static_cast<float*>(z_out), ldz,
+                                                               static_cast<float*>(a_out), lda, rows, r, nproj,
+                                                               variant);
+  else
+    fixup_sigma_kernel<bf16><<<grid_for(items), 256, 0, st>>>(static_cast<const bf16*>(P), ldp, ss_total, d, eps,
+                                                              s_out, static_cast<bf16*>(z_out), ldz,
+                                                              static_cast<bf16*>(a_out), lda, rows, r, nproj, variant);
   BTP_CHECK_LAUNCH();
 }
 
 int fixup_sigma_bwd(const void* z, long long ldz, const void* da, long long ldda, const float* s, int d, void* dP,
-                    long long lddp, float* dss, int rows, int r, int nproj, int variant, cudaStream_t st) {
+                    long long lddp, float* dss, int rows, int r, int nproj, int variant, cudaStream_t st, bool f32) {
   if (rows <= 0 || r <= 0 || nproj <= 0) return BTP_ERR_DIM;
   if (variant != 0 && variant != 1) return BTP_ERR_DIM;
   if (variant == 1 && (r % 16)) return BTP_ERR_DIVISIBILITY;
   if (r % 8 || ldz % 8 || ldda % 8 || lddp % 8) return BTP_ERR_ALIGNMENT;
   if (!al16(z) || !al16(da) || !al16(dP)) return BTP_ERR_ALIGNMENT;
-  fixup_sigma_bwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(z), ldz,
-                                                         static_cast<const bf16*>(da), ldda, s, d,
-                                                         static_cast<bf16*>(dP), lddp, dss, rows, r, nproj, variant);
+  if (f32)
+    fixup_sigma_bwd_kernel<float><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const float*>(z), ldz,
+                                                                  static_cast<const float*>(da), ldda, s, d,
+                                                                  static_cast<float*>(dP), lddp, dss, rows, r, nproj,
+                                                                  variant);
+  else
+    fixup_sigma_bwd_kernel<bf16><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(z), ldz,
+                                                                 static_cast<const bf16*>(da), ldda, s, d,
+                                                                 static_cast<bf16*>(dP), lddp, dss, rows, r, nproj,
+                                                                 variant);
   BTP_CHECK_LAUNCH();
 }
 
 int swiglu(const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows, int cols,
-           cudaStream_t st) {
+           cudaStream_t st, bool f32) {
   if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
   if (cols % 8 || ldg % 8 || ldu % 8 || lda % 8 || !al16(g) || !al16(u) || !al16(act)) return BTP_ERR_ALIGNMENT;
-  swiglu_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(
-      static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu, static_cast<bf16*>(act), lda, rows, cols);
+  const int grid = grid_for((long long)rows * cols / 8);
+  if (f32)
+    swiglu_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(g), ldg, static_cast<const float*>(u), ldu,
+                                               static_cast<float*>(act), lda, rows, cols);
+  else
+    swiglu_kernel<bf16><<<grid, 256, 0, st>>>(static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu,
+                                              static_cast<bf16*>(act), lda, rows, cols);
   BTP_CHECK_LAUNCH();
 }
 
 int swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, const void* dact, long long ldda,
-               void* dg, long long lddg, void* du, long long lddu, int rows, int cols, cudaStream_t st) {
+               void* dg, long long lddg, void* du, long long lddu, int rows, int cols, cudaStream_t st, bool f32) {
   if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
   if (cols % 8 || ldg % 8 || ldu % 8 || ldda % 8 || lddg % 8 || lddu % 8) return BTP_ERR_ALIGNMENT;
   if (!al16(g) || !al16(u) || !al16(dact) || !al16(dg) || !al16(du)) return BTP_ERR_ALIGNMENT;
-  swiglu_bwd_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(
-      static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu, static_cast<const bf16*>(dact), ldda,
-      static_cast<bf16*>(dg), lddg, static_cast<bf16*>(du), lddu, rows, cols);
+  const int grid = grid_for((long long)rows * cols / 8);
+  if (f32)
+    swiglu_bwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(g), ldg, static_cast<const float*>(u),
+                                                   ldu, static_cast<const float*>(dact), ldda,
+                                                   static_cast<float*>(dg), lddg, static_cast<float*>(du), lddu, rows,
+                                                   cols);
+  else
+    swiglu_bwd_kernel<bf16><<<grid, 256, 0, st>>>(static_cast<const bf16*>(g), ldg, static_cast<const bf16*>(u), ldu,
+                                                  static_cast<const bf16*>(dact), ldda, static_cast<bf16*>(dg), lddg,
+                                                  static_cast<bf16*>(du), lddu, rows, cols);
   BTP_CHECK_LAUNCH();
 }
 
 int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, const float* gamma, const float* dss,
                 const void* dres, long long ldr, void* dx, long long lddx, float* dgamma_partial, int max_blocks,
-                int* nblk_out, int rows, int width, cudaStream_t st) {
+                int* nblk_out, int rows, int width, cudaStream_t st, bool f32) {
   if (rows <= 0 || width <= 0 || max_blocks <= 0) return BTP_ERR_DIM;
   if (width % 8 || width > 8192 || lddh % 8 || ldx % 8 || lddx % 8 || (dres && ldr % 8)) return BTP_ERR_ALIGNMENT;
   if (!al16(dh) || !al16(x) || !al16(dx) || !al16(gamma) || (dres && !al16(dres))) return BTP_ERR_ALIGNMENT;
@@ -613,29 +714,34 @@ int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, co
   nblk = (rows + rows_per_block - 1) / rows_per_block;
   const size_t smem = slots > 1 ? (size_t)slots * width * sizeof(float) : 0;
   if (smem > 48 * 1024) return BTP_ERR_DIM;
-  rmsnorm_bwd_kernel<<<nblk, 256, smem, st>>>(static_cast<const bf16*>(dh), lddh, static_cast<const bf16*>(x), ldx,
-                                              gamma, dss, static_cast<const bf16*>(dres), ldr, static_cast<bf16*>(dx),
-                                              lddx, dgamma_partial, rows, width, tpr, rows_per_block);
+  if (f32)
+    rmsnorm_bwd_kernel<float><<<nblk, 256, smem, st>>>(static_cast<const float*>(dh), lddh,
+                                                       static_cast<const float*>(x), ldx, gamma, dss,
+                                                       static_cast<const float*>(dres), ldr, static_cast<float*>(dx),
+                                                       lddx, dgamma_partial, rows, width, tpr, rows_per_block);
+  else
+    rmsnorm_bwd_kernel<bf16><<<nblk, 256, smem, st>>>(static_cast<const bf16*>(dh), lddh, static_cast<const bf16*>(x),
+                                                      ldx, gamma, dss, static_cast<const bf16*>(dres), ldr,
+                                                      static_cast<bf16*>(dx), lddx, dgamma_partial, rows, width, tpr,
+                                                      rows_per_block);
   if (nblk_out) *nblk_out = nblk;
   BTP_CHECK_LAUNCH();
 }
 
-__global__ void __launch_bounds__(256) reduce_rows_scalar_kernel(const float* __restrict__ in, int splits,
-                                                                 long long split_stride, long long ldi, int rows,
-                                                                 int cols, const float* __restrict__ col_scale,
-                                                                 float* __restrict__ out, long long ldo,
-                                                                 int accumulate) {
-  const long long total = (long long)rows * cols;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(idx / cols);
-    const int c = (int)(idx - (long long)row * cols);
-    float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += in[k * split_stride + (long long)row * ldi + c];
-    if (col_scale != nullptr) s *= col_scale[c];
-    float* o = out + (long long)row * ldo + c;
-    *o = accumulate ? *o + s : s;
-  }
+int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma, const float* s,
+                     void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st, bool f32) {
+  if (rows <= 0 || width <= 0) return BTP_ERR_DIM;
+  if (width % 8 || lddn % 8 || ldx % 8 || lddh % 8 || !al16(dn) || !al16(x) || !al16(dh) || !al16(gamma))
+    return BTP_ERR_ALIGNMENT;
+  if (f32)
+    rmsnorm_bwd_prep_kernel<float><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const float*>(dn), lddn,
+                                                                   static_cast<const float*>(x), ldx, gamma, s,
+                                                                   static_cast<float*>(dh), lddh, dss, rows, width);
+  else
+    rmsnorm_bwd_prep_kernel<bf16><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(dn), lddn,
+                                                                  static_cast<const bf16*>(x), ldx, gamma, s,
+                                                                  static_cast<bf16*>(dh), lddh, dss, rows, width);
+  BTP_CHECK_LAUNCH();
 }
 
 int reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
@@ -656,34 +762,31 @@ int reduce_rows(const float* in, int splits, long long split_stride, long long l
 }
 
 int add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows, int cols,
-        cudaStream_t st) {
+        cudaStream_t st, bool f32) {
   if (rows <= 0 || cols <= 0) return BTP_ERR_DIM;
   if (cols % 8 || lda % 8 || ldb % 8 || ldo % 8 || !al16(a) || !al16(b) || !al16(out)) return BTP_ERR_ALIGNMENT;
-  add_kernel<<<grid_for((long long)rows * cols / 8), 256, 0, st>>>(static_cast<const bf16*>(a), lda,
-                                                                   static_cast<const bf16*>(b), ldb,
-                                                                   static_cast<bf16*>(out), ldo, rows, cols);
-  BTP_CHECK_LAUNCH();
-}
-
-int rmsnorm_bwd_prep(const void* dn, long long lddn, const void* x, long long ldx, const float* gamma,
-                     const float* s, void* dh, long long lddh, float* dss, int rows, int width, cudaStream_t st) {
-  if (rows <= 0 || width <= 0) return BTP_ERR_DIM;
-  if (width % 8 || lddn % 8 || ldx % 8 || lddh % 8 || !al16(dn) || !al16(x) || !al16(dh) || !al16(gamma))
-    return BTP_ERR_ALIGNMENT;
-  rmsnorm_bwd_prep_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(dn), lddn,
-                                                          static_cast<const bf16*>(x), ldx, gamma, s,
-                                                          static_cast<bf16*>(dh), lddh, dss, rows, width);
+  const int grid = grid_for((long long)rows * cols / 8);
+  if (f32)
+    add_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(a), lda, static_cast<const float*>(b), ldb,
+                                            static_cast<float*>(out), ldo, rows, cols);
+  else
+    add_kernel<bf16><<<grid, 256, 0, st>>>(static_cast<const bf16*>(a), lda, static_cast<const bf16*>(b), ldb,
+                                           static_cast<bf16*>(out), ldo, rows, cols);
   BTP_CHECK_LAUNCH();
 }
 
 int dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
-        int max_blocks, int* nblk_out, cudaStream_t st) {
+        int max_blocks, int* nblk_out, cudaStream_t st, bool f32) {
   if (rows <= 0 || cols <= 0 || max_blocks <= 0) return BTP_ERR_DIM;
   if (cols % 8 || lda % 8 || ldb % 8 || !al16(a) || !al16(b)) return BTP_ERR_ALIGNMENT;
   int nblk = grid_for((long long)rows * cols / 8);
   if (nblk > max_blocks) nblk = max_blocks;
-  dot_kernel<<<nblk, 256, 0, st>>>(static_cast<const bf16*>(a), lda, static_cast<const bf16*>(b), ldb, rows, cols,
-                                   partial);
+  if (f32)
+    dot_kernel<float><<<nblk, 256, 0, st>>>(static_cast<const float*>(a), lda, static_cast<const float*>(b), ldb, rows,
+                                            cols, partial);
+  else
+    dot_kernel<bf16><<<nblk, 256, 0, st>>>(static_cast<const bf16*>(a), lda, static_cast<const bf16*>(b), ldb, rows,
+                                           cols, partial);
   if (nblk_out) *nblk_out = nblk;
   BTP_CHECK_LAUNCH();
 }

@@ -41,6 +41,9 @@ from .plan import NormMode, PlanError, ShardPlan, Strategy
 BF16 = torch.bfloat16
 F32 = torch.float32
 _VAR = {Variant.SVD: 0, Variant.COLA: 1}
+# bf16: the training path (tcgen05 GEMMs, bf16 activations, fp32 statistics / accumulation);
+# fp32: the parity mode (exact-fp32 SIMT GEMM + fp32 row kernels; north_star 1e-4 tolerance)
+PRECISIONS = {"bf16": BF16, "fp32": F32}
 
 
 def _pick_splits(tiles: int, k_blocks: int, sms: int) -> int:
@@ -74,7 +77,11 @@ class ExecutorBase:
     gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
     fuse_swiglu_bwd = False         # SwiGLU backward in the dgrad GEMM epilogue (False: separate kernel)
 
-    def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float):
+    def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float, precision: str = "bf16"):
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}, got {precision!r}")
+        self.precision = precision
+        self.act = PRECISIONS[precision]  # activation / GEMM-operand dtype
         self.pl, self.cfg, self.shape = pl, pl.cfg, pl.shape
         self.comm = comm if comm is not None else TPComm(1, 0)
         if self.comm.tp != pl.shape.tp:
@@ -88,11 +95,12 @@ class ExecutorBase:
         self._buf: dict[str, torch.Tensor] = {}
         self.saved: dict = {}
 
-    def _dev(self, a, dtype=BF16) -> torch.Tensor:
-        return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype)
+    def _dev(self, a, dtype=None) -> torch.Tensor:
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype or self.act)
 
     # ------------------------------------------------------------------ buffers
-    def buf(self, name: str, shape, dtype=BF16) -> torch.Tensor:
+    def buf(self, name: str, shape, dtype=None) -> torch.Tensor:
+        dtype = dtype or self.act
         t = self._buf.get(name)
         if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
             t = torch.empty(shape, device=self.dev, dtype=dtype)
@@ -183,14 +191,15 @@ class BTPBlockExecutor(ExecutorBase):
     """One rank's shard of a low-rank (svd/cola) block under a BTP plan."""
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None,
-                 device: torch.device | str = "cuda", eps: float = 1e-6, attn_backend: str = "auto"):
+                 device: torch.device | str = "cuda", eps: float = 1e-6, attn_backend: str = "auto",
+                 precision: str = "bf16"):
         if pl.strategy is not Strategy.BOTTLENECK:
             raise PlanError(f"BTPBlockExecutor needs a btp plan, got {pl.strategy.value}")
         if block.variant is not pl.variant:
             raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
         if pl.variant not in _VAR:
             raise PlanError(f"variant {pl.variant.value} is not supported on the device path (svd, cola)")
-        self._setup(pl, comm, device, eps)
+        self._setup(pl, comm, device, eps, precision)
         self.var = _VAR[pl.variant]
         self.online = pl.norm_mode is NormMode.ONLINE
         self.grouping = pl.grouping
@@ -198,7 +207,8 @@ class BTPBlockExecutor(ExecutorBase):
         cfg, tp = self.cfg, self.tp
         self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
         self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
-        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim, attn_backend)
+        self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
+                              "fp32" if precision == "fp32" else attn_backend)
         self._load_weights(block)
 
     # ------------------------------------------------------------------ weights
@@ -208,8 +218,8 @@ class BTPBlockExecutor(ExecutorBase):
         B = {n: t.values for n, t in block.down_factors.items()}
         A = {n: t.values for n, t in block.up_factors.items()}
 
-        def dev(a, dtype=BF16):
-            return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype)
+        def dev(a, dtype=None):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype or self.act)
 
         self.W = {
             "d_qkv": dev(np.concatenate([B[n][:, sl] for n in ("q", "k", "v")], axis=0)),   # [3r, dl]
@@ -328,8 +338,8 @@ class BTPBlockExecutor(ExecutorBase):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x: this rank's residual shard [T, d/tp] bf16. Returns y shard [T, d/tp] bf16."""
         T, dl, fl, r = self.T, self.dl, self.fl, self.r
-        if tuple(x.shape) != (T, dl) or x.dtype != BF16:
-            raise PlanError(f"x shard must be bf16 [{T}, {dl}], got {x.dtype} {tuple(x.shape)}")
+        if tuple(x.shape) != (T, dl) or x.dtype != self.act:
+            raise PlanError(f"x shard must be {self.act} [{T}, {dl}], got {x.dtype} {tuple(x.shape)}")
         self.comm.pass_tag = "forward"
         W = self.W
         S = {"x": x}
@@ -392,8 +402,8 @@ class BTPBlockExecutor(ExecutorBase):
             ws["norm1-rms"], ws["norm2-rms"] = S["s1"].view(T, 1), S["s2"].view(T, 1)
         a_o = ws.get("a_in_o", zs["o"])
         a_d = ws.get("a_in_down", zs["down"])
-        o = torch.empty(T, self.dl, device=self.dev, dtype=BF16)
-        mlp = torch.empty(T, self.dl, device=self.dev, dtype=BF16)
+        o = torch.empty(T, self.dl, device=self.dev, dtype=self.act)
+        mlp = torch.empty(T, self.dl, device=self.dev, dtype=self.act)
         K.gemm(K.Gemm(a_o, self.W["u_o"], o))
         K.gemm(K.Gemm(a_d, self.W["u_d"], mlp))
         ws["o"], ws["mlp"] = o, mlp

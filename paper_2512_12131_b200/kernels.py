@@ -33,6 +33,15 @@ def _ld(t: torch.Tensor | None) -> int:
     return t.stride(-2)
 
 
+def _fn(name: str, t: torch.Tensor) -> str:
+    """bf16 entry point, or its fp32 parity-mode twin for fp32 activations."""
+    if t.dtype == F32:
+        return name + "_f32"
+    if t.dtype != BF16:
+        raise TypeError(f"{name}: activations must be bf16 or fp32, got {t.dtype}")
+    return name
+
+
 def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -66,8 +75,9 @@ class Gemm:
     swiglu_bwd: tuple | None = None         # (g, u, du): acc = dact -> C = dg, du written too
 
     def to_c(self) -> GemmProblem:
-        _check(self.a, BF16, "A")
-        _check(self.b, BF16, "B")
+        op_dtype = F32 if self.a.dtype == F32 else BF16  # fp32 operands -> exact-fp32 parity GEMM
+        _check(self.a, op_dtype, "A")
+        _check(self.b, op_dtype, "B")
         M, K = (self.a.shape[1], self.a.shape[0]) if self.a_mn else (self.a.shape[0], self.a.shape[1])
         if self.b_mn:
             Kb, N = self.b.shape
@@ -109,7 +119,10 @@ class Gemm:
 def gemm(*problems: Gemm, bn: int = 0) -> None:
     """One launch of the persistent tcgen05 GEMM over 1..4 problems."""
     arr = (GemmProblem * len(problems))(*[p.to_c() for p in problems])
-    _native.call("btp_gemm", arr, len(problems), bn, _stream())
+    if problems[0].a.dtype == F32:
+        _native.call("btp_gemm_f32", arr, len(problems), _stream())
+    else:
+        _native.call("btp_gemm", arr, len(problems), bn, _stream())
 
 
 def zero(t: torch.Tensor) -> None:
@@ -119,7 +132,7 @@ def zero(t: torch.Tensor) -> None:
 def rmsnorm_residual(x, gamma, *, branch=None, x_out=None, n_out=None, ss_out=None, rl_out=None, eps=1e-6):
     rows, width = x.shape
     _native.call(
-        "btp_rmsnorm_residual", _p(x), _ld(x), _p(branch), _ld(branch), _p(x_out), _ld(x_out), _p(gamma),
+        _fn("btp_rmsnorm_residual", x), _p(x), _ld(x), _p(branch), _ld(branch), _p(x_out), _ld(x_out), _p(gamma),
         _p(n_out), _ld(n_out), _p(ss_out), _p(rl_out), rows, width, ctypes.c_float(eps), _stream(),
     )
 
@@ -127,7 +140,7 @@ def rmsnorm_residual(x, gamma, *, branch=None, x_out=None, n_out=None, ss_out=No
 def rmsnorm_apply(x, gamma, ss_total, d, n_out, *, rms_out=None, eps=1e-6):
     rows, width = x.shape
     _native.call(
-        "btp_rmsnorm_apply", _p(x), _ld(x), _p(gamma), _p(ss_total), d, ctypes.c_float(eps), _p(n_out),
+        _fn("btp_rmsnorm_apply", x), _p(x), _ld(x), _p(gamma), _p(ss_total), d, ctypes.c_float(eps), _p(n_out),
         _ld(n_out), _p(rms_out), rows, width, _stream(),
     )
 
@@ -135,7 +148,7 @@ def rmsnorm_apply(x, gamma, ss_total, d, n_out, *, rms_out=None, eps=1e-6):
 def fixup_sigma(P, *, r, nproj, variant, z_out=None, a_out=None, ss_total=None, d=1, s_out=None, eps=1e-6):
     rows = P.shape[0]
     _native.call(
-        "btp_fixup_sigma", _p(P), _ld(P), _p(ss_total), d, ctypes.c_float(eps), _p(s_out), _p(z_out),
+        _fn("btp_fixup_sigma", P), _p(P), _ld(P), _p(ss_total), d, ctypes.c_float(eps), _p(s_out), _p(z_out),
         _ld(z_out), _p(a_out), _ld(a_out), rows, r, nproj, variant, _stream(),
     )
 
@@ -143,20 +156,20 @@ def fixup_sigma(P, *, r, nproj, variant, z_out=None, a_out=None, ss_total=None, 
 def fixup_sigma_bwd(z, da, dP, *, r, nproj, variant, s=None, d=1, dss=None):
     rows = z.shape[0]
     _native.call(
-        "btp_fixup_sigma_bwd", _p(z), _ld(z), _p(da), _ld(da), _p(s), d, _p(dP), _ld(dP), _p(dss), rows, r,
+        _fn("btp_fixup_sigma_bwd", z), _p(z), _ld(z), _p(da), _ld(da), _p(s), d, _p(dP), _ld(dP), _p(dss), rows, r,
         nproj, variant, _stream(),
     )
 
 
 def swiglu(g, u, act):
     rows, cols = g.shape
-    _native.call("btp_swiglu", _p(g), _ld(g), _p(u), _ld(u), _p(act), _ld(act), rows, cols, _stream())
+    _native.call(_fn("btp_swiglu", g), _p(g), _ld(g), _p(u), _ld(u), _p(act), _ld(act), rows, cols, _stream())
 
 
 def swiglu_bwd(g, u, dact, dg, du):
     rows, cols = g.shape
     _native.call(
-        "btp_swiglu_bwd", _p(g), _ld(g), _p(u), _ld(u), _p(dact), _ld(dact), _p(dg), _ld(dg), _p(du), _ld(du),
+        _fn("btp_swiglu_bwd", g), _p(g), _ld(g), _p(u), _ld(u), _p(dact), _ld(dact), _p(dg), _ld(dg), _p(du), _ld(du),
         rows, cols, _stream(),
     )
 
@@ -166,7 +179,7 @@ def rmsnorm_bwd(dh, x, gamma, dss, dx, dgamma_partial, *, dres=None) -> int:
     rows, width = x.shape
     nblk = ctypes.c_int(0)
     _native.call(
-        "btp_rmsnorm_bwd", _p(dh), _ld(dh), _p(x), _ld(x), _p(gamma), _p(dss), _p(dres), _ld(dres), _p(dx),
+        _fn("btp_rmsnorm_bwd", dh), _p(dh), _ld(dh), _p(x), _ld(x), _p(gamma), _p(dss), _p(dres), _ld(dres), _p(dx),
         _ld(dx), _p(dgamma_partial), dgamma_partial.shape[0], ctypes.byref(nblk), rows, width, _stream(),
     )
     return nblk.value
@@ -185,12 +198,12 @@ def reduce_rows(parts, out, *, splits=None, col_scale=None, accumulate=False):
 
 def add(a, b, out):
     rows, cols = a.shape
-    _native.call("btp_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), rows, cols, _stream())
+    _native.call(_fn("btp_add", a), _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), rows, cols, _stream())
 
 
 def rmsnorm_bwd_prep(dn, x, gamma, s, dh, dss):
     rows, width = x.shape
-    _native.call("btp_rmsnorm_bwd_prep", _p(dn), _ld(dn), _p(x), _ld(x), _p(gamma), _p(s), _p(dh), _ld(dh),
+    _native.call(_fn("btp_rmsnorm_bwd_prep", dn), _p(dn), _ld(dn), _p(x), _ld(x), _p(gamma), _p(s), _p(dh), _ld(dh),
                  _p(dss), rows, width, _stream())
 
 
@@ -198,7 +211,7 @@ def dot(a, b, partial) -> int:
     """partial: fp32 [max_blocks]; returns the number of partials written (sum them with reduce_rows)."""
     rows, cols = a.shape
     nblk = ctypes.c_int(0)
-    _native.call("btp_dot", _p(a), _ld(a), _p(b), _ld(b), rows, cols, _p(partial), partial.shape[0],
+    _native.call(_fn("btp_dot", a), _p(a), _ld(a), _p(b), _ld(b), rows, cols, _p(partial), partial.shape[0],
                  ctypes.byref(nblk), _stream())
     return nblk.value
 

@@ -47,3 +47,18 @@ def test_full_rank_step(grouping):
         assert rel(st.grads["W"][n], g_ref["W"][n]) < BF16_TOL, n
     assert st.trace.record_tuples("forward") == [
         (p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
+
+
+@pytest.mark.parametrize("strategy", ["vanilla", "full-rank"])
+def test_baselines_fp32_mode(strategy):
+    b, s = 2, 64
+    variant = Variant.FULL_RANK if strategy == "full-rank" else Variant.COLA
+    blk, x, G, oblk = inputs(SMALL, variant, b, s)
+    pl = plan(Strategy(strategy), SMALL, RunShape(b, s, 1), None if strategy == "full-rank" else variant)
+    st = train_step(pl, blk, x, G, precision="fp32")
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, sharded=False)
+    assert rel(st.y.values.reshape(-1, SMALL.d), y_ref) < 1e-4
+    assert rel(st.dx, g_ref["dx"]) < 1e-4
+    grp = "W" if strategy == "full-rank" else "A"
+    for n in O.PROJECTIONS:
+        assert rel(st.grads[grp][n], g_ref[grp][n]) < 1e-4, n

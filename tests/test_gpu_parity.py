@@ -102,3 +102,38 @@ def test_run_with_ckpt_bitwise_and_collective_free():
     assert run.report.reforward_collectives == 0
     assert run.report.delta_mem_bytes > 0
     assert eff_ckpt(run.report) > 0
+
+
+FP32_TOL = 1e-4  # north_star: fp32 mode within 1e-4 relative on activations, gradients and loss
+
+
+@pytest.mark.parametrize("variant", [Variant.COLA, Variant.SVD])
+@pytest.mark.parametrize("online", [True, False])
+def test_fp32_mode_forward_and_grads(variant, online):
+    """fp32 parity mode (exact-fp32 SIMT GEMM + fp32 row kernels) against the float64 oracle."""
+    b, s = 2, 64
+    blk, x, G, oblk = inputs(SMALL, variant, b, s)
+    pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 1), variant, online_norm=online, grouping=True)
+    res = execute_forward(pl, blk, x, capture_workspaces=True, precision="fp32")
+    y_ref, g_ref, ws_ref, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, online=online)
+    _check_ws(res.workspaces[0], ws_ref[0], tol=FP32_TOL)
+    st = train_step(pl, blk, x, G, precision="fp32")
+    assert rel(st.y.values.reshape(-1, SMALL.d), y_ref) < FP32_TOL
+    assert abs(st.loss - loss_ref) / abs(loss_ref) < FP32_TOL
+    assert rel(st.dx, g_ref["dx"]) < FP32_TOL
+    errs = {f"A_{n}": rel(st.grads["A"][n], g_ref["A"][n]) for n in O.PROJECTIONS}
+    errs.update({f"B_{n}": rel(st.grads["B"][n], g_ref["B"][n]) for n in O.PROJECTIONS})
+    errs["gamma1"] = rel(st.grads["gamma1"], g_ref["dgamma1"])
+    errs["gamma2"] = rel(st.grads["gamma2"], g_ref["dgamma2"])
+    bad = {k: v for k, v in errs.items() if v > FP32_TOL}
+    assert not bad, bad
+
+
+def test_fp32_mode_c60m_forward():
+    """CoLA-60M block (BASELINE config #1) in fp32 mode vs the oracle, every intermediate."""
+    b, s = 8, 256
+    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    res = execute_forward(pl, blk, x, capture_workspaces=True, precision="fp32")
+    _, _, ws_ref, _ = oracle_step(oblk, x, G, C60M, b, s)
+    _check_ws(res.workspaces[0], ws_ref[0], tol=FP32_TOL)
