@@ -74,6 +74,11 @@ typedef struct btp_gemm_problem {
  * (grouped up-projections q|k|v and gate|up, simulator.py:655-668). */
 int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream);
 
+/* Tile mode switch for btp_gemm: 1 (default) = CTA-pair tiles (cluster of 2 CTAs on one TPC,
+ * tcgen05.mma.cta_group::2, 256 x BN per pair) for launches with plain/residual epilogues;
+ * 0 = single-CTA 128 x BN tiles everywhere. Returns the previous setting. */
+int btp_gemm_set_pair(int enable);
+
 /* Online RMSNorm (local form) fused with the residual add, one row per warp.
  *   v = x (+ branch); if x_out: x_out = bf16(v); stats use the rounded v
  *   ss[t] = sum_k v^2 ; rms_loc[t] = sqrt(ss/width + eps) ; n = v * gamma / rms_loc

@@ -29,6 +29,7 @@ _STATUS_NAMES = {
 # Every symbol include/btp.h declares; tests check the library exports exactly these.
 EXPORTED_SYMBOLS = (
     "btp_gemm",
+    "btp_gemm_set_pair",
     "btp_rmsnorm_residual",
     "btp_rmsnorm_apply",
     "btp_fixup_sigma",
@@ -120,6 +121,7 @@ _SIGNATURES = {
     "btp_num_sms": [],
     "btp_version": [],
     "btp_gemm_f32": [ctypes.POINTER(GemmProblem), _I, _P],
+    "btp_gemm_set_pair": [_I],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot"):

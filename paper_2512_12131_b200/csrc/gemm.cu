@@ -72,16 +72,22 @@ struct DevParams {
 
 // kSlots: staging slots per chunk buffer (2 for the two-input / two-output swiglu-bwd epilogue,
 // which trades mainloop stages for epilogue staging).
-template <int BN, int kSlots>
+// kPair: CTA-pair mode (cluster of 2, tcgen05.mma.cta_group::2): a 256 x BN tile per pair,
+// each CTA holding 128 rows of A and BN/2 rows of B per stage and its own 128 x BN accumulator.
+// Halving the per-CTA B tile buys a deeper smem pipeline (up to 8 stages).
+template <int BN, int kSlots, bool kPair>
 struct Cfg {
-  static constexpr int kStages = kSlots == 1 ? ((BN == 128) ? 6 : 4) : ((BN == 128) ? 4 : 3);
+  static constexpr int kBRows = kPair ? BN / 2 : BN;
+  static constexpr int kTileM = kPair ? 2 * kBM : kBM;
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;  // double-buffered accumulator (pow2 alloc)
   static constexpr int kEpiWarpBytes = 2 * kSlots * kEpiStageBytes;  // double-buffered chunks
   static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
   static constexpr int kBarrierBytes = 256;
+  static constexpr int kAvail = 232448 - 1024 - kEpiBytes - kBarrierBytes;
+  static constexpr int kStages = (kAvail / kStageBytes) > 8 ? 8 : (kAvail / kStageBytes);
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarrierBytes;
 };
 
@@ -106,9 +112,9 @@ __device__ __forceinline__ TileCoord decode_tile(const DevParams& P, int tile) {
   return t;
 }
 
-template <int BN, int kSlots>
+template <int BN, int kSlots, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ DevParams P) {
-  using C = Cfg<BN, kSlots>;
+  using C = Cfg<BN, kSlots, kPair>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -123,6 +129,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
+  // pair mode: rank within the CTA pair; tiles are distributed over pairs
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const int unit = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < P.num_problems; ++i) {
@@ -138,58 +148,67 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], kPair ? 256 : 128);  // pair: both CTAs' epilogues release the leader's
     }
     for (int b = 0; b < 8; ++b) mbar_init(&aux_bar_all[b], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (kPair) tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // peer barriers must exist before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < P.total_tiles; tile += n_units) {
         const TileCoord tc = decode_tile(P, tile);
         const DevProblem& pr = P.prob[tc.p];
-        const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
+        const int m0 = tc.m_blk * C::kTileM + (int)rank * kBM;     // this CTA's 128 rows of A
+        const int n0 = tc.n_blk * BN + (int)rank * (BN - C::kBRows);  // this CTA's share of B
         const int kb0 = tc.split * pr.kb_per_split;
         const int kb1 = min(kb0 + pr.kb_per_split, pr.k_blocks);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+          // pair: both CTAs' bytes complete on the leader's barrier, which expects both halves
+          const uint32_t fbar = kPair ? (smem_u32(&full_bar[stage]) & kPeerBitMask) : smem_u32(&full_bar[stage]);
+          if (!kPair || rank == 0) mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes * (kPair ? 2 : 1));
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * kBK;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+            if constexpr (kPair) tma_load_2d_pair(dst, m, fbar, c0, c1);
+            else tma_load_2d(dst, m, &full_bar[stage], c0, c1);
+          };
           if (!pr.a_mn) {
-            tma_load_2d(a_dst, &pr.tma_a, &full_bar[stage], k0, m0);
+            load(a_dst, &pr.tma_a, k0, m0);
           } else {
 #pragma unroll
-            for (int c = 0; c < kBM / 64; ++c)
-              tma_load_2d(a_dst + c * 64 * kBK * 2, &pr.tma_a, &full_bar[stage], m0 + c * 64, k0);
+            for (int c = 0; c < kBM / 64; ++c) load(a_dst + c * 64 * kBK * 2, &pr.tma_a, m0 + c * 64, k0);
           }
           if (!pr.b_mn) {
-            tma_load_2d(b_dst, &pr.tma_b, &full_bar[stage], k0, n0);
+            load(b_dst, &pr.tma_b, k0, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_load_2d(b_dst + c * 64 * kBK * 2, &pr.tma_b, &full_bar[stage], n0 + c * 64, k0);
+            for (int c = 0; c < C::kBRows / 64; ++c) load(b_dst + c * 64 * kBK * 2, &pr.tma_b, n0 + c * 64, k0);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 1 && (!kPair || rank == 0)) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA only)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < P.total_tiles; tile += n_units, ++it) {
       const TileCoord tc = decode_tile(P, tile);
       const DevProblem& pr = P.prob[tc.p];
       const int kb0 = tc.split * pr.kb_per_split;
@@ -212,14 +231,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t a_desc = make_sw128_desc(a_base + k * a_step, a_lbo, 1024);
             const uint64_t b_desc = make_sw128_desc(b_base + k * b_step, b_lbo, 1024);
-            umma_bf16(d_tmem, a_desc, b_desc, pr.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (kPair) umma_bf16_pair(d_tmem, a_desc, b_desc, pr.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else umma_bf16(d_tmem, a_desc, b_desc, pr.idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (kPair) umma_commit_pair_mc(&empty_bar[stage], 0x3);  // frees the slot in both CTAs
+          else umma_commit(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
-      if (elect_one()) umma_commit(&tfull_bar[buf]);
+      if (elect_one()) {
+        if constexpr (kPair) umma_commit_pair_mc(&tfull_bar[buf], 0x3);
+        else umma_commit(&tfull_bar[buf]);
+      }
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -243,12 +267,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     };
     int it = 0;
     int chunk_seq = 0;  // running chunk counter -> staging buffer parity
-    for (int tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < P.total_tiles; tile += n_units, ++it) {
       const TileCoord tc = decode_tile(P, tile);
       const DevProblem& pr = P.prob[tc.p];
       const int buf = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = tc.m_blk * kBM, n0 = tc.n_blk * BN;
+      const int m0 = tc.m_blk * C::kTileM + (int)rank * kBM, n0 = tc.n_blk * BN;  // this CTA's 128 rows
       const int n_valid = min(BN, pr.N - n0);
       const int cols_per_chunk = pr.out_fp32 ? 32 : 64;  // 128 bytes of output per row
       const int out_row0 = m0 + q * 32;
@@ -277,16 +301,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         __syncwarp();
         float v[64];
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + buf * BN + c0, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rscale;
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN + c0;
         if (!pr.out_fp32) {
-          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + buf * BN + c0 + 32, r);
+          uint32_t r[64];
+          tmem_ld_32x32b_x64(taddr, r);  // one TMEM round trip per 64-column chunk
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r[j]) * rscale;
+          for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(r[j]) * rscale;
+        } else {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rscale;
         }
         const int col = n0 + c0;
         if (pr.col_scale != nullptr) {
@@ -369,15 +396,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[buf]);
+      if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[buf], 0);  // the leader's MMA reuses the buffer
+      else mbar_arrive(&tempty_bar[buf]);
     }
     if (lane == 0) bulk_wait<0>();
   }
 
-  __syncthreads();
+  // pair: neither CTA may leave (or free TMEM) while the leader can still touch the peer
+  if constexpr (kPair) cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if constexpr (kPair) tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -412,38 +443,71 @@ static int make_tmap(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t o
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
-template <int BN, int kSlots>
+template <int BN, int kSlots, bool kPair>
 static int launch(const DevParams& P, int grid, cudaStream_t stream) {
-  using C = Cfg<BN, kSlots>;
+  using C = Cfg<BN, kSlots, kPair>;
   static_assert(C::kSmemBytes <= 232448, "shared memory budget");
+  static_assert(2 * C::kStages * 8 + 12 * 8 + 8 <= C::kBarrierBytes, "barrier region");
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(gemm_kernel<BN, kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_kernel<BN, kSlots, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
   }
-  gemm_kernel<BN, kSlots><<<grid, kThreads, C::kSmemBytes, stream>>>(P);
+  if constexpr (!kPair) {
+    gemm_kernel<BN, kSlots, kPair><<<grid, kThreads, C::kSmemBytes, stream>>>(P);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, gemm_kernel<BN, kSlots, kPair>, P) != cudaSuccess) return BTP_ERR_CUDA;
+  }
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
-// N-tile choice: persistent CTAs run ceil(tiles / SMs) waves of tiles whose mainloop time is
-// ~ proportional to BN (+ a fixed per-tile cost, ~32 columns' worth); pick the cheapest.
-static int pick_bn(const btp_gemm_problem* probs, int n, int sms) {
+// N-tile choice: persistent units (CTAs, or CTA pairs) run ceil(tiles / units) waves of tiles
+// whose mainloop time is ~ proportional to BN (+ a fixed per-tile cost, ~32 columns' worth).
+static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m) {
+  // pair mode stages BN/2 rows of B per CTA; an MN-major B needs whole 64-element chunks, so
+  // BN = 192 (96 rows) is single-CTA only
   static const int cands[3] = {256, 192, 128};
+  const bool pair = tile_m > kBM;
   int best = 256;
   long long best_cost = -1;
   for (int c = 0; c < 3; ++c) {
+    if (pair && cands[c] == 192) continue;
     const int bn = cands[c];
     long long tiles = 0;
     for (int i = 0; i < n; ++i)
-      tiles += (long long)((probs[i].M + kBM - 1) / kBM) * ((probs[i].N + bn - 1) / bn) * probs[i].splits;
-    const long long waves = (tiles + sms - 1) / sms;
+      tiles += (long long)((probs[i].M + tile_m - 1) / tile_m) * ((probs[i].N + bn - 1) / bn) * probs[i].splits;
+    const long long waves = (tiles + units - 1) / units;
     const long long cost = waves * (bn + 32);
     if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
   }
   return best;
 }
+
+static int g_pair_mode = 1;  // CTA-pair (cta_group::2) tiles for plain epilogues; btp_gemm_set_pair()
+
+}  // namespace btp
+
+extern "C" int btp_gemm_set_pair(int enable) {
+  const int prev = btp::g_pair_mode;
+  btp::g_pair_mode = enable ? 1 : 0;
+  return prev;
+}
+
+namespace btp {
 
 int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream) {
   if (n <= 0 || n > kMaxProblems) return BTP_ERR_DIM;
@@ -463,7 +527,16 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
   }
   int slots = 1;
   for (int i = 0; i < n; ++i) slots = probs[i].epilogue == kEpiSwigluBwd ? 2 : slots;
-  const int BN = (bn_hint == 128 || bn_hint == 192 || bn_hint == 256) ? bn_hint : pick_bn(probs, n, num_sms_cached());
+  // pair tiles win on plain epilogues; the residual epilogue measured slower with them (its
+  // 128-row-per-CTA aux prefetch does not overlap as well), so those launches stay single-CTA
+  bool any_resid = false;
+  for (int i = 0; i < n; ++i) any_resid = any_resid || probs[i].resid != nullptr;
+  const bool pair = g_pair_mode && slots == 1 && !any_resid && num_sms_cached() >= 2;
+  const int tile_m = pair ? 2 * kBM : kBM;
+  const int units = pair ? num_sms_cached() / 2 : num_sms_cached();
+  int BN = (bn_hint == 128 || bn_hint == 192 || bn_hint == 256) ? bn_hint : pick_bn(probs, n, units, tile_m);
+  if (pair && BN == 192) BN = 256;
+  const int b_rows = pair ? BN / 2 : BN;  // rows of B each CTA stages
   DevParams P;
   memset(&P, 0, sizeof(P));
   int tiles = 0;
@@ -474,12 +547,12 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     if (!q.a_mn) rc = make_tmap(&d.tma_a, q.a, q.K, q.M, q.lda, kBK, kBM);
     else         rc = make_tmap(&d.tma_a, q.a, q.M, q.K, q.lda, 64, kBK);
     if (rc) return rc;
-    if (!q.b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN);
+    if (!q.b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, b_rows);
     else         rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
     if (rc) return rc;
     d.a_mn = q.a_mn != 0;
     d.b_mn = q.b_mn != 0;
-    d.idesc = make_idesc_bf16_f32(kBM, BN, d.a_mn, d.b_mn);
+    d.idesc = make_idesc_bf16_f32(tile_m, BN, d.a_mn, d.b_mn);
     rc = make_tmap(&d.tma_c, q.c, q.N, q.M, q.ldc, q.c_fp32 ? 32 : 64, 32, q.c_fp32 != 0);
     if (rc) return rc;
     if (q.resid) {
@@ -498,7 +571,7 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     d.resid = reinterpret_cast<const __nv_bfloat16*>(q.resid);
     d.ld_resid = q.ld_resid;
     d.M = q.M; d.N = q.N; d.K = q.K;
-    d.m_tiles = (q.M + kBM - 1) / kBM;
+    d.m_tiles = (q.M + tile_m - 1) / tile_m;
     d.n_tiles = (q.N + BN - 1) / BN;
     d.k_blocks = (q.K + kBK - 1) / kBK;
     d.splits = q.splits;
@@ -511,16 +584,22 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
   }
   P.num_problems = n;
   P.total_tiles = tiles;
-  int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
-  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (slots == 2) {
-    if (BN == 256) return launch<256, 2>(P, grid, stream);
-    if (BN == 192) return launch<192, 2>(P, grid, stream);
-    return launch<128, 2>(P, grid, stream);
+  int grid_units = tiles < units ? tiles : units;
+  if (max_ctas > 0 && grid_units > max_ctas) grid_units = max_ctas;
+  if (pair) {
+    const int grid = 2 * grid_units;
+    if (BN == 256) return launch<256, 1, true>(P, grid, stream);
+    return launch<128, 1, true>(P, grid, stream);
   }
-  if (BN == 256) return launch<256, 1>(P, grid, stream);
-  if (BN == 192) return launch<192, 1>(P, grid, stream);
-  return launch<128, 1>(P, grid, stream);
+  const int grid = grid_units;
+  if (slots == 2) {
+    if (BN == 256) return launch<256, 2, false>(P, grid, stream);
+    if (BN == 192) return launch<192, 2, false>(P, grid, stream);
+    return launch<128, 2, false>(P, grid, stream);
+  }
+  if (BN == 256) return launch<256, 1, false>(P, grid, stream);
+  if (BN == 192) return launch<192, 1, false>(P, grid, stream);
+  return launch<128, 1, false>(P, grid, stream);
 }
 
 }  // namespace btp

@@ -125,6 +125,11 @@ def gemm(*problems: Gemm, bn: int = 0) -> None:
         _native.call("btp_gemm", arr, len(problems), bn, _stream())
 
 
+def set_pair_mode(enable: bool) -> bool:
+    """CTA-pair (cta_group::2) GEMM tiles on/off; returns the previous setting."""
+    return bool(_native.load().btp_gemm_set_pair(int(enable)))
+
+
 def zero(t: torch.Tensor) -> None:
     _native.call("btp_zero", _p(t), t.numel() * t.element_size(), _stream())
 

@@ -38,10 +38,10 @@ def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q):
         from paper_2512_12131_b200.plan import Strategy, plan
 
         b, s = 2, 64
-        variant = Variant.COLA
+        variant = Variant.FULL_RANK if strategy == "full-rank" else Variant.COLA
         blk, x, G, _ = inputs(SMALL, variant, b, s)
-        pl = plan(Strategy(strategy), SMALL, RunShape(b, s, world), variant, online_norm=online, grouping=grouping,
-                  lowrank_ckpt=ckpt)
+        pl = plan(Strategy(strategy), SMALL, RunShape(b, s, world), None if strategy == "full-rank" else variant,
+                  online_norm=online, grouping=grouping, lowrank_ckpt=ckpt)
         st = train_step(pl, blk, x, G)
         q.put((rank, st.y.values, st.loss, st.dx, st.grads, st.trace.record_tuples("forward"),
                st.trace.record_tuples("backward"), st.trace.record_tuples("reforward"), None))
@@ -120,3 +120,27 @@ def test_vanilla_tp2_matches_oracle(strategy):
         for n in O.PROJECTIONS:
             assert rel(grads["B"][n], g_ref["B"][n][idx, :]) < BF16_TOL, (rank, "B", n)
             assert rel(grads["A"][n], g_ref["A"][n][:, idx]) < BF16_TOL, (rank, "A", n)
+
+
+def test_full_rank_tp2_matches_oracle():
+    """Megatron column->row TP=2 of the full-rank block (the comparison point) vs the oracle."""
+    from tests.gpu_util import BF16_TOL, SMALL, inputs, oracle_step, rel
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import Variant
+
+    b, s = 2, 64
+    res = _run_tp2("full-rank", True, False, False)
+    blk, x, G, oblk = inputs(SMALL, Variant.FULL_RANK, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, sharded=False)
+    dl, fl = SMALL.d // 2, SMALL.d_ff // 2
+    for rank, (_, y, loss, dx, grads, fwd, bwd, *_r) in res.items():
+        assert rel(y.reshape(-1, SMALL.d), y_ref) < BF16_TOL
+        assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
+        assert rel(dx, g_ref["dx"]) < BF16_TOL
+        sl, fsl = slice(rank * dl, (rank + 1) * dl), slice(rank * fl, (rank + 1) * fl)
+        want = {"q": g_ref["W"]["q"][sl], "k": g_ref["W"]["k"][sl], "v": g_ref["W"]["v"][sl],
+                "o": g_ref["W"]["o"][:, sl], "gate": g_ref["W"]["gate"][fsl], "up": g_ref["W"]["up"][fsl],
+                "down": g_ref["W"]["down"][:, fsl]}
+        for n, w in want.items():
+            assert rel(grads["W"][n], w) < BF16_TOL, (rank, n)
+        assert [r[0] for r in fwd] == ["attn", "mlp"]
