@@ -240,9 +240,17 @@ def run_ours(args, cfg):
         Path(args.dump_gemms).write_text(json.dumps(gemm["per_launch"], indent=1))
     peak_burst, peak_sus, hbm, peak_kind = _peaks()
     flops = flops_per_step(cfg, b, s, lowrank=variant is not Variant.FULL_RANK) / tp
+    traffic, traffic_src = None, None
+    tfile = ROOT / "profiles" / "r01_gemm_traffic_summary.json"
+    if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp":
+        t = json.loads(tfile.read_text())
+        traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
     roof = {"bound": "tensor", "kernel": "btp gemm_kernel (all tcgen05 GEMM launches of one step)",
             "achieved": gemm["tflops"], "peak": peak_sus, "unit": "TFLOP/s", "frac": gemm["tflops"] / peak_sus,
-            "traffic": None, "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
+            "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write, ncu)", "traffic_source": traffic_src,
+            "algorithmic_flops_per_launch": gemm["flops"] / max(gemm["launches"], 1),
+            "avg_launch_us": gemm["ms"] * 1e3 / max(gemm["launches"], 1),
+            "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
             "gemm_share_of_step": gemm["ms"] / ms, "gemm_launches_per_step": gemm["launches"],
             "step_frac_of_peak": flops / (ms / 1e3) / 1e12 / peak_sus}
 

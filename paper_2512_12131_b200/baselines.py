@@ -238,11 +238,16 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
                               "fp32" if precision == "fp32" else attn_backend)
         sl, fsl = slice(rk * self.dl, (rk + 1) * self.dl), slice(rk * self.fl, (rk + 1) * self.fl)
         Wf = {n: t.values for n, t in block.full.items()}
+        # d_ff shard padded to a multiple of 8 for 16-byte TMA strides (exact: zero rows / columns)
+        self.flp = -(-self.fl // 8) * 8
+        pad = self.flp - self.fl
+        rows = (lambda a: np.pad(a, ((0, pad), (0, 0)))) if pad else (lambda a: a)
+        cols = (lambda a: np.pad(a, ((0, 0), (0, pad)))) if pad else (lambda a: a)
         self.W = {
-            "qkv": self._dev(np.concatenate([Wf[n][sl, :] for n in "qkv"])),          # [3dl, d] col-parallel
-            "o": self._dev(Wf["o"][:, sl]),                                            # [d, dl]  row-parallel
-            "gu": self._dev(np.concatenate([Wf["gate"][fsl, :], Wf["up"][fsl, :]])),  # [2fl, d]
-            "down": self._dev(Wf["down"][:, fsl]),                                     # [d, fl]
+            "qkv": self._dev(np.concatenate([Wf[n][sl, :] for n in "qkv"])),                   # [3dl, d] col-parallel
+            "o": self._dev(Wf["o"][:, sl]),                                                     # [d, dl]  row-parallel
+            "gu": self._dev(np.concatenate([rows(Wf["gate"][fsl, :]), rows(Wf["up"][fsl, :])])),  # [2flp, d]
+            "down": self._dev(cols(Wf["down"][:, fsl])),                                        # [d, flp]
         }
         self.gamma1 = self._dev(block.gamma1.values, F32)
         self.gamma2 = self._dev(block.gamma2.values, F32)
@@ -260,7 +265,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
                 self._gemm(K.Gemm(inp, Wcat[i * n:(i + 1) * n], out[:, i * n:(i + 1) * n]))
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        T, d, dl, fl = self.T, self.d, self.dl, self.fl
+        T, d, dl, fl = self.T, self.d, self.dl, self.flp
         self.comm.pass_tag = "forward"
         W = self.W
         n1, s1 = self._rnorm(x, self.gamma1, 1)
@@ -286,7 +291,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
         return y
 
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
-        S, W, G, T, d, dl, fl = self.saved, self.W, self.grad, self.T, self.d, self.dl, self.fl
+        S, W, G, T, d, dl, fl = self.saved, self.W, self.grad, self.T, self.d, self.dl, self.flp
         self.comm.pass_tag = "backward"
         dgu = self.buf("dgu", (T, 2 * fl))
         g, u = S["gu"][:, :fl], S["gu"][:, fl:]
@@ -322,7 +327,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
 
     def weight_grads_by_name(self):
         g = {k: v.double().cpu().numpy() for k, v in self.grad.items()}
-        dl, fl = self.dl, self.fl
+        dl, fl, flp = self.dl, self.fl, self.flp
         W = {"q": g["qkv"][:dl], "k": g["qkv"][dl:2 * dl], "v": g["qkv"][2 * dl:], "o": g["o"],
-             "gate": g["gu"][:fl], "up": g["gu"][fl:], "down": g["down"]}
+             "gate": g["gu"][:fl], "up": g["gu"][flp:flp + fl], "down": g["down"][:, :fl]}
         return {"W": W, "gamma1": g["gamma1"], "gamma2": g["gamma2"]}

@@ -207,6 +207,10 @@ class BTPBlockExecutor(ExecutorBase):
         cfg, tp = self.cfg, self.tp
         self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
         self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
+        # d_ff shard padded to a multiple of 8 (16-byte TMA row strides; e.g. CoLA-1B at TP=8 has
+        # fl = 684): zero rows in the gate/up up-factors and zero columns in the down down-factor
+        # make the padding exact (g = u = act = 0 there, and their gradients are 0).
+        self.flp = -(-self.fl // 8) * 8
         self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
                               "fp32" if precision == "fp32" else attn_backend)
         self._load_weights(block)
@@ -221,14 +225,22 @@ class BTPBlockExecutor(ExecutorBase):
         def dev(a, dtype=None):
             return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype or self.act)
 
+        pad = self.flp - self.fl
+
+        def pad_rows(a):  # [fl, r] -> [flp, r]
+            return np.pad(a, ((0, pad), (0, 0))) if pad else a
+
+        def pad_cols(a):  # [r, fl] -> [r, flp]
+            return np.pad(a, ((0, 0), (0, pad))) if pad else a
+
         self.W = {
             "d_qkv": dev(np.concatenate([B[n][:, sl] for n in ("q", "k", "v")], axis=0)),   # [3r, dl]
             "u_qkv": dev(np.stack([A[n][sl, :] for n in ("q", "k", "v")])),                 # [3, dl, r]
             "d_o": dev(B["o"][:, sl]),                                                       # [r, dl]
             "u_o": dev(A["o"][sl, :]),                                                       # [dl, r]
             "d_gu": dev(np.concatenate([B[n][:, sl] for n in ("gate", "up")], axis=0)),     # [2r, dl]
-            "u_gu": dev(np.stack([A[n][fsl, :] for n in ("gate", "up")])),                  # [2, fl, r]
-            "d_d": dev(B["down"][:, fsl]),                                                   # [r, fl]
+            "u_gu": dev(np.stack([pad_rows(A[n][fsl, :]) for n in ("gate", "up")])),        # [2, flp, r]
+            "d_d": dev(pad_cols(B["down"][:, fsl])),                                         # [r, flp]
             "u_d": dev(A["down"][sl, :]),                                                    # [dl, r]
         }
         self.gamma1 = dev(block.gamma1.values[sl], F32)
@@ -248,9 +260,9 @@ class BTPBlockExecutor(ExecutorBase):
             out["A"][n] = g["u_qkv"][i]
         for i, n in enumerate(("gate", "up")):
             out["B"][n] = g["d_gu"][i * r:(i + 1) * r]
-            out["A"][n] = g["u_gu"][i]
+            out["A"][n] = g["u_gu"][i][:self.fl]
         out["B"]["o"], out["A"]["o"] = g["d_o"], g["u_o"]
-        out["B"]["down"], out["A"]["down"] = g["d_d"], g["u_d"]
+        out["B"]["down"], out["A"]["down"] = g["d_d"][:, :self.fl], g["u_d"]
         return out
 
     # ------------------------------------------------------------------ forward pieces
@@ -337,7 +349,7 @@ class BTPBlockExecutor(ExecutorBase):
     # ------------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x: this rank's residual shard [T, d/tp] bf16. Returns y shard [T, d/tp] bf16."""
-        T, dl, fl, r = self.T, self.dl, self.fl, self.r
+        T, dl, fl, r = self.T, self.dl, self.flp, self.r
         if tuple(x.shape) != (T, dl) or x.dtype != self.act:
             raise PlanError(f"x shard must be {self.act} [{T}, {dl}], got {x.dtype} {tuple(x.shape)}")
         self.comm.pass_tag = "forward"
@@ -385,9 +397,9 @@ class BTPBlockExecutor(ExecutorBase):
         qkv, gu = self._buf["qkv"], self._buf["gu"]
         for i, n in enumerate(names3):
             ws[n] = qkv[i]
-        ws["gate"], ws["up"] = gu[0], gu[1]
+        ws["gate"], ws["up"] = gu[0][:, :self.fl], gu[1][:, :self.fl]
         ws["attn"] = S.get("attn", self._buf.get("attn"))
-        ws["x_mid"], ws["act"], ws["y"] = self._buf["x_mid"], self._buf["act"], self._buf["y"]
+        ws["x_mid"], ws["act"], ws["y"] = self._buf["x_mid"], self._buf["act"][:, :self.fl], self._buf["y"]
         zs = {n: S["z_qkv"][i] for i, n in enumerate(names3)}
         zs.update({n: S["z_gu"][i] for i, n in enumerate(names2)})
         zs["o"], zs["down"] = S["z_o"][0], S["z_d"][0]
@@ -413,7 +425,7 @@ class BTPBlockExecutor(ExecutorBase):
     # ------------------------------------------------------------------ recompute (ckpt)
     def _recompute_mlp_inputs(self):
         """Rebuild x_mid, a_gu, gate/up, act, a_d from x and the stored z's; no collective."""
-        S, W, T, dl, fl = self.saved, self.W, self.T, self.dl, self.fl
+        S, W, T, dl, fl = self.saved, self.W, self.T, self.dl, self.flp
         self.comm.pass_tag = "reforward"
         a_o = self._sigma_only(S["z_o"], ("o",), "a_o_rc")
         x_mid = self.buf("x_mid", (T, dl))
@@ -512,7 +524,7 @@ class BTPBlockExecutor(ExecutorBase):
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
         """dy: upstream gradient of this rank's y shard [T, d/tp] bf16. Returns dx shard and fills
         self.grad (fp32) for every local weight."""
-        S, W, T, dl, fl, r = self.saved, self.W, self.T, self.dl, self.fl, self.r
+        S, W, T, dl, fl, r = self.saved, self.W, self.T, self.dl, self.flp, self.r
         if not S:
             raise RuntimeError("backward called before forward")
         if self.ckpt:

@@ -49,6 +49,29 @@ def test_full_rank_step(grouping):
         (p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
 
 
+@pytest.mark.parametrize("strategy", ["btp", "full-rank"])
+def test_dff_shard_padding(strategy):
+    """d_ff shard not a multiple of 8 (like CoLA-1B at TP=8: 5472/8 = 684): the executors pad the
+    shard with zero rows/columns for TMA alignment; results must be unaffected."""
+    from paper_2512_12131_b200.model import ModelConfig
+
+    cfg = ModelConfig(layers=1, heads=4, d=256, d_ff=612, r=64)
+    b, s = 2, 64
+    variant = Variant.FULL_RANK if strategy == "full-rank" else Variant.COLA
+    blk, x, G, oblk = inputs(cfg, variant, b, s)
+    pl = plan(Strategy(strategy), cfg, RunShape(b, s, 1), None if strategy == "full-rank" else variant,
+              online_norm=strategy == "btp", grouping=True)
+    st = train_step(pl, blk, x, G)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, cfg, b, s, sharded=False)
+    assert rel(st.y.values.reshape(-1, cfg.d), y_ref) < BF16_TOL
+    assert rel(st.dx, g_ref["dx"]) < BF16_TOL
+    grp = ("W",) if strategy == "full-rank" else ("A", "B")
+    for gname in grp:
+        for n in O.PROJECTIONS:
+            assert st.grads[gname][n].shape == g_ref[gname][n].shape, (gname, n)
+            assert rel(st.grads[gname][n], g_ref[gname][n]) < BF16_TOL, (gname, n)
+
+
 @pytest.mark.parametrize("strategy", ["vanilla", "full-rank"])
 def test_baselines_fp32_mode(strategy):
     b, s = 2, 64
