@@ -34,6 +34,8 @@ import numpy as np  # noqa: E402
 
 METRIC = "train tokens/s (fwd+bwd) for CoLA block at TP 1/2/4/8; % of bf16 tensor peak"
 UNIT = "tokens/s"
+# optimizer update inside every timed step (both arms)
+ADAMW = dict(lr=1e-4, b1=0.9, b2=0.95, eps=1e-8, wd=0.1)
 
 
 def _peaks():
@@ -97,20 +99,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------- CPU arm
-def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True):
-    """Oracle port (float64 NumPy, BLAS) fwd+bwd on a bounded sample: ONE sequence (b=1) of the
+def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True, optimizer=True):
+    """Oracle port (float64 NumPy, BLAS) fwd+bwd+AdamW on a bounded sample: ONE sequence (b=1) of the
     workload's length s. Returns (tokens_per_s, per-step seconds list, threads)."""
     from oracle import btp_oracle as O
 
     blk = O.build_block(cfg.d, cfg.d_ff, cfg.r, "cola", 0, scale_fan_in=3.0)
     x = O.seeded_fill((s, cfg.d), 10000)
     G = O.loss_projection((s, cfg.d), 30000)
-    times = []
+    times, state = [], {}
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
         y, cache = O.block_forward(blk, x, 1, s, cfg.heads, lean=lean)
-        O.block_backward(blk, cache, G, 1, s, cfg.heads)
+        grads = O.block_backward(blk, cache, G, 1, s, cfg.heads)
+        if optimizer:
+            O.adamw_step(blk, grads, state, **ADAMW)
         times.append(time.perf_counter() - t0)
         if max_steps is not None and len(times) >= max_steps:
             break
@@ -145,10 +149,10 @@ def run_reference(args, cfg):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"CoLA-{args.config} block fwd+bwd, BTP math, b={args.b} s={args.s}",
+        "config": {"workload": f"CoLA-{args.config} block fwd+bwd+AdamW, BTP math, b={args.b} s={args.s}",
                    "sample": f"1 sequence x {args.s} tokens per step (b=1 of {args.b})"},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"b=1 s={args.s} CoLA-{args.config} block fwd+bwd per step, float64 NumPy/BLAS "
+                         "sample": f"b=1 s={args.s} CoLA-{args.config} block fwd+bwd+AdamW per step, float64 NumPy/BLAS "
                                    "restatement of btpsim (reference itself is forward-only)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -185,7 +189,8 @@ def run_ours(args, cfg):
     blk = fan_in_scaled(build_block(cfg, variant, 0))
     x = seeded_fill((b, s, cfg.d), 10000).values
     G = seeded_fill((b, s, cfg.d), 30000).values
-    trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn)
+    trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
+                           optimizer=not args.no_optimizer)
     x_dev, g_dev = trainer.device_inputs(x, G)
 
     def barrier():
@@ -258,12 +263,15 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform inputs, fan-in-scaled random init)",
-        "config": {"workload": f"CoLA-{args.config} decoder block fwd+bwd, {strategy.value} "
+        "config": {"workload": f"CoLA-{args.config} decoder block fwd+bwd{'' if args.no_optimizer else '+AdamW'}, "
+                               f"{strategy.value} "
                                f"{'grouped ' if pl.grouping else ''}{'online-RMSNorm ' if pl.norm_mode.value == 'online' else ''}"
                                f"TP={tp}{' lowrank-ckpt' if pl.lowrank_ckpt else ''}",
                    "d": cfg.d, "d_ff": cfg.d_ff, "r": cfg.r, "heads": cfg.heads, "global_batch": b, "seq_len": s,
                    "tokens_per_step": b * s, "parallelism": f"tp{tp}", "l2": "inputs larger than L2 (no flush)",
-                   "cuda_graph": trainer.graphed, "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
+                   "cuda_graph": trainer.graphed,
+                   "optimizer": None if args.no_optimizer else dict(ADAMW, kind="AdamW fp32 master+moments, fused"),
+                   "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
@@ -274,7 +282,7 @@ def run_ours(args, cfg):
         rate, times, threads = cpu_oracle_rate(cfg, s, seconds_budget=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"b=1 s={s} (1 of {b} sequences) CoLA-{args.config} block fwd+bwd, float64 "
-                                          f"NumPy/BLAS oracle, {len(times)} steps"}
+                                          f"NumPy/BLAS oracle + AdamW, {len(times)} steps"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -295,6 +303,7 @@ def main(argv=None):
     ap.add_argument("--ckpt", action="store_true")
     ap.add_argument("--no-grouping", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-optimizer", action="store_true", help="drop the AdamW update from the step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")

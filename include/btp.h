@@ -189,6 +189,22 @@ int btp_add_f32(const void* a, long long lda, const void* b, long long ldb, void
 int btp_dot_f32(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
                 int max_blocks, int* nblk, void* stream);
 
+/* Fused AdamW over a flat parameter set of n elements (n % 8 == 0): fp32 master weights, fp32
+ * first/second moments and fp32 gradients are updated in one pass and the working copy the
+ * GEMMs read (bf16 for btp_adamw, fp32 for btp_adamw_f32) is rewritten from the master:
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr * ( (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps) + wd * p )
+ * step is read from *step_dev when non-NULL (so a replayed CUDA graph keeps advancing it; bump it
+ * with btp_counter_add after the update), else from `step`.
+ * (the optimizer step over the sharded low-rank factors; absent in the reference.) */
+int btp_adamw(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1,
+              float b2, float eps, float wd, int step, const int* step_dev, void* stream);
+int btp_adamw_f32(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1,
+                  float b2, float eps, float wd, int step, const int* step_dev, void* stream);
+
+/* *ctr += delta on the stream (device-side step counters). */
+int btp_counter_add(int* ctr, int delta, void* stream);
+
 /* Zero `bytes` bytes of device memory on the stream (split-K reduce-add targets). */
 int btp_zero(void* ptr, long long bytes, void* stream);
 

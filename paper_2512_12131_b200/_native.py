@@ -42,6 +42,9 @@ EXPORTED_SYMBOLS = (
     "btp_rmsnorm_bwd_prep",
     "btp_dot",
     "btp_zero",
+    "btp_adamw",
+    "btp_adamw_f32",
+    "btp_counter_add",
     "btp_num_sms",
     "btp_version",
     # fp32 parity-mode twins
@@ -122,6 +125,9 @@ _SIGNATURES = {
     "btp_version": [],
     "btp_gemm_f32": [ctypes.POINTER(GemmProblem), _I, _P],
     "btp_gemm_set_pair": [_I],
+    "btp_adamw": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
+    "btp_adamw_f32": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
+    "btp_counter_add": [_P, _I, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot"):

@@ -153,7 +153,8 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
 
 class BlockTrainer:
     """Persistent block training step on this rank: weights, activations and workspaces stay
-    resident in HBM; one step = forward + loss + backward. At tp == 1 the whole step is captured
+    resident in HBM; one step = forward + loss + backward + fused AdamW update of this rank's
+    parameter shard (fp32 master weights and moments; `optimizer=False` drops the update). At tp == 1 the whole step is captured
     once into a CUDA graph and replayed (the step is ~60 kernel launches).
 
     step_device(x, G): device-resident inputs, no host sync (the bench's `value`).
@@ -164,9 +165,12 @@ class BlockTrainer:
     one CUDA graph each), and every step's loss is read back (the bench's `e2e`)."""
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
-                 attn_backend: str = "auto", use_graph: bool = True):
+                 attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
+                 optimizer: bool = True):
         self.pl = pl
         self.ex = make_executor(pl, block, eps=eps, attn_backend=attn_backend)
+        # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
+        self.adamw = dict(adamw or {}) if optimizer else None
         self.use_graph = use_graph and pl.shape.tp == 1
         self.graphs: dict = {}
         self.graphed = False
@@ -193,6 +197,8 @@ class BlockTrainer:
         y = self.ex.forward(x)
         self.loss_buf = self.ex.loss_device(y, g)
         self.ex.backward(g)
+        if self.adamw is not None:
+            self.ex.optimizer_step(**self.adamw)
 
     def step_device(self, x: torch.Tensor, g: torch.Tensor) -> None:
         if not self.use_graph:
@@ -201,7 +207,8 @@ class BlockTrainer:
         key = (x.data_ptr(), g.data_ptr())
         graph = self.graphs.get(key)
         if graph is None:
-            # eager warm-up allocates every buffer, then capture one step into a graph
+            # the first step runs eagerly (allocating every buffer); one step is then captured into
+            # a graph (capture executes nothing) that later calls replay
             before = self.ex.stats.kernel_launches
             self._eager(x, g)
             self._per_step_launches = self.ex.stats.kernel_launches - before
@@ -216,6 +223,7 @@ class BlockTrainer:
                 self.ex.stats.kernel_launches = saved
             torch.cuda.current_stream().wait_stream(side)
             self.graphs[key], self.graphed = graph, True
+            return
         graph.replay()
         self._replays += 1
 

@@ -89,6 +89,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         }
         self.grad["gamma1"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
         self.grad["gamma2"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+        self._flatten_params()
 
     # ------------------------------------------------------------------ one vanilla chunk group
     def _pair(self, names, inp, Wd, Wu, out_full, chunk_id):
@@ -254,6 +255,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.grad = {k: torch.zeros(v.shape, device=self.dev, dtype=F32) for k, v in self.W.items()}
         self.grad["gamma1"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
         self.grad["gamma2"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
+        self._flatten_params()
 
     def _col(self, inp, Wcat, out, k):
         """Column-parallel GEMM(s): grouped = one launch over the concatenated weight."""

@@ -34,4 +34,7 @@ int add(const void* a, long long lda, const void* b, long long ldb, void* out, l
         cudaStream_t st, bool f32);
 int dot(const void* a, long long lda, const void* b, long long ldb, int rows, int cols, float* partial,
         int max_blocks, int* nblk_out, cudaStream_t st, bool f32);
+int adamw(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1, float b2,
+          float eps, float wd, int step, const int* step_dev, cudaStream_t st, bool f32);
+int counter_add(int* ctr, int delta, cudaStream_t st);
 }  // namespace btp

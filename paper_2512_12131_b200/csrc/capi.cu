@@ -98,6 +98,14 @@ BTP_PAIR(btp_dot, dot,
           int max_blocks, int* nblk, void* stream),
          A_DOT)
 
+#define A_ADAMW(f32) (master, m, v, g, work, n, lr, b1, b2, eps, wd, step, step_dev, ST(stream), f32)
+BTP_PAIR(btp_adamw, adamw,
+         (float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1, float b2,
+          float eps, float wd, int step, const int* step_dev, void* stream),
+         A_ADAMW)
+
+int btp_counter_add(int* ctr, int delta, void* stream) { return btp::counter_add(ctr, delta, ST(stream)); }
+
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,
                     const float* col_scale, float* out, long long ldo, int accumulate, void* stream) {
   return btp::reduce_rows(in, splits, split_stride, ldi, rows, cols, col_scale, out, ldo, accumulate, ST(stream));

@@ -559,6 +559,49 @@ __global__ void __launch_bounds__(256) dot_kernel(const T* __restrict__ a, long 
   }
 }
 
+// ----------------------------------------------------------------------------- fused AdamW
+// One pass over a flat parameter set: fp32 master weights, fp32 moments, fp32 gradients, and the
+// working copy the GEMMs read (bf16, or fp32 in parity mode) rewritten from the master.
+//   m = b1 m + (1-b1) g ; v = b2 v + (1-b2) g^2 ; p -= lr (m/bc1 / (sqrt(v/bc2) + eps) + wd p)
+template <typename T>
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master, float* __restrict__ m,
+                                                    float* __restrict__ v, const float* __restrict__ g,
+                                                    T* __restrict__ work, long long n, float lr, float b1, float b2,
+                                                    float eps, float wd, int step_host,
+                                                    const int* __restrict__ step_dev) {
+  // the step count may live on the device so a replayed CUDA graph keeps advancing it
+  const float step = (float)(step_dev ? *step_dev : step_host);
+  const float bc1 = 1.0f - powf(b1, step), bc2 = 1.0f - powf(b2, step);
+  const long long n8 = n >> 3;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long o = i * 8;
+    float p[8], mm[8], vv[8], gg[8];
+    *reinterpret_cast<float4*>(p) = reinterpret_cast<const float4*>(master + o)[0];
+    *reinterpret_cast<float4*>(p + 4) = reinterpret_cast<const float4*>(master + o)[1];
+    *reinterpret_cast<float4*>(mm) = reinterpret_cast<const float4*>(m + o)[0];
+    *reinterpret_cast<float4*>(mm + 4) = reinterpret_cast<const float4*>(m + o)[1];
+    *reinterpret_cast<float4*>(vv) = reinterpret_cast<const float4*>(v + o)[0];
+    *reinterpret_cast<float4*>(vv + 4) = reinterpret_cast<const float4*>(v + o)[1];
+    *reinterpret_cast<float4*>(gg) = reinterpret_cast<const float4*>(g + o)[0];
+    *reinterpret_cast<float4*>(gg + 4) = reinterpret_cast<const float4*>(g + o)[1];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      mm[j] = b1 * mm[j] + (1.0f - b1) * gg[j];
+      vv[j] = b2 * vv[j] + (1.0f - b2) * gg[j] * gg[j];
+      const float upd = (mm[j] / bc1) / (sqrtf(vv[j] / bc2) + eps) + wd * p[j];
+      p[j] -= lr * upd;
+    }
+    reinterpret_cast<float4*>(master + o)[0] = *reinterpret_cast<float4*>(p);
+    reinterpret_cast<float4*>(master + o)[1] = *reinterpret_cast<float4*>(p + 4);
+    reinterpret_cast<float4*>(m + o)[0] = *reinterpret_cast<float4*>(mm);
+    reinterpret_cast<float4*>(m + o)[1] = *reinterpret_cast<float4*>(mm + 4);
+    reinterpret_cast<float4*>(v + o)[0] = *reinterpret_cast<float4*>(vv);
+    reinterpret_cast<float4*>(v + o)[1] = *reinterpret_cast<float4*>(vv + 4);
+    store8(work + o, p);
+  }
+}
+
 // ============================================================================= launchers
 static inline int grid_for(long long items, int threads = 256) {
   const long long want = (items + threads - 1) / threads;
@@ -772,6 +815,27 @@ int add(const void* a, long long lda, const void* b, long long ldb, void* out, l
   else
     add_kernel<bf16><<<grid, 256, 0, st>>>(static_cast<const bf16*>(a), lda, static_cast<const bf16*>(b), ldb,
                                            static_cast<bf16*>(out), ldo, rows, cols);
+  BTP_CHECK_LAUNCH();
+}
+
+int adamw(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1, float b2,
+          float eps, float wd, int step, const int* step_dev, cudaStream_t st, bool f32) {
+  if (n <= 0 || (step_dev == nullptr && step <= 0)) return BTP_ERR_DIM;
+  if (n % 8 || !al16(master) || !al16(m) || !al16(v) || !al16(g) || !al16(work)) return BTP_ERR_ALIGNMENT;
+  const int grid = grid_for(n / 8);
+  if (f32)
+    adamw_kernel<float><<<grid, 256, 0, st>>>(master, m, v, g, static_cast<float*>(work), n, lr, b1, b2, eps, wd, step,
+                                              step_dev);
+  else
+    adamw_kernel<bf16><<<grid, 256, 0, st>>>(master, m, v, g, static_cast<bf16*>(work), n, lr, b1, b2, eps, wd, step,
+                                             step_dev);
+  BTP_CHECK_LAUNCH();
+}
+
+__global__ void counter_add_kernel(int* c, int delta) { *c += delta; }
+
+int counter_add(int* ctr, int delta, cudaStream_t st) {
+  counter_add_kernel<<<1, 1, 0, st>>>(ctr, delta);
   BTP_CHECK_LAUNCH();
 }
 

@@ -98,6 +98,62 @@ class ExecutorBase:
     def _dev(self, a, dtype=None) -> torch.Tensor:
         return torch.from_numpy(np.ascontiguousarray(a)).to(self.dev, dtype or self.act)
 
+    # ------------------------------------------------------------------ flat parameters + AdamW
+    def _flatten_params(self) -> None:
+        """Re-home every working weight as a view of ONE flat buffer (GEMM operand dtype) and every
+        weight gradient as a view of ONE flat fp32 buffer (segments 8-element aligned), and the
+        two gammas likewise, so the optimizer update is a single fused launch per group."""
+
+        def flat(groups, wdtype):
+            segs, total = [], 0
+            for key, idx, t in groups:
+                segs.append((key, idx, t, total))
+                total += -(-t.numel() // 8) * 8
+            wf = torch.zeros(total, dtype=wdtype, device=self.dev)
+            gf = torch.zeros(total, dtype=F32, device=self.dev)
+            views = []
+            for key, idx, t, off in segs:
+                wv = wf[off:off + t.numel()].view(t.shape)
+                wv.copy_(t)
+                views.append((key, idx, wv, gf[off:off + t.numel()].view(t.shape)))
+            return wf, gf, views
+
+        lin = []
+        for k, v in self.W.items():
+            for i, t in enumerate(v if isinstance(v, list) else [v]):
+                lin.append((k, i if isinstance(v, list) else None, t))
+        self.w_flat, self.g_flat, views = flat(lin, self.act)
+        W, G = {}, {}
+        for key, idx, wv, gv in views:
+            if idx is None:
+                W[key], G[key] = wv, gv
+            else:
+                W.setdefault(key, []).append(wv)
+                G.setdefault(key, []).append(gv)
+        self.gam_flat, self.gam_grad_flat, gviews = flat([("gamma1", None, self.gamma1),
+                                                          ("gamma2", None, self.gamma2)], F32)
+        self.gamma1, self.gamma2 = gviews[0][2], gviews[1][2]
+        G["gamma1"], G["gamma2"] = gviews[0][3], gviews[1][3]
+        self.W, self.grad = W, G
+        self.opt = None
+
+    def optimizer_step(self, lr: float = 1e-4, b1: float = 0.9, b2: float = 0.95, eps: float = 1e-8,
+                       wd: float = 0.1) -> None:
+        """AdamW on this rank's shard of the parameters (fp32 master + moments, created lazily):
+        one fused launch for the linear factors, one for the norm gains (no weight decay)."""
+        if self.opt is None:
+            z = lambda t: torch.zeros(t.numel(), dtype=F32, device=self.dev)  # noqa: E731
+            self.opt = {"master": self.w_flat.float().clone(), "m": z(self.w_flat), "v": z(self.w_flat),
+                        "gm": z(self.gam_flat), "gv": z(self.gam_flat),
+                        "step": torch.ones(1, dtype=torch.int32, device=self.dev)}  # device counter, 1-based
+        o = self.opt
+        K.adamw(o["master"], o["m"], o["v"], self.g_flat, self.w_flat, lr=lr, step_dev=o["step"], b1=b1, b2=b2,
+                eps=eps, wd=wd)
+        K.adamw(self.gam_flat, o["gm"], o["gv"], self.gam_grad_flat, self.gam_flat, lr=lr, step_dev=o["step"], b1=b1,
+                b2=b2, eps=eps, wd=0.0)
+        K.counter_add(o["step"], 1)
+        self.stats.kernel_launches += 3
+
     # ------------------------------------------------------------------ buffers
     def buf(self, name: str, shape, dtype=None) -> torch.Tensor:
         dtype = dtype or self.act
@@ -248,6 +304,7 @@ class BTPBlockExecutor(ExecutorBase):
         self.grad = {k: torch.zeros(v.shape, device=self.dev, dtype=F32) for k, v in self.W.items()}
         self.grad["gamma1"] = torch.zeros(self.dl, device=self.dev, dtype=F32)
         self.grad["gamma2"] = torch.zeros(self.dl, device=self.dev, dtype=F32)
+        self._flatten_params()
 
     def weight_grads_by_name(self) -> dict[str, dict[str, np.ndarray]]:
         """Rank-local gradients keyed like the reference block: {'A': {name: [d_out/tp, r]},

@@ -125,6 +125,22 @@ def gemm(*problems: Gemm, bn: int = 0) -> None:
         _native.call("btp_gemm", arr, len(problems), bn, _stream())
 
 
+def adamw(master, m, v, g, work, *, lr, step=0, step_dev=None, b1=0.9, b2=0.95, eps=1e-8, wd=0.0):
+    """Fused AdamW over flat fp32 buffers; rewrites the working copy `work` (bf16 or fp32).
+    step_dev: int32 device counter read for the bias correction (graph-replay safe)."""
+    n = master.numel()
+    for t in (m, v, g, work):
+        if t.numel() != n:
+            raise ValueError("adamw buffers must all hold the same number of elements")
+    _native.call(_fn("btp_adamw", work), _p(master), _p(m), _p(v), _p(g), _p(work), n, ctypes.c_float(lr),
+                 ctypes.c_float(b1), ctypes.c_float(b2), ctypes.c_float(eps), ctypes.c_float(wd), int(step),
+                 _p(step_dev), _stream())
+
+
+def counter_add(ctr, delta: int = 1):
+    _native.call("btp_counter_add", _p(ctr), int(delta), _stream())
+
+
 def set_pair_mode(enable: bool) -> bool:
     """CTA-pair (cta_group::2) GEMM tiles on/off; returns the previous setting."""
     return bool(_native.load().btp_gemm_set_pair(int(enable)))
