@@ -57,6 +57,13 @@ typedef struct btp_gemm_problem {
    * splits is not fixed (fp32 round-off only). split_stride is unused. */
   int reduce_add;
   /* epilogue: 0 = store (with the optional resid add above);
+   *           1 = rank-r boundary with sigma fused (TP = 1, where no all-reduce separates the
+   *               down-projection from the activation): z = scale * acc -> C (bf16),
+   *               a = crossgate(z) -> c2 (bf16), pairs (j, j + sigma_half) within each
+   *               2*sigma_half-wide projection ([silu(u)*v, silu(v)*u], computed from bf16(z)).
+   *               B must be K-major, N % (2*sigma_half) == 0, sigma_half % 64 == 0; no resid,
+   *               split-K or reduce-add; every problem of the launch must use it.
+   *               Replaces btp_fixup_sigma after the GEMM (model.py:189-196).
    *           2 = SwiGLU backward: acc = dact, resid = g (bf16), aux2 = u (bf16),
    *               C = dg = dact*u*silu'(g), c2 = du = dact*silu(g)   (both bf16, no split-K)
    * Aux inputs are TMA-loaded into the epilogue's swizzled staging buffers, prefetched one
@@ -66,6 +73,7 @@ typedef struct btp_gemm_problem {
   long long ld_aux2;
   void* c2;
   long long ldc2;
+  int sigma_half; /* epilogue 1: r/2 (half-width of the crossgate pairs) */
 } btp_gemm_problem;
 
 /* Grouped/batched tcgen05 GEMM: n (1..4) independent problems in ONE persistent launch.

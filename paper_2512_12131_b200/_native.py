@@ -99,6 +99,7 @@ class GemmProblem(ctypes.Structure):
         ("ld_aux2", ctypes.c_longlong),
         ("c2", ctypes.c_void_p),
         ("ldc2", ctypes.c_longlong),
+        ("sigma_half", ctypes.c_int),
     ]
 
 

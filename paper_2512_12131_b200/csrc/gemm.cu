@@ -40,6 +40,7 @@ constexpr int kEpiStageBytes = 32 * 128;              // one warp's 32 rows x 12
 
 // Epilogue modes (per problem)
 constexpr int kEpiStore = 0;      // C = scale * acc (+ resid if given); store or reduce-add
+constexpr int kEpiSigma = 1;      // rank-r boundary at TP=1: C = z = scale*acc, C2 = crossgate(z)
 constexpr int kEpiSwigluBwd = 2;  // acc = dact; aux g (resid slot), u (aux2): C = dg, C2 = du
 
 struct alignas(64) DevProblem {
@@ -62,6 +63,7 @@ struct alignas(64) DevProblem {
   int a_mn, b_mn;   // operand majors (per problem: a launch may mix dgrad and wgrad problems)
   uint32_t idesc;   // tcgen05 instruction descriptor for this problem
   float alpha;
+  int sig_half;     // kEpiSigma: r/2; an N tile = BN/2 "u" columns + the BN/2 "v" columns r/2 later
 };
 
 struct DevParams {
@@ -175,6 +177,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int n0 = tc.n_blk * BN + (int)rank * (BN - C::kBRows);  // this CTA's share of B
         const int kb0 = tc.split * pr.kb_per_split;
         const int kb1 = min(kb0 + pr.kb_per_split, pr.k_blocks);
+        // sigma tiles pair column blocks [u0, u0 + BN/2) and [u0 + r/2, ...) of B (K-major)
+        int u0 = 0;
+        if (pr.epi == kEpiSigma) {
+          const int npp = 2 * pr.sig_half / BN;
+          const int proj = tc.n_blk / npp;
+          u0 = proj * 2 * pr.sig_half + (tc.n_blk - proj * npp) * (BN / 2);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           // pair: both CTAs' bytes complete on the leader's barrier, which expects both halves
@@ -193,7 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
             for (int c = 0; c < kBM / 64; ++c) load(a_dst + c * 64 * kBK * 2, &pr.tma_a, m0 + c * 64, k0);
           }
-          if (!pr.b_mn) {
+          if (pr.epi == kEpiSigma) {
+            if constexpr (kPair) {
+              load(b_dst, &pr.tma_b, k0, u0 + (int)rank * pr.sig_half);  // leader: u rows, peer: v rows
+            } else {
+              load(b_dst, &pr.tma_b, k0, u0);
+              load(b_dst + (BN / 2) * kBK * 2, &pr.tma_b, k0, u0 + pr.sig_half);
+            }
+          } else if (!pr.b_mn) {
             load(b_dst, &pr.tma_b, k0, n0);
           } else {
 #pragma unroll
@@ -286,6 +302,83 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const bool row_ok = row < pr.M;
       float rscale = pr.alpha;
       if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
+      if (kSlots == 2 && pr.epi == kEpiSigma) {  // (launched with two staging slots per buffer)
+        // accumulator columns [0, BN/2) = u block, [BN/2, BN) = v block of the same projection.
+        // Per 64-column step: z_u, z_v -> C from staging buffer 0 (two slots), then
+        // a_u = silu(u) v, a_v = silu(v) u -> C2 from buffer 1; each buffer is reused only after
+        // its previous TMA store group has read it (one group stays in flight).
+        const int hb = BN / 2;
+        const int npp = 2 * pr.sig_half / BN;
+        const int proj = tc.n_blk / npp;
+        const int u0 = proj * 2 * pr.sig_half + (tc.n_blk - proj * npp) * hb;
+        const int v0 = u0 + pr.sig_half;
+        uint8_t* sz0 = slot_ptr(0, 0);
+        uint8_t* sz1 = slot_ptr(0, kSlots - 1);
+        uint8_t* sa0 = slot_ptr(1, 0);
+        uint8_t* sa1 = slot_ptr(1, kSlots - 1);
+        const uint32_t rz0 = smem_u32(sz0) + lane * 128, rz1 = smem_u32(sz1) + lane * 128;
+        const uint32_t ra0 = smem_u32(sa0) + lane * 128, ra1 = smem_u32(sa1) + lane * 128;
+        const uint32_t tbase = tmem_base + ((q * 32u) << 16) + buf * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < hb; c0 += 64) {
+          uint32_t zu[32], zv[32];
+          {
+            uint32_t r[64];
+            tmem_ld_32x32b_x64(tbase + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              zu[j] = pack_bf16(__uint_as_float(r[2 * j]) * rscale, __uint_as_float(r[2 * j + 1]) * rscale);
+            tmem_ld_32x32b_x64(tbase + hb + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              zv[j] = pack_bf16(__uint_as_float(r[2 * j]) * rscale, __uint_as_float(r[2 * j + 1]) * rscale);
+          }
+          if (c0 + 64 >= hb) {
+            // the accumulator is fully in registers: hand the TMEM buffer back to the MMA warp now
+            tc_fence_before();
+            if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[buf], 0);
+            else mbar_arrive(&tempty_bar[buf]);
+          }
+          if (lane == 0) bulk_wait_read<1>();  // the z buffer's previous group has been read
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            st_shared_v4(rz0 + ((g ^ row_sw) << 4), zu[4 * g], zu[4 * g + 1], zu[4 * g + 2], zu[4 * g + 3]);
+            st_shared_v4(rz1 + ((g ^ row_sw) << 4), zv[4 * g], zv[4 * g + 1], zv[4 * g + 2], zv[4 * g + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pr.tma_c, sz0, u0 + c0, out_row0);
+            tma_store_2d(&pr.tma_c, sz1, v0 + c0, out_row0);
+            bulk_commit();
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float ul = bf16_lo(zu[j]), uh = bf16_hi(zu[j]);
+            const float vl = bf16_lo(zv[j]), vh = bf16_hi(zv[j]);
+            zu[j] = pack_bf16(silu_fast(ul) * vl, silu_fast(uh) * vh);
+            zv[j] = pack_bf16(silu_fast(vl) * ul, silu_fast(vh) * uh);
+          }
+          if (lane == 0) bulk_wait_read<1>();  // the a buffer's previous group has been read
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            st_shared_v4(ra0 + ((g ^ row_sw) << 4), zu[4 * g], zu[4 * g + 1], zu[4 * g + 2], zu[4 * g + 3]);
+            st_shared_v4(ra1 + ((g ^ row_sw) << 4), zv[4 * g], zv[4 * g + 1], zv[4 * g + 2], zv[4 * g + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pr.tma_c2, sa0, u0 + c0, out_row0);
+            tma_store_2d(&pr.tma_c2, sa1, v0 + c0, out_row0);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < n_valid; c0 += cols_per_chunk, ++chunk_seq) {
         const int b = chunk_seq & 1;
@@ -477,15 +570,16 @@ static int launch(const DevParams& P, int grid, cudaStream_t stream) {
 
 // N-tile choice: persistent units (CTAs, or CTA pairs) run ceil(tiles / units) waves of tiles
 // whose mainloop time is ~ proportional to BN (+ a fixed per-tile cost, ~32 columns' worth).
-static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m) {
+static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, int sig_span) {
   // pair mode stages BN/2 rows of B per CTA; an MN-major B needs whole 64-element chunks, so
   // BN = 192 (96 rows) is single-CTA only
   static const int cands[3] = {256, 192, 128};
   const bool pair = tile_m > kBM;
-  int best = 256;
+  int best = sig_span && sig_span % 256 ? 128 : 256;
   long long best_cost = -1;
   for (int c = 0; c < 3; ++c) {
     if (pair && cands[c] == 192) continue;
+    if (sig_span && sig_span % cands[c]) continue;  // a sigma tile must not straddle two projections
     const int bn = cands[c];
     long long tiles = 0;
     for (int i = 0; i < n; ++i)
@@ -520,22 +614,32 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     if (q.resid && (q.c_fp32 || q.ld_resid % 8)) return BTP_ERR_DIM;
     // split-K accumulates through TMA reduce-add into a zero-initialised fp32 output
     if (q.splits > 1 && !q.reduce_add) return BTP_ERR_DIM;
-    if (q.epilogue != kEpiStore && q.epilogue != kEpiSwigluBwd) return BTP_ERR_DIM;
+    if (q.epilogue != kEpiStore && q.epilogue != kEpiSigma && q.epilogue != kEpiSwigluBwd) return BTP_ERR_DIM;
+    if ((q.epilogue == kEpiSigma) != (probs[0].epilogue == kEpiSigma)) return BTP_ERR_DIM;  // homogeneous
+    if (q.epilogue == kEpiSigma &&
+        (q.c_fp32 || q.splits > 1 || q.reduce_add || q.resid || q.b_mn || !q.c2 || q.ldc2 % 8 ||
+         q.sigma_half <= 0 || q.sigma_half % 64 || q.N % (2 * q.sigma_half) ||
+         q.sigma_half != probs[0].sigma_half))
+      return BTP_ERR_DIM;
     if (q.epilogue == kEpiSwigluBwd &&
         (!q.resid || !q.aux2 || !q.c2 || q.c_fp32 || q.splits > 1 || q.reduce_add || q.ld_aux2 % 8 || q.ldc2 % 8))
       return BTP_ERR_DIM;
   }
   int slots = 1;
-  for (int i = 0; i < n; ++i) slots = probs[i].epilogue == kEpiSwigluBwd ? 2 : slots;
+  for (int i = 0; i < n; ++i) slots = probs[i].epilogue != kEpiStore ? 2 : slots;
+  const bool sigma = probs[0].epilogue == kEpiSigma;
   // pair tiles win on plain epilogues; the residual epilogue measured slower with them (its
   // 128-row-per-CTA aux prefetch does not overlap as well), so those launches stay single-CTA
   bool any_resid = false;
   for (int i = 0; i < n; ++i) any_resid = any_resid || probs[i].resid != nullptr;
-  const bool pair = g_pair_mode && slots == 1 && !any_resid && num_sms_cached() >= 2;
+  const bool pair = g_pair_mode && (slots == 1 || sigma) && !any_resid && num_sms_cached() >= 2;
   const int tile_m = pair ? 2 * kBM : kBM;
   const int units = pair ? num_sms_cached() / 2 : num_sms_cached();
-  int BN = (bn_hint == 128 || bn_hint == 192 || bn_hint == 256) ? bn_hint : pick_bn(probs, n, units, tile_m);
+  const int sig_span = probs[0].epilogue == kEpiSigma ? 2 * probs[0].sigma_half : 0;
+  int BN = (bn_hint == 128 || bn_hint == 192 || bn_hint == 256) ? bn_hint
+                                                                 : pick_bn(probs, n, units, tile_m, sig_span);
   if (pair && BN == 192) BN = 256;
+  if (sig_span && (BN == 192 || sig_span % BN)) return BTP_ERR_DIM;
   const int b_rows = pair ? BN / 2 : BN;  // rows of B each CTA stages
   DevParams P;
   memset(&P, 0, sizeof(P));
@@ -547,7 +651,8 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
     if (!q.a_mn) rc = make_tmap(&d.tma_a, q.a, q.K, q.M, q.lda, kBK, kBM);
     else         rc = make_tmap(&d.tma_a, q.a, q.M, q.K, q.lda, 64, kBK);
     if (rc) return rc;
-    if (!q.b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, b_rows);
+    if (q.epilogue == kEpiSigma) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, BN / 2);
+    else if (!q.b_mn) rc = make_tmap(&d.tma_b, q.b, q.K, q.N, q.ldb, kBK, b_rows);
     else         rc = make_tmap(&d.tma_b, q.b, q.N, q.K, q.ldb, 64, kBK);
     if (rc) return rc;
     d.a_mn = q.a_mn != 0;
@@ -560,6 +665,11 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
       if (rc) return rc;
     }
     d.epi = q.epilogue;
+    d.sig_half = q.epilogue == kEpiSigma ? q.sigma_half : 0;
+    if (q.epilogue == kEpiSigma) {
+      rc = make_tmap(&d.tma_c2, q.c2, q.N, q.M, q.ldc2, 64, 32);
+      if (rc) return rc;
+    }
     if (q.epilogue == kEpiSwigluBwd) {
       rc = make_tmap(&d.tma_r2, q.aux2, q.N, q.M, q.ld_aux2, 64, 32);
       if (rc) return rc;
@@ -588,6 +698,7 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
   if (max_ctas > 0 && grid_units > max_ctas) grid_units = max_ctas;
   if (pair) {
     const int grid = 2 * grid_units;
+    if (slots == 2) return BN == 256 ? launch<256, 2, true>(P, grid, stream) : launch<128, 2, true>(P, grid, stream);
     if (BN == 256) return launch<256, 1, true>(P, grid, stream);
     return launch<128, 1, true>(P, grid, stream);
   }

@@ -282,6 +282,16 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t targ
 }
 
 // ---------------------------------------------------------------- misc math
+// silu(x) = x * sigmoid(x) = 0.5 x (1 + tanh(x / 2)) on the MUFU tanh unit (one SFU op; relative
+// error ~2^-11, below the bf16 output rounding). For GEMM epilogues, where 4 warps per SM must
+// transform a whole 128 x BN tile while the next tile's mainloop runs.
+__device__ __forceinline__ float silu_fast(float x) {
+  const float h = 0.5f * x;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+  return fmaf(h, t, h);
+}
+
 __device__ __forceinline__ float sigmoidf_safe(float x) {
   // exp of a non-positive argument only, as the reference sigmoid (tensor.py:121-124)
   const float e = __expf(-fabsf(x));

@@ -44,6 +44,8 @@ _VAR = {Variant.SVD: 0, Variant.COLA: 1}
 # bf16: the training path (tcgen05 GEMMs, bf16 activations, fp32 statistics / accumulation);
 # fp32: the parity mode (exact-fp32 SIMT GEMM + fp32 row kernels; north_star 1e-4 tolerance)
 PRECISIONS = {"bf16": BF16, "fp32": F32}
+# TP = 1: sigma in the down-GEMM epilogue instead of a separate fix-up launch (A/B switch for benches)
+FUSE_SIGMA = True
 
 
 def _pick_splits(tiles: int, k_blocks: int, sms: int) -> int:
@@ -269,6 +271,9 @@ class BTPBlockExecutor(ExecutorBase):
         self.flp = -(-self.fl // 8) * 8
         self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
                               "fp32" if precision == "fp32" else attn_backend)
+        # sigma in the down-GEMM epilogue (GEMM kernel epilogue 1): TP = 1 only (at TP > 1 the
+        # all-reduce sits between GEMM and sigma), cola, bf16, crossgate halves in 64-column blocks
+        self.fuse_sigma = FUSE_SIGMA and precision == "bf16" and tp == 1 and self.var == 1 and self.r % 128 == 0
         self._load_weights(block)
 
     # ------------------------------------------------------------------ weights
@@ -348,6 +353,8 @@ class BTPBlockExecutor(ExecutorBase):
         ss_total = ss if (norm_chunk and self.online) else None
         s_out = self.buf(f"s{s_tag}", (T,), F32) if (norm_chunk and self.online) else None
         a_store = self.buf(f"a_{'_'.join(names)}", (T, k * r)) if self.var == 1 else None
+        if self.fuse_sigma:
+            return self._down_boundary_fused(names, n_in, W, ss, rl, s_tag, norm_chunk, a_store)
         if self.grouping or k == 1:
             P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
             self._gemm(K.Gemm(n_in, W, P, row_scale=row_scale))
@@ -379,6 +386,33 @@ class BTPBlockExecutor(ExecutorBase):
             z.append(P3[i])
             a.append(a_store[:, i * r:(i + 1) * r] if a_store is not None else P3[i])
         return z, a, P3
+
+    def _down_boundary_fused(self, names, n_in, W, ss, rl, s_tag, norm_chunk, a_store):
+        """TP = 1: no all-reduce separates the down GEMM from sigma, so the GEMM epilogue writes
+        z and a = crossgate(z) directly (no P round trip, no fix-up launch). With a single rank,
+        rms_loc is the global rms, so z needs no rescale and s = rms_loc. The (no-op) collectives
+        are still recorded, in plan order."""
+        T, r, k = self.T, self.r, len(names)
+        if norm_chunk and self.online:
+            self._buf[f"s{s_tag}"] = rl
+        if self.grouping or k == 1:
+            P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
+            self._gemm(K.Gemm(n_in, W, P, sigma=(a_store, r // 2)))
+            gid = names[0] if k == 1 else self._gid(names)
+            if norm_chunk and self.online:
+                self.comm.all_reduce_coalesced(P, ss, gid)
+            else:
+                self.comm.all_reduce(P, gid)
+            return ([P[:, i * r:(i + 1) * r] for i in range(k)], [a_store[:, i * r:(i + 1) * r] for i in range(k)],
+                    P)
+        P3 = self.buf(f"P3_{'_'.join(names)}", (k, T, r))
+        for i, nm in enumerate(names):
+            self._gemm(K.Gemm(n_in, W[i * r:(i + 1) * r], P3[i], sigma=(a_store[:, i * r:(i + 1) * r], r // 2)))
+            if norm_chunk and self.online and i == 0:
+                self.comm.all_reduce_coalesced(P3[i], ss, nm)
+            else:
+                self.comm.all_reduce(P3[i], nm)
+        return [P3[i] for i in range(k)], [a_store[:, i * r:(i + 1) * r] for i in range(k)], P3
 
     @staticmethod
     def _gid(names) -> str:

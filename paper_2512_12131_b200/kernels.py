@@ -73,6 +73,7 @@ class Gemm:
     alpha: float = 1.0
     reduce_add: bool = False                # add into C (fp32, zeroed) via TMA reduce; needed for splits > 1
     swiglu_bwd: tuple | None = None         # (g, u, du): acc = dact -> C = dg, du written too
+    sigma: tuple | None = None              # (a_out, r_half): C = z, a_out = crossgate(z) (TP = 1 boundary)
 
     def to_c(self) -> GemmProblem:
         op_dtype = F32 if self.a.dtype == F32 else BF16  # fp32 operands -> exact-fp32 parity GEMM
@@ -92,6 +93,13 @@ class Gemm:
             raise ValueError("split-K / reduce-add GEMMs need an fp32 output")
         split_stride = 0
         resid, epilogue, aux2, c2 = self.resid, 0, None, None
+        sigma_half = 0
+        if self.sigma is not None:
+            a_out, sigma_half = self.sigma
+            _check(a_out, BF16, "a_out")
+            if tuple(a_out.shape) != (M, N):
+                raise ValueError(f"sigma output {tuple(a_out.shape)} != ({M}, {N})")
+            epilogue, c2 = 1, a_out
         if self.swiglu_bwd is not None:
             g, u, du = self.swiglu_bwd
             for t, nm in ((g, "g"), (u, "u"), (du, "du")):
@@ -113,6 +121,7 @@ class Gemm:
             epilogue=epilogue,
             aux2=None if aux2 is None else aux2.data_ptr(), ld_aux2=_ld(aux2),
             c2=None if c2 is None else c2.data_ptr(), ldc2=_ld(c2),
+            sigma_half=int(sigma_half),
         )
 
 

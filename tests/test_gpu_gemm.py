@@ -95,3 +95,50 @@ def test_rejects_misaligned():
 
     with pytest.raises(NativeError):
         K.gemm(K.Gemm(A, B, C))
+
+
+def _crossgate_ref(z, r):
+    """[silu(u) v, silu(v) u] per r-wide projection, from the bf16-rounded z (as the epilogue)."""
+    z = z.float()
+    out = torch.empty_like(z)
+    for p in range(z.shape[1] // r):
+        u, v = z[:, p * r:p * r + r // 2], z[:, p * r + r // 2:(p + 1) * r]
+        out[:, p * r:p * r + r // 2] = torch.nn.functional.silu(u) * v
+        out[:, p * r + r // 2:(p + 1) * r] = torch.nn.functional.silu(v) * u
+    return out
+
+
+@pytest.mark.parametrize("M,r,nproj,Kd", [(300, 128, 3, 512), (2048, 512, 3, 2048), (1000, 256, 2, 1024),
+                                          (4096, 512, 1, 5472), (256, 1024, 1, 512)])
+@pytest.mark.parametrize("pair", [True, False])
+@pytest.mark.parametrize("bn", [0, 128])
+def test_sigma_epilogue(M, r, nproj, Kd, pair, bn):
+    """z = scale * (X @ B^T) and a = crossgate(z) from one launch (the TP = 1 rank-r boundary)."""
+    X, B = _mk(M, Kd), _mk(nproj * r, Kd) * 0.05
+    row = torch.rand(M, device="cuda") + 0.5
+    Z = torch.empty(M, nproj * r, device="cuda", dtype=torch.bfloat16)
+    Aout = torch.full((M, nproj * r), float("nan"), device="cuda", dtype=torch.bfloat16)
+    prev = K.set_pair_mode(pair)
+    try:
+        K.gemm(K.Gemm(X, B, Z, row_scale=row, sigma=(Aout, r // 2)), bn=bn)
+    finally:
+        K.set_pair_mode(prev)
+    z_ref = (X.float() @ B.float().t()) * row[:, None]
+    assert rel(Z, z_ref) < TOL
+    assert rel(Aout, _crossgate_ref(Z, r)) < TOL
+    assert not torch.isnan(Aout.float()).any()
+
+
+def test_sigma_epilogue_rejects_bad_shapes():
+    X, B = _mk(256, 512), _mk(192, 512)
+    Z = torch.empty(256, 192, device="cuda", dtype=torch.bfloat16)
+    A = torch.empty_like(Z)
+    with pytest.raises(Exception):
+        K.gemm(K.Gemm(X, B, Z, sigma=(A, 96)))  # half-width not a multiple of 64
+    X, B = _mk(256, 512), _mk(128, 512)
+    Z = torch.empty(256, 128, device="cuda", dtype=torch.bfloat16)
+    A = torch.empty_like(Z)
+    with pytest.raises(Exception):
+        K.gemm(K.Gemm(X, B, Z, sigma=(A, 64)), bn=256)  # a 256-wide tile would straddle two projections
+    with pytest.raises(Exception):
+        K.gemm(K.Gemm(X, B.t().contiguous(), Z, b_mn=True, sigma=(A, 64)))  # B must be K-major

@@ -47,6 +47,26 @@ def test_forward_workspaces_small(variant, online, grouping):
     ]
 
 
+@pytest.mark.parametrize("fuse_sigma", [True, False])
+@pytest.mark.parametrize("online,grouping", [(True, True), (False, False)])
+def test_forward_workspaces_c60m_sigma_epilogue(fuse_sigma, online, grouping, monkeypatch):
+    """r = 128: z_* and a_in_* come straight out of the down-GEMM epilogue (fuse_sigma) or from
+    the fix-up kernel; both must match the reference workspaces."""
+    from paper_2512_12131_b200 import executor as E
+
+    monkeypatch.setattr(E, "FUSE_SIGMA", fuse_sigma)
+    b, s = 2, 128
+    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=online, grouping=grouping)
+    res = execute_forward(pl, blk, x, capture_workspaces=True)
+    y_ref, _, ws_ref, _ = oracle_step(oblk, x, G, C60M, b, s, online=online)
+    assert rel(res.y.values.reshape(-1, C60M.d), y_ref) < BF16_TOL
+    _check_ws(res.workspaces[0], ws_ref[0])
+    assert res.trace.record_tuples("forward") == [
+        (p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)
+    ]
+
+
 @pytest.mark.parametrize("variant", [Variant.COLA, Variant.SVD])
 @pytest.mark.parametrize("grouping,online,ckpt", [(True, True, False), (False, True, False), (True, False, False),
                                                   (True, True, True), (False, False, True)])
@@ -74,13 +94,21 @@ def test_train_step_grads_small(variant, grouping, online, ckpt):
     assert st.trace.record_tuples("reforward") == []
 
 
-def test_c60m_block_step():
-    """CoLA-60M block (BASELINE config #1 shape) fwd+bwd vs the oracle."""
+@pytest.mark.parametrize("fuse_sigma,grouping,online,ckpt", [(True, True, True, False), (False, True, True, False),
+                                                              (True, False, True, False), (True, True, False, True)])
+def test_c60m_block_step(fuse_sigma, grouping, online, ckpt, monkeypatch):
+    """CoLA-60M block (BASELINE config #1 shape) fwd+bwd vs the oracle. r = 128, so at TP = 1 the
+    down-projections run the sigma-fused GEMM epilogue (fuse_sigma) or GEMM + fix-up kernel."""
+    from paper_2512_12131_b200 import executor as E
+
+    monkeypatch.setattr(E, "FUSE_SIGMA", fuse_sigma)
     b, s = 8, 256
     blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
-    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=online, grouping=grouping,
+              lowrank_ckpt=ckpt)
     st = train_step(pl, blk, x, G)
-    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, C60M, b, s)
+    assert st.executor.fuse_sigma == fuse_sigma
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, C60M, b, s, sharded=False)
     assert rel(st.y.values.reshape(-1, C60M.d), y_ref) < BF16_TOL
     assert abs(st.loss - loss_ref) / abs(loss_ref) < BF16_TOL
     for n in O.PROJECTIONS:

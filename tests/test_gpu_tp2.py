@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q):
+def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q, cfg_name="SMALL", bs=(2, 64)):
     try:
         import torch.distributed as dist
 
@@ -32,15 +32,17 @@ def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q):
         import datetime
 
         dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=180))
-        from tests.gpu_util import SMALL, inputs
+        from tests import gpu_util
+        from tests.gpu_util import inputs
         from paper_2512_12131_b200.api import train_step
         from paper_2512_12131_b200.model import RunShape, Variant
         from paper_2512_12131_b200.plan import Strategy, plan
 
-        b, s = 2, 64
+        b, s = bs
+        cfg = getattr(gpu_util, cfg_name)
         variant = Variant.FULL_RANK if strategy == "full-rank" else Variant.COLA
-        blk, x, G, _ = inputs(SMALL, variant, b, s)
-        pl = plan(Strategy(strategy), SMALL, RunShape(b, s, world), None if strategy == "full-rank" else variant,
+        blk, x, G, _ = inputs(cfg, variant, b, s)
+        pl = plan(Strategy(strategy), cfg, RunShape(b, s, world), None if strategy == "full-rank" else variant,
                   online_norm=online, grouping=grouping, lowrank_ckpt=ckpt)
         st = train_step(pl, blk, x, G)
         q.put((rank, st.y.values, st.loss, st.dx, st.grads, st.trace.record_tuples("forward"),
@@ -52,11 +54,12 @@ def _rank_main(rank, world, port, strategy, grouping, online, ckpt, q):
         q.put((rank, None, None, None, None, None, None, None, traceback.format_exc()))
 
 
-def _run_tp2(strategy, grouping, online, ckpt):
+def _run_tp2(strategy, grouping, online, ckpt, world=2, cfg_name="SMALL", bs=(2, 64)):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, strategy, grouping, online, ckpt, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, strategy, grouping, online, ckpt, q, cfg_name, bs))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -144,3 +147,34 @@ def test_full_rank_tp2_matches_oracle():
         for n, w in want.items():
             assert rel(grads["W"][n], w) < BF16_TOL, (rank, n)
         assert [r[0] for r in fwd] == ["attn", "mlp"]
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_btp_tp4_tp8_c60m_matches_oracle(world):
+    """CoLA-60M (d512, 8 heads, d_ff 1376, r128) at TP=4 and TP=8, one process per rank on one GPU:
+    at TP=8 each rank owns 64 residual columns, one head and 172 d_ff columns (zero-padded to 176
+    for 16-byte TMA strides)."""
+    from tests.gpu_util import BF16_TOL, C60M, inputs, oracle_step, rel
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, enumerate_collectives, plan
+
+    b, s = 2, 128  # (2, 64) has a near-cancelling loss (-1.43 out of sum|y*G| = 16379): ill-conditioned
+    res = _run_tp2("btp", True, True, False, world=world, cfg_name="C60M", bs=(b, s))
+    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, C60M, b, s, tp=world, online=True, sharded=False)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, world), Variant.COLA, online_norm=True, grouping=True)
+    pred = [(p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
+    assert len(res) == world
+    for rank, (_, y, loss, dx, grads, fwd, bwd, _refwd, _) in res.items():
+        assert rel(y.reshape(-1, C60M.d), y_ref) < BF16_TOL
+        assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
+        gr = O.grads_for_rank(g_ref, world, rank, C60M.d, C60M.d_ff)
+        assert rel(dx, gr["dx"]) < BF16_TOL
+        for n in O.PROJECTIONS:
+            assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
+            assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
+        assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
+        assert fwd == pred
+        assert sum(rec[3] for rec in bwd) == 7 * b * s * C60M.r
