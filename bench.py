@@ -54,19 +54,49 @@ def flops_per_step(cfg, b, s, lowrank=True):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every 10 ms (a timed
+    region of ten ~5 ms steps still gets several samples), else nvidia-smi every 200 ms."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits: sw_power_cap 0x4, hw_slowdown 0x8, sw_thermal 0x20, hw_thermal 0x40
+    _BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+             ("sw_power_cap", 0x4))
 
     def __init__(self, index: int = 0):
         self.index = index
         self.rows: list[list[str]] = []
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvidia-smi"
+
+    def _run_nvml(self) -> bool:
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:
+            return False
+        self.source = "nvml"
+        while not self._stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = get_reasons(h)
+            except Exception:
+                break
+            flags = ["Active" if bits & b else "Not Active" for _, b in self._BITS]
+            self.rows.append([str(self.index), str(sm), str(mx), "", hex(bits)] + flags)
+            self._stop.wait(0.01)
+        return True
 
     def _run(self):
+        if self._run_nvml():
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -95,7 +125,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 # ------------------------------------------------------------------------------------- CPU arm
@@ -184,17 +214,37 @@ def run_ours(args, cfg):
     from paper_2512_12131_b200.tensor import seeded_fill
 
     b, s, tp = args.b, args.s, world
+    comm = None
+    if args.emulate_tp:
+        if world != 1:
+            raise SystemExit("--emulate-tp runs one rank's share on ONE GPU (no torchrun)")
+        from paper_2512_12131_b200.comm import TPComm
+
+        tp = args.emulate_tp
+        comm = TPComm.emulated(tp, 0)
     shape = RunShape(b, s, tp)
     strategy = Strategy(args.strategy)
     variant = Variant.FULL_RANK if strategy is Strategy.FULL_RANK else Variant.COLA
     pl = plan(strategy, cfg, shape, None if variant is Variant.FULL_RANK else variant,
               online_norm=strategy is Strategy.BOTTLENECK, grouping=not args.no_grouping,
               lowrank_ckpt=args.ckpt)
-    blk = fan_in_scaled(build_block(cfg, variant, 0))
-    x = seeded_fill((b, s, cfg.d), 10000).values
-    G = seeded_fill((b, s, cfg.d), 30000).values
-    trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
-                           optimizer=not args.no_optimizer)
+    if args.model:
+        # the multi-layer model: embedding shard + L blocks + LM head + cross-entropy
+        from paper_2512_12131_b200.api import ModelTrainer
+        from paper_2512_12131_b200.model import build_model, token_batch
+
+        if strategy is not Strategy.BOTTLENECK:
+            raise SystemExit("--model runs the BTP strategy")
+        mw = build_model(cfg, variant, 0, args.vocab, layers=args.layers or cfg.layers)
+        x, G = token_batch(b, s, args.vocab)
+        trainer = ModelTrainer(pl, mw, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
+                               optimizer=not args.no_optimizer, comm=comm)
+    else:
+        blk = fan_in_scaled(build_block(cfg, variant, 0))
+        x = seeded_fill((b, s, cfg.d), 10000).values
+        G = seeded_fill((b, s, cfg.d), 30000).values
+        trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
+                               optimizer=not args.no_optimizer, comm=comm)
     x_dev, g_dev = trainer.device_inputs(x, G)
 
     def barrier():
@@ -249,9 +299,11 @@ def run_ours(args, cfg):
         Path(args.dump_gemms).write_text(json.dumps(gemm["per_launch"], indent=1))
     peak_burst, peak_sus, hbm, peak_kind = _peaks()
     flops = flops_per_step(cfg, b, s, lowrank=variant is not Variant.FULL_RANK) / tp
+    if args.model:  # L blocks (sharded) + the replicated head: 3 * 2 T d V on every rank
+        flops = flops * trainer.ex.blocks.__len__() + 3 * 2 * b * s * cfg.d * args.vocab
     traffic, traffic_src = None, None
     tfile = ROOT / "profiles" / "r01_gemm_traffic_summary.json"
-    if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp":
+    if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model:
         t = json.loads(tfile.read_text())
         traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
     roof = {"bound": "tensor", "kernel": "btp gemm_kernel (all tcgen05 GEMM launches of one step)",
@@ -267,7 +319,9 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform inputs, fan-in-scaled random init)",
-        "config": {"workload": f"CoLA-{args.config} decoder block fwd+bwd{'' if args.no_optimizer else '+AdamW'}, "
+        "config": {"workload": (f"CoLA-{args.config} model ({len(trainer.ex.blocks)} blocks + d-sharded embedding + "
+                                f"replicated LM head V={args.vocab} + cross-entropy) " if args.model else
+                                f"CoLA-{args.config} decoder block ") + f"fwd+bwd{'' if args.no_optimizer else '+AdamW'}, "
                                f"{strategy.value} "
                                f"{'grouped ' if pl.grouping else ''}{'online-RMSNorm ' if pl.norm_mode.value == 'online' else ''}"
                                f"TP={tp}{' lowrank-ckpt' if pl.lowrank_ckpt else ''}",
@@ -282,6 +336,12 @@ def run_ours(args, cfg):
         "roofline": roof,
         "algorithmic_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
     }
+    if args.emulate_tp:
+        line["metric"] = (f"EMULATED per-rank compute of a TP={tp} step on one GPU (collectives not executed; "
+                          "value = tokens/s if comm were free; not the bench metric)")
+        line["emulated_tp"] = tp
+        line["scaling"] = None
+        args.no_cpu_baseline = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, times, threads = cpu_oracle_rate(cfg, s, seconds_budget=args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
@@ -313,6 +373,12 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
+    ap.add_argument("--model", action="store_true", help="multi-layer model step (embedding + blocks + LM head)")
+    ap.add_argument("--layers", type=int, default=0, help="--model: number of blocks (default: the preset's)")
+    ap.add_argument("--vocab", type=int, default=32000, help="--model: vocabulary size")
+    ap.add_argument("--emulate-tp", type=int, default=0,
+                    help="time ONE rank's compute of a TP=N plan on one GPU, collectives not executed "
+                         "(compute-only; NOT the bench metric)")
     args = ap.parse_args(argv)
     from paper_2512_12131_b200.model import COLA_60M, preset
 

@@ -210,6 +210,33 @@ int btp_adamw(float* master, float* m, float* v, const float* g, void* work, lon
 int btp_adamw_f32(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1,
                   float b2, float eps, float wd, int step, const int* step_dev, void* stream);
 
+/* ---- model boundary around the stack of BTP blocks (absent in the reference,
+ * whose executor stops at the block and its tail all-gather, simulator.py:710-714; the paper
+ * shards the embedding output so the first down-projection is row-split and replicates the
+ * final projection). *_f32 twins take fp32 activations/tables.
+ *
+ * Embedding lookup of this rank's d-shard: out[t, :] = table[ids[t], col0 : col0 + width].
+ * ids int32 [rows]; an id outside [0, vocab) yields a zero row and sets *bad = 1 (bad may be NULL). */
+int btp_embedding_fwd(const int* ids, const void* table, long long ldt, int vocab, int col0, void* out,
+                      long long ldo, int rows, int width, int* bad, void* stream);
+int btp_embedding_fwd_f32(const int* ids, const void* table, long long ldt, int vocab, int col0, void* out,
+                          long long ldo, int rows, int width, int* bad, void* stream);
+/* Embedding backward: dtable[ids[t], :] += dx[t, :] (fp32, zero-initialised; fp32 atomics, so the
+ * order in which repeated ids accumulate is not fixed). */
+int btp_embedding_bwd(const int* ids, const void* dx, long long lddx, int vocab, float* dtable, long long ldg,
+                      int rows, int width, void* stream);
+int btp_embedding_bwd_f32(const int* ids, const void* dx, long long lddx, int vocab, float* dtable, long long ldg,
+                          int rows, int width, void* stream);
+/* Fused softmax cross-entropy over logits [rows, vocab] (vocab % 8 == 0), one pass for the
+ * log-sum-exp and one for the gradient:
+ *   loss_rows[t] = logsumexp(l_t) - l_t[target_t]                         (fp32)
+ *   dlogits[t, j] = scale * (softmax(l_t)_j - [j == target_t])           (may alias logits; NULL = none)
+ * target < 0 is the ignore index (loss 0, zero gradient). Reduce loss_rows with btp_reduce_rows. */
+int btp_cross_entropy(const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows,
+                      void* dlogits, long long ldd, int rows, float scale, void* stream);
+int btp_cross_entropy_f32(const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows,
+                          void* dlogits, long long ldd, int rows, float scale, void* stream);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

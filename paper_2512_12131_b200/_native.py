@@ -59,6 +59,13 @@ EXPORTED_SYMBOLS = (
     "btp_rmsnorm_bwd_prep_f32",
     "btp_add_f32",
     "btp_dot_f32",
+    # model boundary (embedding shard, fused cross-entropy)
+    "btp_embedding_fwd",
+    "btp_embedding_fwd_f32",
+    "btp_embedding_bwd",
+    "btp_embedding_bwd_f32",
+    "btp_cross_entropy",
+    "btp_cross_entropy_f32",
 )
 
 
@@ -129,9 +136,13 @@ _SIGNATURES = {
     "btp_adamw": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
     "btp_adamw_f32": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
     "btp_counter_add": [_P, _I, _P],
+    "btp_embedding_fwd": [_P, _P, _LL, _I, _I, _P, _LL, _I, _I, _P, _P],
+    "btp_embedding_bwd": [_P, _P, _LL, _I, _P, _LL, _I, _I, _P],
+    "btp_cross_entropy": [_P, _LL, _P, _I, _P, _P, _LL, _I, _F, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
-              "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot"):
+              "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",
+              "btp_embedding_fwd", "btp_embedding_bwd", "btp_cross_entropy"):
     _SIGNATURES[_name + "_f32"] = _SIGNATURES[_name]
 
 _lib = None

@@ -65,9 +65,10 @@ def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
 
 
 def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
-                  device=None, attn_backend: str = "auto", precision: str = "bf16"):
-    """Build this rank's executor for the plan's strategy."""
-    comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
+                  device=None, attn_backend: str = "auto", precision: str = "bf16", comm: TPComm | None = None):
+    """Build this rank's executor for the plan's strategy (comm: default = the process group)."""
+    if comm is None:
+        comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:
         return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)
@@ -92,8 +93,8 @@ def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
         return y_sh
     if model_tail:
         return ex.comm.all_gather_cols(y_sh, "final-gather", tag="boundary")
-    if ex.tp == 1:
-        return y_sh
+    if not ex.comm.live:
+        return y_sh if ex.tp == 1 else y_sh.repeat(1, ex.tp)
     # host-side result assembly (the reference concatenates without a record, simulator.py:713)
     parts = [torch.empty_like(y_sh) for _ in range(ex.tp)]
     dist.all_gather(parts, y_sh.contiguous())
@@ -166,12 +167,14 @@ class BlockTrainer:
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
-                 optimizer: bool = True):
+                 optimizer: bool = True, comm: TPComm | None = None, executor=None):
         self.pl = pl
-        self.ex = make_executor(pl, block, eps=eps, attn_backend=attn_backend)
+        self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
+                                                                      comm=comm)
         # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
         self.adamw = dict(adamw or {}) if optimizer else None
-        self.use_graph = use_graph and pl.shape.tp == 1
+        # collectives stay eager (NCCL outside graph capture); a step without live collectives is graphed
+        self.use_graph = use_graph and not self.ex.comm.live
         self.graphs: dict = {}
         self.graphed = False
         self._per_step_launches = 0
@@ -275,7 +278,7 @@ class BlockTrainer:
         self.ex.gemm_timer = []
         self._eager(x, g)  # allocate every buffer outside the capture
         torch.cuda.synchronize()
-        if self.ex.tp > 1:  # collectives stay eager; timings then include host gaps
+        if self.ex.comm.live:  # collectives stay eager; timings then include host gaps
             rec, self.ex.gemm_timer = self.ex.gemm_timer, None
             return self._gemm_summary(rec)
         graph = torch.cuda.CUDAGraph()
@@ -302,3 +305,33 @@ class BlockTrainer:
                for a, b, f, sh in rec]
         return {"ms": ms, "flops": fl, "tflops": fl / (ms / 1e3) / 1e12 if ms else 0.0, "launches": len(rec),
                 "per_launch": per}
+
+
+class ModelTrainer(BlockTrainer):
+    """The same persistent, graph-replayed training step for the multi-layer model
+    (model_executor.ModelExecutor): inputs are int32 token ids and next-token targets [T]
+    (replicated on every TP rank); the loss is the mean cross-entropy of the replicated head."""
+
+    def __init__(self, pl: ShardPlan, mw, *, eps: float = EPS_DEFAULT, attn_backend: str = "auto",
+                 use_graph: bool = True, adamw: dict | None = None, optimizer: bool = True,
+                 comm: TPComm | None = None):
+        from .model_executor import ModelExecutor
+
+        comm = comm if comm is not None else TPComm.from_env(pl.shape.tp, trace=Trace())
+        ex = ModelExecutor(pl, mw, comm, torch.device("cuda", torch.cuda.current_device()), eps, attn_backend)
+        super().__init__(pl, None, use_graph=use_graph, adamw=adamw, optimizer=optimizer, executor=ex)
+
+    # one step's input is the packed int32 [2, T] (ids, targets): fit() then streams both per batch;
+    # the second returned tensor only satisfies the block trainer's (x, G) calling convention
+    @staticmethod
+    def _pack(ids, targets) -> torch.Tensor:
+        return torch.as_tensor(np.stack([np.asarray(ids), np.asarray(targets)]), dtype=torch.int32)
+
+    def device_inputs(self, ids: np.ndarray, targets: np.ndarray):
+        self._x = self._pack(ids, targets).to(self.ex.dev)
+        self._g = self._x[1]
+        return self._x, self._g
+
+    def pinned_host_inputs(self, ids: np.ndarray, targets: np.ndarray):
+        packed = self._pack(ids, targets).pin_memory()
+        return packed, packed[1]

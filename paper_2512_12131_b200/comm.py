@@ -10,6 +10,15 @@ gloo for the multi-process CPU tests.
 
 At tp == 1 nothing is sent, but the record is still written, exactly like the reference's
 single-rank group. Every call records into a `Trace` with the current pass tag.
+
+Two non-default modes, neither used by the training path:
+* `force=True`  — issue the torch.distributed calls even at tp == 1 (a one-rank NCCL group on
+                  the single-GPU box exercises the NCCL code path: coalescing manager, async
+                  work handles, stream ordering).
+* `emulate=True` — `TPComm.emulated(tp, rank)`: one rank's share of a tp-way plan on a single
+                  GPU with NO data exchange (records only). The numbers are wrong by design;
+                  it exists to time the per-rank compute of TP=4/8 shapes on one GPU
+                  (`bench.py --emulate-tp`), and is labelled compute-only wherever reported.
 """
 
 from __future__ import annotations
@@ -21,14 +30,24 @@ from .trace import Trace
 
 
 class TPComm:
-    def __init__(self, tp: int = 1, rank: int = 0, group=None, trace: Trace | None = None):
+    def __init__(self, tp: int = 1, rank: int = 0, group=None, trace: Trace | None = None, *,
+                 force: bool = False, emulate: bool = False):
         self.tp = tp
         self.rank = rank
         self.group = group
         self.trace = trace if trace is not None else Trace()
         self.pass_tag = "forward"
-        if tp > 1 and not dist.is_initialized():
+        self.emulate = emulate
+        if (tp > 1 or force) and not emulate and not dist.is_initialized():
             raise RuntimeError("tp > 1 needs an initialised torch.distributed process group")
+        if emulate and not 0 <= rank < tp:
+            raise ValueError(f"rank {rank} outside tp={tp}")
+        # issue real collectives?
+        self.live = (tp > 1 or force) and not emulate
+
+    @classmethod
+    def emulated(cls, tp: int, rank: int = 0, trace: Trace | None = None) -> "TPComm":
+        return cls(tp, rank, None, trace, emulate=True)
 
     @classmethod
     def from_env(cls, tp: int | None = None, trace: Trace | None = None) -> "TPComm":
@@ -42,7 +61,7 @@ class TPComm:
 
     # ------------------------------------------------------------------ collectives
     def all_reduce(self, buf: torch.Tensor, chunk_id: str, tag: str = "block") -> torch.Tensor:
-        if self.tp > 1:
+        if self.live:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
         return buf
@@ -51,7 +70,7 @@ class TPComm:
         """Asynchronous in-place all-reduce: NCCL runs on its own stream (ordered after the work
         already queued on the current stream) while the caller keeps launching independent
         kernels; `wait(handle)` orders the current stream after the reduction."""
-        work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True) if self.tp > 1 else None
+        work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True) if self.live else None
         self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
         return work
 
@@ -62,15 +81,21 @@ class TPComm:
 
     def all_reduce_coalesced(self, main: torch.Tensor, stat: torch.Tensor, chunk_id: str,
                              tag: str = "block", stat_tag: str = "fused-stat"):
-        if self.tp > 1:
-            if dist.get_backend(self.group) == "nccl":
-                # one ncclGroupStart/End: both reductions ride one launch
-                with dist._coalescing_manager(group=self.group, device=main.device):
-                    dist.all_reduce(main, group=self.group)
-                    dist.all_reduce(stat, group=self.group)
+        if self.live:
+            pg = self.group if self.group is not None else dist.distributed_c10d._get_default_group()
+            if dist.get_backend(pg) == "nccl" and hasattr(pg, "_start_coalescing"):
+                # one ncclGroupStart/End around a bf16 and an fp32 all-reduce: both ride one launch.
+                # (dist._coalescing_manager's all-reduce fast path would hand both tensors to
+                # allreduce_coalesced, which requires ONE dtype and raises for the bf16 + fp32 rider.)
+                pg._start_coalescing(main.device)
+                dist.all_reduce(main, group=pg)
+                dist.all_reduce(stat, group=pg)
+                work = pg._end_coalescing(main.device)
+                if work is not None:
+                    work.wait()  # stream-orders the caller after the grouped reduction
             else:
-                dist.all_reduce(main, group=self.group)
-                dist.all_reduce(stat, group=self.group)
+                dist.all_reduce(main, group=pg)
+                dist.all_reduce(stat, group=pg)
         self.trace.emit("all-reduce-coalesced", chunk_id, tag, main.numel(), self.pass_tag,
                         extras=((stat_tag, stat.numel()),))
         return main, stat
@@ -78,10 +103,12 @@ class TPComm:
     def all_gather_cols(self, shard: torch.Tensor, chunk_id: str, tag: str = "boundary") -> torch.Tensor:
         """Gather [rows, w] shards along the feature axis into [rows, tp*w]."""
         rows, w = shard.shape
-        if self.tp > 1:
+        if self.live:
             stacked = torch.empty((self.tp * rows, w), dtype=shard.dtype, device=shard.device)
             dist.all_gather_into_tensor(stacked, shard.contiguous(), group=self.group)
             out = stacked.view(self.tp, rows, w).permute(1, 0, 2).reshape(rows, self.tp * w)
+        elif self.tp > 1:  # emulated: shape-correct placeholder
+            out = shard.repeat(1, self.tp)
         else:
             out = shard
         self.trace.emit("all-gather", chunk_id, tag, out.numel(), self.pass_tag)

@@ -37,4 +37,11 @@ int dot(const void* a, long long lda, const void* b, long long ldb, int rows, in
 int adamw(float* master, float* m, float* v, const float* g, void* work, long long n, float lr, float b1, float b2,
           float eps, float wd, int step, const int* step_dev, cudaStream_t st, bool f32);
 int counter_add(int* ctr, int delta, cudaStream_t st);
+// model boundary (modelops.cu)
+int embedding_fwd(const int* ids, const void* table, long long ldt, int vocab, int col0, void* out, long long ldo,
+                  int rows, int width, int* bad, cudaStream_t st, bool f32);
+int embedding_bwd(const int* ids, const void* dx, long long lddx, int vocab, float* dtable, long long ldg, int rows,
+                  int width, cudaStream_t st, bool f32);
+int cross_entropy(const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows, void* dlogits,
+                  long long ldd, int rows, float scale, cudaStream_t st, bool f32);
 }  // namespace btp

@@ -104,6 +104,24 @@ BTP_PAIR(btp_adamw, adamw,
           float eps, float wd, int step, const int* step_dev, void* stream),
          A_ADAMW)
 
+#define A_EMB_FWD(f32) (ids, table, ldt, vocab, col0, out, ldo, rows, width, bad, ST(stream), f32)
+BTP_PAIR(btp_embedding_fwd, embedding_fwd,
+         (const int* ids, const void* table, long long ldt, int vocab, int col0, void* out, long long ldo, int rows,
+          int width, int* bad, void* stream),
+         A_EMB_FWD)
+
+#define A_EMB_BWD(f32) (ids, dx, lddx, vocab, dtable, ldg, rows, width, ST(stream), f32)
+BTP_PAIR(btp_embedding_bwd, embedding_bwd,
+         (const int* ids, const void* dx, long long lddx, int vocab, float* dtable, long long ldg, int rows, int width,
+          void* stream),
+         A_EMB_BWD)
+
+#define A_XENT(f32) (logits, ldl, targets, vocab, loss_rows, dlogits, ldd, rows, scale, ST(stream), f32)
+BTP_PAIR(btp_cross_entropy, cross_entropy,
+         (const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows, void* dlogits,
+          long long ldd, int rows, float scale, void* stream),
+         A_XENT)
+
 int btp_counter_add(int* ctr, int delta, void* stream) { return btp::counter_add(ctr, delta, ST(stream)); }
 
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,

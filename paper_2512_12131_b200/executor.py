@@ -222,7 +222,7 @@ class ExecutorBase:
         out = self.buf("loss", (1,), F32)
         K.reduce_rows(part[:nb].view(nb, 1, 1), out.view(1, 1))
         self.stats.kernel_launches += 2
-        if self.tp > 1 and self.residual_sharded:
+        if self.comm.live and self.residual_sharded:
             import torch.distributed as dist
 
             dist.all_reduce(out)  # loss assembly across d-shards (outside the block's collective log)

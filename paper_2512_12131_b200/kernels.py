@@ -246,5 +246,31 @@ def dot(a, b, partial) -> int:
     return nblk.value
 
 
+def embedding_fwd(ids, table, out, *, col0=0, bad=None):
+    """out[t, :] = table[ids[t], col0:col0+width] (this rank's d-shard); ids int32 [T]."""
+    _check(ids, torch.int32, "ids")
+    rows, width = out.shape
+    _native.call(_fn("btp_embedding_fwd", out), _p(ids), _p(table), _ld(table), table.shape[0], int(col0), _p(out),
+                 _ld(out), rows, width, _p(bad), _stream())
+
+
+def embedding_bwd(ids, dx, dtable):
+    """dtable[ids[t], :] += dx[t, :] (fp32, zeroed by the caller)."""
+    _check(ids, torch.int32, "ids")
+    _check(dtable, F32, "dtable")
+    rows, width = dx.shape
+    _native.call(_fn("btp_embedding_bwd", dx), _p(ids), _p(dx), _ld(dx), dtable.shape[0], _p(dtable), _ld(dtable),
+                 rows, width, _stream())
+
+
+def cross_entropy(logits, targets, loss_rows, *, dlogits=None, scale=1.0):
+    """loss_rows[t] = lse(logits_t) - logits_t[target]; dlogits = scale*(softmax - onehot) (may alias)."""
+    _check(targets, torch.int32, "targets")
+    _check(loss_rows, F32, "loss_rows")
+    rows, vocab = logits.shape
+    _native.call(_fn("btp_cross_entropy", logits), _p(logits), _ld(logits), _p(targets), vocab, _p(loss_rows),
+                 _p(dlogits), _ld(dlogits), rows, ctypes.c_float(scale), _stream())
+
+
 def num_sms() -> int:
     return _native.load().btp_num_sms()

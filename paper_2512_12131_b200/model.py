@@ -168,3 +168,54 @@ def fan_in_scaled(block: DecoderBlockWeights, gain: float = 3.0) -> DecoderBlock
     return dataclasses.replace(
         block, full=scale(block.full), down_factors=scale(block.down_factors), up_factors=scale(block.up_factors)
     )
+
+
+# ----------------------------------------------------------------------------- model boundary
+# SURVEY §8f row 1 (absent in the reference, whose executor stops at one block + the tail
+# all-gather, simulator.py:710-714): L blocks chained through the d-sharded residual, fed by a
+# d-sharded token embedding (the paper shards the embedding output so the first down-projection
+# is row-split), a final RMSNorm and a replicated LM head with mean next-token
+# cross-entropy. Builder-defined seeding: block l from seed + 1000*l, embedding / final gain /
+# head from seed + 50000 / 50001 / 50002 (head fan-in scaled like the blocks).
+LAYER_SEED_STRIDE = 1000
+
+
+@dataclass(frozen=True)
+class ModelWeights:
+    cfg: ModelConfig
+    variant: Variant
+    vocab: int
+    blocks: tuple[DecoderBlockWeights, ...]
+    embedding: Tensor      # [vocab, d]
+    final_gamma: Tensor    # [d]
+    head: Tensor           # [vocab, d]
+
+    @property
+    def layers(self) -> int:
+        return len(self.blocks)
+
+
+def build_model(cfg: ModelConfig, variant: Variant, seed: int, vocab: int, layers: int | None = None,
+                scaled: bool = True, element_bytes: int = 2) -> ModelWeights:
+    """`layers` defaults to cfg.layers; `scaled` applies the parity recipe (fan_in_scaled) to every block."""
+    n = cfg.layers if layers is None else layers
+    if vocab <= 0 or n <= 0:
+        raise ValueError("vocab and layers must be positive")
+    blocks = []
+    for l in range(n):
+        blk = build_block(cfg, variant, seed + LAYER_SEED_STRIDE * l, element_bytes)
+        blocks.append(fan_in_scaled(blk) if scaled else blk)
+    head = seeded_fill((vocab, cfg.d), seed + 50002, element_bytes)
+    if scaled:
+        head = Tensor(head.values * np.sqrt(3.0 / cfg.d), element_bytes)
+    return ModelWeights(cfg, variant, vocab, tuple(blocks), seeded_fill((vocab, cfg.d), seed + 50000, element_bytes),
+                        seeded_fill((cfg.d,), seed + 50001, element_bytes), head)
+
+
+def token_batch(b: int, s: int, vocab: int, seed: int = 40000) -> tuple[np.ndarray, np.ndarray]:
+    """Synthetic next-token data: SplitMix64 stream mod vocab, [b, s+1] -> (inputs, targets), each int64 [b*s]."""
+    from .tensor import splitmix64
+
+    raw = splitmix64(seed, b * (s + 1))
+    ids = (raw % np.uint64(vocab)).astype(np.int64).reshape(b, s + 1)
+    return ids[:, :-1].reshape(-1), ids[:, 1:].reshape(-1)

@@ -75,3 +75,19 @@ def test_single_rank_still_records():
     comm.all_reduce(buf, "solo")
     assert comm.trace.record_tuples() == [("solo", "all-reduce", "block", 4, ())]
     assert torch.equal(buf, torch.ones(2, 2))
+
+
+def test_emulated_comm_records_without_exchange():
+    """TPComm.emulated: one rank's share of a tp-way plan on one device, no process group; every
+    collective is recorded with the reference schema but nothing is exchanged."""
+    comm = TPComm.emulated(8, 3)
+    assert comm.tp == 8 and comm.rank == 3 and not comm.live
+    buf = torch.full((4, 2), 2.0)
+    comm.all_reduce(buf, "o")
+    comm.all_reduce_coalesced(buf, torch.ones(4), "qkv")
+    assert comm.wait(comm.all_reduce_start(buf, "down")) is None
+    assert torch.equal(buf, torch.full((4, 2), 2.0))
+    assert comm.all_gather_cols(torch.ones(4, 2), "final-gather").shape == (4, 16)
+    assert [r[0] for r in comm.trace.record_tuples()] == ["o", "qkv", "down", "final-gather"]
+    with pytest.raises(ValueError):
+        TPComm.emulated(2, 2)

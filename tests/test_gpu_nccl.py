@@ -1,0 +1,100 @@
+"""The NCCL code path of the TP communicator on the single-GPU box.
+
+NCCL refuses two ranks on one device, so the multi-rank numerics are covered over gloo
+(test_gpu_tp2.py). Here a ONE-rank NCCL process group runs the same step with every collective
+really issued (`TPComm(force=True)`): in-place all-reduces, the coalesced bf16+fp32 rider inside
+one NCCL group, the async backward all-reduce handles overlapping the weight-gradient GEMM, the
+loss all-reduce and the tail all-gather. A one-rank sum is the identity, so y, the loss and dx must be
+bit-identical to the record-only tp == 1 run (weight gradients to fp32 reduce-add order)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _main(port, q):
+    try:
+        import datetime
+
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, timeout=datetime.timedelta(seconds=120),
+                                device_id=torch.device("cuda", 0))
+        from tests.gpu_util import SMALL, inputs
+        from paper_2512_12131_b200.api import BlockTrainer, make_executor, train_step
+        from paper_2512_12131_b200.comm import TPComm
+        from paper_2512_12131_b200.model import RunShape, Variant
+        from paper_2512_12131_b200.plan import Strategy, plan
+        from paper_2512_12131_b200.trace import Trace
+
+        b, s = 2, 64
+        blk, x, G, _ = inputs(SMALL, Variant.COLA, b, s)
+        out = {}
+        for grouping in (True, False):
+            pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 1), Variant.COLA, online_norm=True,
+                      grouping=grouping)
+            ref = train_step(pl, blk, x, G)
+            ex = make_executor(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True))
+            assert ex.comm.live and dist.get_backend() == "nccl"
+            got = train_step(pl, blk, x, G, executor=ex)
+            torch.cuda.synchronize()
+            same = {"y": np.array_equal(ref.y.values, got.y.values), "loss": ref.loss == got.loss,
+                    "dx": np.array_equal(ref.dx, got.dx)}
+            # weight gradients: split-K partials meet in an fp32 reduce-add whose order is not fixed
+            for fam in ("A", "B"):
+                for n, g in ref.grads[fam].items():
+                    same[f"d{fam}_{n}"] = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g)) < 1e-6
+            out[grouping] = (same, got.trace.record_tuples("forward") == ref.trace.record_tuples("forward"),
+                             len(got.trace.record_tuples("backward")))
+        # the trainer loop with live NCCL collectives (eager, not graphed)
+        pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+        tr = BlockTrainer(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True), adamw=dict(lr=1e-3))
+        xh, gh = tr.pinned_host_inputs(x.values, G.values)
+        losses = tr.fit([xh, xh, xh], gh)
+        gathered = tr.ex.comm.all_gather_cols(torch.ones(4, 8, device="cuda"), "final-gather")
+        out["trainer"] = (tr.use_graph, losses, tuple(gathered.shape))
+        dist.destroy_process_group()
+        q.put((out, None))
+    except Exception:
+        import traceback
+
+        q.put((None, traceback.format_exc()))
+
+
+def test_nccl_one_rank_step_is_bit_identical():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_main, args=(_port(), q))
+    p.start()
+    try:
+        out, err = q.get(timeout=600)
+    finally:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert err is None, err
+    for grouping in (True, False):
+        same, fwd_equal, n_bwd = out[grouping]
+        assert all(same.values()), (grouping, {k: v for k, v in same.items() if not v})
+        assert fwd_equal
+        assert n_bwd == (4 if grouping else 7)
+    graphed, losses, gshape = out["trainer"]
+    assert not graphed                          # live collectives keep the step eager
+    assert all(np.isfinite(losses)) and losses[0] != losses[-1]  # AdamW moved the weights
+    assert gshape == (4, 8)
