@@ -244,7 +244,7 @@ def run_ours(args, cfg):
         x = seeded_fill((b, s, cfg.d), 10000).values
         G = seeded_fill((b, s, cfg.d), 30000).values
         trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
-                               optimizer=not args.no_optimizer, comm=comm)
+                               optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary)
     x_dev, g_dev = trainer.device_inputs(x, G)
 
     def barrier():
@@ -328,6 +328,7 @@ def run_ours(args, cfg):
                    "d": cfg.d, "d_ff": cfg.d_ff, "r": cfg.r, "heads": cfg.heads, "global_batch": b, "seq_len": s,
                    "tokens_per_step": b * s, "parallelism": f"tp{tp}", "l2": "inputs larger than L2 (no flush)",
                    "cuda_graph": trainer.graphed,
+                   "boundary": args.boundary if tp > 1 else "none (tp=1)",
                    "optimizer": None if args.no_optimizer else dict(ADAMW, kind="AdamW fp32 master+moments, fused"),
                    "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
         "clocks": clk.summary(),
@@ -373,6 +374,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
+    ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer"],
+                    help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
     ap.add_argument("--model", action="store_true", help="multi-layer model step (embedding + blocks + LM head)")
     ap.add_argument("--layers", type=int, default=0, help="--model: number of blocks (default: the preset's)")
     ap.add_argument("--vocab", type=int, default=32000, help="--model: vocabulary size")

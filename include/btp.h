@@ -237,6 +237,35 @@ int btp_cross_entropy(const void* logits, long long ldl, const int* targets, int
 int btp_cross_entropy_f32(const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows,
                           void* dlogits, long long ldd, int rows, float scale, void* stream);
 
+/* ---- chunk boundaries over NVLink/NVSwitch peer memory ----------------
+ * Replaces the SimGroup all-reduce (+ rider) at each BTP chunk boundary (simulator.py:153-181,
+ * :592-653) AND the post-reduce fix-up + sigma (btp_fixup_sigma) with one kernel per chunk and
+ * pass: reduce-scatter by pulling the rows this rank owns (T/tp consecutive rows, rank order sum
+ * in fp32), fix-up + sigma on them, all-gather by pushing the results into every rank's buffer.
+ * Every `*_peers` argument is a DEVICE array of tp pointers (rank order) into the symmetric
+ * buffers of all ranks (peer-mapped memory); all bf16 row-major [T, W] with W = nproj * r.
+ *
+ * Flags: `flags` is this rank's symmetric uint32 array [nslots * tp]; `peer_flags` the device
+ * array of every rank's flags pointer; `epoch` this rank's local uint32 [nslots] signal counters.
+ * btp_peer_signal: after the stream's previous work, epoch[slot]++ and store it (release, system
+ * scope) into flags_j[slot * tp + rank] of every rank j. btp_peer_wait: the stream waits until every
+ * rank's flag for the slot has reached this rank's epoch[slot] (acquire, system scope). */
+int btp_peer_signal(unsigned int* const* peer_flags, unsigned int* epoch, int slot, int rank, int tp, void* stream);
+int btp_peer_wait(const unsigned int* flags, const unsigned int* epoch, int slot, int tp, void* stream);
+/* Forward boundary: for owned rows t: P = sum_j P_j[t]; s = sqrt(sum_j ss_j[t]/d + eps) (ss_peers
+ * NULL: s = 1); z_own[t - rank*T/tp] = bf16(P/s); s_own likewise (may be NULL); a = sigma(z)
+ * (variant 1 crossgate over (j, j + r/2) pairs of each r-wide projection, 0 identity) stored into
+ * a_j[t] of every rank. Call between a "ready" wait and a "done" signal. */
+int btp_peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, int tp, int rank, int T, int W,
+                          int r, int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
+                          void* stream);
+/* Backward boundary: for owned rows t: da = sum_j da_j[t]; dz = sigma'(z_own) da; dP = dz / s
+ * (s_own NULL: s = 1) stored into dP_j[t] of every rank; with s_own: dss_j[t] = -<dz, z>/(2 s^2 d)
+ * for every rank (dss_peers may be NULL). Replaces the backward all-reduce + btp_fixup_sigma_bwd. */
+int btp_peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
+                          const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
+                          void* stream);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

@@ -66,6 +66,11 @@ EXPORTED_SYMBOLS = (
     "btp_embedding_bwd_f32",
     "btp_cross_entropy",
     "btp_cross_entropy_f32",
+    # chunk boundaries over peer memory
+    "btp_peer_signal",
+    "btp_peer_wait",
+    "btp_peer_boundary_fwd",
+    "btp_peer_boundary_bwd",
 )
 
 
@@ -139,6 +144,10 @@ _SIGNATURES = {
     "btp_embedding_fwd": [_P, _P, _LL, _I, _I, _P, _LL, _I, _I, _P, _P],
     "btp_embedding_bwd": [_P, _P, _LL, _I, _P, _LL, _I, _I, _P],
     "btp_cross_entropy": [_P, _LL, _P, _I, _P, _P, _LL, _I, _F, _P],
+    "btp_peer_signal": [_P, _P, _I, _I, _I, _P],
+    "btp_peer_wait": [_P, _P, _I, _I, _P],
+    "btp_peer_boundary_fwd": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
+    "btp_peer_boundary_bwd": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",

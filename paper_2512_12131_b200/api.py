@@ -65,10 +65,23 @@ def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
 
 
 def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
-                  device=None, attn_backend: str = "auto", precision: str = "bf16", comm: TPComm | None = None):
-    """Build this rank's executor for the plan's strategy (comm: default = the process group)."""
+                  device=None, attn_backend: str = "auto", precision: str = "bf16", comm: TPComm | None = None,
+                  boundary: str = "nccl"):
+    """Build this rank's executor for the plan's strategy (comm: default = the process group).
+
+    boundary="peer" (BTP, tp > 1): the chunk boundaries run as fused reduce-scatter -> fix-up/sigma
+    -> all-gather kernels over NVLink peer memory (torch symmetric-memory heap, csrc/peer.cu)
+    instead of NCCL all-reduces + a fix-up launch."""
     if comm is None:
         comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
+        if boundary == "peer" and pl.strategy is Strategy.BOTTLENECK:
+            from .peer import PeerComm
+
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            comm = TPComm(comm.tp, comm.rank, comm.group, comm.trace,
+                          peer=PeerComm(comm.tp, comm.rank, dev, provider="symmetric_memory"))
+    elif boundary not in ("nccl", "peer"):
+        raise ValueError(f"boundary must be 'nccl' or 'peer', got {boundary!r}")
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:
         return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)
@@ -167,10 +180,10 @@ class BlockTrainer:
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
-                 optimizer: bool = True, comm: TPComm | None = None, executor=None):
+                 optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl"):
         self.pl = pl
         self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
-                                                                      comm=comm)
+                                                                      comm=comm, boundary=boundary)
         # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
         self.adamw = dict(adamw or {}) if optimizer else None
         # collectives stay eager (NCCL outside graph capture); a step without live collectives is graphed

@@ -31,19 +31,24 @@ from .trace import Trace
 
 class TPComm:
     def __init__(self, tp: int = 1, rank: int = 0, group=None, trace: Trace | None = None, *,
-                 force: bool = False, emulate: bool = False):
+                 force: bool = False, emulate: bool = False, peer=None):
         self.tp = tp
         self.rank = rank
         self.group = group
         self.trace = trace if trace is not None else Trace()
         self.pass_tag = "forward"
         self.emulate = emulate
-        if (tp > 1 or force) and not emulate and not dist.is_initialized():
+        # peer: a peer.PeerComm — the BTP chunk boundaries then run as fused reduce-scatter /
+        # fix-up / all-gather kernels over peer memory instead of NCCL all-reduces
+        self.peer = peer
+        if peer is not None and (peer.tp != tp or peer.rank != rank):
+            raise ValueError("peer communicator disagrees on (tp, rank)")
+        if (tp > 1 or force) and not emulate and peer is None and not dist.is_initialized():
             raise RuntimeError("tp > 1 needs an initialised torch.distributed process group")
         if emulate and not 0 <= rank < tp:
             raise ValueError(f"rank {rank} outside tp={tp}")
-        # issue real collectives?
-        self.live = (tp > 1 or force) and not emulate
+        # issue real torch.distributed collectives? (a peer-only group has no process group)
+        self.live = (tp > 1 or force) and not emulate and dist.is_initialized()
 
     @classmethod
     def emulated(cls, tp: int, rank: int = 0, trace: Trace | None = None) -> "TPComm":

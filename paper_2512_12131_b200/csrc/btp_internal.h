@@ -1,6 +1,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "../../include/btp.h"
 
 namespace btp {
@@ -44,4 +46,13 @@ int embedding_bwd(const int* ids, const void* dx, long long lddx, int vocab, flo
                   int width, cudaStream_t st, bool f32);
 int cross_entropy(const void* logits, long long ldl, const int* targets, int vocab, float* loss_rows, void* dlogits,
                   long long ldd, int rows, float scale, cudaStream_t st, bool f32);
+// peer-memory chunk boundaries (peer.cu)
+int peer_signal(uint32_t* const* peer_flags, uint32_t* epoch, int slot, int rank, int tp, cudaStream_t st);
+int peer_wait(const uint32_t* flags, const uint32_t* epoch, int slot, int tp, cudaStream_t st);
+int peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, int tp, int rank, int T, int W, int r,
+                      int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
+                      cudaStream_t st);
+int peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
+                      const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
+                      cudaStream_t st);
 }  // namespace btp

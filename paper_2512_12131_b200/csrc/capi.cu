@@ -122,6 +122,28 @@ BTP_PAIR(btp_cross_entropy, cross_entropy,
           long long ldd, int rows, float scale, void* stream),
          A_XENT)
 
+int btp_peer_signal(unsigned int* const* peer_flags, unsigned int* epoch, int slot, int rank, int tp, void* stream) {
+  return btp::peer_signal(peer_flags, epoch, slot, rank, tp, ST(stream));
+}
+
+int btp_peer_wait(const unsigned int* flags, const unsigned int* epoch, int slot, int tp, void* stream) {
+  return btp::peer_wait(flags, epoch, slot, tp, ST(stream));
+}
+
+int btp_peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, int tp, int rank, int T, int W,
+                          int r, int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
+                          void* stream) {
+  return btp::peer_boundary_fwd(P_peers, ss_peers, tp, rank, T, W, r, variant, d, eps, z_own, s_own, a_peers,
+                                ST(stream));
+}
+
+int btp_peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
+                          const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
+                          void* stream) {
+  return btp::peer_boundary_bwd(da_peers, tp, rank, T, W, r, variant, d, z_own, s_own, dP_peers, dss_peers,
+                                ST(stream));
+}
+
 int btp_counter_add(int* ctr, int delta, void* stream) { return btp::counter_add(ctr, delta, ST(stream)); }
 
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,

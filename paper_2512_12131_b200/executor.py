@@ -33,6 +33,7 @@ import numpy as np
 import torch
 
 from . import kernels as K
+from . import peer
 from .attention import Attention
 from .comm import TPComm
 from .model import DecoderBlockWeights, Variant
@@ -159,6 +160,12 @@ class ExecutorBase:
     # ------------------------------------------------------------------ buffers
     def buf(self, name: str, shape, dtype=None) -> torch.Tensor:
         dtype = dtype or self.act
+        pc = getattr(self, "peer", None)
+        if pc is not None and pc.has(name):  # symmetric (peer-mapped) buffer of the fused boundaries
+            t = pc.buf(name)
+            if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+                raise PlanError(f"symmetric buffer {name}: {t.dtype} {tuple(t.shape)} != {dtype} {tuple(shape)}")
+            return t
         t = self._buf.get(name)
         if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
             t = torch.empty(shape, device=self.dev, dtype=dtype)
@@ -274,7 +281,30 @@ class BTPBlockExecutor(ExecutorBase):
         # sigma in the down-GEMM epilogue (GEMM kernel epilogue 1): TP = 1 only (at TP > 1 the
         # all-reduce sits between GEMM and sigma), cola, bf16, crossgate halves in 64-column blocks
         self.fuse_sigma = FUSE_SIGMA and precision == "bf16" and tp == 1 and self.var == 1 and self.r % 128 == 0
+        # chunk boundaries over peer memory (csrc/peer.cu): one fused reduce-scatter -> fix-up/sigma
+        # -> all-gather kernel per boundary and pass instead of an NCCL all-reduce + fix-up launch
+        self.peer = getattr(self.comm, "peer", None)
+        if self.peer is not None:
+            if not (self.grouping and self.online and not self.ckpt and precision == "bf16"):
+                raise PlanError("peer-memory boundaries need grouping, the online norm, bf16 and no low-rank ckpt")
+            if self.T % tp:
+                raise PlanError(f"peer-memory boundaries need T={self.T} divisible by tp={tp}")
+            self.fuse_sigma = False
+            self.peer.setup(self._peer_specs())
         self._load_weights(block)
+
+    CHUNKS = (("q", "k", "v"), ("o",), ("gate", "up"), ("down",))
+
+    def _peer_specs(self):
+        """Symmetric buffers of the peer boundaries, identical (names, shapes, order) on every rank:
+        per chunk the down-GEMM partial P, the pushed activation a, the up-GEMM dgrad partial dA and
+        the pushed dP; the online-norm riders ss1/ss2 and the pushed norm-statistic grads dss1/dss2."""
+        T, r, specs = self.T, self.r, []
+        for names in self.CHUNKS:
+            key, W = "_".join(names), len(names) * self.r
+            specs += [(f"{pre}_{key}", (T, W), self.act) for pre in ("P", "a", "dA", "dP")]
+        specs += [(nm, (T,), F32) for nm in ("ss1", "ss2", "dss1", "dss2")]
+        return specs
 
     # ------------------------------------------------------------------ weights
     def _load_weights(self, block: DecoderBlockWeights) -> None:
@@ -352,6 +382,8 @@ class BTPBlockExecutor(ExecutorBase):
         row_scale = rl if (norm_chunk and self.online) else None
         ss_total = ss if (norm_chunk and self.online) else None
         s_out = self.buf(f"s{s_tag}", (T,), F32) if (norm_chunk and self.online) else None
+        if self.peer is not None:
+            return self._down_boundary_peer(names, n_in, W, rl, s_tag, norm_chunk)
         a_store = self.buf(f"a_{'_'.join(names)}", (T, k * r)) if self.var == 1 else None
         if self.fuse_sigma:
             return self._down_boundary_fused(names, n_in, W, ss, rl, s_tag, norm_chunk, a_store)
@@ -413,6 +445,31 @@ class BTPBlockExecutor(ExecutorBase):
             else:
                 self.comm.all_reduce(P3[i], nm)
         return [P3[i] for i in range(k)], [a_store[:, i * r:(i + 1) * r] for i in range(k)], P3
+
+    def _down_boundary_peer(self, names, n_in, W, rl, s_tag, norm_chunk):
+        """Row-parallel down GEMM into the symmetric P, then ONE kernel: pull-reduce this rank's
+        T/tp rows of every rank's P (+ the ss rider), z = P/s and a = sigma(z) on them, push a into
+        every rank's a. z and s stay for the owned rows only (the backward needs nothing else)."""
+        T, r, k, tp = self.T, self.r, len(names), self.tp
+        key = "_".join(names)
+        P = self.buf(f"P_{key}", (T, k * r))
+        self._gemm(K.Gemm(n_in, W, P, row_scale=rl if norm_chunk else None))
+        pc = self.peer
+        pc.exchange(peer.READY)
+        z_own = self.buf(f"zown_{key}", (T // tp, k * r))
+        s_own = self.buf(f"s{s_tag}", (T // tp,), F32) if norm_chunk else None
+        a = self.buf(f"a_{key}", (T, k * r))
+        peer.boundary_fwd(pc, f"P_{key}", f"ss{s_tag}" if norm_chunk else None, T, k * r, r, self.var, self.d,
+                          self.eps, z_own, s_own, f"a_{key}")
+        pc.exchange(peer.DONE)
+        self.stats.kernel_launches += 5
+        gid = names[0] if k == 1 else self._gid(names)
+        if norm_chunk:
+            self.comm.trace.emit("all-reduce-coalesced", gid, "block", T * k * r, self.comm.pass_tag,
+                                 extras=(("fused-stat", T),))
+        else:
+            self.comm.trace.emit("all-reduce", gid, "block", T * k * r, self.comm.pass_tag)
+        return ([z_own[:, i * r:(i + 1) * r] for i in range(k)], [a[:, i * r:(i + 1) * r] for i in range(k)], z_own)
 
     @staticmethod
     def _gid(names) -> str:
@@ -545,6 +602,8 @@ class BTPBlockExecutor(ExecutorBase):
         all-reduce of da_P started asynchronously (NCCL's stream) while the independent weight
         gradient GEMM runs, then sigma-bwd (+ norm-bwd prologue) in place once the sum landed.
         zP is the stored z (= all-reduce buffer of the forward): [T, k*r] grouped, [k, T, r] not."""
+        if self.peer is not None:
+            return self._up_bwd_peer(names, dgrad_probs, wgrad_pairs, zP, s, dss_name)
         if self.grouping or len(dgrad_probs) == 1:
             self._gemm(*dgrad_probs)
         else:
@@ -559,6 +618,27 @@ class BTPBlockExecutor(ExecutorBase):
         for h in handles:
             self.comm.wait(h)
         return self._sigma_bwd(names, da_P, zP, s, dss_name)
+
+    def _up_bwd_peer(self, names, dgrad_probs, wgrad_pairs, z_own, s_own, dss_name):
+        """dgrad into the symmetric dA -> "ready" -> weight-gradient GEMM (independent, covers the
+        peers' arrival) -> ONE kernel: pull-reduce the owned rows of every rank's dA, sigma-bwd +
+        normalisation-bwd on them, push dP (and dss) into every rank -> "done"."""
+        T, r, k = self.T, self.r, len(names)
+        key = "_".join(names)
+        self._gemm(*dgrad_probs)
+        pc = self.peer
+        pc.signal(peer.READY)
+        self._wgrad(wgrad_pairs)
+        pc.wait(peer.READY)
+        dP = self.buf(f"dP_{key}", (T, k * r))
+        dss = self.buf(dss_name, (T,), F32) if s_own is not None else None
+        peer.boundary_bwd(pc, f"dA_{key}", T, k * r, r, self.var, self.d, z_own, s_own, f"dP_{key}",
+                          dss_name if s_own is not None else None)
+        pc.exchange(peer.DONE)
+        self.stats.kernel_launches += 5
+        self.comm.trace.emit("all-reduce", names[0] if k == 1 else self._gid(names), "block", T * k * r,
+                             self.comm.pass_tag)
+        return dP, dss
 
     def _sigma_bwd(self, names, da_P, zP, s, dss_name):
         k, r, T = len(names), self.r, self.T

@@ -1,0 +1,144 @@
+"""Symmetric peer-memory heap + signal flags for the fused BTP chunk boundaries (csrc/peer.cu).
+
+Every rank carves the SAME list of buffers at the SAME offsets out of one heap allocation, so a
+buffer's address on rank j is `base_j + offset`. The boundary kernels receive, per buffer, a
+device array of the tp addresses (rank order) and pull/push rows over NVLink.
+
+Two providers of the per-rank heap bases:
+
+* `symmetric_memory` (the box): `torch.distributed._symmetric_memory.empty` + `rendezvous`
+  over the job's process group — cuMem allocations exported to and mapped by every peer GPU.
+  PyTorch is only plumbing here: the kernels that move and reduce the data are libbtp's.
+* `VirtualPeers` (tests): tp ranks as tp threads of ONE process on ONE GPU, each with its own
+  CUDA stream; the "peer" buffers are plain device allocations of the same GPU. The kernels,
+  flags and executor code are exactly those of the multi-GPU path, so the single-GPU box can
+  check the multi-rank numerics and the signal/wait protocol.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import torch
+
+from . import _native
+
+READY, DONE = 0, 1   # flag slots: "my partial is written" / "my pushes have landed"
+N_SLOTS = 2
+_ALIGN = 256
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class VirtualPeers:
+    """Registry shared by the tp threads of a single-GPU multi-rank run."""
+
+    def __init__(self, tp: int):
+        self.tp = tp
+        self.bases = [0] * tp
+        self._barrier = threading.Barrier(tp, timeout=300)  # a dead rank breaks the barrier, not the test
+
+    def exchange(self, rank: int, base: int) -> list[int]:
+        self.bases[rank] = base
+        self._barrier.wait()
+        out = list(self.bases)
+        self._barrier.wait()  # nobody re-registers before everyone has read
+        return out
+
+    def barrier(self):
+        self._barrier.wait()
+
+
+class PeerComm:
+    """One rank's view of the symmetric heap: named buffers, peer pointer arrays, flags."""
+
+    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None):
+        if not 1 <= tp <= 8:
+            raise ValueError(f"peer boundaries support 1 <= tp <= 8, got {tp}")
+        self.tp, self.rank = tp, rank
+        self.dev = torch.device(device)
+        self.provider = provider
+        self.group = group
+        self.heap = None
+        self._bufs: dict[str, torch.Tensor] = {}
+        self._ptrs: dict[str, torch.Tensor] = {}
+        self.epoch = torch.zeros(N_SLOTS, dtype=torch.int32, device=self.dev)
+
+    # ------------------------------------------------------------------ heap
+    def setup(self, specs) -> None:
+        """specs: ordered [(name, shape, dtype)], identical on every rank. Allocates the heap,
+        exchanges bases, zeroes the flags, and synchronises the ranks once."""
+        layout, off = [], N_SLOTS * self.tp * 4
+        off = -(-off // _ALIGN) * _ALIGN
+        for name, shape, dtype in specs:
+            n = 1
+            for s in shape:
+                n *= int(s)
+            nbytes = n * torch.empty((), dtype=dtype).element_size()
+            layout.append((name, tuple(shape), dtype, off, nbytes))
+            off = -(-(off + nbytes) // _ALIGN) * _ALIGN
+        total = off
+        if isinstance(self.provider, VirtualPeers):
+            self.heap = torch.empty(total, dtype=torch.uint8, device=self.dev)
+            self.heap[: N_SLOTS * self.tp * 4].zero_()
+            torch.cuda.synchronize(self.dev)
+            bases = self.provider.exchange(self.rank, self.heap.data_ptr())
+        elif self.provider == "symmetric_memory":
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+
+            self.heap = symm_mem.empty(total, dtype=torch.uint8, device=self.dev)
+            self.heap[: N_SLOTS * self.tp * 4].zero_()
+            torch.cuda.synchronize(self.dev)
+            group = self.group if self.group is not None else dist.group.WORLD
+            hdl = symm_mem.rendezvous(self.heap, group)
+            bases = [int(p) for p in hdl.buffer_ptrs]
+            dist.barrier(group=group)  # every rank's flags are zero before anyone signals
+        else:
+            raise ValueError(f"unknown peer provider {self.provider!r}")
+        if len(bases) != self.tp:
+            raise RuntimeError(f"peer heap rendezvous returned {len(bases)} bases for tp={self.tp}")
+        self.bases = bases
+        self._flags_ptrs = torch.tensor(bases, dtype=torch.int64, device=self.dev)
+        for name, shape, dtype, o, nbytes in layout:
+            self._bufs[name] = self.heap[o:o + nbytes].view(dtype).view(shape)
+            self._ptrs[name] = torch.tensor([b + o for b in bases], dtype=torch.int64, device=self.dev)
+        torch.cuda.synchronize(self.dev)
+
+    def has(self, name: str) -> bool:
+        return name in self._bufs
+
+    def buf(self, name: str) -> torch.Tensor:
+        return self._bufs[name]
+
+    def ptrs(self, name: str):
+        return ctypes.c_void_p(self._ptrs[name].data_ptr())
+
+    # ------------------------------------------------------------------ signals
+    def signal(self, slot: int) -> None:
+        _native.call("btp_peer_signal", ctypes.c_void_p(self._flags_ptrs.data_ptr()),
+                     ctypes.c_void_p(self.epoch.data_ptr()), slot, self.rank, self.tp, _stream())
+
+    def wait(self, slot: int) -> None:
+        _native.call("btp_peer_wait", ctypes.c_void_p(self.heap.data_ptr()), ctypes.c_void_p(self.epoch.data_ptr()),
+                     slot, self.tp, _stream())
+
+    def exchange(self, slot: int = READY) -> None:
+        """signal + wait: a device-side barrier across the ranks on the current stream."""
+        self.signal(slot)
+        self.wait(slot)
+
+
+def boundary_fwd(pc: PeerComm, P_name, ss_name, T, W, r, variant, d, eps, z_own, s_own, a_name) -> None:
+    _native.call("btp_peer_boundary_fwd", pc.ptrs(P_name), pc.ptrs(ss_name) if ss_name else None, pc.tp, pc.rank,
+                 T, W, r, variant, d, ctypes.c_float(eps), ctypes.c_void_p(z_own.data_ptr()),
+                 ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None, pc.ptrs(a_name), _stream())
+
+
+def boundary_bwd(pc: PeerComm, da_name, T, W, r, variant, d, z_own, s_own, dP_name, dss_name) -> None:
+    _native.call("btp_peer_boundary_bwd", pc.ptrs(da_name), pc.tp, pc.rank, T, W, r, variant, d,
+                 ctypes.c_void_p(z_own.data_ptr()), ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None,
+                 pc.ptrs(dP_name), pc.ptrs(dss_name) if dss_name else None, _stream())
