@@ -290,7 +290,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     e2e = {"value": b * s / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
-           "d2h_bytes_per_step": 4, "loss": losses[-1], "api": "BlockTrainer.fit (pinned host batches, loss read back per step)",
+           "d2h_bytes_per_step": 4, "loss": losses[-1], "api": "BlockTrainer.fit (pinned host batches H2D per step on a copy stream; each step's loss copied D2H behind it and read by the host one step later)",
            "h2d_once_per_call_bytes": int(gh.numel() * gh.element_size())}
 
     # ---- roofline of the dominant kernel (the tcgen05 GEMM family), timed live per launch

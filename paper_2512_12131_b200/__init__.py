@@ -4,7 +4,9 @@ Drop-in for the BTP path of the reference package `btpsim` (pkg/src/btpsim/__ini
 the same config / plan / execution names, with the block computed on sm_100a tensor cores
 through libbtp.so (include/btp.h) and the TP collectives on NCCL. Additions the reference does
 not have: `train_step` (forward + backward), `BlockTrainer` (resident, CUDA-graph replayed
-training step), and the naive-TP / full-rank executors on the same kernels.
+training step with fused AdamW), the naive-TP / full-rank executors on the same kernels, the
+multi-layer model (`build_model`, `ModelTrainer`) and the peer-memory chunk boundaries
+(`boundary="peer"`).
 """
 
 from .tensor import DimensionError, DivisibilityError, Tensor, seeded_fill, tensor, zeros
@@ -16,23 +18,26 @@ from .model import (
     RunShape,
     Variant,
     build_block,
+    ModelWeights,
+    build_model,
     fan_in_scaled,
     preset,
     projection_dims,
+    token_batch,
 )
 from .plan import NormMode, PlanError, ShardPlan, Strategy, apply_grouping, describe, enumerate_collectives, plan
 from .trace import CollectiveRecord, Trace, ring_transfer_elements, trace_volume
-from .api import BlockTrainer, SimResult, StepResult, execute_forward, make_executor, train_step
+from .api import BlockTrainer, ModelTrainer, SimResult, StepResult, execute_forward, make_executor, train_step
 from .checkpointing import CkptPolicy, CkptReport, eff_ckpt, run_with_ckpt
 
 __all__ = [
     "Tensor", "tensor", "zeros", "seeded_fill", "DimensionError", "DivisibilityError",
     "ModelConfig", "RunShape", "Variant", "PRESETS", "COLA_60M", "preset", "projection_dims",
-    "DecoderBlockWeights", "build_block", "fan_in_scaled",
+    "DecoderBlockWeights", "build_block", "fan_in_scaled", "ModelWeights", "build_model", "token_batch",
     "Strategy", "NormMode", "ShardPlan", "PlanError", "plan", "apply_grouping", "describe",
     "enumerate_collectives",
     "CollectiveRecord", "Trace", "trace_volume", "ring_transfer_elements",
-    "execute_forward", "train_step", "make_executor", "BlockTrainer", "SimResult", "StepResult",
+    "execute_forward", "train_step", "make_executor", "BlockTrainer", "ModelTrainer", "SimResult", "StepResult",
     "CkptPolicy", "CkptReport", "eff_ckpt", "run_with_ckpt",
 ]
 

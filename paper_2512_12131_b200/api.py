@@ -244,7 +244,11 @@ class BlockTrainer:
         self._replays += 1
 
     def fit(self, x_hosts, G_host: torch.Tensor) -> list[float]:
-        """Pipelined steps over pinned-host input shards; returns every step's loss (read back)."""
+        """Pipelined steps over pinned-host input shards; returns every step's loss.
+
+        Every step's loss is copied device->host (4 bytes into a pinned ring) right behind the
+        step on the compute stream, and the host reads it one step later, after it has already
+        queued the next step, so the GPU never idles on the host's read-back round trip."""
         dev = self.ex.dev
         if self._slots is None:
             shape, dt = x_hosts[0].shape, x_hosts[0].dtype
@@ -259,6 +263,9 @@ class BlockTrainer:
         with torch.cuda.stream(copy):
             self._slots[0].copy_(x_hosts[0], non_blocking=True)
             copied[0].record(copy)
+        if getattr(self, "_loss_host", None) is None:
+            self._loss_host = torch.zeros(2, dtype=torch.float32).pin_memory()
+        read = [torch.cuda.Event(), torch.cuda.Event()]
         losses = []
         for i in range(len(x_hosts)):
             s = i & 1
@@ -272,7 +279,15 @@ class BlockTrainer:
                     copied[ns].record(copy)
             self.step_device(self._slots[s], self._target)
             consumed[s].record(main)
-            losses.append(float(self.loss_buf.item()))
+            self._loss_host[s:s + 1].copy_(self.loss_buf.view(1), non_blocking=True)  # D2H, this step
+            read[s].record(main)
+            if i >= 1:  # the previous step's loss, read while this step runs
+                read[s ^ 1].synchronize()
+                losses.append(float(self._loss_host[s ^ 1]))
+        if x_hosts:
+            last = (len(x_hosts) - 1) & 1
+            read[last].synchronize()
+            losses.append(float(self._loss_host[last]))
         return losses
 
     def step(self, x_host: torch.Tensor, g_host: torch.Tensor) -> float:
