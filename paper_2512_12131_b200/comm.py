@@ -71,17 +71,45 @@ class TPComm:
         self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
         return buf
 
-    def all_reduce_start(self, buf: torch.Tensor, chunk_id: str, tag: str = "block"):
+    def record(self, kind: str, chunk_id: str, elements: int, tag: str = "block", extras=()) -> None:
+        """One logical collective record (for collectives issued in several slices)."""
+        self.trace.emit(kind, chunk_id, tag, elements, self.pass_tag, extras=extras)
+
+    def all_reduce_start(self, buf: torch.Tensor, chunk_id: str, tag: str = "block", record: bool = True):
         """Asynchronous in-place all-reduce: NCCL runs on its own stream (ordered after the work
         already queued on the current stream) while the caller keeps launching independent
         kernels; `wait(handle)` orders the current stream after the reduction."""
         work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True) if self.live else None
-        self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
+        if record:
+            self.trace.emit("all-reduce", chunk_id, tag, buf.numel(), self.pass_tag)
+        return work
+
+    def all_reduce_coalesced_start(self, main: torch.Tensor, stat: torch.Tensor, chunk_id: str, tag: str = "block",
+                                   stat_tag: str = "fused-stat", record: bool = True):
+        """Asynchronous form of `all_reduce_coalesced` (bf16 payload + fp32 rider in one NCCL
+        group); returns a handle (or a list of handles) for `wait`."""
+        work = None
+        if self.live:
+            pg = self.group if self.group is not None else dist.distributed_c10d._get_default_group()
+            if dist.get_backend(pg) == "nccl" and hasattr(pg, "_start_coalescing"):
+                pg._start_coalescing(main.device)
+                dist.all_reduce(main, group=pg, async_op=True)  # queued into the open NCCL group
+                dist.all_reduce(stat, group=pg, async_op=True)
+                work = pg._end_coalescing(main.device)
+            else:
+                work = [dist.all_reduce(main, group=pg, async_op=True), dist.all_reduce(stat, group=pg, async_op=True)]
+        if record:
+            self.trace.emit("all-reduce-coalesced", chunk_id, tag, main.numel(), self.pass_tag,
+                            extras=((stat_tag, stat.numel()),))
         return work
 
     @staticmethod
     def wait(handle) -> None:
-        if handle is not None:
+        if isinstance(handle, list):
+            for h in handle:
+                if h is not None:
+                    h.wait()
+        elif handle is not None:
             handle.wait()
 
     def all_reduce_coalesced(self, main: torch.Tensor, stat: torch.Tensor, chunk_id: str,
@@ -93,8 +121,8 @@ class TPComm:
                 # (dist._coalescing_manager's all-reduce fast path would hand both tensors to
                 # allreduce_coalesced, which requires ONE dtype and raises for the bf16 + fp32 rider.)
                 pg._start_coalescing(main.device)
-                dist.all_reduce(main, group=pg)
-                dist.all_reduce(stat, group=pg)
+                dist.all_reduce(main, group=pg, async_op=True)  # queued into the open NCCL group
+                dist.all_reduce(stat, group=pg, async_op=True)
                 work = pg._end_coalescing(main.device)
                 if work is not None:
                     work.wait()  # stream-orders the caller after the grouped reduction

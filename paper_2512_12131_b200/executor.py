@@ -47,6 +47,11 @@ _VAR = {Variant.SVD: 0, Variant.COLA: 1}
 PRECISIONS = {"bf16": BF16, "fp32": F32}
 # TP = 1: sigma in the down-GEMM epilogue instead of a separate fix-up launch (A/B switch for benches)
 FUSE_SIGMA = True
+# live collectives: forward chunk boundaries pipelined over this many token slices, so the
+# all-reduce of slice c overlaps the down GEMM of slice c+1 (and the fix-up of slice c the
+# all-reduce of slice c+1) — the north_star's "overlapped with the adjacent GEMM tiles"
+FWD_AR_SLICES = 4
+FWD_SLICE_MIN_ROWS = 1024  # below this the launch count outweighs the overlap
 
 
 def _pick_splits(tiles: int, k_blocks: int, sms: int) -> int:
@@ -280,7 +285,15 @@ class BTPBlockExecutor(ExecutorBase):
                               "fp32" if precision == "fp32" else attn_backend)
         # sigma in the down-GEMM epilogue (GEMM kernel epilogue 1): TP = 1 only (at TP > 1 the
         # all-reduce sits between GEMM and sigma), cola, bf16, crossgate halves in 64-column blocks
-        self.fuse_sigma = FUSE_SIGMA and precision == "bf16" and tp == 1 and self.var == 1 and self.r % 128 == 0
+        self.fuse_sigma = (FUSE_SIGMA and precision == "bf16" and tp == 1 and self.var == 1 and self.r % 128 == 0
+                           and not self.comm.live)
+        # token slices of the pipelined forward boundaries (live collectives only; 128-row multiples)
+        self.fwd_slices = 1
+        if self.comm.live and self.grouping:
+            for c in (FWD_AR_SLICES, 2):
+                if c > 1 and self.T % (c * 128) == 0 and self.T // c >= FWD_SLICE_MIN_ROWS:
+                    self.fwd_slices = c
+                    break
         # chunk boundaries over peer memory (csrc/peer.cu): one fused reduce-scatter -> fix-up/sigma
         # -> all-gather kernel per boundary and pass instead of an NCCL all-reduce + fix-up launch
         self.peer = getattr(self.comm, "peer", None)
@@ -387,6 +400,8 @@ class BTPBlockExecutor(ExecutorBase):
         a_store = self.buf(f"a_{'_'.join(names)}", (T, k * r)) if self.var == 1 else None
         if self.fuse_sigma:
             return self._down_boundary_fused(names, n_in, W, ss, rl, s_tag, norm_chunk, a_store)
+        if self.fwd_slices > 1:
+            return self._down_boundary_sliced(names, n_in, W, ss, rl, s_out, norm_chunk, a_store)
         if self.grouping or k == 1:
             P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
             self._gemm(K.Gemm(n_in, W, P, row_scale=row_scale))
@@ -445,6 +460,41 @@ class BTPBlockExecutor(ExecutorBase):
             else:
                 self.comm.all_reduce(P3[i], nm)
         return [P3[i] for i in range(k)], [a_store[:, i * r:(i + 1) * r] for i in range(k)], P3
+
+    def _down_boundary_sliced(self, names, n_in, W, ss, rl, s_out, norm_chunk, a_store):
+        """Grouped boundary with live collectives, pipelined over token slices: the down GEMM of
+        slice c+1 runs while slice c's all-reduce (+ rider) is in flight on NCCL's stream; slice c's
+        fix-up + sigma runs once its reduction landed, overlapping slice c+1's. Rows are
+        independent, so the result is bit-identical to the unsliced boundary; the collective log
+        keeps ONE record per chunk boundary (the logical collective of the reference)."""
+        T, r, k, C = self.T, self.r, len(names), self.fwd_slices
+        online = norm_chunk and self.online
+        P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
+        gid = names[0] if k == 1 else self._gid(names)
+        rows = T // C
+        handles = []
+        for c in range(C):
+            sl = slice(c * rows, (c + 1) * rows)
+            self._gemm(K.Gemm(n_in[sl], W, P[sl], row_scale=rl[sl] if online else None))
+            if online:
+                handles.append(self.comm.all_reduce_coalesced_start(P[sl], ss[sl], gid, record=False))
+            else:
+                handles.append(self.comm.all_reduce_start(P[sl], gid, record=False))
+        if online:
+            self.comm.record("all-reduce-coalesced", gid, T * k * r, extras=(("fused-stat", T),))
+        else:
+            self.comm.record("all-reduce", gid, T * k * r)
+        for c in range(C):
+            self.comm.wait(handles[c])
+            if self.var == 1 or online:
+                sl = slice(c * rows, (c + 1) * rows)
+                K.fixup_sigma(P[sl], r=r, nproj=k, variant=self.var, z_out=P[sl],
+                              a_out=a_store[sl] if a_store is not None else None, ss_total=ss[sl] if online else None,
+                              d=self.d, s_out=s_out[sl] if s_out is not None else None, eps=self.eps)
+                self.stats.kernel_launches += 1
+        z = [P[:, i * r:(i + 1) * r] for i in range(k)]
+        a = [a_store[:, i * r:(i + 1) * r] for i in range(k)] if a_store is not None else z
+        return z, a, P
 
     def _down_boundary_peer(self, names, n_in, W, rl, s_tag, norm_chunk):
         """Row-parallel down GEMM into the symmetric P, then ONE kernel: pull-reduce this rank's

@@ -3,7 +3,8 @@
 NCCL refuses two ranks on one device, so the multi-rank numerics are covered over gloo
 (test_gpu_tp2.py). Here a ONE-rank NCCL process group runs the same step with every collective
 really issued (`TPComm(force=True)`): in-place all-reduces, the coalesced bf16+fp32 rider inside
-one NCCL group, the async backward all-reduce handles overlapping the weight-gradient GEMM, the
+one NCCL group, the forward boundaries pipelined over token slices with async (coalesced)
+all-reduces, the async backward all-reduce handles overlapping the weight-gradient GEMM, the
 loss all-reduce and the tail all-gather. A one-rank sum is the identity, so y, the loss and dx must be
 bit-identical to the record-only tp == 1 run (weight gradients to fp32 reduce-add order)."""
 
@@ -43,7 +44,10 @@ def _main(port, q):
         from paper_2512_12131_b200.plan import Strategy, plan
         from paper_2512_12131_b200.trace import Trace
 
-        b, s = 2, 64
+        from paper_2512_12131_b200 import executor as E
+
+        E.FUSE_SIGMA = False  # live collectives separate GEMM and sigma; compare like with like
+        b, s = 4, 1024       # T = 4096: the forward boundaries pipeline over 4 token slices
         blk, x, G, _ = inputs(SMALL, Variant.COLA, b, s)
         out = {}
         for grouping in (True, False):
@@ -52,6 +56,7 @@ def _main(port, q):
             ref = train_step(pl, blk, x, G)
             ex = make_executor(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True))
             assert ex.comm.live and dist.get_backend() == "nccl"
+            assert ex.fwd_slices == (4 if grouping else 1)
             got = train_step(pl, blk, x, G, executor=ex)
             torch.cuda.synchronize()
             same = {"y": np.array_equal(ref.y.values, got.y.values), "loss": ref.loss == got.loss,
@@ -59,7 +64,7 @@ def _main(port, q):
             # weight gradients: split-K partials meet in an fp32 reduce-add whose order is not fixed
             for fam in ("A", "B"):
                 for n, g in ref.grads[fam].items():
-                    same[f"d{fam}_{n}"] = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g)) < 1e-6
+                    same[f"d{fam}_{n}"] = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g)) < 1e-4
             out[grouping] = (same, got.trace.record_tuples("forward") == ref.trace.record_tuples("forward"),
                              len(got.trace.record_tuples("backward")))
         # the trainer loop with live NCCL collectives (eager, not graphed)

@@ -178,3 +178,31 @@ def test_btp_tp4_tp8_c60m_matches_oracle(world):
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred
         assert sum(rec[3] for rec in bwd) == 7 * b * s * C60M.r
+
+
+def test_btp_tp2_sliced_forward_boundaries():
+    """T = 2048: the forward chunk boundaries pipeline over two token slices (async all-reduce of
+    slice 0 under the down GEMM of slice 1), across two real ranks."""
+    from tests.gpu_util import BF16_TOL, SMALL, inputs, oracle_step, rel
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, enumerate_collectives, plan
+
+    b, s = 2, 1024
+    res = _run_tp2("btp", True, True, False, bs=(b, s))
+    blk, x, G, oblk = inputs(SMALL, Variant.COLA, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, tp=2, sharded=False)
+    pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 2), Variant.COLA, online_norm=True, grouping=True)
+    pred = [(p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
+    # L = sum(y * G) nearly cancels at this shape (|L| ~ 2 of sum|y*G| ~ 1e5): judge the loss error
+    # against the magnitude of its terms
+    scale = float(np.sum(np.abs(y_ref * G.values.reshape(-1, SMALL.d))))
+    for rank, (_, y, loss, dx, grads, fwd, _bwd, _rf, _) in res.items():
+        assert rel(y.reshape(-1, SMALL.d), y_ref) < BF16_TOL
+        assert abs(loss - loss_ref) / scale < BF16_TOL
+        gr = O.grads_for_rank(g_ref, 2, rank, SMALL.d, SMALL.d_ff)
+        assert rel(dx, gr["dx"]) < BF16_TOL
+        for n in O.PROJECTIONS:
+            assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
+            assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        assert fwd == pred  # one record per chunk boundary although each is issued in slices
