@@ -83,7 +83,8 @@ typedef struct btp_gemm_problem {
 int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream);
 
 /* Tile mode switch for btp_gemm: 1 (default) = CTA-pair tiles (cluster of 2 CTAs on one TPC,
- * tcgen05.mma.cta_group::2, 256 x BN per pair) for launches with plain/residual epilogues;
+ * tcgen05.mma.cta_group::2, 256 x BN per pair) for launches with plain / sigma epilogues
+ * (residual epilogues stay single-CTA); 2 = pair tiles for residual epilogues too;
  * 0 = single-CTA 128 x BN tiles everywhere. Returns the previous setting. */
 int btp_gemm_set_pair(int enable);
 

@@ -591,13 +591,14 @@ static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, 
   return best;
 }
 
-static int g_pair_mode = 1;  // CTA-pair (cta_group::2) tiles for plain epilogues; btp_gemm_set_pair()
+// CTA-pair (cta_group::2) tiles: 0 never, 1 plain / sigma epilogues, 2 also residual epilogues
+static int g_pair_mode = 1;
 
 }  // namespace btp
 
 extern "C" int btp_gemm_set_pair(int enable) {
   const int prev = btp::g_pair_mode;
-  btp::g_pair_mode = enable ? 1 : 0;
+  btp::g_pair_mode = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
   return prev;
 }
 
@@ -632,7 +633,7 @@ int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas,
   // 128-row-per-CTA aux prefetch does not overlap as well), so those launches stay single-CTA
   bool any_resid = false;
   for (int i = 0; i < n; ++i) any_resid = any_resid || probs[i].resid != nullptr;
-  const bool pair = g_pair_mode && (slots == 1 || sigma) && !any_resid && num_sms_cached() >= 2;
+  const bool pair = g_pair_mode && (slots == 1 || sigma) && (!any_resid || g_pair_mode == 2) && num_sms_cached() >= 2;
   const int tile_m = pair ? 2 * kBM : kBM;
   const int units = pair ? num_sms_cached() / 2 : num_sms_cached();
   const int sig_span = probs[0].epilogue == kEpiSigma ? 2 * probs[0].sigma_half : 0;

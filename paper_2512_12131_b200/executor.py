@@ -54,19 +54,22 @@ FWD_AR_SLICES = 4
 FWD_SLICE_MIN_ROWS = 1024  # below this the launch count outweighs the overlap
 
 
-def _pick_splits(tiles: int, k_blocks: int, sms: int) -> int:
-    """Split-K factor for a weight-gradient GEMM: fill >= ~90% of the SM waves while keeping
-    >= 8 k-blocks (512 tokens) per split."""
-    best, best_eff = 1, 0.0
+def _pick_splits(tiles: int, k_blocks: int, units: int) -> int:
+    """Split-K factor for a weight-gradient GEMM (the reduction runs over the T tokens).
+
+    tiles: 256 x 256 CTA-pair output tiles of one split; units: CTA pairs (SMs / 2). Cost model,
+    fitted to measured B200 sweeps (tests/gpu_gemm_ab.py, tests/gpu_gemm_ab2.py): a launch takes
+    waves x (k-blocks per split + ~5 k-blocks of per-tile epilogue / pipeline fill), with
+    waves = ceil(tiles * splits / units). Keeps >= 4 k-blocks (256 tokens) per split; ties go to
+    fewer splits (less reduce-add traffic)."""
+    best, best_cost = 1, None
     for s in range(1, 17):
-        if k_blocks // s < 8:
+        kb = -(-k_blocks // s)
+        if s > 1 and kb < 4:
             break
-        waves = math.ceil(tiles * s / sms)
-        eff = tiles * s / (waves * sms)
-        if eff >= 0.9:
-            return s
-        if eff > best_eff + 1e-9:
-            best, best_eff = s, eff
+        cost = -(-tiles * s // units) * (kb + 5)
+        if best_cost is None or cost < best_cost:
+            best, best_cost = s, cost
     return best
 
 
@@ -214,8 +217,8 @@ class ExecutorBase:
         out = (dY^T X) (* col_scale) via split-K and a deterministic reduction."""
         T = pairs[0][0].shape[0]
         kb = (T + 63) // 64
-        tiles = sum(math.ceil(dy.shape[1] / 128) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
-        splits = _pick_splits(tiles, kb, self.sms)
+        tiles = sum(math.ceil(dy.shape[1] / 256) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
+        splits = _pick_splits(tiles, kb, max(self.sms // 2, 1))
         if splits == 1:
             self._gemm(*[K.Gemm(dy, x, o, a_mn=True, b_mn=True, col_scale=col_scale) for dy, x, o in pairs])
             return

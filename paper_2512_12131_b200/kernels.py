@@ -150,9 +150,10 @@ def counter_add(ctr, delta: int = 1):
     _native.call("btp_counter_add", _p(ctr), int(delta), _stream())
 
 
-def set_pair_mode(enable: bool) -> bool:
-    """CTA-pair (cta_group::2) GEMM tiles on/off; returns the previous setting."""
-    return bool(_native.load().btp_gemm_set_pair(int(enable)))
+def set_pair_mode(mode: int) -> int:
+    """CTA-pair (cta_group::2) GEMM tiles: 0 off, 1 plain/sigma epilogues (default), 2 also residual
+    epilogues; returns the previous setting."""
+    return int(_native.load().btp_gemm_set_pair(int(mode)))
 
 
 def zero(t: torch.Tensor) -> None:
