@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], kPair ? 256 : 128);  // pair: both CTAs' epilogues release the leader's
+      // one arrival per epilogue warp (pair: both CTAs' four warps release the leader's buffer)
+      mbar_init(&tempty_bar[b], kPair ? 8 : 4);
     }
     for (int b = 0; b < 8; ++b) mbar_init(&aux_bar_all[b], 1);
     fence_barrier_init();
@@ -281,6 +282,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       tma_load_2d(slot_ptr(b, 0), &pr.tma_r, &aux_bar[b], col, row0);
       if (naux == 2) tma_load_2d(slot_ptr(b, 1), &pr.tma_r2, &aux_bar[b], col, row0);
     };
+    // hand TMEM accumulator buffer `b` back to the MMA warp: every lane's tcgen05.ld has completed
+    // (tcgen05.wait::ld), the warp converges, and ONE lane orders and arrives for the warp
+    auto release_tmem = [&](int b) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[b], 0);
+        else mbar_arrive(&tempty_bar[b]);
+      }
+    };
     int it = 0;
     int chunk_seq = 0;  // running chunk counter -> staging buffer parity
     for (int tile = unit; tile < P.total_tiles; tile += n_units, ++it) {
@@ -335,12 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             for (int j = 0; j < 32; ++j)
               zv[j] = pack_bf16(__uint_as_float(r[2 * j]) * rscale, __uint_as_float(r[2 * j + 1]) * rscale);
           }
-          if (c0 + 64 >= hb) {
-            // the accumulator is fully in registers: hand the TMEM buffer back to the MMA warp now
-            tc_fence_before();
-            if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[buf], 0);
-            else mbar_arrive(&tempty_bar[buf]);
-          }
+          if (c0 + 64 >= hb) release_tmem(buf);  // accumulator fully in registers: free the TMEM buffer now
           if (lane == 0) bulk_wait_read<1>();  // the z buffer's previous group has been read
           __syncwarp();
 #pragma unroll
@@ -408,6 +414,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rscale;
         }
+        // last chunk of the tile in registers: the MMA warp may overwrite this TMEM buffer while
+        // the chunk is still being converted and stored
+        if (c0 + cols_per_chunk >= n_valid) release_tmem(buf);
         const int col = n0 + c0;
         if (pr.col_scale != nullptr) {
           const int lim = min(cols_per_chunk, n_valid - c0);
@@ -488,9 +497,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           bulk_commit();
         }
       }
-      tc_fence_before();
-      if constexpr (kPair) mbar_arrive_cluster(&tempty_bar[buf], 0);  // the leader's MMA reuses the buffer
-      else mbar_arrive(&tempty_bar[buf]);
     }
     if (lane == 0) bulk_wait<0>();
   }
