@@ -209,6 +209,8 @@ def run_ours(args, cfg):
 
     if args.no_fuse_sigma:
         _executor.FUSE_SIGMA = False
+    if args.concurrent_wgrad:
+        _executor.ExecutorBase.concurrent_wgrad = True
     from paper_2512_12131_b200.model import RunShape, Variant, build_block, fan_in_scaled
     from paper_2512_12131_b200.plan import Strategy, plan
     from paper_2512_12131_b200.tensor import seeded_fill
@@ -370,6 +372,7 @@ def main(argv=None):
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-optimizer", action="store_true", help="drop the AdamW update from the step")
     ap.add_argument("--no-fuse-sigma", action="store_true", help="TP=1: separate fix-up/sigma kernel (A/B)")
+    ap.add_argument("--concurrent-wgrad", action="store_true", help="weight-gradient GEMMs on a side stream (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")

@@ -302,7 +302,19 @@ class BlockTrainer:
     def time_gemms(self, x: torch.Tensor, g: torch.Tensor) -> dict:
         """One step with every GEMM launch bracketed by CUDA events on its stream. The step is
         captured into a CUDA graph (events as record nodes) and replayed, so each interval is
-        device time only — no host enqueue gaps."""
+        device time only — no host enqueue gaps. The weight-gradient GEMMs run serialised here
+        (not on their side stream), so each interval is one kernel's own duration."""
+        execs = [self.ex] + list(getattr(self.ex, "blocks", []))
+        saved_cc = [e.concurrent_wgrad for e in execs]
+        for e in execs:
+            e.concurrent_wgrad = False
+        try:
+            return self._time_gemms(x, g)
+        finally:
+            for e, c in zip(execs, saved_cc):
+                e.concurrent_wgrad = c
+
+    def _time_gemms(self, x: torch.Tensor, g: torch.Tensor) -> dict:
         self.ex.gemm_timer = []
         self._eager(x, g)  # allocate every buffer outside the capture
         torch.cuda.synchronize()

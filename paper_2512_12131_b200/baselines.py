@@ -205,6 +205,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
                        "d_qkv", "u_qkv", dn1, ["qkv"])
         dx = self.buf("dx", (T, d))
         self._rnorm_bwd(dn1, S["x"], self.gamma1, S["s1"], dx_mid, dx, "gamma1")
+        self._join_side()
         return dx
 
     def weight_grads_by_name(self):
@@ -325,6 +326,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.comm.all_reduce(dn1, "attn")
         dx = self.buf("dx", (T, d))
         self._rnorm_bwd(dn1, S["x"], self.gamma1, S["s1"], dx_mid, dx, "gamma1")
+        self._join_side()
         return dx
 
     def weight_grads_by_name(self):

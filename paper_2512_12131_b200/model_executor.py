@@ -141,6 +141,7 @@ class ModelExecutor(ExecutorBase):
         K.zero(self.grad["embedding"])
         K.embedding_bwd(self._ids, dy_sh, self.grad["embedding"])
         self.stats.kernel_launches += 2
+        self._join_side()
         return dy_sh
 
     def optimizer_step(self, **hp) -> None:

@@ -165,3 +165,28 @@ def test_fp32_mode_c60m_forward():
     res = execute_forward(pl, blk, x, capture_workspaces=True, precision="fp32")
     _, _, ws_ref, _ = oracle_step(oblk, x, G, C60M, b, s)
     _check_ws(res.workspaces[0], ws_ref[0], tol=FP32_TOL)
+
+
+def test_concurrent_wgrad_stream_matches_serial(monkeypatch):
+    """Weight-gradient GEMMs on the side stream (concurrent with dgrads / row kernels) give the same
+    step as the serial schedule: y, loss, dx bit-identical, weight grads to reduce-add order."""
+    import numpy as np
+
+    from tests.gpu_util import C60M, inputs, rel
+    from paper_2512_12131_b200 import executor as E
+    from paper_2512_12131_b200.api import train_step
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, plan
+
+    b, s = 4, 256
+    blk, x, G, _ = inputs(C60M, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    monkeypatch.setattr(E.ExecutorBase, "concurrent_wgrad", False)
+    ser = train_step(pl, blk, x, G)
+    monkeypatch.setattr(E.ExecutorBase, "concurrent_wgrad", True)
+    con = train_step(pl, blk, x, G)
+    assert np.array_equal(ser.y.values, con.y.values) and np.array_equal(ser.dx, con.dx)
+    assert ser.loss == con.loss
+    for fam in ("A", "B"):
+        for n, g in ser.grads[fam].items():
+            assert rel(con.grads[fam][n], g) < 1e-4, (fam, n)

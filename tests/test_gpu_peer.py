@@ -39,16 +39,20 @@ def _run_virtual(tp, cfg, b, s, variant="cola", steps=1):
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    old = os.environ.get("CUDA_MODULE_LOADING")
-    os.environ["CUDA_MODULE_LOADING"] = "EAGER"
+    # EAGER: see above. 32 hardware work queues: tp ranks x (main + side streams) must not alias
+    # onto shared queues, where a rank's spinning wait kernel would block another rank's work.
+    env = {"CUDA_MODULE_LOADING": "EAGER", "CUDA_DEVICE_MAX_CONNECTIONS": "32"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         p = ctx.Process(target=_virtual_main, args=(tp, cfg, b, s, variant, steps, q))
         p.start()
     finally:
-        if old is None:
-            os.environ.pop("CUDA_MODULE_LOADING", None)
-        else:
-            os.environ["CUDA_MODULE_LOADING"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     try:
         res, err = q.get(timeout=900)
     finally:
