@@ -294,8 +294,10 @@ __device__ __forceinline__ float silu_fast(float x) {
 
 __device__ __forceinline__ float sigmoidf_safe(float x) {
   // exp of a non-positive argument only, as the reference sigmoid (tensor.py:121-124)
+  // 1 + e lies in [1, 2]: the MUFU reciprocal (__fdividef) is accurate to ~1 ulp there, and avoids
+  // the IEEE-division call sequence (the row kernels using this were issue-bound on it)
   const float e = __expf(-fabsf(x));
-  const float inv = 1.0f / (1.0f + e);
+  const float inv = __fdividef(1.0f, 1.0f + e);
   return x >= 0.0f ? inv : e * inv;
 }
 

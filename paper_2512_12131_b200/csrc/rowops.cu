@@ -571,7 +571,10 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master, 
                                                     const int* __restrict__ step_dev) {
   // the step count may live on the device so a replayed CUDA graph keeps advancing it
   const float step = (float)(step_dev ? *step_dev : step_host);
-  const float bc1 = 1.0f - powf(b1, step), bc2 = 1.0f - powf(b2, step);
+  // bias corrections folded into two per-thread reciprocals; the per-element quotient uses the MUFU
+  // reciprocal and sqrt(v) = v * rsqrt(v) (the IEEE div / sqrt call sequences made this kernel
+  // issue-bound rather than HBM-bound)
+  const float ibc1 = 1.0f / (1.0f - powf(b1, step)), ibc2 = 1.0f / (1.0f - powf(b2, step));
   const long long n8 = n >> 3;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8;
        i += (long long)gridDim.x * blockDim.x) {
@@ -589,7 +592,9 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master, 
     for (int j = 0; j < 8; ++j) {
       mm[j] = b1 * mm[j] + (1.0f - b1) * gg[j];
       vv[j] = b2 * vv[j] + (1.0f - b2) * gg[j] * gg[j];
-      const float upd = (mm[j] / bc1) / (sqrtf(vv[j] / bc2) + eps) + wd * p[j];
+      const float vh = vv[j] * ibc2;
+      const float root = vh > 0.0f ? vh * rsqrtf(vh) : 0.0f;
+      const float upd = __fdividef(mm[j] * ibc1, root + eps) + wd * p[j];
       p[j] -= lr * upd;
     }
     reinterpret_cast<float4*>(master + o)[0] = *reinterpret_cast<float4*>(p);
