@@ -42,7 +42,7 @@ class _ReplicatedNormMixin:
         T, d = self.T, self.d
         dss = self.buf("dss_r", (T,), F32)
         K.rmsnorm_bwd_prep(dn, x, gamma, s, dn, dss)
-        gparts = self.buf("gparts", (2 * self.sms, d), F32)
+        gparts = self.buf("gparts", (4 * self.sms, d), F32)
         nb = K.rmsnorm_bwd(dn, x, gamma, dss, dx_out, gparts, dres=dres)
         K.reduce_rows(gparts[:nb].view(nb, 1, d), self.grad[gkey].view(1, d))
         self.stats.kernel_launches += 3

@@ -357,20 +357,29 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const T* __restrict__ 
   for (int q = 0; q < kNormBwdMaxGroups; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
-  for (int row = r0 + slot; row < r1; row += slots) {
+  // two rows per iteration (row, row + slots): both rows' loads are in flight together
+  for (int row = r0 + slot; row < r1; row += 2 * slots) {
+    const int rowb = row + slots;
+    const bool hasb = rowb < r1;
     const float two_dss = 2.0f * dss[row];
+    const float two_dssb = hasb ? 2.0f * dss[rowb] : 0.f;
 #pragma unroll
     for (int q = 0; q < kNormBwdMaxGroups; ++q) {
       const int c = cg + q * tpr;
       if (c < nch) {
-        float fh[8], fx[8], fr[8], g[8];
+        float fh[8], fx[8], fr[8], g[8], hb[8], xb[8], rb[8];
         load8(dh + (long long)row * lddh + c * 8, fh);
         load8(x + (long long)row * ldx + c * 8, fx);
+        if (hasb) {
+          load8(dh + (long long)rowb * lddh + c * 8, hb);
+          load8(x + (long long)rowb * ldx + c * 8, xb);
+        }
         if (dres != nullptr) {
           load8(dres + (long long)row * ldr + c * 8, fr);
+          if (hasb) load8(dres + (long long)rowb * ldr + c * 8, rb);
         } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) fr[j] = 0.f;
+          for (int j = 0; j < 8; ++j) fr[j] = rb[j] = 0.f;
         }
         load_gamma8(gamma + c * 8, g);
         float o[8];
@@ -380,6 +389,14 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const T* __restrict__ 
           acc[q][j] = fmaf(fh[j], fx[j], acc[q][j]);
         }
         store8(dx + (long long)row * lddx + c * 8, o);
+        if (hasb) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            o[j] = rb[j] + hb[j] * g[j] + two_dssb * xb[j];
+            acc[q][j] = fmaf(hb[j], xb[j], acc[q][j]);
+          }
+          store8(dx + (long long)rowb * lddx + c * 8, o);
+        }
       }
     }
   }
@@ -607,6 +624,229 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master, 
   }
 }
 
+
+// ----------------------------------------------------------------------------- TMA row pipeline
+// HBM-bound per-row kernels (RMSNorm forward / backward) stream their input rows through a ring
+// of shared-memory stages filled by 1-D bulk copies (cp.async.bulk, completion on an mbarrier per
+// stage): one thread keeps `stages` rows of every input in flight per block, so the memory system
+// sees deep, register-free parallelism (the register-staged warp-per-row versions were
+// latency-bound at ~60 % of HBM bandwidth). A block owns a contiguous range of rows; its 256
+// threads split each row into 8-element chunks (thread t owns chunks t, t+256, ...), so per-column
+// state (gamma, the dgamma partial) stays in registers for the whole block.
+constexpr int kPipeThreads = 256;
+
+struct RowPipe {
+  uint8_t* smem;
+  uint64_t* bars;
+  uint32_t stage_bytes;
+  int stages;
+
+  __device__ __forceinline__ uint8_t* stage(int i) const { return smem + (size_t)(i % stages) * stage_bytes; }
+  __device__ __forceinline__ void wait(int i) const { mbar_wait(&bars[i % stages], (uint32_t)((i / stages) & 1)); }
+};
+
+__device__ __forceinline__ RowPipe make_pipe(uint8_t* sm, int stages, uint32_t stage_bytes) {
+  RowPipe rp;
+  rp.smem = sm;
+  rp.stage_bytes = stage_bytes;
+  rp.stages = stages;
+  rp.bars = reinterpret_cast<uint64_t*>(sm + (size_t)stages * stage_bytes);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&rp.bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  return rp;
+}
+
+// one thread: bring row `row` of up to three row-major inputs into the stage of pipeline slot i
+template <typename T>
+__device__ __forceinline__ void pipe_issue(const RowPipe& rp, int i, long long row, uint32_t row_bytes, const T* a,
+                                           long long lda, const T* b, long long ldb, const T* c, long long ldc) {
+  uint8_t* dst = rp.stage(i);
+  uint64_t* bar = &rp.bars[i % rp.stages];
+  const int n = 1 + (b != nullptr) + (c != nullptr);
+  mbar_arrive_expect_tx(bar, n * row_bytes);
+  bulk_load_1d(dst, a + row * lda, row_bytes, bar);
+  if (b != nullptr) bulk_load_1d(dst + row_bytes, b + row * ldb, row_bytes, bar);
+  if (c != nullptr) bulk_load_1d(dst + (b != nullptr ? 2 : 1) * row_bytes, c + row * ldc, row_bytes, bar);
+}
+
+// Online RMSNorm (+ residual) forward over rows [r0, r1) of this block, same contract as
+// rmsnorm_residual_kernel, warp-specialised: warp 8 streams rows into `stages` (<= 16) smem stages
+// with bulk copies (full barrier per stage), warps 0..7 each own every 8th row — the row statistic
+// is a warp reduction (no block barrier per row) — and release the stage (empty barrier) once read.
+constexpr int kFwdMaxStages = 16;
+constexpr int kFwdConsumers = 8;
+
+template <typename T, int NCH>
+__global__ void __launch_bounds__(32 * (kFwdConsumers + 1)) rmsnorm_residual_pipe_kernel(
+    const T* __restrict__ x, long long ldx, const T* __restrict__ branch, long long ldb, T* __restrict__ x_out,
+    long long ldo, const float* __restrict__ gamma, T* __restrict__ n_out, long long ldn, float* __restrict__ ss_out,
+    float* __restrict__ rl_out, int rows, int width, float eps, int rows_per_block, int kFwdStages) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int r0 = blockIdx.x * rows_per_block;
+  const int n = min(rows, r0 + rows_per_block) - r0;
+  if (n <= 0) return;
+  const uint32_t row_bytes = (uint32_t)width * sizeof(T);
+  const uint32_t stage_bytes = row_bytes * (branch != nullptr ? 2 : 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)kFwdStages * stage_bytes);
+  uint64_t* empty = full + kFwdMaxStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFwdStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == kFwdConsumers) {  // producer warp
+    if (lane == 0) {
+      for (int i = 0; i < n; ++i) {
+        const int s = i % kFwdStages;
+        if (i >= kFwdStages) mbar_wait(&empty[s], (uint32_t)(((i / kFwdStages) - 1) & 1));
+        uint8_t* dst = sm + (size_t)s * stage_bytes;
+        const long long row = r0 + i;
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        bulk_load_1d(dst, x + row * ldx, row_bytes, &full[s]);
+        if (branch != nullptr) bulk_load_1d(dst + row_bytes, branch + row * ldb, row_bytes, &full[s]);
+      }
+    }
+    return;
+  }
+  const int nch = width >> 3;
+  for (int i = warp; i < n; i += kFwdConsumers) {
+    const int s = i % kFwdStages;
+    const long long row = r0 + i;
+    mbar_wait(&full[s], (uint32_t)((i / kFwdStages) & 1));
+    const T* sx = reinterpret_cast<const T*>(sm + (size_t)s * stage_bytes);
+    const T* sb = sx + width;
+    typename Vec8<T>::Raw keep[NCH];
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const int c = lane + 32 * q;
+      if (c < nch) {
+        typename Vec8<T>::Raw w = Vec8<T>::ld(sx + c * 8);
+        if (branch != nullptr) {
+          float fx[8], fb[8];
+          Vec8<T>::unpack(w, fx);
+          load8(sb + c * 8, fb);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) fx[j] += fb[j];
+          w = Vec8<T>::pack(fx);
+          if (x_out != nullptr) Vec8<T>::st(x_out + row * ldo + c * 8, w);
+        }
+        keep[q] = w;
+        float f[8];
+        Vec8<T>::unpack(w, f);  // statistics of the stored (rounded) value
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ss = fmaf(f[j], f[j], ss);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the row is in registers: the stage may be refilled
+    ss = warp_sum(ss);
+    const float rl = sqrtf(ss / (float)width + eps);
+    if (lane == 0) {
+      if (ss_out) ss_out[row] = ss;
+      if (rl_out) rl_out[row] = rl;
+    }
+    if (n_out == nullptr) continue;
+    const float inv = 1.0f / rl;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const int c = lane + 32 * q;
+      if (c < nch) {
+        float f[8], g[8];
+        Vec8<T>::unpack(keep[q], f);
+        load_gamma8(gamma + c * 8, g);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = f[j] * g[j] * inv;
+        store8(n_out + row * ldn + c * 8, f);
+      }
+    }
+  }
+}
+
+// Online/sync RMSNorm backward over rows [r0, r1) of this block (contract of rmsnorm_bwd_kernel):
+// dx = dres + dh * gamma + 2 x dss ; dgamma partial row per block (this thread's columns).
+template <typename T, int G>
+__global__ void __launch_bounds__(kPipeThreads) rmsnorm_bwd_pipe_kernel(
+    const T* __restrict__ dh, long long lddh, const T* __restrict__ x, long long ldx, const float* __restrict__ gamma,
+    const float* __restrict__ dss, const T* __restrict__ dres, long long ldr, T* __restrict__ dx, long long lddx,
+    float* __restrict__ dgamma_partial, int rows, int width, int rows_per_block, int stages) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int r0 = blockIdx.x * rows_per_block;
+  const int n = max(0, min(rows, r0 + rows_per_block) - r0);
+  const int nch = width >> 3;
+  float acc[G][8];
+#pragma unroll
+  for (int q = 0; q < G; ++q)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
+  if (n > 0) {
+    const uint32_t row_bytes = (uint32_t)width * sizeof(T);
+    const int narr = dres != nullptr ? 3 : 2;
+    const RowPipe rp = make_pipe(sm, stages, narr * row_bytes);
+    if (threadIdx.x == 0)
+      for (int i = 0; i < min(stages, n); ++i) pipe_issue<T>(rp, i, r0 + i, row_bytes, dh, lddh, x, ldx, dres, ldr);
+    float g[G][8];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int c = threadIdx.x + q * kPipeThreads;
+      if (c < nch) load_gamma8(gamma + c * 8, g[q]);
+    }
+    for (int i = 0; i < n; ++i) {
+      const long long row = r0 + i;
+      rp.wait(i);
+      const T* sdh = reinterpret_cast<const T*>(rp.stage(i));
+      const T* sx = sdh + width;
+      const T* sr = sx + width;
+      const float two_dss = 2.0f * dss[row];
+      float o[G][8];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int c = threadIdx.x + q * kPipeThreads;
+        if (c < nch) {
+          float fh[8], fx[8], fr[8];
+          load8(sdh + c * 8, fh);
+          load8(sx + c * 8, fx);
+          if (dres != nullptr) {
+            load8(sr + c * 8, fr);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) fr[j] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            o[q][j] = fr[j] + fh[j] * g[q][j] + two_dss * fx[j];
+            acc[q][j] = fmaf(fh[j], fx[j], acc[q][j]);
+          }
+        }
+      }
+      __syncthreads();  // every thread is done reading stage i: refill it
+      if (threadIdx.x == 0 && i + stages < n)
+        pipe_issue<T>(rp, i + stages, row + stages, row_bytes, dh, lddh, x, ldx, dres, ldr);
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int c = threadIdx.x + q * kPipeThreads;
+        if (c < nch) store8(dx + row * lddx + c * 8, o[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int c = threadIdx.x + q * kPipeThreads;
+    if (c < nch) {
+      float* out = dgamma_partial + (long long)blockIdx.x * width + c * 8;
+      reinterpret_cast<float4*>(out)[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+      reinterpret_cast<float4*>(out)[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
+    }
+  }
+}
+
 // ============================================================================= launchers
 static inline int grid_for(long long items, int threads = 256) {
   const long long want = (items + threads - 1) / threads;
@@ -618,10 +858,68 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 
 #define BTP_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA
 
+// stages of the row pipeline for a given per-row stage size: ~72 KB of rows in flight per block,
+// so three 256-thread blocks share one SM's shared memory
+static inline int pipe_stages(uint32_t stage_bytes) {
+  int st = (int)((72u * 1024u) / stage_bytes);
+  return st < 2 ? 2 : (st > 8 ? 8 : st);
+}
+
+static inline size_t pipe_smem(int stages, uint32_t stage_bytes) {
+  return (size_t)stages * stage_bytes + (size_t)stages * sizeof(uint64_t);
+}
+
+template <typename Kern>
+static bool pipe_configure(Kern k, size_t smem) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+}
+
+template <typename T, int NCH>
+static int rmsnorm_residual_pipe_t(const T* x, long long ldx, const T* b, long long ldb, T* xo, long long ldo,
+                                   const float* gamma, T* no, long long ldn, float* ss_out, float* rl_out, int rows,
+                                   int width, float eps, cudaStream_t st) {
+  const uint32_t stage_bytes = (uint32_t)width * sizeof(T) * (b != nullptr ? 2 : 1);
+  int stages = (int)((64u * 1024u) / stage_bytes);  // ~64 KB of rows in flight per block
+  stages = stages < 2 ? 2 : (stages > kFwdMaxStages ? kFwdMaxStages : stages);
+  const size_t smem = (size_t)stages * stage_bytes + 2 * kFwdMaxStages * sizeof(uint64_t);
+  if (smem > 220 * 1024 || !pipe_configure(rmsnorm_residual_pipe_kernel<T, NCH>, smem)) return BTP_ERR_CUDA;
+  int per_sm = (int)((220 * 1024) / smem);
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+  int nblk = per_sm * num_sms_cached();
+  const int rpb = (rows + nblk - 1) / nblk;
+  nblk = (rows + rpb - 1) / rpb;
+  rmsnorm_residual_pipe_kernel<T, NCH><<<nblk, 32 * (kFwdConsumers + 1), smem, st>>>(
+      x, ldx, b, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows, width, eps, rpb, stages);
+  BTP_CHECK_LAUNCH();
+}
+
 template <typename T>
 static int rmsnorm_residual_t(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
                               long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
                               float* rl_out, int rows, int width, float eps, cudaStream_t st) {
+  {  // TMA row pipeline (rows are 16-byte aligned: checked by the caller)
+    const T* xb = static_cast<const T*>(x);
+    const T* bb = static_cast<const T*>(branch);
+    T* xo = static_cast<T*>(x_out);
+    T* no = static_cast<T*>(n_out);
+    const int nch = width / 8;
+    if (nch <= 32 * 2)
+      return rmsnorm_residual_pipe_t<T, 2>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows, width, eps,
+                                           st);
+    if (nch <= 32 * 8)
+      return rmsnorm_residual_pipe_t<T, 8>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows, width, eps,
+                                           st);
+    return rmsnorm_residual_pipe_t<T, 32>(xb, ldx, bb, ldb, xo, ldo, gamma, no, ldn, ss_out, rl_out, rows, width, eps,
+                                          st);
+  }
+}
+
+// register-staged warp-per-row form (kept for reference / A-B; not dispatched)
+template <typename T>
+[[maybe_unused]] static int rmsnorm_residual_regs_t(const void* x, long long ldx, const void* branch, long long ldb,
+                                                    void* x_out, long long ldo, const float* gamma, void* n_out,
+                                                    long long ldn, float* ss_out, float* rl_out, int rows, int width,
+                                                    float eps, cudaStream_t st) {
   const int blocks = (rows + 7) / 8;
   const int nch = width / 8;
   const T* xb = static_cast<const T*>(x);
@@ -753,25 +1051,33 @@ int rmsnorm_bwd(const void* dh, long long lddh, const void* x, long long ldx, co
   if (width % 8 || width > 8192 || lddh % 8 || ldx % 8 || lddx % 8 || (dres && ldr % 8)) return BTP_ERR_ALIGNMENT;
   if (!al16(dh) || !al16(x) || !al16(dx) || !al16(gamma) || (dres && !al16(dres))) return BTP_ERR_ALIGNMENT;
   const int nch = width / 8;
-  int tpr = 256;
-  while (tpr > 32 && tpr / 2 >= nch) tpr /= 2;
-  if (nch > tpr * kNormBwdMaxGroups) return BTP_ERR_DIM;
-  const int slots = 256 / tpr;
-  int nblk = max_blocks;
-  int rows_per_block = (rows + nblk - 1) / nblk;
+  // TMA row pipeline: one resident wave of 3 blocks per SM (bounded by the caller's partial rows)
+  int nblk = 3 * num_sms_cached();
+  if (nblk > max_blocks) nblk = max_blocks;
+  const int rows_per_block = (rows + nblk - 1) / nblk;
   nblk = (rows + rows_per_block - 1) / rows_per_block;
-  const size_t smem = slots > 1 ? (size_t)slots * width * sizeof(float) : 0;
-  if (smem > 48 * 1024) return BTP_ERR_DIM;
-  if (f32)
-    rmsnorm_bwd_kernel<float><<<nblk, 256, smem, st>>>(static_cast<const float*>(dh), lddh,
-                                                       static_cast<const float*>(x), ldx, gamma, dss,
-                                                       static_cast<const float*>(dres), ldr, static_cast<float*>(dx),
-                                                       lddx, dgamma_partial, rows, width, tpr, rows_per_block);
-  else
-    rmsnorm_bwd_kernel<bf16><<<nblk, 256, smem, st>>>(static_cast<const bf16*>(dh), lddh, static_cast<const bf16*>(x),
-                                                      ldx, gamma, dss, static_cast<const bf16*>(dres), ldr,
-                                                      static_cast<bf16*>(dx), lddx, dgamma_partial, rows, width, tpr,
-                                                      rows_per_block);
+  const uint32_t stage_bytes = (uint32_t)width * (f32 ? 4u : 2u) * (dres != nullptr ? 3u : 2u);
+  const int stages = pipe_stages(stage_bytes);
+  const size_t smem = pipe_smem(stages, stage_bytes);
+  if (smem > 200 * 1024) return BTP_ERR_DIM;
+  const int G = nch <= kPipeThreads ? 1 : (nch <= 2 * kPipeThreads ? 2 : 4);
+#define BTP_NB_LAUNCH(T, GG)                                                                                       \
+  do {                                                                                                             \
+    if (!pipe_configure(rmsnorm_bwd_pipe_kernel<T, GG>, smem)) return BTP_ERR_CUDA;                               \
+    rmsnorm_bwd_pipe_kernel<T, GG><<<nblk, kPipeThreads, smem, st>>>(                                              \
+        static_cast<const T*>(dh), lddh, static_cast<const T*>(x), ldx, gamma, dss, static_cast<const T*>(dres), \
+        ldr, static_cast<T*>(dx), lddx, dgamma_partial, rows, width, rows_per_block, stages);                     \
+  } while (0)
+  if (f32) {
+    if (G == 1) BTP_NB_LAUNCH(float, 1);
+    else if (G == 2) BTP_NB_LAUNCH(float, 2);
+    else BTP_NB_LAUNCH(float, 4);
+  } else {
+    if (G == 1) BTP_NB_LAUNCH(bf16, 1);
+    else if (G == 2) BTP_NB_LAUNCH(bf16, 2);
+    else BTP_NB_LAUNCH(bf16, 4);
+  }
+#undef BTP_NB_LAUNCH
   if (nblk_out) *nblk_out = nblk;
   BTP_CHECK_LAUNCH();
 }

@@ -768,7 +768,7 @@ class BTPBlockExecutor(ExecutorBase):
                 self._gemm(K.Gemm(dP[i], W[i * r:(i + 1) * r], dh, b_mn=True, resid=dh if i else None))
             g = self.grad[grad_key]
             self._wgrad([(dP[i], x_res, g[i * r:(i + 1) * r]) for i in range(k)], col_scale=gamma)
-        gparts = self.buf("gparts", (2 * self.sms, dl), F32)
+        gparts = self.buf("gparts", (4 * self.sms, dl), F32)
         nb = K.rmsnorm_bwd(dh, x_res, gamma, dss, dx_out, gparts, dres=dres)
         K.reduce_rows(gparts[:nb].view(nb, 1, dl), self.grad[gamma_key].view(1, dl))
         self.stats.kernel_launches += 2

@@ -131,7 +131,7 @@ class ModelExecutor(ExecutorBase):
         dss = self.buf("final_dss", (T,), F32)
         K.rmsnorm_bwd_prep(dhn, y, self.final_gamma, self._buf["final_rms"], dhn, dss)
         dy = self.buf("dy_full", (T, d))
-        gparts = self.buf("final_gparts", (2 * self.sms, d), F32)
+        gparts = self.buf("final_gparts", (4 * self.sms, d), F32)
         nb = K.rmsnorm_bwd(dhn, y, self.final_gamma, dss, dy, gparts)
         K.reduce_rows(gparts[:nb].view(nb, 1, d), self.grad["gamma1"].view(1, d))
         self.stats.kernel_launches += 3

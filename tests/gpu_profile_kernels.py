@@ -35,6 +35,15 @@ elif name == "rmsnorm":
     x, g = rnd(T, d), rnd(d, dtype=f32)
     n, ss, rl = torch.empty_like(x), torch.empty(T, device=dev, dtype=f32), torch.empty(T, device=dev, dtype=f32)
     run = lambda: K.rmsnorm_residual(x, g, n_out=n, ss_out=ss, rl_out=rl)  # noqa: E731
+elif name == "rmsnorm_bwd":   # dx = dres + dh*gamma + 2 x dss, dgamma partials [16384 x 2048]
+    dh, x, dres, g = rnd(T, d), rnd(T, d), rnd(T, d), rnd(d, dtype=f32)
+    dss, dx = torch.rand(T, device=dev, dtype=f32), torch.empty(T, d, device=dev, dtype=bf)
+    parts = torch.empty(4 * 148, d, device=dev, dtype=f32)
+    run = lambda: K.rmsnorm_bwd(dh, x, g, dss, dx, parts, dres=dres)  # noqa: E731
+elif name == "dot":           # loss partials <y, G> over [16384 x 2048]
+    y, G2 = rnd(T, d), rnd(T, d)
+    part = torch.empty(4 * 148, device=dev, dtype=f32)
+    run = lambda: K.dot(y, G2, part)  # noqa: E731
 elif name == "swiglu":
     g, u, a = rnd(T, f), rnd(T, f), torch.empty(T, f, device=dev, dtype=bf)
     run = lambda: K.swiglu(g, u, a)  # noqa: E731
