@@ -575,7 +575,9 @@ static int launch(const DevParams& P, int grid, cudaStream_t stream) {
 }
 
 // N-tile choice: persistent units (CTAs, or CTA pairs) run ceil(tiles / units) waves of tiles
-// whose mainloop time is ~ proportional to BN (+ a fixed per-tile cost, ~32 columns' worth).
+// whose time is ~ BN + a fixed per-tile cost. For CTA pairs that cost is ~192 columns' worth:
+// a 256 x 128 pair tile takes ~0.71x (not 0.5x) of a 256 x 256 one (measured on B200,
+// tests/gpu_gemm_bn.py), so BN = 256 wins unless its last wave is nearly empty.
 static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, int sig_span) {
   // pair mode stages BN/2 rows of B per CTA; an MN-major B needs whole 64-element chunks, so
   // BN = 192 (96 rows) is single-CTA only
@@ -591,7 +593,7 @@ static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, 
     for (int i = 0; i < n; ++i)
       tiles += (long long)((probs[i].M + tile_m - 1) / tile_m) * ((probs[i].N + bn - 1) / bn) * probs[i].splits;
     const long long waves = (tiles + units - 1) / units;
-    const long long cost = waves * (bn + 32);
+    const long long cost = waves * (bn + (pair ? 192 : 32));
     if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = bn; }
   }
   return best;

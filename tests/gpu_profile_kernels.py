@@ -31,6 +31,13 @@ elif name == "down_sigma":    # grouped down q|k|v with the crossgate epilogue (
 elif name == "up_resid":      # o up-projection + residual: [16384 x 2048], K = 512
     a, w, x, o = rnd(T, r), rnd(d, r), rnd(T, d), torch.empty(T, d, device=dev, dtype=bf)
     run = lambda: K.gemm(K.Gemm(a, w, o, resid=x))  # noqa: E731
+elif name == "dgrad_gu":      # gate|up up-projection dgrad: 2 x [16384 x 512], K = 5472, B MN-major
+    dg, w, o = rnd(2, T, f), rnd(2, f, r), torch.empty(2, T, r, device=dev, dtype=bf)
+    run = lambda: K.gemm(*[K.Gemm(dg[i], w[i], o[i], b_mn=True) for i in range(2)])  # noqa: E731
+elif name == "down_gu":       # gate|up down + sigma at TP=1: [16384 x 1024], K = 2048
+    n, w = rnd(T, d), rnd(2 * r, d)
+    P, A = torch.empty(T, 2 * r, device=dev, dtype=bf), torch.empty(T, 2 * r, device=dev, dtype=bf)
+    run = lambda: K.gemm(K.Gemm(n, w, P, sigma=(A, r // 2)))  # noqa: E731
 elif name == "rmsnorm":
     x, g = rnd(T, d), rnd(d, dtype=f32)
     n, ss, rl = torch.empty_like(x), torch.empty(T, device=dev, dtype=f32), torch.empty(T, device=dev, dtype=f32)
