@@ -180,14 +180,19 @@ class BlockTrainer:
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
-                 optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl"):
+                 optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl",
+                 graph_collectives: bool = True):
         self.pl = pl
         self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
                                                                       comm=comm, boundary=boundary)
         # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
         self.adamw = dict(adamw or {}) if optimizer else None
-        # collectives stay eager (NCCL outside graph capture); a step without live collectives is graphed
-        self.use_graph = use_graph and not self.ex.comm.live
+        # A step without live collectives is always graphed. With live NCCL collectives the whole
+        # step (NCCL kernels included) is captured too when graph_collectives — the TP > 1 step is
+        # ~100 launches per rank — and falls back to eager launches if the capture is refused.
+        live = self.ex.comm.live
+        nccl = live and dist.get_backend(self.ex.comm.group) == "nccl"
+        self.use_graph = use_graph and (not live or (nccl and graph_collectives))
         self.graphs: dict = {}
         self.graphed = False
         self._per_step_launches = 0
@@ -232,11 +237,22 @@ class BlockTrainer:
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                saved = self.ex.stats.kernel_launches
-                with torch.cuda.graph(graph, stream=side):
-                    self._eager(x, g)
+            saved = self.ex.stats.kernel_launches
+            n_rec = len(self.ex.comm.trace.records)
+            try:
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(graph, stream=side):
+                        self._eager(x, g)
+            except Exception as exc:  # capture refused (e.g. a backend without graph support): stay eager
+                import warnings
+
+                warnings.warn(f"CUDA-graph capture of the training step failed ({exc}); running eagerly")
+                torch.cuda.synchronize()
+                self.use_graph = False
+                return
+            finally:
                 self.ex.stats.kernel_launches = saved
+                del self.ex.comm.trace.records[n_rec:]  # a capture issues no collectives
             torch.cuda.current_stream().wait_stream(side)
             self.graphs[key], self.graphed = graph, True
             return

@@ -67,13 +67,17 @@ def _main(port, q):
                     same[f"d{fam}_{n}"] = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g)) < 1e-4
             out[grouping] = (same, got.trace.record_tuples("forward") == ref.trace.record_tuples("forward"),
                              len(got.trace.record_tuples("backward")))
-        # the trainer loop with live NCCL collectives (eager, not graphed)
+        # the trainer loop with live NCCL collectives: CUDA-graph captured (NCCL kernels inside the
+        # graph) vs eager launches from the same initial weights
         pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
-        tr = BlockTrainer(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True), adamw=dict(lr=1e-3))
-        xh, gh = tr.pinned_host_inputs(x.values, G.values)
-        losses = tr.fit([xh, xh, xh], gh)
+        runs = {}
+        for graphs in (True, False):
+            tr = BlockTrainer(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True), adamw=dict(lr=1e-3),
+                              graph_collectives=graphs)
+            xh, gh = tr.pinned_host_inputs(x.values, G.values)
+            runs[graphs] = (tr.graphed, tr.fit([xh, xh, xh, xh], gh))
         gathered = tr.ex.comm.all_gather_cols(torch.ones(4, 8, device="cuda"), "final-gather")
-        out["trainer"] = (tr.use_graph, losses, tuple(gathered.shape))
+        out["trainer"] = (runs, tuple(gathered.shape))
         dist.destroy_process_group()
         q.put((out, None))
     except Exception:
@@ -99,7 +103,9 @@ def test_nccl_one_rank_step_is_bit_identical():
         assert all(same.values()), (grouping, {k: v for k, v in same.items() if not v})
         assert fwd_equal
         assert n_bwd == (4 if grouping else 7)
-    graphed, losses, gshape = out["trainer"]
-    assert not graphed                          # live collectives keep the step eager
+    runs, gshape = out["trainer"]
+    (graphed, losses), (eager_graphed, eager_losses) = runs[True], runs[False]
+    assert graphed and not eager_graphed        # the NCCL step was captured into a CUDA graph
     assert all(np.isfinite(losses)) and losses[0] != losses[-1]  # AdamW moved the weights
+    np.testing.assert_allclose(losses, eager_losses, rtol=1e-3)  # replay == eager (split-K order aside)
     assert gshape == (4, 8)
