@@ -879,8 +879,10 @@ static int rmsnorm_residual_pipe_t(const T* x, long long ldx, const T* b, long l
                                    const float* gamma, T* no, long long ldn, float* ss_out, float* rl_out, int rows,
                                    int width, float eps, cudaStream_t st) {
   const uint32_t stage_bytes = (uint32_t)width * sizeof(T) * (b != nullptr ? 2 : 1);
-  int stages = (int)((64u * 1024u) / stage_bytes);  // ~64 KB of rows in flight per block
-  stages = stages < 2 ? 2 : (stages > kFwdMaxStages ? kFwdMaxStages : stages);
+  // Each of the 8 consumer warps owns rows w, w+8, ...; with a multiple of 8 stages every stage is
+  // only ever awaited by ONE warp, in order (a warp may never wait more than one phase ahead on an
+  // mbarrier). 16 stages when they fit in ~96 KB, else 8.
+  const int stages = 16u * stage_bytes <= 96u * 1024u ? 16 : kFwdConsumers;
   const size_t smem = (size_t)stages * stage_bytes + 2 * kFwdMaxStages * sizeof(uint64_t);
   if (smem > 220 * 1024 || !pipe_configure(rmsnorm_residual_pipe_kernel<T, NCH>, smem)) return BTP_ERR_CUDA;
   int per_sm = (int)((220 * 1024) / smem);
@@ -894,9 +896,17 @@ static int rmsnorm_residual_pipe_t(const T* x, long long ldx, const T* b, long l
 }
 
 template <typename T>
+static int rmsnorm_residual_regs_t(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
+                                   long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
+                                   float* rl_out, int rows, int width, float eps, cudaStream_t st);
+
+template <typename T>
 static int rmsnorm_residual_t(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
                               long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
                               float* rl_out, int rows, int width, float eps, cudaStream_t st) {
+  if ((size_t)kFwdConsumers * width * sizeof(T) * (branch != nullptr ? 2 : 1) > 192 * 1024)
+    return rmsnorm_residual_regs_t<T>(x, ldx, branch, ldb, x_out, ldo, gamma, n_out, ldn, ss_out, rl_out, rows, width,
+                                      eps, st);
   {  // TMA row pipeline (rows are 16-byte aligned: checked by the caller)
     const T* xb = static_cast<const T*>(x);
     const T* bb = static_cast<const T*>(branch);
@@ -914,12 +924,11 @@ static int rmsnorm_residual_t(const void* x, long long ldx, const void* branch, 
   }
 }
 
-// register-staged warp-per-row form (kept for reference / A-B; not dispatched)
+// register-staged warp-per-row form: rows too wide for 8 smem stages
 template <typename T>
-[[maybe_unused]] static int rmsnorm_residual_regs_t(const void* x, long long ldx, const void* branch, long long ldb,
-                                                    void* x_out, long long ldo, const float* gamma, void* n_out,
-                                                    long long ldn, float* ss_out, float* rl_out, int rows, int width,
-                                                    float eps, cudaStream_t st) {
+static int rmsnorm_residual_regs_t(const void* x, long long ldx, const void* branch, long long ldb, void* x_out,
+                                   long long ldo, const float* gamma, void* n_out, long long ldn, float* ss_out,
+                                   float* rl_out, int rows, int width, float eps, cudaStream_t st) {
   const int blocks = (rows + 7) / 8;
   const int nch = width / 8;
   const T* xb = static_cast<const T*>(x);

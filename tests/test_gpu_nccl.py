@@ -75,7 +75,8 @@ def _main(port, q):
             tr = BlockTrainer(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True), adamw=dict(lr=1e-3),
                               graph_collectives=graphs)
             xh, gh = tr.pinned_host_inputs(x.values, G.values)
-            runs[graphs] = (tr.graphed, tr.fit([xh, xh, xh, xh], gh))
+            losses = tr.fit([xh, xh, xh, xh], gh)
+            runs[graphs] = (tr.graphed, losses)
         gathered = tr.ex.comm.all_gather_cols(torch.ones(4, 8, device="cuda"), "final-gather")
         out["trainer"] = (runs, tuple(gathered.shape))
         dist.destroy_process_group()
