@@ -82,6 +82,20 @@ typedef struct btp_gemm_problem {
  * (grouped up-projections q|k|v and gate|up, simulator.py:655-668). */
 int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream);
 
+/* btp_gemm with the reduce-scatter of a BTP chunk boundary fused into the epilogue (SURVEY §8f
+ * row 2; replaces the row-parallel GEMM + the reduce half of SimGroup.all_reduce, simulator.py:
+ * 605-616): output rows [o * rows_per_owner, (o + 1) * rows_per_owner) of every problem are
+ * reduce-added from the epilogue's registers (red.global.add.v4.f32, 16 B per op, the fp32 add
+ * performed at the destination) into owners[o] — rank o's fp32 [rows_per_owner, width] buffer (ld),
+ * normally peer-mapped memory of another GPU — at columns col0[p] + n, as the tiles finish,
+ * instead of being stored. Plain epilogue only (row /
+ * column scale allowed; no residual, split-K or fp32 output); problem c pointers may be NULL.
+ * The owners' buffers must hold zeros (or the partial sums of other ranks) before the launch;
+ * the reduced values are complete once every rank's launch has finished (signal with
+ * btp_peer_signal on the same stream). owners / col0 are HOST arrays (n_owners / n entries). */
+int btp_gemm_scatter(const btp_gemm_problem* problems, int n, int bn_hint, void* const* owners, int n_owners,
+                     int rows_per_owner, int width, long long ld, const int* col0, void* stream);
+
 /* Tile mode switch for btp_gemm: 1 (default) = CTA-pair tiles (cluster of 2 CTAs on one TPC,
  * tcgen05.mma.cta_group::2, 256 x BN per pair) for launches with plain / sigma epilogues
  * (residual epilogues stay single-CTA); 2 = pair tiles for residual epilogues too;
@@ -266,6 +280,17 @@ int btp_peer_boundary_fwd(const void* const* P_peers, const float* const* ss_pee
 int btp_peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
                           const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
                           void* stream);
+
+/* The boundary halves that follow btp_gemm_scatter: the partial sums of every rank have already been
+ * reduce-added into this rank's owned rows R_own (fp32 [T/tp, W], local); the kernel reads them
+ * (and re-zeroes them for the next use), then does the same fix-up / sigma / push (forward) or
+ * sigma-bwd / push (backward) as btp_peer_boundary_fwd / _bwd. */
+int btp_peer_boundary_fwd_local(void* R_own, const float* const* ss_peers, int tp, int rank, int T, int W, int r,
+                                int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
+                                void* stream);
+int btp_peer_boundary_bwd_local(void* R_own, int tp, int rank, int T, int W, int r, int variant, int d,
+                                const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
+                                void* stream);
 
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);

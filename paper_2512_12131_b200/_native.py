@@ -29,6 +29,7 @@ _STATUS_NAMES = {
 # Every symbol include/btp.h declares; tests check the library exports exactly these.
 EXPORTED_SYMBOLS = (
     "btp_gemm",
+    "btp_gemm_scatter",
     "btp_gemm_set_pair",
     "btp_rmsnorm_residual",
     "btp_rmsnorm_apply",
@@ -71,6 +72,8 @@ EXPORTED_SYMBOLS = (
     "btp_peer_wait",
     "btp_peer_boundary_fwd",
     "btp_peer_boundary_bwd",
+    "btp_peer_boundary_fwd_local",
+    "btp_peer_boundary_bwd_local",
 )
 
 
@@ -122,6 +125,8 @@ _F = ctypes.c_float
 
 _SIGNATURES = {
     "btp_gemm": [ctypes.POINTER(GemmProblem), _I, _I, _P],
+    "btp_gemm_scatter": [ctypes.POINTER(GemmProblem), _I, _I, ctypes.POINTER(_P), _I, _I, _I, _LL,
+                         ctypes.POINTER(_I), _P],
     "btp_rmsnorm_residual": [_P, _LL, _P, _LL, _P, _LL, _P, _P, _LL, _P, _P, _I, _I, _F, _P],
     "btp_rmsnorm_apply": [_P, _LL, _P, _P, _I, _F, _P, _LL, _P, _I, _I, _P],
     "btp_fixup_sigma": [_P, _LL, _P, _I, _F, _P, _P, _LL, _P, _LL, _I, _I, _I, _I, _P],
@@ -148,6 +153,8 @@ _SIGNATURES = {
     "btp_peer_wait": [_P, _P, _I, _I, _P],
     "btp_peer_boundary_fwd": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
     "btp_peer_boundary_bwd": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "btp_peer_boundary_fwd_local": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
+    "btp_peer_boundary_bwd_local": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",

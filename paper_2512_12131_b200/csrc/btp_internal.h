@@ -8,6 +8,17 @@
 namespace btp {
 int num_sms_cached();
 int gemm_launch(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream);
+// scatter epilogue: each problem's output rows are reduce-added into the owning rank's buffer
+struct ScatterSpec {
+  int n_owners;             // tp
+  void* const* owners;      // host array: each owner's bf16 [rows_per_owner, width] buffer (ld)
+  int rows_per_owner;       // T / tp, multiple of 32
+  int width;                // columns of the owners' buffers
+  long long ld;
+  const int* col0;          // host array: first owner column of each problem
+};
+int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int max_ctas, cudaStream_t stream,
+                        const ScatterSpec* sc);
 int gemm_f32_launch(const btp_gemm_problem* probs, int n, cudaStream_t stream);
 // f32 = false: bf16 activations (training path); true: fp32 activations (parity mode)
 int rmsnorm_residual(const void* x, long long ldx, const void* branch, long long ldb, void* x_out, long long ldo,
@@ -51,8 +62,8 @@ int peer_signal(uint32_t* const* peer_flags, uint32_t* epoch, int slot, int rank
 int peer_wait(const uint32_t* flags, const uint32_t* epoch, int slot, int tp, cudaStream_t st);
 int peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, int tp, int rank, int T, int W, int r,
                       int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
-                      cudaStream_t st);
+                      cudaStream_t st, void* R_own = nullptr);
 int peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
                       const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
-                      cudaStream_t st);
+                      cudaStream_t st, void* R_own = nullptr);
 }  // namespace btp

@@ -30,6 +30,13 @@ int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream)
   return btp::gemm_launch(problems, n, bn_hint, 0, ST(stream));
 }
 
+int btp_gemm_scatter(const btp_gemm_problem* problems, int n, int bn_hint, void* const* owners, int n_owners,
+                     int rows_per_owner, int width, long long ld, const int* col0, void* stream) {
+  if (owners == nullptr || col0 == nullptr) return BTP_ERR_DIM;
+  const btp::ScatterSpec sc{n_owners, owners, rows_per_owner, width, ld, col0};
+  return btp::gemm_launch_scatter(problems, n, bn_hint, 0, ST(stream), &sc);
+}
+
 int btp_gemm_f32(const btp_gemm_problem* problems, int n, void* stream) {
   return btp::gemm_f32_launch(problems, n, ST(stream));
 }
@@ -142,6 +149,22 @@ int btp_peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, 
                           void* stream) {
   return btp::peer_boundary_bwd(da_peers, tp, rank, T, W, r, variant, d, z_own, s_own, dP_peers, dss_peers,
                                 ST(stream));
+}
+
+int btp_peer_boundary_fwd_local(void* R_own, const float* const* ss_peers, int tp, int rank, int T, int W, int r,
+                                int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
+                                void* stream) {
+  if (R_own == nullptr) return BTP_ERR_DIM;
+  return btp::peer_boundary_fwd(nullptr, ss_peers, tp, rank, T, W, r, variant, d, eps, z_own, s_own, a_peers,
+                                ST(stream), R_own);
+}
+
+int btp_peer_boundary_bwd_local(void* R_own, int tp, int rank, int T, int W, int r, int variant, int d,
+                                const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
+                                void* stream) {
+  if (R_own == nullptr) return BTP_ERR_DIM;
+  return btp::peer_boundary_bwd(nullptr, tp, rank, T, W, r, variant, d, z_own, s_own, dP_peers, dss_peers,
+                                ST(stream), R_own);
 }
 
 int btp_counter_add(int* ctr, int delta, void* stream) { return btp::counter_add(ctr, delta, ST(stream)); }

@@ -129,10 +129,22 @@ __global__ void peer_wait_kernel(const uint32_t* __restrict__ flags, const uint3
 
 // Forward boundary: one warp per owned row; lane work units = 8 "u" + 8 "v" columns (cola) or 8
 // columns (svd) of one projection.
+// kLocal: the partials were already reduce-added into this rank's owned rows R_own [rows_own, W]
+// by the other ranks' scatter GEMMs (btp_gemm_scatter): read them locally (and re-zero them for the
+// next use) instead of pulling every rank's P.
+__device__ __forceinline__ void own_sum8(float* R_own, long long off, float (&acc)[8]) {
+  float4* p = reinterpret_cast<float4*>(R_own + off);
+  const float4 a = __ldcv(p), b = __ldcv(p + 1);
+  acc[0] = a.x; acc[1] = a.y; acc[2] = a.z; acc[3] = a.w; acc[4] = b.x; acc[5] = b.y; acc[6] = b.z; acc[7] = b.w;
+  p[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  p[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+template <bool kLocal>
 __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
-    const bf16* const* __restrict__ P_peers, const float* const* __restrict__ ss_peers, int tp, int row0, int rows_own,
-    int W, int r, int variant, float inv_d, float eps, bf16* __restrict__ z_own, float* __restrict__ s_own,
-    bf16* const* __restrict__ a_peers) {
+    const bf16* const* __restrict__ P_peers, float* __restrict__ R_own, const float* const* __restrict__ ss_peers,
+    int tp, int row0, int rows_own, int W, int r, int variant, float inv_d, float eps, bf16* __restrict__ z_own,
+    float* __restrict__ s_own, bf16* const* __restrict__ a_peers) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < rows_own; i += gridDim.x * warps) {
@@ -152,8 +164,13 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
       if (variant == 1) {
         const int cu = p * r + g * 8, cv = cu + (r >> 1);
         float zu[8], zv[8];
-        pull_sum8(P_peers, tp, row * W + cu, zu);
-        pull_sum8(P_peers, tp, row * W + cv, zv);
+        if constexpr (kLocal) {
+          own_sum8(R_own, (long long)i * W + cu, zu);
+          own_sum8(R_own, (long long)i * W + cv, zv);
+        } else {
+          pull_sum8(P_peers, tp, row * W + cu, zu);
+          pull_sum8(P_peers, tp, row * W + cv, zv);
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) { zu[e] *= inv; zv[e] *= inv; }
         const uint4 wu = pack8(zu), wv = pack8(zv);
@@ -175,7 +192,8 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
       } else {
         const int c = p * r + g * 8;
         float z[8];
-        pull_sum8(P_peers, tp, row * W + c, z);
+        if constexpr (kLocal) own_sum8(R_own, (long long)i * W + c, z);
+        else pull_sum8(P_peers, tp, row * W + c, z);
 #pragma unroll
         for (int e = 0; e < 8; ++e) z[e] *= inv;
         const uint4 wz = pack8(z);
@@ -187,8 +205,10 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
   __threadfence_system();  // pushes visible system-wide before the "done" signal
 }
 
+template <bool kLocal>
 __global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
-    const bf16* const* __restrict__ da_peers, int tp, int row0, int rows_own, int W, int r, int variant, float inv_d,
+    const bf16* const* __restrict__ da_peers, float* __restrict__ R_own, int tp, int row0, int rows_own, int W, int r,
+    int variant, float inv_d,
     const bf16* __restrict__ z_own, const float* __restrict__ s_own, bf16* const* __restrict__ dP_peers,
     float* const* __restrict__ dss_peers) {
   const int warps = blockDim.x >> 5;
@@ -205,8 +225,13 @@ __global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
       if (variant == 1) {
         const int cu = p * r + g * 8, cv = cu + (r >> 1);
         float du_[8], dv_[8], zu[8], zv[8];
-        pull_sum8(da_peers, tp, row * W + cu, du_);
-        pull_sum8(da_peers, tp, row * W + cv, dv_);
+        if constexpr (kLocal) {
+          own_sum8(R_own, (long long)i * W + cu, du_);
+          own_sum8(R_own, (long long)i * W + cv, dv_);
+        } else {
+          pull_sum8(da_peers, tp, row * W + cu, du_);
+          pull_sum8(da_peers, tp, row * W + cv, dv_);
+        }
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + cu), zu);
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + cv), zv);
         float gu[8], gv[8];
@@ -229,7 +254,8 @@ __global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
       } else {
         const int c = p * r + g * 8;
         float dd[8], zz[8];
-        pull_sum8(da_peers, tp, row * W + c, dd);
+        if constexpr (kLocal) own_sum8(R_own, (long long)i * W + c, dd);
+        else pull_sum8(da_peers, tp, row * W + c, dd);
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + c), zz);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -279,25 +305,35 @@ static int check_geometry(int tp, int rank, int T, int W, int r, int variant) {
 
 int peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, int tp, int rank, int T, int W, int r,
                       int variant, int d, float eps, void* z_own, float* s_own, void* const* a_peers,
-                      cudaStream_t st) {
+                      cudaStream_t st, void* R_own) {
   if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
-  if (d <= 0 || !z_own || !a_peers || !P_peers || !a16p(z_own)) return BTP_ERR_DIM;
+  if (d <= 0 || !z_own || !a_peers || (!P_peers && !R_own) || !a16p(z_own)) return BTP_ERR_DIM;
   const int rows_own = T / tp;
-  peer_boundary_fwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
-      reinterpret_cast<const bf16* const*>(P_peers), ss_peers, tp, rank * rows_own, rows_own, W, r, variant,
-      1.0f / (float)d, eps, static_cast<bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(a_peers));
+  if (R_own != nullptr)
+    peer_boundary_fwd_kernel<true><<<rows_grid(rows_own), 256, 0, st>>>(
+        nullptr, static_cast<float*>(R_own), ss_peers, tp, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
+        eps, static_cast<bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(a_peers));
+  else
+    peer_boundary_fwd_kernel<false><<<rows_grid(rows_own), 256, 0, st>>>(
+        reinterpret_cast<const bf16* const*>(P_peers), nullptr, ss_peers, tp, rank * rows_own, rows_own, W, r, variant,
+        1.0f / (float)d, eps, static_cast<bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(a_peers));
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
 int peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
                       const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
-                      cudaStream_t st) {
+                      cudaStream_t st, void* R_own) {
   if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
-  if (d <= 0 || !z_own || !dP_peers || !da_peers || !a16p(z_own)) return BTP_ERR_DIM;
+  if (d <= 0 || !z_own || !dP_peers || (!da_peers && !R_own) || !a16p(z_own)) return BTP_ERR_DIM;
   const int rows_own = T / tp;
-  peer_boundary_bwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
-      reinterpret_cast<const bf16* const*>(da_peers), tp, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
-      static_cast<const bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(dP_peers), dss_peers);
+  if (R_own != nullptr)
+    peer_boundary_bwd_kernel<true><<<rows_grid(rows_own), 256, 0, st>>>(
+        nullptr, static_cast<float*>(R_own), tp, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
+        static_cast<const bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(dP_peers), dss_peers);
+  else
+    peer_boundary_bwd_kernel<false><<<rows_grid(rows_own), 256, 0, st>>>(
+        reinterpret_cast<const bf16* const*>(da_peers), nullptr, tp, rank * rows_own, rows_own, W, r, variant,
+        1.0f / (float)d, static_cast<const bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(dP_peers), dss_peers);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 

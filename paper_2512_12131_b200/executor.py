@@ -26,6 +26,7 @@ it MN-major); up weights [d_out/tp, r]; all weight grads fp32.
 
 from __future__ import annotations
 
+import dataclasses
 import math
 from dataclasses import dataclass, field
 
@@ -232,6 +233,23 @@ class ExecutorBase:
             torch.cuda.current_stream(self.dev).wait_stream(self._side_stream)
             self._side_pending = False
 
+    def _gemm_scatter(self, *probs: K.Gemm, owner_buf: str, col0) -> None:
+        """A GEMM launch whose epilogue reduce-adds each row block into the owning rank's
+        `owner_buf` (peer memory) — the row-parallel partial and its reduce-scatter in one kernel."""
+        pc = self.peer
+        W = pc.buf(owner_buf).shape[1]
+        flops = 0
+        for p in probs:
+            M = p.a.shape[1] if p.a_mn else p.a.shape[0]
+            Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
+            N = p.b.shape[1] if p.b_mn else p.b.shape[0]
+            flops += 2 * M * N * Kd
+        K.gemm_scatter(*probs, owners=pc.host_ptrs(owner_buf), rows_per_owner=self.T // self.tp, width=W, ld=W,
+                       col0=col0)
+        self.stats.gemm_launches += 1
+        self.stats.kernel_launches += 1
+        self.stats.gemm_flops += flops
+
     def _wgrad(self, pairs, col_scale=None):
         if not self.concurrent_wgrad:
             return self._wgrad_now(pairs, col_scale)
@@ -345,9 +363,14 @@ class BTPBlockExecutor(ExecutorBase):
         per chunk the down-GEMM partial P, the pushed activation a, the up-GEMM dgrad partial dA and
         the pushed dP; the online-norm riders ss1/ss2 and the pushed norm-statistic grads dss1/dss2."""
         T, r, specs = self.T, self.r, []
+        scatter = getattr(self.comm.peer, "scatter", False)
         for names in self.CHUNKS:
             key, W = "_".join(names), len(names) * self.r
-            specs += [(f"{pre}_{key}", (T, W), self.act) for pre in ("P", "a", "dA", "dP")]
+            if scatter:  # reduce targets: this rank's owned rows, written by every rank's scatter GEMM
+                specs += [(f"R_{key}", (T // self.tp, W), F32), (f"RdA_{key}", (T // self.tp, W), F32)]
+                specs += [(f"{pre}_{key}", (T, W), self.act) for pre in ("a", "dP")]
+            else:
+                specs += [(f"{pre}_{key}", (T, W), self.act) for pre in ("P", "a", "dA", "dP")]
         specs += [(nm, (T,), F32) for nm in ("ss1", "ss2", "dss1", "dss2")]
         return specs
 
@@ -534,15 +557,25 @@ class BTPBlockExecutor(ExecutorBase):
         every rank's a. z and s stay for the owned rows only (the backward needs nothing else)."""
         T, r, k, tp = self.T, self.r, len(names), self.tp
         key = "_".join(names)
-        P = self.buf(f"P_{key}", (T, k * r))
-        self._gemm(K.Gemm(n_in, W, P, row_scale=rl if norm_chunk else None))
         pc = self.peer
-        pc.exchange(peer.READY)
         z_own = self.buf(f"zown_{key}", (T // tp, k * r))
         s_own = self.buf(f"s{s_tag}", (T // tp,), F32) if norm_chunk else None
         a = self.buf(f"a_{key}", (T, k * r))
-        peer.boundary_fwd(pc, f"P_{key}", f"ss{s_tag}" if norm_chunk else None, T, k * r, r, self.var, self.d,
-                          self.eps, z_own, s_own, f"a_{key}")
+        ss_name = f"ss{s_tag}" if norm_chunk else None
+        if pc.scatter:
+            # ONE kernel for GEMM + reduce-scatter: every output row block is reduce-added into its
+            # owner's R buffer over NVLink as the tiles finish; then only owned rows are read
+            self._gemm_scatter(K.Gemm(n_in, W, None, row_scale=rl if norm_chunk else None), owner_buf=f"R_{key}",
+                               col0=[0])
+            pc.exchange(peer.READY)
+            peer.boundary_fwd_local(pc, f"R_{key}", ss_name, T, k * r, r, self.var, self.d, self.eps, z_own, s_own,
+                                    f"a_{key}")
+        else:
+            P = self.buf(f"P_{key}", (T, k * r))
+            self._gemm(K.Gemm(n_in, W, P, row_scale=rl if norm_chunk else None))
+            pc.exchange(peer.READY)
+            peer.boundary_fwd(pc, f"P_{key}", ss_name, T, k * r, r, self.var, self.d, self.eps, z_own, s_own,
+                              f"a_{key}")
         pc.exchange(peer.DONE)
         self.stats.kernel_launches += 5
         gid = names[0] if k == 1 else self._gid(names)
@@ -707,15 +740,23 @@ class BTPBlockExecutor(ExecutorBase):
         normalisation-bwd on them, push dP (and dss) into every rank -> "done"."""
         T, r, k = self.T, self.r, len(names)
         key = "_".join(names)
-        self._gemm(*dgrad_probs)
         pc = self.peer
+        if pc.scatter:  # dgrad + reduce-scatter in one kernel, into the owners' RdA buffers
+            self._gemm_scatter(*[dataclasses.replace(q, c=None) for q in dgrad_probs], owner_buf=f"RdA_{key}",
+                               col0=[i * r for i in range(len(dgrad_probs))])
+        else:
+            self._gemm(*dgrad_probs)
         pc.signal(peer.READY)
         self._wgrad(wgrad_pairs)
         pc.wait(peer.READY)
         dP = self.buf(f"dP_{key}", (T, k * r))
         dss = self.buf(dss_name, (T,), F32) if s_own is not None else None
-        peer.boundary_bwd(pc, f"dA_{key}", T, k * r, r, self.var, self.d, z_own, s_own, f"dP_{key}",
-                          dss_name if s_own is not None else None)
+        if pc.scatter:
+            peer.boundary_bwd_local(pc, f"RdA_{key}", T, k * r, r, self.var, self.d, z_own, s_own, f"dP_{key}",
+                                    dss_name if s_own is not None else None)
+        else:
+            peer.boundary_bwd(pc, f"dA_{key}", T, k * r, r, self.var, self.d, z_own, s_own, f"dP_{key}",
+                              dss_name if s_own is not None else None)
         pc.exchange(peer.DONE)
         self.stats.kernel_launches += 5
         self.comm.trace.emit("all-reduce", names[0] if k == 1 else self._gid(names), "block", T * k * r,

@@ -63,7 +63,7 @@ class Gemm:
 
     a: torch.Tensor
     b: torch.Tensor
-    c: torch.Tensor
+    c: torch.Tensor | None    # None only for gemm_scatter (the output goes to the owners' buffers)
     a_mn: bool = False
     b_mn: bool = False
     row_scale: torch.Tensor | None = None
@@ -86,9 +86,9 @@ class Gemm:
             N, Kb = self.b.shape
         if Kb != K:
             raise ValueError(f"GEMM inner dims disagree: A {tuple(self.a.shape)} B {tuple(self.b.shape)}")
-        if tuple(self.c.shape) != (M, N):
+        if self.c is not None and tuple(self.c.shape) != (M, N):
             raise ValueError(f"GEMM output {tuple(self.c.shape)} != ({M}, {N})")
-        c_fp32 = self.c.dtype == F32
+        c_fp32 = self.c is not None and self.c.dtype == F32
         if (self.splits > 1 or self.reduce_add) and not c_fp32:
             raise ValueError("split-K / reduce-add GEMMs need an fp32 output")
         split_stride = 0
@@ -110,7 +110,8 @@ class Gemm:
         return GemmProblem(
             a=self.a.data_ptr(), lda=_ld(self.a), a_mn=int(self.a_mn),
             b=self.b.data_ptr(), ldb=_ld(self.b), b_mn=int(self.b_mn),
-            c=self.c.data_ptr(), ldc=_ld(self.c), c_fp32=int(c_fp32),
+            c=None if self.c is None else self.c.data_ptr(), ldc=N if self.c is None else _ld(self.c),
+            c_fp32=int(c_fp32),
             M=M, N=N, K=K,
             row_scale=None if self.row_scale is None else self.row_scale.data_ptr(),
             col_scale=None if self.col_scale is None else self.col_scale.data_ptr(),
@@ -132,6 +133,16 @@ def gemm(*problems: Gemm, bn: int = 0) -> None:
         _native.call("btp_gemm_f32", arr, len(problems), _stream())
     else:
         _native.call("btp_gemm", arr, len(problems), bn, _stream())
+
+
+def gemm_scatter(*problems: Gemm, owners, rows_per_owner: int, width: int, ld: int, col0, bn: int = 0) -> None:
+    """One tcgen05 GEMM launch whose epilogue reduce-adds each output row block into the owning
+    rank's buffer (owners: tp device addresses, rank order) at columns col0[p] + n."""
+    arr = (GemmProblem * len(problems))(*[p.to_c() for p in problems])
+    own = (ctypes.c_void_p * len(owners))(*[int(o) for o in owners])
+    cols = (ctypes.c_int * len(col0))(*[int(c) for c in col0])
+    _native.call("btp_gemm_scatter", arr, len(problems), bn, own, len(owners), int(rows_per_owner), int(width),
+                 int(ld), cols, _stream())
 
 
 def adamw(master, m, v, g, work, *, lr, step=0, step_dev=None, b1=0.9, b2=0.95, eps=1e-8, wd=0.0):

@@ -55,14 +55,19 @@ class VirtualPeers:
 class PeerComm:
     """One rank's view of the symmetric heap: named buffers, peer pointer arrays, flags."""
 
-    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None):
+    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None, scatter: bool = True):
         if not 1 <= tp <= 8:
             raise ValueError(f"peer boundaries support 1 <= tp <= 8, got {tp}")
         self.tp, self.rank = tp, rank
         self.dev = torch.device(device)
         self.provider = provider
         self.group = group
+        # scatter=True: the producing GEMM reduce-adds its output straight into the owning ranks'
+        # buffers (btp_gemm_scatter, tile by tile) and the boundary kernel only reads its own rows;
+        # scatter=False: the GEMM stores locally and the boundary kernel pulls every rank's partial
+        self.scatter = scatter
         self.heap = None
+        self._hptrs: dict[str, list[int]] = {}
         self._bufs: dict[str, torch.Tensor] = {}
         self._ptrs: dict[str, torch.Tensor] = {}
         self.epoch = torch.zeros(N_SLOTS, dtype=torch.int32, device=self.dev)
@@ -83,7 +88,7 @@ class PeerComm:
         total = off
         if isinstance(self.provider, VirtualPeers):
             self.heap = torch.empty(total, dtype=torch.uint8, device=self.dev)
-            self.heap[: N_SLOTS * self.tp * 4].zero_()
+            self.heap.zero_()  # flags, and the reduce-add targets of the scatter GEMMs
             torch.cuda.synchronize(self.dev)
             bases = self.provider.exchange(self.rank, self.heap.data_ptr())
         elif self.provider == "symmetric_memory":
@@ -91,7 +96,7 @@ class PeerComm:
             import torch.distributed._symmetric_memory as symm_mem
 
             self.heap = symm_mem.empty(total, dtype=torch.uint8, device=self.dev)
-            self.heap[: N_SLOTS * self.tp * 4].zero_()
+            self.heap.zero_()  # flags, and the reduce-add targets of the scatter GEMMs
             torch.cuda.synchronize(self.dev)
             group = self.group if self.group is not None else dist.group.WORLD
             hdl = symm_mem.rendezvous(self.heap, group)
@@ -105,7 +110,8 @@ class PeerComm:
         self._flags_ptrs = torch.tensor(bases, dtype=torch.int64, device=self.dev)
         for name, shape, dtype, o, nbytes in layout:
             self._bufs[name] = self.heap[o:o + nbytes].view(dtype).view(shape)
-            self._ptrs[name] = torch.tensor([b + o for b in bases], dtype=torch.int64, device=self.dev)
+            self._hptrs[name] = [b + o for b in bases]
+            self._ptrs[name] = torch.tensor(self._hptrs[name], dtype=torch.int64, device=self.dev)
         torch.cuda.synchronize(self.dev)
 
     def has(self, name: str) -> bool:
@@ -116,6 +122,10 @@ class PeerComm:
 
     def ptrs(self, name: str):
         return ctypes.c_void_p(self._ptrs[name].data_ptr())
+
+    def host_ptrs(self, name: str) -> list[int]:
+        """Every rank's address of buffer `name`, rank order (host ints, for tensor maps)."""
+        return self._hptrs[name]
 
     # ------------------------------------------------------------------ signals
     def signal(self, slot: int) -> None:
@@ -142,3 +152,17 @@ def boundary_bwd(pc: PeerComm, da_name, T, W, r, variant, d, z_own, s_own, dP_na
     _native.call("btp_peer_boundary_bwd", pc.ptrs(da_name), pc.tp, pc.rank, T, W, r, variant, d,
                  ctypes.c_void_p(z_own.data_ptr()), ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None,
                  pc.ptrs(dP_name), pc.ptrs(dss_name) if dss_name else None, _stream())
+
+
+def boundary_fwd_local(pc: PeerComm, R_name, ss_name, T, W, r, variant, d, eps, z_own, s_own, a_name) -> None:
+    _native.call("btp_peer_boundary_fwd_local", ctypes.c_void_p(pc.buf(R_name).data_ptr()),
+                 pc.ptrs(ss_name) if ss_name else None, pc.tp, pc.rank, T, W, r, variant, d, ctypes.c_float(eps),
+                 ctypes.c_void_p(z_own.data_ptr()), ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None,
+                 pc.ptrs(a_name), _stream())
+
+
+def boundary_bwd_local(pc: PeerComm, R_name, T, W, r, variant, d, z_own, s_own, dP_name, dss_name) -> None:
+    _native.call("btp_peer_boundary_bwd_local", ctypes.c_void_p(pc.buf(R_name).data_ptr()), pc.tp, pc.rank, T, W, r,
+                 variant, d, ctypes.c_void_p(z_own.data_ptr()),
+                 ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None, pc.ptrs(dP_name),
+                 pc.ptrs(dss_name) if dss_name else None, _stream())

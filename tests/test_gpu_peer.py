@@ -20,16 +20,16 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _virtual_main(tp, cfg, b, s, variant, steps, q):
+def _virtual_main(tp, cfg, b, s, variant, steps, q, scatter=True):
     try:
-        q.put((_run_virtual_threads(tp, cfg, b, s, variant, steps), None))
+        q.put((_run_virtual_threads(tp, cfg, b, s, variant, steps, scatter), None))
     except BaseException:
         import traceback
 
         q.put((None, traceback.format_exc()))
 
 
-def _run_virtual(tp, cfg, b, s, variant="cola", steps=1):
+def _run_virtual(tp, cfg, b, s, variant="cola", steps=1, scatter=True):
     """Runs the tp threads in a fresh process with eager module loading: with lazy loading, the
     first launch of a not-yet-loaded kernel (e.g. cuDNN's attention) waits for the device to go
     idle, which a peer's spinning wait kernel on the SAME GPU never lets happen (on the multi-GPU
@@ -45,7 +45,7 @@ def _run_virtual(tp, cfg, b, s, variant="cola", steps=1):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
-        p = ctx.Process(target=_virtual_main, args=(tp, cfg, b, s, variant, steps, q))
+        p = ctx.Process(target=_virtual_main, args=(tp, cfg, b, s, variant, steps, q, scatter))
         p.start()
     finally:
         for k, v in old.items():
@@ -64,7 +64,7 @@ def _run_virtual(tp, cfg, b, s, variant="cola", steps=1):
     return res, blk, x, G, oblk
 
 
-def _run_virtual_threads(tp, cfg, b, s, variant, steps):
+def _run_virtual_threads(tp, cfg, b, s, variant, steps, scatter=True):
     from tests.gpu_util import inputs
     from paper_2512_12131_b200.api import shard_input
     from paper_2512_12131_b200.comm import TPComm
@@ -104,7 +104,7 @@ def _run_virtual_threads(tp, cfg, b, s, variant, steps):
             torch.cuda.set_device(0)
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                pc = PeerComm(tp, rank, "cuda:0", provider=vp)
+                pc = PeerComm(tp, rank, "cuda:0", provider=vp, scatter=scatter)
                 comm = TPComm(tp, rank, trace=Trace(), peer=pc)
                 pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, tp), var, online_norm=True, grouping=True)
                 ex = BTPBlockExecutor(pl, blk, comm, "cuda:0", attn_backend=backend)
@@ -133,15 +133,19 @@ def _run_virtual_threads(tp, cfg, b, s, variant, steps):
     return res
 
 
-@pytest.mark.parametrize("tp,variant", [(2, "cola"), (4, "cola"), (2, "svd")])
-def test_peer_boundaries_match_oracle(tp, variant):
+@pytest.mark.parametrize("tp,variant,scatter", [(2, "cola", True), (4, "cola", True), (2, "svd", True),
+                                                (2, "cola", False), (4, "cola", False)])
+def test_peer_boundaries_match_oracle(tp, variant, scatter):
+    """scatter=True: the down / dgrad GEMMs reduce-add their row blocks into the owning ranks'
+    buffers (GEMM + reduce-scatter in one kernel); scatter=False: GEMM stores locally and the
+    boundary kernel pulls every rank's partial."""
     from tests.gpu_util import BF16_TOL, SMALL, oracle_step, rel
     from oracle import btp_oracle as O
     from paper_2512_12131_b200.model import RunShape, Variant
     from paper_2512_12131_b200.plan import Strategy, enumerate_collectives, plan
 
     b, s = 2, 64
-    res, blk, x, G, oblk = _run_virtual(tp, SMALL, b, s, variant, steps=2)
+    res, blk, x, G, oblk = _run_virtual(tp, SMALL, b, s, variant, steps=2, scatter=scatter)
     y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, tp=tp, sharded=False)
     pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, tp), Variant(variant), online_norm=True, grouping=True)
     pred = [(p.chunk_id, p.kind, p.tag, p.elements, p.extras) for p in enumerate_collectives(pl)]
@@ -245,4 +249,7 @@ def test_symmetric_memory_provider_one_rank():
             p.kill()
     assert err is None, err
     worst = max(errs, key=errs.get)
-    assert errs[worst] < 1e-2, errs  # fused-sigma GEMM path vs peer path: bf16 rounding points differ
+    # two bf16 pipelines with different rounding points (fused-sigma GEMM epilogue vs scatter GEMM +
+    # fp32 reduce + boundary kernel), each within 2e-2 of the float64 oracle (the other tests): their
+    # mutual distance is bounded by the sum
+    assert errs[worst] < 4e-2, errs
