@@ -85,8 +85,8 @@ int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream)
 /* btp_gemm with the reduce-scatter of a BTP chunk boundary fused into the epilogue (SURVEY §8f
  * row 2; replaces the row-parallel GEMM + the reduce half of SimGroup.all_reduce, simulator.py:
  * 605-616): output rows [o * rows_per_owner, (o + 1) * rows_per_owner) of every problem are
- * reduce-added from the epilogue's registers (red.global.add.v4.f32, 16 B per op, the fp32 add
- * performed at the destination) into owners[o] — rank o's fp32 [rows_per_owner, width] buffer (ld),
+ * TMA reduce-added in 32 x 32 fp32 chunks (the add performed at the destination) into owners[o] —
+ * rank o's fp32 [rows_per_owner, width] buffer (row stride ld, rows_per_owner % 32 == 0),
  * normally peer-mapped memory of another GPU — at columns col0[p] + n, as the tiles finish,
  * instead of being stored. Plain epilogue only (row /
  * column scale allowed; no residual, split-K or fp32 output); problem c pointers may be NULL.

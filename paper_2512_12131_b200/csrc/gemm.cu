@@ -73,17 +73,16 @@ struct DevParams {
   DevProblem prob[kMaxProblems];
   int num_problems;
   int total_tiles;
-  // Scatter mode (the GEMM half of a BTP chunk boundary over peer memory): every output row is
-  // reduce-added from registers (red.global.add.v4.f32, 16 B per op; the fp32 add is performed at
-  // the destination) into the fp32 buffer of the rank owning it — rows [o * scatter_rows,
+  // Scatter mode (the GEMM half of a BTP chunk boundary over peer memory): every 32-row x 32-column
+  // fp32 output chunk is TMA reduce-added (cp.reduce.async.bulk.tensor .add, the fp32 add performed
+  // at the destination) into the buffer of the rank owning those rows — rows [o * scatter_rows,
   // (o + 1) * scatter_rows) belong to rank o — instead of being stored locally: the reduce-scatter
-  // of the row-parallel partial happens tile by tile inside the GEMM, over NVLink. fp32 keeps the
-  // cross-rank sum at one rounding (a bf16 destination add rounds once per rank: measured 2.07e-2
-  // on a TP=4 gradient against the 2e-2 bar).
+  // of the row-parallel partial happens tile by tile inside the GEMM, over NVLink. fp32 because
+  // sm_100a's tensor reduce has no bf16 add, and it keeps the cross-rank sum at one rounding
+  // (per-row register red.add was 3.6x slower: one row per lane is uncoalesced).
   int scatter_n;
   int scatter_rows;
-  long long scatter_ld;
-  float* scatter[kMaxOwners];
+  CUtensorMap scatter[kMaxOwners];
 };
 
 // kSlots: staging slots per chunk buffer (2 for the two-input / two-output swiglu-bwd epilogue,
@@ -477,24 +476,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           continue;
         }
-        if (P.scatter_n > 0) {
-          // reduce-add this lane's row chunk into the owning rank's fp32 buffer (16 B ops)
-          const int grow = out_row0 + lane;
-          if (grow < pr.M) {
-            const int owner = grow / P.scatter_rows;
-            float* dst = P.scatter[owner] + (long long)(grow - owner * P.scatter_rows) * P.scatter_ld +
-                         pr.scatter_col0 + col;
-            const int lim = min(64, n_valid - c0);
-#pragma unroll
-            for (int g4 = 0; g4 < 16; ++g4) {
-              if (g4 * 4 < lim)
-                asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + g4 * 4),
-                             "f"(v[4 * g4]), "f"(v[4 * g4 + 1]), "f"(v[4 * g4 + 2]), "f"(v[4 * g4 + 3])
-                             : "memory");
-            }
-          }
-          continue;
-        }
         if (aux) {
           // residual chunk (same swizzled layout as the output), read then overwritten in place
 #pragma unroll
@@ -524,7 +505,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         __syncwarp();
         if (lane == 0) {
           // out-of-range rows / columns of the box are clipped by the TMA unit
-          if (pr.reduce_add) {
+          if (P.scatter_n > 0) {
+            // whole 32-row chunks beyond M (the second CTA of a pair on a short last tile) have no
+            // owner: skip them (M is a multiple of 32 in scatter mode)
+            if (out_row0 < pr.M) {
+              const int owner = out_row0 / P.scatter_rows;
+              tma_reduce_add_2d(&P.scatter[owner], slot_ptr(b, 0), pr.scatter_col0 + col,
+                                out_row0 - owner * P.scatter_rows);
+            }
+          } else if (pr.reduce_add) {
             tma_reduce_add_2d(&pr.tma_c, slot_ptr(b, 0), col, out_row0);
           } else {
             tma_store_2d(&pr.tma_c, slot_ptr(b, 0), col, out_row0);
@@ -533,8 +522,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
       }
     }
-    if (lane == 0) bulk_wait<0>();
-    if (P.scatter_n > 0) __threadfence_system();  // this lane's peer reduce-adds are visible system-wide
+    if (lane == 0) {
+      bulk_wait<0>();
+      if (P.scatter_n > 0) __threadfence_system();  // the peer reduce-adds are complete and visible
+    }
   }
 
   // pair: neither CTA may leave (or free TMEM) while the leader can still touch the peer
@@ -750,7 +741,7 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
     d.k_blocks = (q.K + kBK - 1) / kBK;
     d.splits = q.splits;
     d.kb_per_split = (d.k_blocks + q.splits - 1) / q.splits;
-    d.out_fp32 = q.c_fp32;
+    d.out_fp32 = sc != nullptr ? 1 : q.c_fp32;  // scatter: fp32 chunks reduce-added into the owners
     d.reduce_add = q.reduce_add;
     d.alpha = q.alpha == 0.0f ? 1.0f : q.alpha;
     d.tile_start = tiles;
@@ -761,10 +752,9 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
   if (sc != nullptr) {
     P.scatter_n = sc->n_owners;
     P.scatter_rows = sc->rows_per_owner;
-    P.scatter_ld = sc->ld;
     for (int j = 0; j < sc->n_owners; ++j) {
-      if (reinterpret_cast<uintptr_t>(sc->owners[j]) & 15) return BTP_ERR_ALIGNMENT;
-      P.scatter[j] = static_cast<float*>(sc->owners[j]);
+      const int rc = make_tmap(&P.scatter[j], sc->owners[j], sc->width, sc->rows_per_owner, sc->ld, 32, 32, true);
+      if (rc) return rc;
     }
   }
   int grid_units = tiles < units ? tiles : units;

@@ -55,16 +55,20 @@ class VirtualPeers:
 class PeerComm:
     """One rank's view of the symmetric heap: named buffers, peer pointer arrays, flags."""
 
-    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None, scatter: bool = True):
+    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None, scatter: bool = False):
         if not 1 <= tp <= 8:
             raise ValueError(f"peer boundaries support 1 <= tp <= 8, got {tp}")
         self.tp, self.rank = tp, rank
         self.dev = torch.device(device)
         self.provider = provider
         self.group = group
-        # scatter=True: the producing GEMM reduce-adds its output straight into the owning ranks'
-        # buffers (btp_gemm_scatter, tile by tile) and the boundary kernel only reads its own rows;
-        # scatter=False: the GEMM stores locally and the boundary kernel pulls every rank's partial
+        # scatter=False (default): the GEMM stores locally and the boundary kernel pulls every rank's
+        # bf16 partial (incoming link direction) while pushing a / dP (outgoing) — both NVLink
+        # directions busy at once. scatter=True: the producing GEMM reduce-adds its output into the
+        # owning ranks' fp32 buffers tile by tile (btp_gemm_scatter: GEMM + reduce-scatter in one
+        # kernel, the transfer overlapped with the MMA) — but fp32 (sm_100a has no bf16 tensor
+        # reduce) doubles the reduce-scatter bytes and both halves then use the outgoing direction,
+        # so it only wins when the GEMM is long against the transfer (see DESIGN.md §5).
         self.scatter = scatter
         self.heap = None
         self._hptrs: dict[str, list[int]] = {}

@@ -38,6 +38,15 @@ elif name == "down_gu":       # gate|up down + sigma at TP=1: [16384 x 1024], K 
     n, w = rnd(T, d), rnd(2 * r, d)
     P, A = torch.empty(T, 2 * r, device=dev, dtype=bf), torch.empty(T, 2 * r, device=dev, dtype=bf)
     run = lambda: K.gemm(K.Gemm(n, w, P, sigma=(A, r // 2)))  # noqa: E731
+elif name in ("down7b_plain", "down7b_scatter"):  # 7B TP=8 q|k|v down GEMM [16384 x 3072], K=512
+    n7, w7 = rnd(T, 512), rnd(3072, 512)
+    if name == "down7b_plain":
+        P7 = torch.empty(T, 3072, device=dev, dtype=bf)
+        run = lambda: K.gemm(K.Gemm(n7, w7, P7))  # noqa: E731
+    else:  # reduce-added into 8 owners' fp32 [2048 x 3072] buffers (virtual peers: same GPU)
+        owners = [torch.zeros(T // 8, 3072, device=dev, dtype=f32) for _ in range(8)]
+        run = lambda: K.gemm_scatter(K.Gemm(n7, w7, None), owners=[o.data_ptr() for o in owners],  # noqa: E731
+                                     rows_per_owner=T // 8, width=3072, ld=3072, col0=[0])
 elif name == "rmsnorm":
     x, g = rnd(T, d), rnd(d, dtype=f32)
     n, ss, rl = torch.empty_like(x), torch.empty(T, device=dev, dtype=f32), torch.empty(T, device=dev, dtype=f32)

@@ -142,3 +142,25 @@ def test_sigma_epilogue_rejects_bad_shapes():
         K.gemm(K.Gemm(X, B, Z, sigma=(A, 64)), bn=256)  # a 256-wide tile would straddle two projections
     with pytest.raises(Exception):
         K.gemm(K.Gemm(X, B.t().contiguous(), Z, b_mn=True, sigma=(A, 64)))  # B must be K-major
+
+
+@pytest.mark.parametrize("M,N,Kd,nprob,b_mn,tp", [(128, 64, 128, 3, True, 2), (256, 192, 256, 1, False, 2),
+                                                 (512, 64, 512, 2, True, 4), (2048, 512, 256, 1, False, 8),
+                                                 (16384, 3072, 512, 1, False, 8)])
+def test_gemm_scatter_reduce_into_owners(M, N, Kd, nprob, b_mn, tp):
+    """btp_gemm_scatter: each problem's rows are reduce-added (fp32) into the owning rank's buffer
+    at its column offset; two launches accumulate (the owners' buffers start at zero)."""
+    torch.manual_seed(M + N)
+    A = [_mk(M, Kd) for _ in range(nprob)]
+    B = [_mk(Kd, N) if b_mn else _mk(N, Kd) for _ in range(nprob)]
+    W = nprob * N
+    owners = [torch.zeros(M // tp, W, device="cuda") for _ in range(tp)]
+    probs = [K.Gemm(A[i], B[i], None, b_mn=b_mn) for i in range(nprob)]
+    for _ in range(2):
+        K.gemm_scatter(*probs, owners=[o.data_ptr() for o in owners], rows_per_owner=M // tp, width=W, ld=W,
+                       col0=[i * N for i in range(nprob)])
+    torch.cuda.synchronize()
+    full = torch.cat(owners, 0)
+    for i in range(nprob):
+        ref = A[i].float() @ (B[i].float() if b_mn else B[i].float().t())
+        assert rel(full[:, i * N:(i + 1) * N] / 2, ref) < TOL
