@@ -334,99 +334,7 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const T* __restrict__ g
 }
 
 // ----------------------------------------------------------------------------- K3 backward
-// Block of 256 threads: tpr threads per row (8 columns each, looping over column groups),
-// 256/tpr rows in flight. dgamma partial per block, combined across row slots in smem.
-constexpr int kNormBwdMaxGroups = 4;  // width <= 256 * 8 * 4 = 8192
-template <typename T>
-__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const T* __restrict__ dh, long long lddh,
-                                                          const T* __restrict__ x, long long ldx,
-                                                          const float* __restrict__ gamma,
-                                                          const float* __restrict__ dss, const T* __restrict__ dres,
-                                                          long long ldr, T* __restrict__ dx, long long lddx,
-                                                          float* __restrict__ dgamma_partial, int rows, int width,
-                                                          int tpr, int rows_per_block) {
-  extern __shared__ float red[];  // [256/tpr][width] when rows in flight > 1
-  const int nch = width >> 3;
-  const int slot = threadIdx.x / tpr;
-  const int cg = threadIdx.x - slot * tpr;
-  const int slots = blockDim.x / tpr;
-  const int r0 = blockIdx.x * rows_per_block;
-  const int r1 = min(rows, r0 + rows_per_block);
-  float acc[kNormBwdMaxGroups][8];
-#pragma unroll
-  for (int q = 0; q < kNormBwdMaxGroups; ++q)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[q][j] = 0.f;
-  // two rows per iteration (row, row + slots): both rows' loads are in flight together
-  for (int row = r0 + slot; row < r1; row += 2 * slots) {
-    const int rowb = row + slots;
-    const bool hasb = rowb < r1;
-    const float two_dss = 2.0f * dss[row];
-    const float two_dssb = hasb ? 2.0f * dss[rowb] : 0.f;
-#pragma unroll
-    for (int q = 0; q < kNormBwdMaxGroups; ++q) {
-      const int c = cg + q * tpr;
-      if (c < nch) {
-        float fh[8], fx[8], fr[8], g[8], hb[8], xb[8], rb[8];
-        load8(dh + (long long)row * lddh + c * 8, fh);
-        load8(x + (long long)row * ldx + c * 8, fx);
-        if (hasb) {
-          load8(dh + (long long)rowb * lddh + c * 8, hb);
-          load8(x + (long long)rowb * ldx + c * 8, xb);
-        }
-        if (dres != nullptr) {
-          load8(dres + (long long)row * ldr + c * 8, fr);
-          if (hasb) load8(dres + (long long)rowb * ldr + c * 8, rb);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) fr[j] = rb[j] = 0.f;
-        }
-        load_gamma8(gamma + c * 8, g);
-        float o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          o[j] = fr[j] + fh[j] * g[j] + two_dss * fx[j];
-          acc[q][j] = fmaf(fh[j], fx[j], acc[q][j]);
-        }
-        store8(dx + (long long)row * lddx + c * 8, o);
-        if (hasb) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            o[j] = rb[j] + hb[j] * g[j] + two_dssb * xb[j];
-            acc[q][j] = fmaf(hb[j], xb[j], acc[q][j]);
-          }
-          store8(dx + (long long)rowb * lddx + c * 8, o);
-        }
-      }
-    }
-  }
-  // combine the row slots, ascending slot order
-  if (slots == 1) {
-#pragma unroll
-    for (int q = 0; q < kNormBwdMaxGroups; ++q) {
-      const int c = cg + q * tpr;
-      if (c < nch) {
-        float* out = dgamma_partial + (long long)blockIdx.x * width + c * 8;
-        reinterpret_cast<float4*>(out)[0] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-        reinterpret_cast<float4*>(out)[1] = make_float4(acc[q][4], acc[q][5], acc[q][6], acc[q][7]);
-      }
-    }
-    return;
-  }
-#pragma unroll
-  for (int q = 0; q < kNormBwdMaxGroups; ++q) {
-    const int c = cg + q * tpr;
-    if (c < nch)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) red[slot * width + c * 8 + j] = acc[q][j];
-  }
-  __syncthreads();
-  for (int col = threadIdx.x; col < width; col += blockDim.x) {
-    float s = 0.f;
-    for (int sl = 0; sl < slots; ++sl) s += red[sl * width + col];
-    dgamma_partial[(long long)blockIdx.x * width + col] = s;
-  }
-}
+// (rmsnorm_bwd_pipe_kernel below: the TMA row-pipeline form)
 
 // Full-width RMSNorm n = x*gamma/s (baselines): dn -> dh = dn / s (in place allowed) and
 // dss = -<dn, gamma*x> / (2 s^3 d), so rmsnorm_bwd finishes dx and dgamma.
