@@ -42,3 +42,20 @@ def test_sass_has_tcgen05_and_tma():
     if not sass:
         pytest.skip("cuobjdump unavailable")
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_gemm_problem_layout_matches_header_and_docs():
+    """The ctypes GemmProblem, the btp_gemm_problem struct of include/btp.h and the binding example
+    in INTEGRATION.md list the same fields in the same order (a mismatch silently corrupts calls)."""
+    hdr = (ROOT / "include" / "btp.h").read_text()
+    body = hdr[hdr.index("typedef struct btp_gemm_problem {"):hdr.index("} btp_gemm_problem;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    hdr_fields = []
+    for decl in re.findall(r"^\s*([^;{}]+);", body.split("{", 1)[1], flags=re.M):
+        first, *rest = [t.strip() for t in decl.split(",")]
+        hdr_fields += [first.split()[-1].lstrip("*")] + [r.lstrip("*") for r in rest]
+    ctypes_fields = [f[0] for f in _native.GemmProblem._fields_]
+    doc = (ROOT / "INTEGRATION.md").read_text()
+    doc = doc[doc.index("class btp_gemm_problem"):doc.index("lib.btp_gemm.argtypes")]
+    doc_fields = re.findall(r'\("(\w+)", ctypes\.c_\w+\)', doc)
+    assert hdr_fields == ctypes_fields == doc_fields
