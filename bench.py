@@ -70,27 +70,38 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         self.source = "nvidia-smi"
-
-    def _run_nvml(self) -> bool:
+        # NVML is initialised here, before the timed region: nvmlInit can take longer than a whole
+        # ten-step region, which then went unsampled
+        self._nvml = None
         try:
             import pynvml
 
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self._nvml = (pynvml, h, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), get_reasons)
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self) -> bool:
+        pynvml, h, mx, get_reasons = self._nvml
+        try:
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = get_reasons(h)
         except Exception:
             return False
-        self.source = "nvml"
+        flags = ["Active" if bits & b else "Not Active" for _, b in self._BITS]
+        self.rows.append([str(self.index), str(sm), str(mx), "", hex(bits)] + flags)
+        return True
+
+    def _run_nvml(self) -> bool:
+        if self._nvml is None:
+            return False
         while not self._stop.is_set():
-            try:
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                bits = get_reasons(h)
-            except Exception:
+            if not self._sample_nvml():
                 break
-            flags = ["Active" if bits & b else "Not Active" for _, b in self._BITS]
-            self.rows.append([str(self.index), str(sm), str(mx), "", hex(bits)] + flags)
             self._stop.wait(0.01)
         return True
 
