@@ -27,7 +27,9 @@ it MN-major); up weights [d_out/tp, r]; all weight grads fp32.
 from __future__ import annotations
 
 import dataclasses
+import functools
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -53,6 +55,27 @@ FUSE_SIGMA = True
 # all-reduce of slice c+1) — the north_star's "overlapped with the adjacent GEMM tiles"
 FWD_AR_SLICES = 4
 FWD_SLICE_MIN_ROWS = 1024  # below this the launch count outweighs the overlap
+
+
+_NVTX = os.environ.get("BTP_NVTX", "0") == "1"
+
+
+def _nvtx(fn):
+    """NVTX range around an executor stage (BTP_NVTX=1; e.g. for Nsight Systems timelines): the
+    range is named after the stage and the chunk it works on (`names` argument)."""
+    if not _NVTX:
+        return fn
+
+    @functools.wraps(fn)
+    def wrapped(self, *args, **kwargs):
+        names = args[0] if args and isinstance(args[0], tuple) else ()
+        torch.cuda.nvtx.range_push(f"{fn.__name__.strip('_')}:{'|'.join(names)}:{self.comm.pass_tag}")
+        try:
+            return fn(self, *args, **kwargs)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    return wrapped
 
 
 def _pick_splits(tiles: int, k_blocks: int, units: int) -> int:
@@ -426,6 +449,7 @@ class BTPBlockExecutor(ExecutorBase):
         return out
 
     # ------------------------------------------------------------------ forward pieces
+    @_nvtx
     def _norm(self, x, gamma, tag):
         """Online: n = x*gamma/rms_loc, ss -> rider. Sync: stat AR then global normalisation."""
         T, dl = self.T, self.dl
@@ -443,6 +467,7 @@ class BTPBlockExecutor(ExecutorBase):
         self.stats.kernel_launches += 2
         return n, ss, None, s
 
+    @_nvtx
     def _down_boundary(self, names, n_in, W, ss, rl, s_tag, norm_chunk: bool):
         """Row-parallel down GEMM(s) -> all-reduce(s) -> fix-up + sigma.
         Returns (z views, a views, P storage); z aliases the all-reduce buffer."""
@@ -601,6 +626,7 @@ class BTPBlockExecutor(ExecutorBase):
             self.stats.kernel_launches += 1
         return [a_store[:, i * r:(i + 1) * r] for i in range(k)]
 
+    @_nvtx
     def _up(self, a_list, W_list, outs, resid=None):
         probs = [K.Gemm(a, w, o, resid=resid) for a, w, o in zip(a_list, W_list, outs)]
         if self.grouping:
@@ -712,6 +738,7 @@ class BTPBlockExecutor(ExecutorBase):
         S.update(a_qkv=a_qkv, qkv=qkv, attn=attn, actx=actx)
 
     # ------------------------------------------------------------------ backward pieces
+    @_nvtx
     def _up_bwd(self, names, dgrad_probs, wgrad_pairs, da_P, zP, s, dss_name):
         """Backward of one chunk boundary: dgrad of the up-projection(s) into da_P, then the rank-r
         all-reduce of da_P started asynchronously (NCCL's stream) while the independent weight
@@ -795,6 +822,7 @@ class BTPBlockExecutor(ExecutorBase):
             return [da[:, i * r:(i + 1) * r] for i in range(len(names))]
         return [da[i] for i in range(len(names))]
 
+    @_nvtx
     def _down_bwd(self, names, dP, W, x_res, gamma, dres, dx_out, dss, grad_key, gamma_key):
         """dh = dP @ W (dgrad) ; dW = (dP^T x) * gamma (wgrad) ; dx = dres + dh*gamma + 2 x dss."""
         T, dl, r, k = self.T, self.dl, self.r, len(names)
