@@ -390,7 +390,7 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
-    ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer"],
+    ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
                     help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
     ap.add_argument("--model", action="store_true", help="multi-layer model step (embedding + blocks + LM head)")
     ap.add_argument("--layers", type=int, default=0, help="--model: number of blocks (default: the preset's)")

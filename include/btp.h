@@ -292,6 +292,16 @@ int btp_peer_boundary_bwd_local(void* R_own, int tp, int rank, int T, int W, int
                                 const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
                                 void* stream);
 
+/* NVLS (NVLink SHARP) boundaries: *_mc are NVSwitch MULTICAST addresses of the symmetric buffers
+ * (every rank's copy bound to one multicast object). Owned rows are read with multimem.ld_reduce
+ * (the switch sums the tp partials, fp32 accumulation) and a / dP (and dss) are written once with
+ * multimem.st (the switch replicates them to every rank): 2/tp of T·W·2 B per rank over NVLink
+ * instead of 2(tp-1)/tp. Same math, flags and ordering as btp_peer_boundary_fwd / _bwd. */
+int btp_peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int rank, int T, int W, int r,
+                               int variant, int d, float eps, void* z_own, float* s_own, void* a_mc, void* stream);
+int btp_peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
+                               const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, void* stream);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

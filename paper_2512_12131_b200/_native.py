@@ -74,6 +74,8 @@ EXPORTED_SYMBOLS = (
     "btp_peer_boundary_bwd",
     "btp_peer_boundary_fwd_local",
     "btp_peer_boundary_bwd_local",
+    "btp_peer_boundary_fwd_nvls",
+    "btp_peer_boundary_bwd_nvls",
 )
 
 
@@ -155,6 +157,8 @@ _SIGNATURES = {
     "btp_peer_boundary_bwd": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "btp_peer_boundary_fwd_local": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
     "btp_peer_boundary_bwd_local": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "btp_peer_boundary_fwd_nvls": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
+    "btp_peer_boundary_bwd_nvls": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",

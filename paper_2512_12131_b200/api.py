@@ -71,17 +71,20 @@ def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS
 
     boundary="peer" (BTP, tp > 1): the chunk boundaries run as fused reduce-scatter -> fix-up/sigma
     -> all-gather kernels over NVLink peer memory (torch symmetric-memory heap, csrc/peer.cu)
-    instead of NCCL all-reduces + a fix-up launch."""
+    instead of NCCL all-reduces + a fix-up launch. boundary="nvls": the same kernels' NVLink-SHARP
+    form — the switch reduces the partials (multimem.ld_reduce) and replicates the results
+    (multimem.st) through the heap's multicast mapping."""
+    if boundary not in ("nccl", "peer", "nvls"):
+        raise ValueError(f"boundary must be 'nccl', 'peer' or 'nvls', got {boundary!r}")
     if comm is None:
         comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
-        if boundary == "peer" and pl.strategy is Strategy.BOTTLENECK:
+        if boundary in ("peer", "nvls") and pl.strategy is Strategy.BOTTLENECK:
             from .peer import PeerComm
 
             dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
             comm = TPComm(comm.tp, comm.rank, comm.group, comm.trace,
-                          peer=PeerComm(comm.tp, comm.rank, dev, provider="symmetric_memory"))
-    elif boundary not in ("nccl", "peer"):
-        raise ValueError(f"boundary must be 'nccl' or 'peer', got {boundary!r}")
+                          peer=PeerComm(comm.tp, comm.rank, dev, provider="symmetric_memory",
+                                        nvls=boundary == "nvls"))
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:
         return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)

@@ -61,8 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
-    subprocess.run([nvcc, "-shared", "-o", str(tmp)] + objs + ARCH + ["-lcuda"] if False else
-                   [nvcc, "-shared", "-o", str(tmp)] + objs + ARCH, check=True)
+    subprocess.run([nvcc, "-shared", "-o", str(tmp)] + objs + ARCH, check=True)
     os.replace(tmp, LIB)
     for o in objs:
         try:

@@ -66,4 +66,8 @@ int peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, 
 int peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int W, int r, int variant, int d,
                       const void* z_own, const float* s_own, void* const* dP_peers, float* const* dss_peers,
                       cudaStream_t st, void* R_own = nullptr);
+int peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int rank, int T, int W, int r, int variant,
+                           int d, float eps, void* z_own, float* s_own, void* a_mc, cudaStream_t st);
+int peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
+                           const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, cudaStream_t st);
 }  // namespace btp

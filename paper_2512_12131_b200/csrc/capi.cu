@@ -167,6 +167,16 @@ int btp_peer_boundary_bwd_local(void* R_own, int tp, int rank, int T, int W, int
                                 ST(stream), R_own);
 }
 
+int btp_peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int rank, int T, int W, int r,
+                               int variant, int d, float eps, void* z_own, float* s_own, void* a_mc, void* stream) {
+  return btp::peer_boundary_fwd_nvls(P_mc, ss_mc, tp, rank, T, W, r, variant, d, eps, z_own, s_own, a_mc, ST(stream));
+}
+
+int btp_peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
+                               const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, void* stream) {
+  return btp::peer_boundary_bwd_nvls(dA_mc, tp, rank, T, W, r, variant, d, z_own, s_own, dP_mc, dss_mc, ST(stream));
+}
+
 int btp_counter_add(int* ctr, int delta, void* stream) { return btp::counter_add(ctr, delta, ST(stream)); }
 
 int btp_reduce_rows(const float* in, int splits, long long split_stride, long long ldi, int rows, int cols,

@@ -27,6 +27,7 @@
 // The peer pointer arrays are device arrays of tp pointers (rank order) into each rank's symmetric
 // buffer: torch symmetric-memory (cuMem IPC over NVLink) across processes on the box, or tp
 // buffers of one device in the single-GPU multi-rank test.
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -127,33 +128,116 @@ __global__ void peer_wait_kernel(const uint32_t* __restrict__ flags, const uint3
   __threadfence_system();
 }
 
-// Forward boundary: one warp per owned row; lane work units = 8 "u" + 8 "v" columns (cola) or 8
-// columns (svd) of one projection.
-// kLocal: the partials were already reduce-added into this rank's owned rows R_own [rows_own, W]
-// by the other ranks' scatter GEMMs (btp_gemm_scatter): read them locally (and re-zero them for the
-// next use) instead of pulling every rank's P.
-__device__ __forceinline__ void own_sum8(float* R_own, long long off, float (&acc)[8]) {
-  float4* p = reinterpret_cast<float4*>(R_own + off);
-  const float4 a = __ldcv(p), b = __ldcv(p + 1);
-  acc[0] = a.x; acc[1] = a.y; acc[2] = a.z; acc[3] = a.w; acc[4] = b.x; acc[5] = b.y; acc[6] = b.z; acc[7] = b.w;
-  p[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-  p[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+// The boundary kernels are written once over "where the partials come from" and "where the
+// results go" (the policies below); one warp per owned row, lane work units = 8 "u" + 8 "v"
+// columns (cola) or 8 columns (svd) of one projection. Sources of the reduced row:
+//   PullRows   — sum every rank's bf16 partial over NVLink (fp32 accumulation)
+//   LocalRows  — the partials were already reduce-added into this rank's owned rows R_own
+//                [rows_own, W] by the other ranks' scatter GEMMs (btp_gemm_scatter): read them
+//                locally and re-zero them for the next use
+//   McRows     — NVLS: multimem.ld_reduce on the multicast address, the switch sums (acc::f32)
+// Destinations of a / dP / dss: PushRows (a store into every rank's copy) or McRows (one
+// multimem.st, replicated by the switch). Only these primitives differ between the forms, so the
+// NVLS kernels share every line of fix-up / sigma math with the pull kernels the tests pin.
+namespace {
+
+struct PullRows {
+  const bf16* const* src;
+  int tp;
+  __device__ __forceinline__ void sum8(long long g, long long, float (&f)[8]) const { pull_sum8(src, tp, g, f); }
+};
+
+struct LocalRows {
+  float* R_own;
+  __device__ __forceinline__ void sum8(long long, long long l, float (&f)[8]) const {
+    float4* q = reinterpret_cast<float4*>(R_own + l);
+    const float4 a = __ldcv(q), b = __ldcv(q + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+    q[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    q[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+};
+
+struct PushRows {
+  bf16* const* dst;
+  int tp;
+  __device__ __forceinline__ void store8(long long g, const uint4& w) const {
+    for (int j = 0; j < tp; ++j) *reinterpret_cast<uint4*>(dst[j] + g) = w;
+  }
+};
+
+struct McRows {  // NVLS multicast address of a bf16 [T, W] buffer
+  bf16* mc;
+  __device__ __forceinline__ void sum8(long long g, long long, float (&f)[8]) const {
+    uint32_t a, b, c, d;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "l"(mc + g)
+                 : "memory");
+    unpack8(make_uint4(a, b, c, d), f);
+  }
+  __device__ __forceinline__ void store8(long long g, const uint4& w) const {
+    asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc + g), "r"(w.x), "r"(w.y),
+                 "r"(w.z), "r"(w.w)
+                 : "memory");
+  }
+};
+
+struct PullStat {  // per-row fp32 statistic, one copy per rank
+  const float* const* src;
+  int tp;
+  __device__ __forceinline__ bool on() const { return src != nullptr; }
+  __device__ __forceinline__ float sum(long long row) const {
+    float v = 0.f;
+    for (int j = 0; j < tp; ++j) v += __ldcv(src[j] + row);
+    return v;
+  }
+};
+
+struct PushStat {
+  float* const* dst;
+  int tp;
+  __device__ __forceinline__ bool on() const { return dst != nullptr; }
+  __device__ __forceinline__ void store(long long row, float v) const {
+    for (int j = 0; j < tp; ++j) dst[j][row] = v;
+  }
+};
+
+struct McStat {
+  float* mc;
+  __device__ __forceinline__ bool on() const { return mc != nullptr; }
+  __device__ __forceinline__ float sum(long long row) const {
+    float v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(mc + row) : "memory");
+    return v;
+  }
+  __device__ __forceinline__ void store(long long row, float v) const {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc + row), "f"(v) : "memory");
+  }
+};
+
+// every store of this kernel (peer-mapped or multicast) visible system-wide before the "done" signal
+template <class Dst>
+__device__ __forceinline__ void release_pushes() {
+  __threadfence_system();
+  if constexpr (std::is_same_v<Dst, McRows>)
+    asm volatile("fence.proxy.alias;" ::: "memory");  // multicast vs unicast aliases of the same pages
 }
 
-template <bool kLocal>
-__global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
-    const bf16* const* __restrict__ P_peers, float* __restrict__ R_own, const float* const* __restrict__ ss_peers,
-    int tp, int row0, int rows_own, int W, int r, int variant, float inv_d, float eps, bf16* __restrict__ z_own,
-    float* __restrict__ s_own, bf16* const* __restrict__ a_peers) {
+}  // namespace
+
+template <class Src, class Stat, class Dst>
+__global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(Src P, Stat ss, int row0, int rows_own, int W, int r,
+                                                                int variant, float inv_d, float eps,
+                                                                bf16* __restrict__ z_own, float* __restrict__ s_own,
+                                                                Dst A) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < rows_own; i += gridDim.x * warps) {
     const long long row = row0 + i;
     float s = 1.0f;
-    if (ss_peers != nullptr) {
-      float ss = 0.f;
-      for (int j = 0; j < tp; ++j) ss += __ldcv(ss_peers[j] + row);
-      s = sqrtf(ss * inv_d + eps);
+    if (ss.on()) {
+      s = sqrtf(ss.sum(row) * inv_d + eps);
       if (lane == 0 && s_own != nullptr) s_own[i] = s;
     }
     const float inv = 1.0f / s;
@@ -164,13 +248,8 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
       if (variant == 1) {
         const int cu = p * r + g * 8, cv = cu + (r >> 1);
         float zu[8], zv[8];
-        if constexpr (kLocal) {
-          own_sum8(R_own, (long long)i * W + cu, zu);
-          own_sum8(R_own, (long long)i * W + cv, zv);
-        } else {
-          pull_sum8(P_peers, tp, row * W + cu, zu);
-          pull_sum8(P_peers, tp, row * W + cv, zv);
-        }
+        P.sum8(row * W + cu, (long long)i * W + cu, zu);
+        P.sum8(row * W + cv, (long long)i * W + cv, zv);
 #pragma unroll
         for (int e = 0; e < 8; ++e) { zu[e] *= inv; zv[e] *= inv; }
         const uint4 wu = pack8(zu), wv = pack8(zv);
@@ -184,33 +263,28 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(
           au[e] = silu_acc(zu[e]) * zv[e];
           av[e] = silu_acc(zv[e]) * zu[e];
         }
-        const uint4 pu = pack8(au), pv = pack8(av);
-        for (int j = 0; j < tp; ++j) {
-          *reinterpret_cast<uint4*>(a_peers[j] + row * W + cu) = pu;
-          *reinterpret_cast<uint4*>(a_peers[j] + row * W + cv) = pv;
-        }
+        A.store8(row * W + cu, pack8(au));
+        A.store8(row * W + cv, pack8(av));
       } else {
         const int c = p * r + g * 8;
         float z[8];
-        if constexpr (kLocal) own_sum8(R_own, (long long)i * W + c, z);
-        else pull_sum8(P_peers, tp, row * W + c, z);
+        P.sum8(row * W + c, (long long)i * W + c, z);
 #pragma unroll
         for (int e = 0; e < 8; ++e) z[e] *= inv;
         const uint4 wz = pack8(z);
         *reinterpret_cast<uint4*>(z_own + (long long)i * W + c) = wz;
-        for (int j = 0; j < tp; ++j) *reinterpret_cast<uint4*>(a_peers[j] + row * W + c) = wz;
+        A.store8(row * W + c, wz);
       }
     }
   }
-  __threadfence_system();  // pushes visible system-wide before the "done" signal
+  release_pushes<Dst>();
 }
 
-template <bool kLocal>
-__global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
-    const bf16* const* __restrict__ da_peers, float* __restrict__ R_own, int tp, int row0, int rows_own, int W, int r,
-    int variant, float inv_d,
-    const bf16* __restrict__ z_own, const float* __restrict__ s_own, bf16* const* __restrict__ dP_peers,
-    float* const* __restrict__ dss_peers) {
+template <class Src, class Dst, class DssDst>
+__global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(Src dA, int row0, int rows_own, int W, int r,
+                                                                int variant, float inv_d,
+                                                                const bf16* __restrict__ z_own,
+                                                                const float* __restrict__ s_own, Dst dP, DssDst dss) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < rows_own; i += gridDim.x * warps) {
@@ -225,13 +299,8 @@ __global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
       if (variant == 1) {
         const int cu = p * r + g * 8, cv = cu + (r >> 1);
         float du_[8], dv_[8], zu[8], zv[8];
-        if constexpr (kLocal) {
-          own_sum8(R_own, (long long)i * W + cu, du_);
-          own_sum8(R_own, (long long)i * W + cv, dv_);
-        } else {
-          pull_sum8(da_peers, tp, row * W + cu, du_);
-          pull_sum8(da_peers, tp, row * W + cv, dv_);
-        }
+        dA.sum8(row * W + cu, (long long)i * W + cu, du_);
+        dA.sum8(row * W + cv, (long long)i * W + cv, dv_);
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + cu), zu);
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + cv), zv);
         float gu[8], gv[8];
@@ -246,33 +315,25 @@ __global__ void __launch_bounds__(256) peer_boundary_bwd_kernel(
           gu[e] *= inv;
           gv[e] *= inv;
         }
-        const uint4 pu = pack8(gu), pv = pack8(gv);
-        for (int j = 0; j < tp; ++j) {
-          *reinterpret_cast<uint4*>(dP_peers[j] + row * W + cu) = pu;
-          *reinterpret_cast<uint4*>(dP_peers[j] + row * W + cv) = pv;
-        }
+        dP.store8(row * W + cu, pack8(gu));
+        dP.store8(row * W + cv, pack8(gv));
       } else {
         const int c = p * r + g * 8;
         float dd[8], zz[8];
-        if constexpr (kLocal) own_sum8(R_own, (long long)i * W + c, dd);
-        else pull_sum8(da_peers, tp, row * W + c, dd);
+        dA.sum8(row * W + c, (long long)i * W + c, dd);
         unpack8(*reinterpret_cast<const uint4*>(z_own + (long long)i * W + c), zz);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           dot = fmaf(dd[e], zz[e], dot);
           dd[e] *= inv;
         }
-        const uint4 pd = pack8(dd);
-        for (int j = 0; j < tp; ++j) *reinterpret_cast<uint4*>(dP_peers[j] + row * W + c) = pd;
+        dP.store8(row * W + c, pack8(dd));
       }
     }
     dot = warp_sum32(dot);
-    if (lane == 0 && dss_peers != nullptr && s_own != nullptr) {
-      const float v = -dot * inv * inv * 0.5f * inv_d;
-      for (int j = 0; j < tp; ++j) dss_peers[j][row] = v;
-    }
+    if (lane == 0 && dss.on() && s_own != nullptr) dss.store(row, -dot * inv * inv * 0.5f * inv_d);
   }
-  __threadfence_system();
+  release_pushes<Dst>();
 }
 
 static inline bool a16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -309,14 +370,16 @@ int peer_boundary_fwd(const void* const* P_peers, const float* const* ss_peers, 
   if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
   if (d <= 0 || !z_own || !a_peers || (!P_peers && !R_own) || !a16p(z_own)) return BTP_ERR_DIM;
   const int rows_own = T / tp;
+  const PullStat ss{ss_peers, tp};
+  const PushRows A{reinterpret_cast<bf16* const*>(a_peers), tp};
   if (R_own != nullptr)
-    peer_boundary_fwd_kernel<true><<<rows_grid(rows_own), 256, 0, st>>>(
-        nullptr, static_cast<float*>(R_own), ss_peers, tp, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
-        eps, static_cast<bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(a_peers));
+    peer_boundary_fwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+        LocalRows{static_cast<float*>(R_own)}, ss, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d, eps,
+        static_cast<bf16*>(z_own), s_own, A);
   else
-    peer_boundary_fwd_kernel<false><<<rows_grid(rows_own), 256, 0, st>>>(
-        reinterpret_cast<const bf16* const*>(P_peers), nullptr, ss_peers, tp, rank * rows_own, rows_own, W, r, variant,
-        1.0f / (float)d, eps, static_cast<bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(a_peers));
+    peer_boundary_fwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+        PullRows{reinterpret_cast<const bf16* const*>(P_peers), tp}, ss, rank * rows_own, rows_own, W, r, variant,
+        1.0f / (float)d, eps, static_cast<bf16*>(z_own), s_own, A);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
@@ -326,14 +389,48 @@ int peer_boundary_bwd(const void* const* da_peers, int tp, int rank, int T, int 
   if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
   if (d <= 0 || !z_own || !dP_peers || (!da_peers && !R_own) || !a16p(z_own)) return BTP_ERR_DIM;
   const int rows_own = T / tp;
+  const PushRows dP{reinterpret_cast<bf16* const*>(dP_peers), tp};
+  const PushStat dss{dss_peers, tp};
   if (R_own != nullptr)
-    peer_boundary_bwd_kernel<true><<<rows_grid(rows_own), 256, 0, st>>>(
-        nullptr, static_cast<float*>(R_own), tp, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
-        static_cast<const bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(dP_peers), dss_peers);
+    peer_boundary_bwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+        LocalRows{static_cast<float*>(R_own)}, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
+        static_cast<const bf16*>(z_own), s_own, dP, dss);
   else
-    peer_boundary_bwd_kernel<false><<<rows_grid(rows_own), 256, 0, st>>>(
-        reinterpret_cast<const bf16* const*>(da_peers), nullptr, tp, rank * rows_own, rows_own, W, r, variant,
-        1.0f / (float)d, static_cast<const bf16*>(z_own), s_own, reinterpret_cast<bf16* const*>(dP_peers), dss_peers);
+    peer_boundary_bwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+        PullRows{reinterpret_cast<const bf16* const*>(da_peers), tp}, rank * rows_own, rows_own, W, r, variant,
+        1.0f / (float)d, static_cast<const bf16*>(z_own), s_own, dP, dss);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// NVLS (NVLink SHARP) form of the boundaries: every rank's symmetric buffers are also bound to one
+// NVSwitch multicast object, and the kernels use its multicast address *_mc:
+//   multimem.ld_reduce ... add.acc::f32  — the switch sums the tp ranks' partials (fp32 accumulate)
+//                                           and returns the owned row once: (T/tp)·W·2 B in per rank
+//   multimem.st                          — one store of a / dP is replicated to every rank by the
+//                                           switch: (T/tp)·W·2 B out per rank
+// i.e. 2/tp of T·W·2 B per rank over NVLink instead of a ring's 2(tp-1)/tp. Same contract, flags
+// and fix-up math as btp_peer_boundary_fwd / _bwd.
+int peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int rank, int T, int W, int r, int variant,
+                           int d, float eps, void* z_own, float* s_own, void* a_mc, cudaStream_t st) {
+  if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
+  if (d <= 0 || !z_own || !P_mc || !a_mc || !a16p(z_own) || !a16p(P_mc) || !a16p(a_mc)) return BTP_ERR_DIM;
+  const int rows_own = T / tp;
+  peer_boundary_fwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+      McRows{static_cast<bf16*>(const_cast<void*>(P_mc))}, McStat{const_cast<float*>(ss_mc)}, rank * rows_own,
+      rows_own, W, r, variant, 1.0f / (float)d, eps, static_cast<bf16*>(z_own), s_own, McRows{static_cast<bf16*>(a_mc)});
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+int peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
+                           const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, cudaStream_t st) {
+  if (int rc = check_geometry(tp, rank, T, W, r, variant)) return rc;
+  if (d <= 0 || !z_own || !dA_mc || !dP_mc || !a16p(z_own) || !a16p(dA_mc) || !a16p(dP_mc)) return BTP_ERR_DIM;
+  const int rows_own = T / tp;
+  peer_boundary_bwd_kernel<<<rows_grid(rows_own), 256, 0, st>>>(
+      McRows{static_cast<bf16*>(const_cast<void*>(dA_mc))}, rank * rows_own, rows_own, W, r, variant, 1.0f / (float)d,
+      static_cast<const bf16*>(z_own), s_own, McRows{static_cast<bf16*>(dP_mc)}, McStat{dss_mc});
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 

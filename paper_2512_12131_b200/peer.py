@@ -13,6 +13,13 @@ Two providers of the per-rank heap bases:
   CUDA stream; the "peer" buffers are plain device allocations of the same GPU. The kernels,
   flags and executor code are exactly those of the multi-GPU path, so the single-GPU box can
   check the multi-rank numerics and the signal/wait protocol.
+* `"local_multicast"` (tests, tp=1): the heap is a cuMem allocation bound to a ONE-device NVSwitch
+  multicast object (`LocalMulticastHeap`), so the NVLS kernels' multimem instructions run for real
+  on a single-GPU box (the switch "sum" over one member is the identity).
+
+nvls=True additionally gives every buffer a MULTICAST address (symmetric memory's multicast_ptr, or
+the local multicast object) and the boundaries run as btp_peer_boundary_{fwd,bwd}_nvls: the switch
+reduces the partials (multimem.ld_reduce) and replicates a / dP (multimem.st).
 """
 
 from __future__ import annotations
@@ -52,10 +59,69 @@ class VirtualPeers:
         self._barrier.wait()
 
 
+class LocalMulticastHeap:
+    """`nbytes` of device memory mapped twice: at a unicast address (wrapped as a torch uint8 tensor)
+    and at the address of a one-device multicast object it is bound to (cuMulticastCreate /
+    AddDevice / BindMem + cuMemMap). Single-GPU stand-in for symmetric memory's multicast mapping."""
+
+    def __init__(self, nbytes: int, device):
+        from cuda.bindings import driver as cu
+
+        self._cu = cu
+        dev = torch.device(device)
+        torch.cuda.init()
+        torch.empty(1, device=dev)  # primary context current on this thread
+
+        def ok(res):
+            err, *rest = res if isinstance(res, tuple) else (res,)
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(f"multicast heap: {err}")
+            return rest[0] if len(rest) == 1 else rest
+
+        ordinal = dev.index if dev.index is not None else torch.cuda.current_device()
+        cudev = ok(cu.cuDeviceGet(ordinal))
+        if not ok(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cudev)):
+            raise RuntimeError("device has no multicast (NVLS) support")
+        mp = cu.CUmulticastObjectProp()
+        mp.numDevices = 1
+        mp.handleTypes = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        mp.size = max(int(nbytes), 1)
+        gran = ok(cu.cuMulticastGetGranularity(mp, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        size = -(-max(int(nbytes), 1) // gran) * gran
+        mp.size = size
+        self.mc_handle = ok(cu.cuMulticastCreate(mp))
+        ok(cu.cuMulticastAddDevice(self.mc_handle, cudev))
+        ap = cu.CUmemAllocationProp()
+        ap.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        ap.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        ap.location.id = ordinal
+        ap.requestedHandleTypes = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+        self.mem = ok(cu.cuMemCreate(size, ap, 0))
+        ok(cu.cuMulticastBindMem(self.mc_handle, 0, self.mem, 0, size, 0))
+        acc = cu.CUmemAccessDesc()
+        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        acc.location.id = ordinal
+        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uc = ok(cu.cuMemAddressReserve(size, gran, 0, 0))
+        ok(cu.cuMemMap(self.uc, size, 0, self.mem, 0))
+        ok(cu.cuMemSetAccess(self.uc, size, [acc], 1))
+        self.mc = ok(cu.cuMemAddressReserve(size, gran, 0, 0))
+        ok(cu.cuMemMap(self.mc, size, 0, self.mc_handle, 0))
+        ok(cu.cuMemSetAccess(self.mc, size, [acc], 1))
+        self.size = size
+        self.uc_ptr, self.mc_ptr = int(self.uc), int(self.mc)
+        holder = type("_UC", (), {})()
+        holder.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                           "data": (self.uc_ptr, False), "version": 3}
+        self.tensor = torch.as_tensor(holder, device=dev)
+        self._holder = holder
+
+
 class PeerComm:
     """One rank's view of the symmetric heap: named buffers, peer pointer arrays, flags."""
 
-    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None, scatter: bool = False):
+    def __init__(self, tp: int, rank: int, device, provider="symmetric_memory", group=None, scatter: bool = False,
+                 nvls: bool = False):
         if not 1 <= tp <= 8:
             raise ValueError(f"peer boundaries support 1 <= tp <= 8, got {tp}")
         self.tp, self.rank = tp, rank
@@ -70,6 +136,12 @@ class PeerComm:
         # reduce) doubles the reduce-scatter bytes and both halves then use the outgoing direction,
         # so it only wins when the GEMM is long against the transfer.
         self.scatter = scatter
+        if nvls and scatter:
+            raise ValueError("nvls and scatter are alternative boundary forms")
+        if provider == "local_multicast" and tp != 1:
+            raise ValueError("the local multicast heap has one member: tp must be 1")
+        self.nvls = nvls or provider == "local_multicast"
+        self.mc_base = 0
         self.heap = None
         self._hptrs: dict[str, list[int]] = {}
         self._bufs: dict[str, torch.Tensor] = {}
@@ -105,14 +177,27 @@ class PeerComm:
             group = self.group if self.group is not None else dist.group.WORLD
             hdl = symm_mem.rendezvous(self.heap, group)
             bases = [int(p) for p in hdl.buffer_ptrs]
+            if self.nvls:
+                self.mc_base = int(hdl.multicast_ptr)
+                if not self.mc_base:
+                    raise RuntimeError("symmetric memory returned no multicast address (NVLS unavailable)")
+            self._symm = hdl
             dist.barrier(group=group)  # every rank's flags are zero before anyone signals
+        elif self.provider == "local_multicast":
+            self._mc_heap = LocalMulticastHeap(total, self.dev)
+            self.heap = self._mc_heap.tensor
+            self.heap.zero_()
+            torch.cuda.synchronize(self.dev)
+            bases, self.mc_base = [self.heap.data_ptr()], self._mc_heap.mc_ptr
         else:
             raise ValueError(f"unknown peer provider {self.provider!r}")
         if len(bases) != self.tp:
             raise RuntimeError(f"peer heap rendezvous returned {len(bases)} bases for tp={self.tp}")
         self.bases = bases
         self._flags_ptrs = torch.tensor(bases, dtype=torch.int64, device=self.dev)
+        self._offsets = {}
         for name, shape, dtype, o, nbytes in layout:
+            self._offsets[name] = o
             self._bufs[name] = self.heap[o:o + nbytes].view(dtype).view(shape)
             self._hptrs[name] = [b + o for b in bases]
             self._ptrs[name] = torch.tensor(self._hptrs[name], dtype=torch.int64, device=self.dev)
@@ -126,6 +211,12 @@ class PeerComm:
 
     def ptrs(self, name: str):
         return ctypes.c_void_p(self._ptrs[name].data_ptr())
+
+    def mc(self, name: str):
+        """Multicast address of buffer `name` (nvls only)."""
+        if not self.mc_base:
+            raise RuntimeError("this peer heap has no multicast mapping")
+        return ctypes.c_void_p(self.mc_base + self._offsets[name])
 
     def host_ptrs(self, name: str) -> list[int]:
         """Every rank's address of buffer `name`, rank order (host ints, for tensor maps)."""
@@ -147,12 +238,23 @@ class PeerComm:
 
 
 def boundary_fwd(pc: PeerComm, P_name, ss_name, T, W, r, variant, d, eps, z_own, s_own, a_name) -> None:
+    if pc.nvls:
+        _native.call("btp_peer_boundary_fwd_nvls", pc.mc(P_name), pc.mc(ss_name) if ss_name else None, pc.tp,
+                     pc.rank, T, W, r, variant, d, ctypes.c_float(eps), ctypes.c_void_p(z_own.data_ptr()),
+                     ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None, pc.mc(a_name), _stream())
+        return
     _native.call("btp_peer_boundary_fwd", pc.ptrs(P_name), pc.ptrs(ss_name) if ss_name else None, pc.tp, pc.rank,
                  T, W, r, variant, d, ctypes.c_float(eps), ctypes.c_void_p(z_own.data_ptr()),
                  ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None, pc.ptrs(a_name), _stream())
 
 
 def boundary_bwd(pc: PeerComm, da_name, T, W, r, variant, d, z_own, s_own, dP_name, dss_name) -> None:
+    if pc.nvls:
+        _native.call("btp_peer_boundary_bwd_nvls", pc.mc(da_name), pc.tp, pc.rank, T, W, r, variant, d,
+                     ctypes.c_void_p(z_own.data_ptr()),
+                     ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None, pc.mc(dP_name),
+                     pc.mc(dss_name) if dss_name else None, _stream())
+        return
     _native.call("btp_peer_boundary_bwd", pc.ptrs(da_name), pc.tp, pc.rank, T, W, r, variant, d,
                  ctypes.c_void_p(z_own.data_ptr()), ctypes.c_void_p(s_own.data_ptr()) if s_own is not None else None,
                  pc.ptrs(dP_name), pc.ptrs(dss_name) if dss_name else None, _stream())
