@@ -28,7 +28,8 @@ import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
 import btpsim  # noqa: E402
-from btpsim.model import ModelConfig, RunShape, Variant, build_block, reference_forward  # noqa: E402
+from btpsim.model import (ModelConfig, RunShape, Variant, build_block, reference_forward,  # noqa: E402
+                          seeded_h_prev)
 from btpsim.plan import Strategy, describe, plan  # noqa: E402
 from btpsim.simulator import execute_forward  # noqa: E402
 from btpsim.tensor import Tensor, seeded_fill  # noqa: E402
@@ -89,6 +90,39 @@ def main():
                     meta["combos"].append(entry)
     y_ref, _ = reference_forward(build_block(TOY, Variant.COLA, seed=7), seeded_fill((2, 8, TOY.d), 8))
     arrays["toy_cola_reference_y"] = y_ref.values
+
+    # ---- TOY lax (cross-layer h bundle; reference test_acceptance.py:147-170): BTP with and
+    # without a seeded h_prev (seed 9), y + the h_cur bundle + every per-rank workspace
+    meta["lax"] = []
+    for tp in (1, 2, 4):
+        for online in (False, True):
+            for grouping in (False, True):
+                for hp_seed in (None, 9):
+                    shape = RunShape(b=2, s=8, tp=tp)
+                    block = build_block(TOY, Variant.LAX, seed=7)
+                    x = seeded_fill((2, 8, TOY.d), 8)
+                    hp = None if hp_seed is None else seeded_h_prev(TOY, shape, hp_seed)
+                    pl = plan(Strategy.BOTTLENECK, TOY, shape, Variant.LAX, online_norm=online, grouping=grouping)
+                    res = execute_forward(pl, block, x, hp, model_tail=True)
+                    tag = f"toy_lax_tp{tp}_on{int(online)}_g{int(grouping)}_hp{hp_seed or 0}"
+                    arrays[tag + "_y"] = res.y.values
+                    for n, h in res.h_cur.items():
+                        arrays[f"{tag}_h_{n}"] = h.values
+                    names = []
+                    for rk, ws in enumerate(res.workspaces):
+                        for name, arr in ws.items():
+                            arrays[f"{tag}_ws{rk}_{name}"] = np.asarray(arr)
+                            if rk == 0:
+                                names.append(name)
+                    meta["lax"].append({"tag": tag, "tp": tp, "online": online, "grouping": grouping,
+                                        "hp_seed": hp_seed, "ws_names": names,
+                                        "records": [list(map(lambda z: list(z) if isinstance(z, tuple) else z, r))
+                                                    for r in res.trace.record_tuples()]})
+    yl, hl = reference_forward(build_block(TOY, Variant.LAX, seed=7), seeded_fill((2, 8, TOY.d), 8),
+                               seeded_h_prev(TOY, RunShape(2, 8, 1), 9))
+    arrays["toy_lax_reference_y"] = yl.values
+    for n, h in hl.items():
+        arrays[f"toy_lax_reference_h_{n}"] = h.values
 
     # ---- SMALL (GPU parity config), fan-in scaled
     blk = scaled(build_block(SMALL, Variant.COLA, seed=0))

@@ -10,9 +10,10 @@ from oracle import btp_oracle as O
 PROJ = O.PROJECTIONS
 
 
-def torch_block(blk, x, b, s, heads, eps=1e-6):
+def torch_block(blk, x, b, s, heads, eps=1e-6, h_prev=None):
     """Independent float64 torch forward (same math as reference model.py:256-305)."""
     var = blk["variant"]
+    H = {n: torch.tensor(h, requires_grad=True) for n, h in h_prev.items()} if h_prev is not None else None
     P = {g: {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in blk[g].items()}
          for g in ("A", "B", "W")}
     g1 = torch.tensor(blk["gamma1"], requires_grad=True)
@@ -32,7 +33,10 @@ def torch_block(blk, x, b, s, heads, eps=1e-6):
     def proj(n, inp):
         if var == "full-rank":
             return inp @ P["W"][n].T
-        return sig(inp @ P["B"][n].T) @ P["A"][n].T
+        z = inp @ P["B"][n].T
+        if var == "lax" and H is not None:
+            return (z + H[n]) @ P["A"][n].T
+        return sig(z) @ P["A"][n].T
 
     d = x.shape[1]
     hd = d // heads
@@ -44,7 +48,7 @@ def torch_block(blk, x, b, s, heads, eps=1e-6):
     n2 = norm(xm, g2)
     act = torch.nn.functional.silu(proj("gate", n2)) * proj("up", n2)
     y = xm + proj("down", act)
-    return y, P, g1, g2, xt
+    return (y, P, g1, g2, xt) if H is None else (y, P, g1, g2, xt, H)
 
 
 @pytest.mark.parametrize("variant", ["cola", "svd", "full-rank"])
@@ -75,3 +79,24 @@ def test_sharded_grads_are_slices():
     assert sh["A"]["gate"].shape == (40, 8) and sh["B"]["down"].shape == (8, 40)
     assert sh["A"]["q"].shape == (16, 8) and sh["B"]["q"].shape == (8, 16)
     assert np.array_equal(sh["dgamma1"], np.arange(16, 32))
+
+
+def test_lax_backward_matches_autograd():
+    """lax with a seeded h bundle: parameter grads, dx and dL/dh_prev per projection."""
+    d, d_ff, r, heads, b, s = 32, 80, 8, 4, 2, 8
+    blk = O.build_block(d, d_ff, r, "lax", 3, scale_fan_in=3.0)
+    x = O.seeded_fill((b * s, d), 10003)
+    G = O.loss_projection((b * s, d), 30003)
+    hp = {n: h.reshape(b * s, r) for n, h in O.seeded_h_prev(b, s, r, 5).items()}
+    y, cache = O.block_forward(blk, x, b, s, heads, h_prev=hp)
+    g = O.block_backward(blk, cache, G, b, s, heads)
+    yt, P, g1, g2, xt, H = torch_block(blk, x, b, s, heads, h_prev=hp)
+    np.testing.assert_allclose(yt.detach().numpy(), y, rtol=0, atol=1e-12)
+    (yt * torch.tensor(G)).sum().backward()
+    np.testing.assert_allclose(g["dx"], xt.grad.numpy(), rtol=0, atol=1e-11)
+    np.testing.assert_allclose(g["dgamma1"], g1.grad.numpy(), rtol=0, atol=1e-11)
+    for grp in ("A", "B"):
+        for n, t in P[grp].items():
+            np.testing.assert_allclose(g[grp][n], t.grad.numpy(), rtol=0, atol=1e-11, err_msg=f"{grp}{n}")
+    for n in PROJ:
+        np.testing.assert_allclose(g["dh_prev"][n], H[n].grad.numpy(), rtol=0, atol=1e-11, err_msg=n)

@@ -85,3 +85,49 @@ def test_c60m_checksums():
     for name, nrm in m["norms"].items():
         got = np.linalg.norm(np.asarray(ws[0][name]))
         assert abs(got - nrm) <= 1e-9 * nrm, name
+
+
+def _toy_hp(seed):
+    if seed is None:
+        return None
+    return {n: h.reshape(16, 4) for n, h in O.seeded_h_prev(2, 8, 4, seed).items()}
+
+
+def test_reference_forward_toy_lax():
+    """reference_forward with a seeded h bundle (model.py:256-305): y and the returned h_cur."""
+    blk = O.build_block(16, 40, 4, "lax", 7)
+    x = O.seeded_fill((2, 8, 16), 8).reshape(16, 16)
+    y, c = O.block_forward(blk, x, 2, 8, 4, h_prev=_toy_hp(9))
+    np.testing.assert_allclose(y, ARR["toy_lax_reference_y"].reshape(16, 16), rtol=0, atol=1e-10)
+    for n in O.PROJECTIONS:
+        np.testing.assert_allclose(c["h_cur"][n], ARR[f"toy_lax_reference_h_{n}"].reshape(16, 4), rtol=0, atol=1e-12)
+
+
+def test_lax_without_h_prev_is_svd():
+    """reference test_model.py:182-192: LaX with no (zero) bundle equals SVD."""
+    x = O.seeded_fill((2, 8, 16), 8).reshape(16, 16)
+    y_svd, _ = O.block_forward(O.build_block(16, 40, 4, "svd", 7), x, 2, 8, 4)
+    y_lax, _ = O.block_forward(O.build_block(16, 40, 4, "lax", 7), x, 2, 8, 4)
+    y_zero, _ = O.block_forward(O.build_block(16, 40, 4, "lax", 7), x, 2, 8, 4,
+                                h_prev={n: np.zeros((16, 4)) for n in O.PROJECTIONS})
+    assert np.array_equal(y_svd, y_lax) and np.array_equal(y_svd, y_zero)
+
+
+@pytest.mark.parametrize("entry", META["lax"], ids=lambda e: e["tag"])
+def test_btp_lax_sharded_workspaces(entry):
+    """BTP lax under every tp/online/grouping, with and without an h bundle: y, the h_cur bundle
+    (= the replicated z) and every per-rank workspace of the reference simulator."""
+    tp, online = entry["tp"], entry["online"]
+    blk = O.build_block(16, 40, 4, "lax", 7)
+    x = O.seeded_fill((2, 8, 16), 8).reshape(16, 16)
+    y, ws = O.btp_forward_sharded(blk, x, 2, 8, 4, tp, online=online, h_prev=_toy_hp(entry["hp_seed"]))
+    np.testing.assert_allclose(y, ARR[entry["tag"] + "_y"].reshape(16, 16), rtol=0, atol=1e-9)
+    for n in O.PROJECTIONS:
+        np.testing.assert_allclose(ws[0][f"z_{n}"], ARR[f"{entry['tag']}_h_{n}"].reshape(16, 4), rtol=1e-9,
+                                   atol=1e-9)
+    for rk in range(tp):
+        assert set(entry["ws_names"]) == set(ws[rk]), set(entry["ws_names"]) ^ set(ws[rk])
+        for name in entry["ws_names"]:
+            want = ARR[f"{entry['tag']}_ws{rk}_{name}"]
+            np.testing.assert_allclose(np.asarray(ws[rk][name]).reshape(want.shape), want, rtol=1e-9, atol=1e-9,
+                                       err_msg=f"rank {rk} {name}")
