@@ -169,7 +169,8 @@ int btp_reduce_rows(const float* in, int splits, long long split_stride, long lo
                     const float* col_scale, float* out, long long ldo, int accumulate, void* stream);
 
 /* out = a + b (bf16, elementwise over rows x cols). Replicated residual adds of the baselines
- * (simulator.py:367, :395, :523, :540). */
+ * (simulator.py:367, :395, :523, :540), and the lax merge a = z + h_prev of the reduced rank-r
+ * projection with the previous layer's bundle (simulator.py:260-265). */
 int btp_add(const void* a, long long lda, const void* b, long long ldb, void* out, long long ldo, int rows,
             int cols, void* stream);
 

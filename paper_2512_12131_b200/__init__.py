@@ -23,7 +23,9 @@ from .model import (
     fan_in_scaled,
     preset,
     projection_dims,
+    seeded_h_prev,
     token_batch,
+    zero_h_prev,
 )
 from .plan import NormMode, PlanError, ShardPlan, Strategy, apply_grouping, describe, enumerate_collectives, plan
 from .trace import CollectiveRecord, Trace, ring_transfer_elements, trace_volume
@@ -34,6 +36,7 @@ __all__ = [
     "Tensor", "tensor", "zeros", "seeded_fill", "DimensionError", "DivisibilityError",
     "ModelConfig", "RunShape", "Variant", "PRESETS", "COLA_60M", "preset", "projection_dims",
     "DecoderBlockWeights", "build_block", "fan_in_scaled", "ModelWeights", "build_model", "token_batch",
+    "zero_h_prev", "seeded_h_prev",
     "Strategy", "NormMode", "ShardPlan", "PlanError", "plan", "apply_grouping", "describe",
     "enumerate_collectives",
     "CollectiveRecord", "Trace", "trace_volume", "ring_transfer_elements",

@@ -51,6 +51,8 @@ class StepResult:
     trace: Trace
     plan: ShardPlan
     executor: object
+    h_cur: dict | None = None     # lax: {projection: Tensor [b, s, r]} (the bundle for the next layer)
+    dh_prev: dict | None = None   # lax with an h_prev: {projection: dL/dh_prev [b, s, r]} (float64 host)
 
 
 def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
@@ -120,11 +122,12 @@ def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
 def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *, eps: float = EPS_DEFAULT,
                     model_tail: bool = False, trace: Trace | None = None, capture_workspaces: bool = False,
                     attn_backend: str = "auto", precision: str = "bf16") -> SimResult:
-    """Run one block forward under the plan on the GPU; returns the gathered logical y."""
-    if h_prev is not None and block.variant is Variant.LAX:
-        raise PlanError("the lax variant is outside the device path (SURVEY §2.1: out of scope)")
+    """Run one block forward under the plan on the GPU; returns the gathered logical y (and, for
+    lax, the h_cur bundle; h_prev is given logically, {projection: Tensor [b, s, r]}, as in the
+    reference simulator.py:268-316)."""
     xv = _check_inputs(pl, block, x)
     ex = make_executor(pl, block, eps=eps, trace=trace, attn_backend=attn_backend, precision=precision)
+    _stage_h_prev(ex, block, h_prev)
     x_sh = shard_input(ex, xv)
     y_sh = ex.forward(x_sh)
     y = _gather_y(ex, y_sh, model_tail)
@@ -134,12 +137,30 @@ def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *
     b, s, d = xv.shape
     y_host = y.double().cpu().numpy().reshape(b, s, d)
     eb = x.element_bytes if isinstance(x, Tensor) else 2
-    return SimResult(Tensor(y_host, eb), None, ex.comm.trace, ws, pl)
+    return SimResult(Tensor(y_host, eb), _h_cur(ex, b, s, eb), ex.comm.trace, ws, pl)
+
+
+def _stage_h_prev(ex, block: DecoderBlockWeights, h_prev) -> None:
+    if block.variant is not Variant.LAX:
+        return  # the reference ignores a bundle handed to a non-lax block (simulator.py:297)
+    if h_prev is not None:
+        h_prev = {k: (v.values if isinstance(v, Tensor) else np.asarray(v)) for k, v in h_prev.items()}
+    ex.set_h_prev(h_prev)
+
+
+def _h_cur(ex, b, s, eb=2):
+    """The lax bundle {projection: Tensor [b, s, r]} (replicated: read from this rank), else None."""
+    if not getattr(ex, "lax", False):
+        return None
+    torch.cuda.synchronize(ex.dev)
+    return {n: Tensor(h.double().cpu().numpy().reshape(b, s, -1), eb) for n, h in ex.h_cur.items()}
 
 
 def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: float = EPS_DEFAULT,
-               attn_backend: str = "auto", executor=None, precision: str = "bf16") -> StepResult:
+               attn_backend: str = "auto", executor=None, precision: str = "bf16", h_prev=None) -> StepResult:
     """Forward + backward of the block for the builder-defined loss L = sum(y * G) (dL/dy = G).
+    lax: h_prev ({projection: [b, s, r]}) is merged after each reduction; the result carries the
+    h_cur bundle and dL/dh_prev.
 
     G defaults to the loss projection seeded_fill((b, s, d), 30000)."""
     from .tensor import seeded_fill
@@ -151,12 +172,16 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
     Gv = G.values if isinstance(G, Tensor) else np.asarray(G)
     ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
                                                              precision=precision)
+    _stage_h_prev(ex, block, h_prev)
     x_sh = shard_input(ex, xv)
     g_sh = shard_input(ex, Gv)
     y_sh = ex.forward(x_sh)
+    h_cur = _h_cur(ex, b, s)
     loss = ex.loss(y_sh, g_sh)
     dx = ex.backward(g_sh)
     y = _gather_y(ex, y_sh, False)
+    dh = getattr(ex, "dh_prev", None)
+    dh_host = None if dh is None else {n: t.double().cpu().numpy().reshape(b, s, -1) for n, t in dh.items()}
     return StepResult(
         y=Tensor(y.double().cpu().numpy().reshape(b, s, d)),
         loss=loss,
@@ -165,6 +190,8 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
         trace=ex.comm.trace,
         plan=pl,
         executor=ex,
+        h_cur=h_cur,
+        dh_prev=dh_host,
     )
 
 

@@ -85,7 +85,7 @@ _RECOMPUTED = ("x_mid", "gu", "act", "qkv", "attn", "a_o", "a_gu", "a_d", "a_qkv
 def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPolicy, h_prev=None, *,
                   eps: float = EPS_DEFAULT, model_tail: bool = False) -> CkptRun:
     """Device analogue of the reference's run_with_ckpt (checkpointing.py:109-163)."""
-    from .api import _check_inputs, make_executor, shard_input
+    from .api import _check_inputs, _stage_h_prev, make_executor, shard_input
 
     if policy is CkptPolicy.LOWRANK_BOUNDARY and pl.strategy is Strategy.FULL_RANK:
         raise PlanError("lowrank-boundary checkpointing stores rank-r tensors; the full-rank strategy has none")
@@ -94,6 +94,7 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
     xv = _check_inputs(pl, block, x)
     full_pl = replace(pl, lowrank_ckpt=False)
     ex = make_executor(full_pl, block, eps=eps)
+    _stage_h_prev(ex, block, h_prev)
     x_sh = shard_input(ex, xv)
     y = ex.forward(x_sh).clone()
     without = ex.saved_activation_bytes()
@@ -107,6 +108,7 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
 
     ck_pl = replace(pl, lowrank_ckpt=True)
     ck = make_executor(ck_pl, block, eps=eps)
+    _stage_h_prev(ck, block, h_prev)
     ck.forward(x_sh)
     with_ = ck.saved_activation_bytes()
     f0 = ck.stats.gemm_flops

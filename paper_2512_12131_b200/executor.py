@@ -44,7 +44,9 @@ from .plan import NormMode, PlanError, ShardPlan, Strategy
 
 BF16 = torch.bfloat16
 F32 = torch.float32
-_VAR = {Variant.SVD: 0, Variant.COLA: 1}
+# sigma kernel variant per model variant: lax applies no activation (its merge with the previous
+# layer's bundle is a plain add after the reduction, simulator.py:260-265)
+_VAR = {Variant.SVD: 0, Variant.COLA: 1, Variant.LAX: 0}
 # bf16: the training path (tcgen05 GEMMs, bf16 activations, fp32 statistics / accumulation);
 # fp32: the parity mode (exact-fp32 SIMT GEMM + fp32 row kernels; north_star 1e-4 tolerance)
 PRECISIONS = {"bf16": BF16, "fp32": F32}
@@ -331,7 +333,7 @@ class ExecutorBase:
 
 
 class BTPBlockExecutor(ExecutorBase):
-    """One rank's shard of a low-rank (svd/cola) block under a BTP plan."""
+    """One rank's shard of a low-rank (svd/cola/lax) block under a BTP plan."""
 
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None,
                  device: torch.device | str = "cuda", eps: float = 1e-6, attn_backend: str = "auto",
@@ -341,9 +343,14 @@ class BTPBlockExecutor(ExecutorBase):
         if block.variant is not pl.variant:
             raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
         if pl.variant not in _VAR:
-            raise PlanError(f"variant {pl.variant.value} is not supported on the device path (svd, cola)")
+            raise PlanError(f"variant {pl.variant.value} is not supported on the device path (svd, cola, lax)")
         self._setup(pl, comm, device, eps, precision)
         self.var = _VAR[pl.variant]
+        # lax (simulator.py:247-265): a = z + h_prev[name] after the reduction, h_cur = z. The
+        # bundle is replicated like z; set_h_prev() stages it per chunk ([T, k*r] like P).
+        self.lax = pl.variant is Variant.LAX
+        self.has_h_prev = False
+        self.dh_prev: dict | None = None
         self.online = pl.norm_mode is NormMode.ONLINE
         self.grouping = pl.grouping
         self.ckpt = pl.lowrank_ckpt
@@ -615,9 +622,62 @@ class BTPBlockExecutor(ExecutorBase):
     def _gid(names) -> str:
         return {("q", "k", "v"): "qkv", ("gate", "up"): "gate_up"}[tuple(names)]
 
+    # ------------------------------------------------------------------ lax h bundle
+    def set_h_prev(self, h_prev) -> None:
+        """Stage the previous layer's lax bundle {projection: [T, r]} (host or device arrays,
+        replicated on every rank) for the next forward; None = the first-layer boundary (a = z,
+        bitwise the svd block, reference test_model.py:182-192)."""
+        if h_prev is None:
+            self.has_h_prev = False
+            return
+        if not self.lax:
+            raise PlanError(f"h_prev is a lax input; this block is {self.pl.variant.value}")
+        if self.peer is not None:
+            raise PlanError("lax with an h bundle runs on the NCCL boundaries (the peer kernels push a = z)")
+        T, r = self.T, self.r
+        for names in self.CHUNKS:
+            hp = self.buf(f"hp_{'_'.join(names)}", (T, len(names) * r))
+            for i, n in enumerate(names):
+                v = h_prev[n]
+                v = torch.as_tensor(np.asarray(v).reshape(T, r)) if not isinstance(v, torch.Tensor) else v.reshape(T, r)
+                hp[:, i * r:(i + 1) * r].copy_(v.to(self.dev, self.act), non_blocking=True)
+        self.has_h_prev = True
+
+    def _lax_merge(self, names, z_views, out_name):
+        """a = z + h_prev per projection into `out_name` [T, k*r] (btp_add; one launch when the z
+        views are the column blocks of one [T, k*r] buffer)."""
+        T, r, k = self.T, self.r, len(names)
+        hp = self._buf[f"hp_{'_'.join(names)}"]
+        out = self.buf(out_name, (T, k * r))
+        z0 = z_views[0]
+        base = z0 if k == 1 else None
+        if k > 1 and z0.stride(0) == k * r and all(z.data_ptr() == z0.data_ptr() + i * r * z0.element_size()
+                                                    for i, z in enumerate(z_views)):
+            base = z0.as_strided((T, k * r), (k * r, 1))
+        if base is not None:
+            K.add(base, hp, out)
+            self.stats.kernel_launches += 1
+        else:
+            for i, z in enumerate(z_views):
+                K.add(z, hp[:, i * r:(i + 1) * r], out[:, i * r:(i + 1) * r])
+                self.stats.kernel_launches += 1
+        return [out[:, i * r:(i + 1) * r] for i in range(k)]
+
+    def _a_input(self, names, z_views, a_views):
+        """What the up-projection consumes; records the lax h_cur (= z, before the merge)."""
+        if not self.lax:
+            return a_views
+        for n, a in zip(names, a_views):  # a == z for lax (no sigma); full rows in every mode
+            self.h_cur[n] = a
+        if not self.has_h_prev:
+            return a_views
+        return self._lax_merge(names, a_views, f"alax_{'_'.join(names)}")
+
     def _sigma_only(self, z_views, names, out_name):
-        """a = sigma(z) for stored z (checkpoint recompute); svd: a = z."""
+        """a = sigma(z) for stored z (checkpoint recompute); svd: a = z; lax: z (+ h_prev)."""
         if self.var == 0:
+            if self.lax and self.has_h_prev:
+                return self._lax_merge(names, z_views, out_name)
             return z_views
         T, r, k = self.T, self.r, len(z_views)
         a_store = self.buf(out_name, (T, k * r))
@@ -644,20 +704,24 @@ class BTPBlockExecutor(ExecutorBase):
         self.comm.pass_tag = "forward"
         W = self.W
         S = {"x": x}
+        self.h_cur = {}
         # ---- attention half
         n1, ss1, rl1, s1 = self._norm(x, self.gamma1, 1)
         z_qkv, a_qkv, P_qkv = self._down_boundary(("q", "k", "v"), n1, W["d_qkv"], ss1, rl1, 1, True)
+        a_qkv = self._a_input(("q", "k", "v"), z_qkv, a_qkv)
         S["s1"] = s1 if s1 is not None else self._buf["s1"]
         qkv = self.buf("qkv", (3, T, dl))
         self._up(a_qkv, [W["u_qkv"][i] for i in range(3)], [qkv[i] for i in range(3)])
         attn, actx = self.attn.forward(qkv[0], qkv[1], qkv[2])
         self._buf["attn"] = attn
         z_o, a_o, P_o = self._down_boundary(("o",), attn, W["d_o"], None, None, 0, False)
+        a_o = self._a_input(("o",), z_o, a_o)
         x_mid = self.buf("x_mid", (T, dl))
         self._up(a_o, [W["u_o"]], [x_mid], resid=x)
         # ---- mlp half
         n2, ss2, rl2, s2 = self._norm(x_mid, self.gamma2, 2)
         z_gu, a_gu, P_gu = self._down_boundary(("gate", "up"), n2, W["d_gu"], ss2, rl2, 2, True)
+        a_gu = self._a_input(("gate", "up"), z_gu, a_gu)
         S["s2"] = s2 if s2 is not None else self._buf["s2"]
         gu = self.buf("gu", (2, T, fl))
         self._up(a_gu, [W["u_gu"][0], W["u_gu"][1]], [gu[0], gu[1]])
@@ -665,6 +729,7 @@ class BTPBlockExecutor(ExecutorBase):
         K.swiglu(gu[0], gu[1], act)
         self.stats.kernel_launches += 1
         z_d, a_d, P_d = self._down_boundary(("down",), act, W["d_d"], None, None, 0, False)
+        a_d = self._a_input(("down",), z_d, a_d)
         y = self.buf("y", (T, dl))
         self._up(a_d, [W["u_d"]], [y], resid=x_mid)
         # ---- what backward keeps
@@ -694,8 +759,10 @@ class BTPBlockExecutor(ExecutorBase):
         zs["o"], zs["down"] = S["z_o"][0], S["z_d"][0]
         for n, z in zs.items():
             ws[f"z_{n}"] = z
-        if self.var == 1:
-            for key, names in (("a_q_k_v", names3), ("a_gate_up", names2), ("a_o", ("o",)), ("a_down", ("down",))):
+        if self.var == 1 or (self.lax and self.has_h_prev):
+            pre = "a_" if self.var == 1 else "alax_"
+            for key, names in ((pre + "q_k_v", names3), (pre + "gate_up", names2), (pre + "o", ("o",)),
+                               (pre + "down", ("down",))):
                 a = self._buf[key]
                 for i, n in enumerate(names):
                     ws[f"a_in_{n}"] = a[:, i * r:(i + 1) * r]
@@ -792,23 +859,31 @@ class BTPBlockExecutor(ExecutorBase):
 
     def _sigma_bwd(self, names, da_P, zP, s, dss_name):
         k, r, T = len(names), self.r, self.T
+        out = da_P
+        if self.lax and self.has_h_prev:
+            # dL/dh_prev = dL/da (the merge is an add): keep the reduced da, write dP beside it
+            out = self.buf(f"dPlax_{'_'.join(names)}", tuple(da_P.shape))
+            views = self._da_views(names, da_P)
+            if self.dh_prev is None:
+                self.dh_prev = {}
+            self.dh_prev.update(zip(names, views))
         if self.grouping or k == 1:
             dss = self.buf(dss_name, (T,), F32) if s is not None else None
-            K.fixup_sigma_bwd(zP, da_P, da_P, r=r, nproj=k, variant=self.var, s=s, d=self.d, dss=dss)
+            K.fixup_sigma_bwd(zP, da_P, out, r=r, nproj=k, variant=self.var, s=s, d=self.d, dss=dss)
             self.stats.kernel_launches += 1
-            return da_P, dss
+            return out, dss
         # ungrouped: the norm statistic gradient sums over the projections
         parts = self.buf(f"{dss_name}_parts", (k, 1, T), F32) if s is not None else None
         for i in range(k):
-            K.fixup_sigma_bwd(zP[i], da_P[i], da_P[i], r=r, nproj=1, variant=self.var, s=s, d=self.d,
+            K.fixup_sigma_bwd(zP[i], da_P[i], out[i], r=r, nproj=1, variant=self.var, s=s, d=self.d,
                               dss=None if parts is None else parts[i, 0])
             self.stats.kernel_launches += 1
         if s is None:
-            return da_P, None
+            return out, None
         dss = self.buf(dss_name, (T,), F32)
         K.reduce_rows(parts, dss.view(1, T))
         self.stats.kernel_launches += 1
-        return da_P, dss
+        return out, dss
 
     def _da_buffer(self, names):
         T, r, k = self.T, self.r, len(names)
@@ -852,6 +927,7 @@ class BTPBlockExecutor(ExecutorBase):
         if self.ckpt:
             self._recompute_mlp_inputs()
         self.comm.pass_tag = "backward"
+        self.dh_prev = None
         G = self.grad
         # ---------------- mlp down chunk: y = x_mid + a_d @ Wu_d^T
         names = ("down",)

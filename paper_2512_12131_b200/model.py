@@ -152,6 +152,20 @@ def build_block(cfg: ModelConfig, variant: Variant, seed: int, element_bytes: in
     return DecoderBlockWeights(cfg, variant, full, down, up, g1, g2)
 
 
+def zero_h_prev(cfg: ModelConfig, shape: RunShape, element_bytes: int = 2) -> dict[str, Tensor]:
+    """The lax first-layer boundary bundle: zeros for all seven projections (model.py:308-315)."""
+    if cfg.r is None:
+        raise ValueError("h bundle needs cfg.r")
+    return {n: Tensor(np.zeros((shape.b, shape.s, cfg.r)), element_bytes) for n in PROJECTIONS}
+
+
+def seeded_h_prev(cfg: ModelConfig, shape: RunShape, seed: int, element_bytes: int = 2) -> dict[str, Tensor]:
+    """Deterministic nonzero lax bundle: projection i gets fill((b, s, r), seed + 7 i) (model.py:318-325)."""
+    if cfg.r is None:
+        raise ValueError("h bundle needs cfg.r")
+    return {n: seeded_fill((shape.b, shape.s, cfg.r), seed + 7 * i, element_bytes) for i, n in enumerate(PROJECTIONS)}
+
+
 def fan_in_scaled(block: DecoderBlockWeights, gain: float = 3.0) -> DecoderBlockWeights:
     """The parity recipe: every linear factor times sqrt(gain / fan_in).
 

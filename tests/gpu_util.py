@@ -25,12 +25,19 @@ def inputs(cfg, variant, b, s, seed=0):
     return blk, x, G, oblk
 
 
-def oracle_step(oblk, x, G, cfg, b, s, tp=1, online=True, sharded=True):
+def oracle_step(oblk, x, G, cfg, b, s, tp=1, online=True, sharded=True, h_prev=None):
+    """h_prev (lax): {projection: Tensor/array [b, s, r]}; grads then hold dh_prev and the
+    returned cache's h_cur is in grads["h_cur"]."""
     T = b * s
     x2 = x.values.reshape(T, cfg.d)
     G2 = G.values.reshape(T, cfg.d)
-    y, cache = O.block_forward(oblk, x2, b, s, cfg.heads)
+    hp = None
+    if h_prev is not None:
+        hp = {n: np.asarray(getattr(v, "values", v)).reshape(T, cfg.r) for n, v in h_prev.items()}
+    y, cache = O.block_forward(oblk, x2, b, s, cfg.heads, h_prev=hp)
     grads = O.block_backward(oblk, cache, G2, b, s, cfg.heads)
-    ws = O.btp_forward_sharded(oblk, x2, b, s, cfg.heads, tp, online=online)[1] if sharded else None
+    if "h_cur" in cache:
+        grads["h_cur"] = cache["h_cur"]
+    ws = O.btp_forward_sharded(oblk, x2, b, s, cfg.heads, tp, online=online, h_prev=hp)[1] if sharded else None
     loss = float(np.sum(y * G2))
     return y, grads, ws, loss
