@@ -350,7 +350,9 @@ class BTPBlockExecutor(ExecutorBase):
         # bundle is replicated like z; set_h_prev() stages it per chunk ([T, k*r] like P).
         self.lax = pl.variant is Variant.LAX
         self.has_h_prev = False
+        self.h_prev: dict | None = None
         self.dh_prev: dict | None = None
+        self.dh_cur_in: dict | None = None  # lax models: dL/dh_cur from the next layer's merge
         self.online = pl.norm_mode is NormMode.ONLINE
         self.grouping = pl.grouping
         self.ckpt = pl.lowrank_ckpt
@@ -628,40 +630,62 @@ class BTPBlockExecutor(ExecutorBase):
         replicated on every rank) for the next forward; None = the first-layer boundary (a = z,
         bitwise the svd block, reference test_model.py:182-192)."""
         if h_prev is None:
-            self.has_h_prev = False
+            self.set_h_prev_device(None)
             return
-        if not self.lax:
-            raise PlanError(f"h_prev is a lax input; this block is {self.pl.variant.value}")
-        if self.peer is not None:
-            raise PlanError("lax with an h bundle runs on the NCCL boundaries (the peer kernels push a = z)")
         T, r = self.T, self.r
+        views = {}
         for names in self.CHUNKS:
             hp = self.buf(f"hp_{'_'.join(names)}", (T, len(names) * r))
             for i, n in enumerate(names):
                 v = h_prev[n]
                 v = torch.as_tensor(np.asarray(v).reshape(T, r)) if not isinstance(v, torch.Tensor) else v.reshape(T, r)
                 hp[:, i * r:(i + 1) * r].copy_(v.to(self.dev, self.act), non_blocking=True)
+                views[n] = hp[:, i * r:(i + 1) * r]
+        self.set_h_prev_device(views)
+
+    def set_h_prev_device(self, views) -> None:
+        """The bundle as device [T, r] views that stay valid through forward AND backward (a
+        multi-layer lax model passes the previous block's h_cur views: no copy)."""
+        if views is None:
+            self.h_prev = None
+            self.has_h_prev = False
+            return
+        if not self.lax:
+            raise PlanError(f"h_prev is a lax input; this block is {self.pl.variant.value}")
+        if self.peer is not None:
+            raise PlanError("lax with an h bundle runs on the NCCL boundaries (the peer kernels push a = z)")
+        self.h_prev = dict(views)
         self.has_h_prev = True
 
-    def _lax_merge(self, names, z_views, out_name):
-        """a = z + h_prev per projection into `out_name` [T, k*r] (btp_add; one launch when the z
-        views are the column blocks of one [T, k*r] buffer)."""
+    @staticmethod
+    def _blocks_of(views, T, r):
+        """[T, k*r] tensor whose column blocks are `views`, or None if they are not laid out so."""
+        v0, k = views[0], len(views)
+        if k == 1:
+            return v0
+        if v0.stride() != (k * r, 1) or any(v.data_ptr() != v0.data_ptr() + i * r * v0.element_size()
+                                             for i, v in enumerate(views)):
+            return None
+        return v0.as_strided((T, k * r), (k * r, 1))
+
+    def _lax_add(self, a_views, b_views, out_name, names):
+        """out[:, i*r:(i+1)*r] = a_i + b_i (btp_add; one launch when both sides are [T, k*r] blocks)."""
         T, r, k = self.T, self.r, len(names)
-        hp = self._buf[f"hp_{'_'.join(names)}"]
         out = self.buf(out_name, (T, k * r))
-        z0 = z_views[0]
-        base = z0 if k == 1 else None
-        if k > 1 and z0.stride(0) == k * r and all(z.data_ptr() == z0.data_ptr() + i * r * z0.element_size()
-                                                    for i, z in enumerate(z_views)):
-            base = z0.as_strided((T, k * r), (k * r, 1))
-        if base is not None:
-            K.add(base, hp, out)
+        A, B = self._blocks_of(a_views, T, r), self._blocks_of(b_views, T, r)
+        if A is not None and B is not None:
+            K.add(A, B, out)
             self.stats.kernel_launches += 1
         else:
-            for i, z in enumerate(z_views):
-                K.add(z, hp[:, i * r:(i + 1) * r], out[:, i * r:(i + 1) * r])
+            for i in range(k):
+                K.add(a_views[i], b_views[i], out[:, i * r:(i + 1) * r])
                 self.stats.kernel_launches += 1
-        return [out[:, i * r:(i + 1) * r] for i in range(k)]
+        return out
+
+    def _lax_merge(self, names, z_views, out_name):
+        """a = z + h_prev per projection into `out_name` [T, k*r]."""
+        out = self._lax_add(z_views, [self.h_prev[n] for n in names], out_name, names)
+        return [out[:, i * self.r:(i + 1) * self.r] for i in range(len(names))]
 
     def _a_input(self, names, z_views, a_views):
         """What the up-projection consumes; records the lax h_cur (= z, before the merge)."""
@@ -859,7 +883,7 @@ class BTPBlockExecutor(ExecutorBase):
 
     def _sigma_bwd(self, names, da_P, zP, s, dss_name):
         k, r, T = len(names), self.r, self.T
-        out = da_P
+        out = None
         if self.lax and self.has_h_prev:
             # dL/dh_prev = dL/da (the merge is an add): keep the reduced da, write dP beside it
             out = self.buf(f"dPlax_{'_'.join(names)}", tuple(da_P.shape))
@@ -867,6 +891,19 @@ class BTPBlockExecutor(ExecutorBase):
             if self.dh_prev is None:
                 self.dh_prev = {}
             self.dh_prev.update(zip(names, views))
+        if self.lax and self.dh_cur_in is not None:
+            # h_cur = z also feeds the next layer's merge: dz = da + dL/dh_cur
+            key = f"dzlax_{'_'.join(names)}"
+            if self.grouping or k == 1:
+                dz = self._lax_add(self._da_views(names, da_P), [self.dh_cur_in[n] for n in names], key, names)
+            else:
+                dz = self.buf(key, (k, T, r))
+                for i, n in enumerate(names):
+                    K.add(da_P[i], self.dh_cur_in[n], dz[i])
+                    self.stats.kernel_launches += 1
+            da_P = dz
+        if out is None:
+            out = da_P  # in place
         if self.grouping or k == 1:
             dss = self.buf(dss_name, (T,), F32) if s is not None else None
             K.fixup_sigma_bwd(zP, da_P, out, r=r, nproj=k, variant=self.var, s=s, d=self.d, dss=dss)

@@ -14,6 +14,10 @@ projection on every TP rank. Here, per rank:
             -> this rank's column slice of dy (the head is replicated, so no collective)
             -> L x BTPBlockExecutor.backward -> btp_embedding_bwd into the table-shard gradient
 
+lax models chain the rank-r bundle: block l's h_cur (its reduced z, a device view that stays
+resident) is block l+1's h_prev (zero bundle = none at l = 0, reference model.py:264-266); in
+backward block l+1's dL/dh_prev arrives at block l as dL/dh_cur and joins dz before its sigma-bwd.
+
 The block executors share this executor's communicator (one collective log) and launch
 counters; every kernel is a libbtp.so entry point.
 """
@@ -87,8 +91,12 @@ class ModelExecutor(ExecutorBase):
         x = self.buf("emb_out", (T, self.dl))
         K.embedding_fwd(ids, self.W["embedding"], x)
         self.stats.kernel_launches += 1
+        h = None
         for ex in self.blocks:
+            if ex.lax:
+                ex.set_h_prev_device(h)
             x = ex.forward(x)
+            h = ex.h_cur if ex.lax else None
         self.comm.pass_tag = "forward"
         return x
 
@@ -136,8 +144,12 @@ class ModelExecutor(ExecutorBase):
         K.reduce_rows(gparts[:nb].view(nb, 1, d), self.grad["gamma1"].view(1, d))
         self.stats.kernel_launches += 3
         dy_sh = dy[:, self.rank * self.dl:(self.rank + 1) * self.dl]            # replicated head: local slice
+        dh = None
         for ex in reversed(self.blocks):
+            if ex.lax:
+                ex.dh_cur_in = dh
             dy_sh = ex.backward(dy_sh)
+            dh = ex.dh_prev if ex.lax else None
         K.zero(self.grad["embedding"])
         K.embedding_bwd(self._ids, dy_sh, self.grad["embedding"])
         self.stats.kernel_launches += 2

@@ -16,14 +16,14 @@ pytestmark = pytest.mark.gpu
 L, V, B, S = 2, 256, 2, 64
 
 
-def _setup():
+def _setup(variant="cola", layers=L):
     from tests.gpu_util import SMALL
     from oracle import btp_oracle as O
     from paper_2512_12131_b200.model import ModelConfig, Variant, build_model, token_batch
 
-    cfg = ModelConfig(layers=L, heads=SMALL.heads, d=SMALL.d, d_ff=SMALL.d_ff, r=SMALL.r)
-    mw = build_model(cfg, Variant.COLA, 0, V)
-    om = O.build_model(cfg.d, cfg.d_ff, cfg.r, "cola", 0, V, L)
+    cfg = ModelConfig(layers=layers, heads=SMALL.heads, d=SMALL.d, d_ff=SMALL.d_ff, r=SMALL.r)
+    mw = build_model(cfg, Variant(variant), 0, V)
+    om = O.build_model(cfg.d, cfg.d_ff, cfg.r, variant, 0, V, layers)
     ids, tg = token_batch(B, S, V)
     loss, cache = O.model_forward(om, ids, tg, B, S, cfg.heads)
     g = O.model_backward(om, cache, B, S, cfg.heads)
@@ -39,7 +39,7 @@ def _check_grads(got, want, tp=1, rank=0, cfg=None):
     assert rel(got["dhead"], want["dhead"]) < BF16_TOL
     assert rel(got["dfinal_gamma"], want["dfinal_gamma"]) < BF16_TOL
     assert rel(got["dembedding"], want["dembedding"][:, sl]) < BF16_TOL
-    for l in range(L):
+    for l in range(len(want["blocks"])):
         gr = O.grads_for_rank(want["blocks"][l], tp, rank, cfg.d, cfg.d_ff)
         gb = got["blocks"][l]
         for n in O.PROJECTIONS:
@@ -64,6 +64,23 @@ def test_model_step_matches_oracle(grouping, ckpt):
     # collective log: every block's 4 (or 7) forward chunk boundaries, then the tail gather
     fwd = ex.comm.trace.record_tuples("forward")
     assert fwd[-1][0] == "final-gather" and len(fwd) == L * (4 if grouping else 7) + 1
+
+
+@pytest.mark.parametrize("grouping,ckpt", [(True, False), (False, False), (True, True)])
+def test_lax_model_chains_the_bundle(grouping, ckpt):
+    """lax model: block l's h_cur feeds block l+1's merge, and dL/dh_prev flows back into block
+    l's dz — every block's gradients against the oracle model (3 layers: two merges)."""
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.model_executor import model_train_step
+    from paper_2512_12131_b200.plan import Strategy, plan
+
+    cfg, mw, ids, tg, loss_ref, g_ref = _setup("lax", 3)
+    pl = plan(Strategy.BOTTLENECK, cfg, RunShape(B, S, 1), Variant.LAX, online_norm=True, grouping=grouping,
+              lowrank_ckpt=ckpt)
+    loss, ex = model_train_step(pl, mw, ids, tg)
+    assert abs(loss - loss_ref) / abs(loss_ref) < 2e-2
+    _check_grads(ex.model_grads(), g_ref, cfg=cfg)
+    assert not ex.blocks[0].has_h_prev and ex.blocks[1].has_h_prev and ex.blocks[2].has_h_prev
 
 
 def test_model_trainer_graph_replay_and_adamw():
@@ -92,7 +109,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, variant="cola", layers=L):
     try:
         import datetime
 
@@ -105,8 +122,8 @@ def _rank_main(rank, world, port, q):
         from paper_2512_12131_b200.model_executor import model_train_step
         from paper_2512_12131_b200.plan import Strategy, plan
 
-        cfg, mw, ids, tg, _, _ = _setup()
-        pl = plan(Strategy.BOTTLENECK, cfg, RunShape(B, S, world), Variant.COLA, online_norm=True, grouping=True)
+        cfg, mw, ids, tg, _, _ = _setup(variant, layers)
+        pl = plan(Strategy.BOTTLENECK, cfg, RunShape(B, S, world), Variant(variant), online_norm=True, grouping=True)
         loss, ex = model_train_step(pl, mw, ids, tg)
         q.put((rank, loss, ex.model_grads(), ex.comm.trace.record_tuples("forward"), None))
         dist.destroy_process_group()
@@ -116,12 +133,13 @@ def _rank_main(rank, world, port, q):
         q.put((rank, None, None, None, traceback.format_exc()))
 
 
-def test_model_tp2_matches_oracle():
-    cfg, _, _, _, loss_ref, g_ref = _setup()
+@pytest.mark.parametrize("variant,layers", [("cola", L), ("lax", 3)])
+def test_model_tp2_matches_oracle(variant, layers):
+    cfg, _, _, _, loss_ref, g_ref = _setup(variant, layers)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, variant, layers)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}

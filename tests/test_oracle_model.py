@@ -6,8 +6,14 @@ import numpy as np
 from oracle import btp_oracle as O
 
 
-def test_model_backward_matches_finite_differences():
-    m = O.build_model(16, 40, 4, "cola", 7, 24, 2)
+import pytest
+
+
+@pytest.mark.parametrize("variant,layers", [("cola", 2), ("lax", 3)])
+def test_model_backward_matches_finite_differences(variant, layers):
+    """lax: the h bundle chains the layers (h_cur of layer l is layer l+1's h_prev), so layer 0's
+    down factors also receive gradient through every later layer's merge."""
+    m = O.build_model(16, 40, 4, variant, 7, 24, layers)
     ids, tg = O.token_batch(2, 8, 24)
     loss, c = O.model_forward(m, ids, tg, 2, 8, 4)
     assert np.isfinite(loss) and 0 < loss < 10
