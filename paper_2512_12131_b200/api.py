@@ -148,12 +148,28 @@ def _stage_h_prev(ex, block: DecoderBlockWeights, h_prev) -> None:
     ex.set_h_prev(h_prev)
 
 
+def _bundle_host(ex, views: dict, b, s) -> dict:
+    """{projection: float64 [b, s, r]} from device views: replicated under BTP (read this rank's),
+    r-sliced per rank under naive TP (gathered; lax slices are contiguous, simulator.py:440-447)."""
+    out = {}
+    for n, h in views.items():
+        if not getattr(ex, "residual_sharded", True) and ex.tp > 1:
+            if ex.comm.live:
+                parts = [torch.empty_like(h.contiguous()) for _ in range(ex.tp)]
+                dist.all_gather(parts, h.contiguous())
+                h = torch.cat(parts, dim=1)
+            else:
+                h = h.repeat(1, ex.tp)
+        out[n] = h.double().cpu().numpy().reshape(b, s, -1)
+    return out
+
+
 def _h_cur(ex, b, s, eb=2):
-    """The lax bundle {projection: Tensor [b, s, r]} (replicated: read from this rank), else None."""
+    """The lax bundle {projection: Tensor [b, s, r]} for the next layer, else None."""
     if not getattr(ex, "lax", False):
         return None
     torch.cuda.synchronize(ex.dev)
-    return {n: Tensor(h.double().cpu().numpy().reshape(b, s, -1), eb) for n, h in ex.h_cur.items()}
+    return {n: Tensor(v, eb) for n, v in _bundle_host(ex, ex.h_cur, b, s).items()}
 
 
 def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: float = EPS_DEFAULT,
@@ -181,7 +197,7 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
     dx = ex.backward(g_sh)
     y = _gather_y(ex, y_sh, False)
     dh = getattr(ex, "dh_prev", None)
-    dh_host = None if dh is None else {n: t.double().cpu().numpy().reshape(b, s, -1) for n, t in dh.items()}
+    dh_host = None if dh is None else _bundle_host(ex, dh, b, s)
     return StepResult(
         y=Tensor(y.double().cpu().numpy().reshape(b, s, d)),
         loss=loss,

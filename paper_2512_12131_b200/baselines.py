@@ -24,7 +24,7 @@ from .executor import BF16, F32, ExecutorBase
 from .model import DecoderBlockWeights, Variant
 from .plan import PlanError, ShardPlan, Strategy, cola_pair_indices, col_shard_bounds
 
-_VAR = {Variant.SVD: 0, Variant.COLA: 1}
+_VAR = {Variant.SVD: 0, Variant.COLA: 1, Variant.LAX: 0}
 
 
 class _ReplicatedNormMixin:
@@ -56,10 +56,15 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         if pl.strategy is not Strategy.VANILLA:
             raise PlanError(f"VanillaExecutor needs a vanilla plan, got {pl.strategy.value}")
         if block.variant is not pl.variant or pl.variant not in _VAR:
-            raise PlanError(f"vanilla device path supports svd/cola blocks matching the plan")
+            raise PlanError(f"vanilla device path supports svd/cola/lax blocks matching the plan")
         self._setup(pl, comm, device, eps, precision)
         cfg = self.cfg
         self.var = _VAR[pl.variant]
+        # lax (simulator.py:440-447): each rank merges its r-slice of the bundle into its z shard
+        self.lax = pl.variant is Variant.LAX
+        self.has_h_prev = False
+        self.h_cur: dict = {}
+        self.dh_prev: dict | None = None
         self.grouping = pl.grouping
         self.r, self.d, self.d_ff = cfg.r, cfg.d, cfg.d_ff
         self.rl = cfg.r // self.tp
@@ -70,6 +75,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
             idx = cola_pair_indices(cfg.r, self.tp, self.rank)
         else:
             idx = np.arange(*col_shard_bounds(cfg.r, self.tp, self.rank))
+        self._r_idx = idx
         B = {n: t.values[idx, :] for n, t in block.down_factors.items()}     # [r/tp, d_in]
         A = {n: t.values[:, idx] for n, t in block.up_factors.items()}       # [d_out, r/tp]
         self.W = {
@@ -91,6 +97,28 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.grad["gamma2"] = torch.zeros(cfg.d, device=self.dev, dtype=F32)
         self._flatten_params()
 
+    # ------------------------------------------------------------------ lax bundle
+    _CHUNK_NAMES = {"qkv": ("q", "k", "v"), "gate_up": ("gate", "up"), "o": ("o",), "down": ("down",),
+                    "q": ("q",), "k": ("k",), "v": ("v",), "gate": ("gate",), "up": ("up",)}
+
+    def set_h_prev(self, h_prev) -> None:
+        """The logical bundle {projection: [T, r]} (replicated); each rank keeps its r-slice per
+        chunk id, so the merge is one btp_add per chunk."""
+        if h_prev is None:
+            self.has_h_prev = False
+            return
+        if not self.lax:
+            raise PlanError(f"h_prev is a lax input; this block is {self.pl.variant.value}")
+        T, rl = self.T, self.rl
+        idx = torch.as_tensor(self._r_idx)
+        for cid, names in self._CHUNK_NAMES.items():
+            hp = self.buf(f"hp_{cid}", (T, len(names) * rl))
+            for i, n in enumerate(names):
+                v = h_prev[n]
+                v = torch.as_tensor(np.asarray(v).reshape(T, -1)) if not isinstance(v, torch.Tensor) else v.reshape(T, -1)
+                hp[:, i * rl:(i + 1) * rl].copy_(v[:, idx].to(self.dev, self.act))
+        self.has_h_prev = True
+
     # ------------------------------------------------------------------ one vanilla chunk group
     def _pair(self, names, inp, Wd, Wu, out_full, chunk_id):
         """down (col-parallel over r) -> local sigma -> up (row-parallel over r) -> AR of the
@@ -102,8 +130,15 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
             a = self.buf(f"a_{chunk_id}", (T, k * rl))
             K.fixup_sigma(z, r=rl, nproj=k, variant=1, z_out=z, a_out=a)
             self.stats.kernel_launches += 1
+        elif self.lax and self.has_h_prev:
+            a = self.buf(f"alax_{chunk_id}", (T, k * rl))
+            K.add(z, self._buf[f"hp_{chunk_id}"], a)
+            self.stats.kernel_launches += 1
         else:
             a = z
+        if self.lax:  # h_cur = z: this rank's r-slice (the API gathers the full bundle)
+            for i, n in enumerate(names):
+                self.h_cur[n] = z[:, i * rl:(i + 1) * rl]
         widths = [w.shape[0] for w in Wu]
         offs = np.cumsum([0] + widths)
         probs = [K.Gemm(a[:, i * rl:(i + 1) * rl], Wu[i], out_full[:, offs[i]:offs[i + 1]]) for i in range(k)]
@@ -134,6 +169,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         T, d, f = self.T, self.d, self.d_ff
         self.comm.pass_tag = "forward"
+        self.h_cur = {}
         W = self.W
         n1, s1 = self._rnorm(x, self.gamma1, 1)
         (q, k, v), z_qkv, a_qkv = self._pairs(("q", "k", "v"), n1, W["d_qkv"], W["u_qkv"], "qkv", [d, d, d])
@@ -178,6 +214,11 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
                     K.fixup_sigma_bwd(zs[i], dz[:, i * rl:(i + 1) * rl], dz[:, i * rl:(i + 1) * rl], r=rl, nproj=1,
                                       variant=1)
             self.stats.kernel_launches += 1
+        if self.lax and self.has_h_prev:  # the merge is an add: dL/dh_prev slice = dz (rank-local)
+            if self.dh_prev is None:
+                self.dh_prev = {}
+            for i, n in enumerate(names):
+                self.dh_prev[n] = dz[:, i * rl:(i + 1) * rl]
         self._wgrad([(dz, inp, G[gkey_d])])
         self._gemm(K.Gemm(dz, Wd_all, din_full, b_mn=True))
         self.comm.all_reduce(din_full, chunk_ids[0])
@@ -185,6 +226,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
         S, W, T, d, f = self.saved, self.W, self.T, self.d, self.d_ff
         self.comm.pass_tag = "backward"
+        self.dh_prev = None
         dact = self.buf("dact", (T, f))
         self._pair_bwd(("down",), [dy], S["z_d"], S["a_d"], W["d_d"], [W["u_d"]], S["act"], "d_d", "u_d", dact,
                        ["down"])

@@ -122,7 +122,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, online, grouping, q):
+def _rank_main(rank, world, port, online, grouping, q, strategy="btp"):
     try:
         import datetime
 
@@ -134,7 +134,7 @@ def _rank_main(rank, world, port, online, grouping, q):
         b, s = 2, 64
         blk, x, G, _ = inputs(SMALL, Variant.LAX, b, s)
         hp = seeded_h_prev(SMALL, RunShape(b, s, world), 5)
-        pl = plan(Strategy.BOTTLENECK, SMALL, RunShape(b, s, world), Variant.LAX, online_norm=online,
+        pl = plan(Strategy(strategy), SMALL, RunShape(b, s, world), Variant.LAX, online_norm=online,
                   grouping=grouping)
         st = train_step(pl, blk, x, G, h_prev=hp)
         q.put((rank, dict(y=st.y.values, loss=st.loss, dx=st.dx, grads=st.grads,
@@ -147,12 +147,11 @@ def _rank_main(rank, world, port, online, grouping, q):
         q.put((rank, None, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("online,grouping", [(True, True), (False, False)])
-def test_lax_tp2_matches_oracle(online, grouping):
+def _spawn_tp2(online, grouping, strategy):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, online, grouping, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, online, grouping, q, strategy)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -166,6 +165,12 @@ def test_lax_tp2_matches_oracle(online, grouping):
             p.join(timeout=60 if len(res) == 2 else 1)
             if p.is_alive():
                 p.kill()
+    return res
+
+
+@pytest.mark.parametrize("online,grouping", [(True, True), (False, False)])
+def test_lax_tp2_matches_oracle(online, grouping):
+    res = _spawn_tp2(online, grouping, "btp")
     b, s = 2, 64
     blk, x, G, oblk = inputs(SMALL, Variant.LAX, b, s)
     hp = seeded_h_prev(SMALL, RunShape(b, s, 2), 5)
@@ -185,3 +190,43 @@ def test_lax_tp2_matches_oracle(online, grouping):
         bad = {k: v for k, v in errs.items() if v > BF16_TOL}
         assert not bad, (rank, bad)
         assert o["fwd"] == pred
+
+
+# ---------------------------------------------------------------- naive-TP baseline with lax
+def _vanilla_check(o, g_ref, y_ref, loss_ref, tp, rank):
+    from paper_2512_12131_b200.plan import col_shard_bounds
+
+    lo, hi = col_shard_bounds(SMALL.r, tp, rank)
+    assert rel(o["y"].reshape(-1, SMALL.d), y_ref) < BF16_TOL
+    assert abs(o["loss"] - loss_ref) / abs(loss_ref) < BF16_TOL
+    errs = {"dx": rel(o["dx"], g_ref["dx"])}   # replicated residual: full dx on every rank
+    for n in O.PROJECTIONS:
+        errs[f"A_{n}"] = rel(o["grads"]["A"][n], g_ref["A"][n][:, lo:hi])
+        errs[f"B_{n}"] = rel(o["grads"]["B"][n], g_ref["B"][n][lo:hi, :])
+        errs[f"h_{n}"] = rel(o["h_cur"][n], g_ref["h_cur"][n])       # gathered over the r-slices
+        errs[f"dh_{n}"] = rel(o["dh_prev"][n], g_ref["dh_prev"][n])
+    bad = {k: v for k, v in errs.items() if v > BF16_TOL}
+    assert not bad, (rank, bad)
+
+
+@pytest.mark.parametrize("grouping", [True, False])
+def test_lax_vanilla_tp1(grouping):
+    b, s = 2, 64
+    blk, x, G, oblk = inputs(SMALL, Variant.LAX, b, s)
+    hp = seeded_h_prev(SMALL, RunShape(b, s, 1), 5)
+    pl = plan(Strategy.VANILLA, SMALL, RunShape(b, s, 1), Variant.LAX, online_norm=False, grouping=grouping)
+    st = train_step(pl, blk, x, G, h_prev=hp)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, sharded=False, h_prev=hp)
+    o = dict(y=st.y.values, loss=st.loss, dx=st.dx, grads=st.grads, dh_prev=st.dh_prev,
+             h_cur={n: t.values for n, t in st.h_cur.items()})
+    _vanilla_check(o, g_ref, y_ref, loss_ref, 1, 0)
+
+
+def test_lax_vanilla_tp2():
+    res = _spawn_tp2(False, True, "vanilla")
+    b, s = 2, 64
+    blk, x, G, oblk = inputs(SMALL, Variant.LAX, b, s)
+    hp = seeded_h_prev(SMALL, RunShape(b, s, 2), 5)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, SMALL, b, s, sharded=False, h_prev=hp)
+    for rank, o in res.items():
+        _vanilla_check(o, g_ref, y_ref, loss_ref, 2, rank)
