@@ -239,7 +239,7 @@ def run_ours(args, cfg):
         comm = TPComm.emulated(tp, 0)
     shape = RunShape(b, s, tp)
     strategy = Strategy(args.strategy)
-    variant = Variant.FULL_RANK if strategy is Strategy.FULL_RANK else Variant.COLA
+    variant = Variant.FULL_RANK if strategy is Strategy.FULL_RANK else Variant(args.variant)
     pl = plan(strategy, cfg, shape, None if variant is Variant.FULL_RANK else variant,
               online_norm=strategy is Strategy.BOTTLENECK, grouping=not args.no_grouping,
               lowrank_ckpt=args.ckpt)
@@ -260,6 +260,10 @@ def run_ours(args, cfg):
         G = seeded_fill((b, s, cfg.d), 30000).values
         trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
                                optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary)
+        if variant is Variant.LAX:  # a resident previous-layer bundle, like G (the merge runs every step)
+            from paper_2512_12131_b200.model import seeded_h_prev
+
+            trainer.ex.set_h_prev({n: h.values for n, h in seeded_h_prev(cfg, shape, 20000).items()})
     x_dev, g_dev = trainer.device_inputs(x, G)
 
     def barrier():
@@ -336,7 +340,9 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform inputs, fan-in-scaled random init)",
         "config": {"workload": (f"CoLA-{args.config} model ({len(trainer.ex.blocks)} blocks + d-sharded embedding + "
                                 f"replicated LM head V={args.vocab} + cross-entropy) " if args.model else
-                                f"CoLA-{args.config} decoder block ") + f"fwd+bwd{'' if args.no_optimizer else '+AdamW'}, "
+                                f"CoLA-{args.config} decoder block ")
+                               + (f"[{variant.value} variant] " if variant not in (Variant.COLA, Variant.FULL_RANK)
+                                  else "") + f"fwd+bwd{'' if args.no_optimizer else '+AdamW'}, "
                                f"{strategy.value} "
                                f"{'grouped ' if pl.grouping else ''}{'online-RMSNorm ' if pl.norm_mode.value == 'online' else ''}"
                                f"TP={tp}{' lowrank-ckpt' if pl.lowrank_ckpt else ''}",
@@ -380,6 +386,8 @@ def main(argv=None):
     ap.add_argument("--b", type=int, default=4)
     ap.add_argument("--s", type=int, default=4096)
     ap.add_argument("--strategy", default="btp", choices=["btp", "vanilla", "full-rank"])
+    ap.add_argument("--variant", default="cola", choices=["cola", "svd", "lax"],
+                    help="low-rank block variant (lax: merges a resident seeded h bundle every step)")
     ap.add_argument("--ckpt", action="store_true")
     ap.add_argument("--no-grouping", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
