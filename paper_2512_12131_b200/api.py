@@ -260,35 +260,49 @@ class BlockTrainer:
         xs, gs = shard_input(self.ex, np.asarray(x)).cpu(), shard_input(self.ex, np.asarray(G)).cpu()
         return xs.pin_memory(), gs.pin_memory()
 
-    def _eager(self, x, g):
-        y = self.ex.forward(x)
-        self.loss_buf = self.ex.loss_device(y, g)
+    def _fwd(self, x):
+        self._y = self.ex.forward(x)
+
+    def _tail(self, g):
+        self.loss_buf = self.ex.loss_device(self._y, g)
         self.ex.backward(g)
         if self.adamw is not None:
             self.ex.optimizer_step(**self.adamw)
 
-    def step_device(self, x: torch.Tensor, g: torch.Tensor) -> None:
+    def _eager(self, x, g, g_ready=None):
+        self._fwd(x)
+        if g_ready is not None:
+            torch.cuda.current_stream().wait_event(g_ready)
+        self._tail(g)
+
+    def step_device(self, x: torch.Tensor, g: torch.Tensor, g_ready=None) -> None:
+        """One step on device-resident inputs. g_ready (optional CUDA event): the forward only
+        needs x, so the loss-side input g may still be in flight — the stream waits for it between
+        the forward and the loss (fit() uses this to hide its one-time G copy behind step 0)."""
         if not self.use_graph:
-            self._eager(x, g)
+            self._eager(x, g, g_ready)
             return
         key = (x.data_ptr(), g.data_ptr())
-        graph = self.graphs.get(key)
-        if graph is None:
-            # the first step runs eagerly (allocating every buffer); one step is then captured into
-            # a graph (capture executes nothing) that later calls replay
+        graphs = self.graphs.get(key)
+        if graphs is None:
+            # the first step runs eagerly (allocating every buffer); the step is then captured as
+            # two graphs — forward, and loss + backward + update (sharing one memory pool) — that
+            # later calls replay back to back
             before = self.ex.stats.kernel_launches
-            self._eager(x, g)
+            self._eager(x, g, g_ready)
             self._per_step_launches = self.ex.stats.kernel_launches - before
             torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
+            g_fwd, g_tail = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             saved = self.ex.stats.kernel_launches
             n_rec = len(self.ex.comm.trace.records)
             try:
                 with torch.cuda.stream(side):
-                    with torch.cuda.graph(graph, stream=side):
-                        self._eager(x, g)
+                    with torch.cuda.graph(g_fwd, stream=side):
+                        self._fwd(x)
+                    with torch.cuda.graph(g_tail, stream=side, pool=g_fwd.pool()):
+                        self._tail(g)
             except Exception as exc:  # capture refused (e.g. a backend without graph support): stay eager
                 import warnings
 
@@ -300,9 +314,13 @@ class BlockTrainer:
                 self.ex.stats.kernel_launches = saved
                 del self.ex.comm.trace.records[n_rec:]  # a capture issues no collectives
             torch.cuda.current_stream().wait_stream(side)
-            self.graphs[key], self.graphed = graph, True
+            self.graphs[key], self.graphed = (g_fwd, g_tail), True
             return
-        graph.replay()
+        g_fwd, g_tail = graphs
+        g_fwd.replay()
+        if g_ready is not None:
+            torch.cuda.current_stream().wait_event(g_ready)
+        g_tail.replay()
         self._replays += 1
 
     def fit(self, x_hosts, G_host: torch.Tensor) -> list[float]:
@@ -318,13 +336,16 @@ class BlockTrainer:
             self._target = torch.empty(G_host.shape, dtype=G_host.dtype, device=dev)
             self._copy_stream = torch.cuda.Stream(device=dev)
         main, copy = torch.cuda.current_stream(), self._copy_stream
-        self._target.copy_(G_host, non_blocking=True)
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        g_copied = torch.cuda.Event()
         copy.wait_stream(main)
         with torch.cuda.stream(copy):
             self._slots[0].copy_(x_hosts[0], non_blocking=True)
             copied[0].record(copy)
+            # G (the loss projection) is needed only after step 0's forward: its copy runs under it
+            self._target.copy_(G_host, non_blocking=True)
+            g_copied.record(copy)
         if getattr(self, "_loss_host", None) is None:
             self._loss_host = torch.zeros(2, dtype=torch.float32).pin_memory()
         read = [torch.cuda.Event(), torch.cuda.Event()]
@@ -339,7 +360,7 @@ class BlockTrainer:
                 with torch.cuda.stream(copy):
                     self._slots[ns].copy_(x_hosts[i + 1], non_blocking=True)
                     copied[ns].record(copy)
-            self.step_device(self._slots[s], self._target)
+            self.step_device(self._slots[s], self._target, g_ready=g_copied if i == 0 else None)
             consumed[s].record(main)
             self._loss_host[s:s + 1].copy_(self.loss_buf.view(1), non_blocking=True)  # D2H, this step
             read[s].record(main)
