@@ -739,13 +739,15 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
     d.m_tiles = (q.M + tile_m - 1) / tile_m;
     d.n_tiles = (q.N + BN - 1) / BN;
     d.k_blocks = (q.K + kBK - 1) / kBK;
-    d.splits = q.splits;
     d.kb_per_split = (d.k_blocks + q.splits - 1) / q.splits;
+    // splits that would start past the last k-block (e.g. 64 k-blocks in 9 splits of 8) are
+    // dropped: an empty split's tile would reduce-add an accumulator no MMA ever wrote
+    d.splits = (d.k_blocks + d.kb_per_split - 1) / d.kb_per_split;
     d.out_fp32 = sc != nullptr ? 1 : q.c_fp32;  // scatter: fp32 chunks reduce-added into the owners
     d.reduce_add = q.reduce_add;
     d.alpha = q.alpha == 0.0f ? 1.0f : q.alpha;
     d.tile_start = tiles;
-    tiles += d.m_tiles * d.n_tiles * q.splits;
+    tiles += d.m_tiles * d.n_tiles * d.splits;
   }
   P.num_problems = n;
   P.total_tiles = tiles;

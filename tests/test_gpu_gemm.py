@@ -47,8 +47,10 @@ def test_scales_fp32_out_and_residual():
     assert rel(Cb, 2 * (A.float() @ B.float().t()) + R.float()) < TOL
 
 
-@pytest.mark.parametrize("splits", [2, 4, 9])
+@pytest.mark.parametrize("splits", [2, 4, 9, 13, 64])
 def test_split_k_reduce_add(splits):
+    """K = 4096 = 64 k-blocks: 9 splits of 8 (and 13 of 5) leave trailing splits empty — they are
+    dropped, not reduce-added as an unwritten accumulator."""
     dY, X = _mk(4096, 512), _mk(4096, 2048)
     dW = torch.empty(512, 2048, device="cuda")
     K.zero(dW)
