@@ -23,6 +23,17 @@ for r in rows[h + 1:]:
     agg[n][0] += 1
     agg[n][1] += v
     seq.append((n, v))
+if "--period" in sys.argv:
+    # exactly one step: the launches between two consecutive occurrences of an anchor kernel that
+    # runs once per step (a step is periodic, so any such window is one whole step)
+    anchor = sys.argv[sys.argv.index("--period") + 1]
+    idx = [i for i, (n, _) in enumerate(seq) if anchor in n]
+    seq = seq[idx[0]:idx[1]]
+    steps = 1.0
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for n, v in seq:
+        agg[n][0] += 1
+        agg[n][1] += v
 tot = sum(v for _, v in agg.values())
 print(f"total {tot / 1e3 / steps:.1f} us/step over {len(seq)} launches ({steps} steps)")
 for n, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
