@@ -190,3 +190,26 @@ def test_concurrent_wgrad_stream_matches_serial(monkeypatch):
     for fam in ("A", "B"):
         for n, g in ser.grads[fam].items():
             assert rel(con.grads[fam][n], g) < 1e-4, (fam, n)
+
+
+@pytest.mark.parametrize("preset_name,b,s", [("1b", 1, 256), ("7b", 1, 256)])
+def test_paper_width_blocks_vs_oracle(preset_name, b, s):
+    """The paper's CoLA-1B / CoLA-7B block widths (d 2048/4096, d_ff 5472/11008, r 512/1024: the
+    sigma epilogue with r/2 = 256/512, BN choices, the d_ff tail tile of 5472 = 21.4 x 256) at a
+    short sequence, fwd + bwd against the float64 oracle."""
+    from paper_2512_12131_b200.model import preset
+
+    cfg = preset(preset_name)
+    blk, x, G, oblk = inputs(cfg, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    st = train_step(pl, blk, x, G)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, cfg, b, s, sharded=False)
+    assert rel(st.y.values.reshape(-1, cfg.d), y_ref) < BF16_TOL
+    assert abs(st.loss - loss_ref) / abs(loss_ref) < BF16_TOL
+    assert rel(st.dx, g_ref["dx"]) < BF16_TOL
+    errs = {f"A_{n}": rel(st.grads["A"][n], g_ref["A"][n]) for n in O.PROJECTIONS}
+    errs.update({f"B_{n}": rel(st.grads["B"][n], g_ref["B"][n]) for n in O.PROJECTIONS})
+    errs["gamma1"] = rel(st.grads["gamma1"], g_ref["dgamma1"])
+    errs["gamma2"] = rel(st.grads["gamma2"], g_ref["dgamma2"])
+    bad = {k: v for k, v in errs.items() if v > BF16_TOL}
+    assert not bad, bad
