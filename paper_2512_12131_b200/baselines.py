@@ -62,6 +62,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.var = _VAR[pl.variant]
         # lax (simulator.py:440-447): each rank merges its r-slice of the bundle into its z shard
         self.lax = pl.variant is Variant.LAX
+        self.ckpt = pl.lowrank_ckpt
         self.has_h_prev = False
         self.h_cur: dict = {}
         self.dh_prev: dict | None = None
@@ -126,6 +127,11 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         T, rl, k = self.T, self.rl, len(names)
         z = self.buf(f"z_{chunk_id}", (T, k * rl))
         self._gemm(K.Gemm(inp, Wd, z))
+        return z, self._pair_up(names, z, Wu, out_full, chunk_id)
+
+    def _pair_up(self, names, z, Wu, out_full, chunk_id):
+        """The chunk from its stored z on (also the checkpoint re-forward: it replays the AR)."""
+        T, rl, k = self.T, self.rl, len(names)
         if self.var == 1:
             a = self.buf(f"a_{chunk_id}", (T, k * rl))
             K.fixup_sigma(z, r=rl, nproj=k, variant=1, z_out=z, a_out=a)
@@ -147,20 +153,29 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
             self.comm.all_reduce(out_full, chunk_id)
         else:
             raise AssertionError("ungrouped path handled by caller")
-        return z, a
+        return a
 
-    def _pairs(self, names, inp, Wd_all, Wu_list, chunk_grouped, widths):
-        """Grouped: one chunk. Ungrouped: one chunk per projection (separate buffers + ARs)."""
+    def _pairs(self, names, inp, Wd_all, Wu_list, chunk_grouped, widths, z_stored=None):
+        """Grouped: one chunk. Ungrouped: one chunk per projection (separate buffers + ARs).
+        z_stored (checkpoint re-forward): skip the down GEMMs, start from the kept z's."""
         T, rl = self.T, self.rl
         if self.grouping:
             full = self.buf(f"F_{chunk_grouped}", (T, sum(widths)))
-            z, a = self._pair(names, inp, Wd_all, Wu_list, full, chunk_grouped)
+            if z_stored is None:
+                z, a = self._pair(names, inp, Wd_all, Wu_list, full, chunk_grouped)
+            else:
+                z = z_stored[0]
+                a = self._pair_up(names, z, Wu_list, full, chunk_grouped)
             offs = np.cumsum([0] + widths)
             return [full[:, offs[i]:offs[i + 1]] for i in range(len(names))], [z], [a]
         outs, zs, as_ = [], [], []
         for i, n in enumerate(names):
             full = self.buf(f"F_{n}", (T, widths[i]))
-            z, a = self._pair((n,), inp, Wd_all[i * rl:(i + 1) * rl], [Wu_list[i]], full, n)
+            if z_stored is None:
+                z, a = self._pair((n,), inp, Wd_all[i * rl:(i + 1) * rl], [Wu_list[i]], full, n)
+            else:
+                z = z_stored[i]
+                a = self._pair_up((n,), z, [Wu_list[i]], full, n)
             outs.append(full)
             zs.append(z)
             as_.append(a)
@@ -186,10 +201,54 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         y = self.buf("y", (T, d))
         K.add(x_mid, mlp, y)
         self.stats.kernel_launches += 2
-        self.saved = dict(x=x, n1=n1, s1=s1, z_qkv=z_qkv, a_qkv=a_qkv, q=q, k=k, v=v, attn=attn, actx=actx, z_o=[z_o],
-                          a_o=[a_o], x_mid=x_mid, n2=n2, s2=s2, z_gu=z_gu, a_gu=a_gu, g=g, u=u, act=act, z_d=[z_d],
-                          a_d=[a_d])
+        if self.ckpt:
+            # low-rank boundary checkpoint (reference checkpointing.py): keep x and the rank-local
+            # z shards; backward re-forwards the rest, replaying the chunk all-reduces
+            self.saved = dict(x=x, z_qkv=z_qkv, z_o=[z_o], z_gu=z_gu, z_d=[z_d])
+        else:
+            self.saved = dict(x=x, n1=n1, s1=s1, z_qkv=z_qkv, a_qkv=a_qkv, q=q, k=k, v=v, attn=attn, actx=actx,
+                              z_o=[z_o], a_o=[a_o], x_mid=x_mid, n2=n2, s2=s2, z_gu=z_gu, a_gu=a_gu, g=g, u=u,
+                              act=act, z_d=[z_d], a_d=[a_d])
         return y
+
+    # names the checkpoint re-forward rebuilds (compared bitwise with the plain forward's)
+    RECOMPUTED = ("n1", "q", "k", "v", "attn", "x_mid", "n2", "g", "u", "act", "a_qkv", "a_o", "a_gu", "a_d")
+
+    def _reforward(self) -> None:
+        """Everything backward needs, from x and the kept z shards: norms and sigma are local, but
+        each up-projection output is a row-parallel PARTIAL over r, so its all-reduce is replayed
+        (qkv, o, gate_up; the down chunk's output feeds nothing backward needs)."""
+        S, W, T, d, f = self.saved, self.W, self.T, self.d, self.d_ff
+        self.comm.pass_tag = "reforward"
+        x = S["x"]
+        n1, s1 = self._rnorm(x, self.gamma1, 1)
+        (q, k, v), _, a_qkv = self._pairs(("q", "k", "v"), None, None, W["u_qkv"], "qkv", [d, d, d],
+                                          z_stored=S["z_qkv"])
+        attn, actx = self.attn.forward(q, k, v)
+        o_full = self.buf("F_o", (T, d))
+        a_o = self._pair_up(("o",), S["z_o"][0], [W["u_o"]], o_full, "o")
+        x_mid = self.buf("x_mid", (T, d))
+        n2, s2 = self._rnorm(x, self.gamma2, 2, branch=o_full, x_out=x_mid)
+        (g, u), _, a_gu = self._pairs(("gate", "up"), None, None, W["u_gu"], "gate_up", [f, f], z_stored=S["z_gu"])
+        act = self.buf("act", (T, f))
+        K.swiglu(g, u, act)
+        self.stats.kernel_launches += 1
+        a_d = self._sigma_local(("down",), S["z_d"][0], "down")
+        S.update(n1=n1, s1=s1, a_qkv=a_qkv, q=q, k=k, v=v, attn=attn, actx=actx, a_o=[a_o], x_mid=x_mid, n2=n2,
+                 s2=s2, a_gu=a_gu, g=g, u=u, act=act, a_d=[a_d])
+
+    def _sigma_local(self, names, z, chunk_id):
+        T, rl, k = self.T, self.rl, len(names)
+        if self.var == 1:
+            a = self.buf(f"a_{chunk_id}", (T, k * rl))
+            K.fixup_sigma(z, r=rl, nproj=k, variant=1, z_out=z, a_out=a)
+        elif self.lax and self.has_h_prev:
+            a = self.buf(f"alax_{chunk_id}", (T, k * rl))
+            K.add(z, self._buf[f"hp_{chunk_id}"], a)
+        else:
+            return z
+        self.stats.kernel_launches += 1
+        return a
 
     # ------------------------------------------------------------------ backward
     def _pair_bwd(self, names, dout_list, zs, as_, Wd_all, Wu_list, inp, gkey_d, gkey_u, din_full, chunk_ids):
@@ -224,6 +283,10 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.comm.all_reduce(din_full, chunk_ids[0])
 
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
+        if not self.saved:
+            raise RuntimeError("backward called before forward")
+        if self.ckpt:
+            self._reforward()
         S, W, T, d, f = self.saved, self.W, self.T, self.d, self.d_ff
         self.comm.pass_tag = "backward"
         self.dh_prev = None

@@ -318,6 +318,19 @@ class ExecutorBase:
     def loss(self, y: torch.Tensor, G: torch.Tensor) -> float:
         return float(self.loss_device(y, G).item())
 
+    def saved_activation_elements(self) -> int:
+        """Elements of activations held between forward and backward (distinct storages)."""
+        seen, total = set(), 0
+        for v in self.saved.values():
+            ts = v if isinstance(v, (list, tuple)) else [v]
+            for t in ts:
+                if isinstance(t, torch.Tensor):
+                    key = t.untyped_storage().data_ptr()
+                    if key not in seen:
+                        seen.add(key)
+                        total += t.untyped_storage().nbytes() // t.element_size()
+        return total
+
     def saved_activation_bytes(self) -> int:
         """Bytes of activations held between forward and backward (distinct storages)."""
         seen, total = set(), 0
