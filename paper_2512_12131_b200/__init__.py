@@ -29,7 +29,9 @@ from .model import (
 )
 from .plan import NormMode, PlanError, ShardPlan, Strategy, apply_grouping, describe, enumerate_collectives, plan
 from .trace import CollectiveRecord, Trace, ring_transfer_elements, trace_volume
-from .api import BlockTrainer, ModelTrainer, SimResult, StepResult, execute_forward, make_executor, train_step
+from .api import (BlockTrainer, ModelTrainer, SimResult, StepResult, execute_forward, make_executor,
+                  reference_forward, train_step)
+from .tensor_ops import batched_matmul, matmul, swiglu
 from .checkpointing import CkptPolicy, CkptReport, eff_ckpt, run_with_ckpt
 
 __all__ = [
@@ -40,7 +42,7 @@ __all__ = [
     "Strategy", "NormMode", "ShardPlan", "PlanError", "plan", "apply_grouping", "describe",
     "enumerate_collectives",
     "CollectiveRecord", "Trace", "trace_volume", "ring_transfer_elements",
-    "execute_forward", "train_step", "make_executor", "BlockTrainer", "ModelTrainer", "SimResult", "StepResult",
+    "execute_forward", "reference_forward", "matmul", "batched_matmul", "swiglu", "train_step", "make_executor", "BlockTrainer", "ModelTrainer", "SimResult", "StepResult",
     "CkptPolicy", "CkptReport", "eff_ckpt", "run_with_ckpt",
 ]
 

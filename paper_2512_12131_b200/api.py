@@ -22,7 +22,7 @@ from . import kernels as K
 from .comm import TPComm
 from .executor import BTPBlockExecutor
 from .model import EPS_DEFAULT, DecoderBlockWeights, Variant
-from .plan import PlanError, ShardPlan, Strategy
+from .plan import PlanError, ShardPlan, Strategy, plan
 from .tensor import Tensor
 from .trace import Trace
 
@@ -138,6 +138,28 @@ def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *
     y_host = y.double().cpu().numpy().reshape(b, s, d)
     eb = x.element_bytes if isinstance(x, Tensor) else 2
     return SimResult(Tensor(y_host, eb), _h_cur(ex, b, s, eb), ex.comm.trace, ws, pl)
+
+
+def reference_forward(block: DecoderBlockWeights, x, h_prev=None, eps: float = EPS_DEFAULT, *,
+                      precision: str = "fp32"):
+    """Single-device forward of one block (reference model.py:256-305) on the GPU: a TP = 1 plan of
+    the block's own variant (BTP for low-rank blocks, Megatron for full-rank; at one rank both
+    are the plain block). Returns (y Tensor [b, s, d], h_cur bundle for lax else None).
+    precision="fp32" (default) keeps it within the north_star 1e-4 of the float64 reference."""
+    from .model import RunShape
+
+    xv = x.values if isinstance(x, Tensor) else np.asarray(x)
+    if xv.ndim != 3 or xv.shape[2] != block.cfg.d:
+        from .tensor import DimensionError
+
+        raise DimensionError(f"x must be [b, s, d={block.cfg.d}], got {tuple(xv.shape)}")
+    b, s, _ = xv.shape
+    if block.variant is Variant.FULL_RANK:
+        pl = plan(Strategy.FULL_RANK, block.cfg, RunShape(b, s, 1))
+    else:
+        pl = plan(Strategy.BOTTLENECK, block.cfg, RunShape(b, s, 1), block.variant, online_norm=True, grouping=True)
+    res = execute_forward(pl, block, x, h_prev, eps=eps, precision=precision)
+    return res.y, res.h_cur
 
 
 def _stage_h_prev(ex, block: DecoderBlockWeights, h_prev) -> None:
