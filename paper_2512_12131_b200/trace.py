@@ -84,3 +84,21 @@ def ring_transfer_elements(trace: Trace, tp: int, pass_tag: str | None = None) -
         if pass_tag is None or rec.pass_tag == pass_tag
         for _, e, _ in rec.payloads()
     )
+
+
+def tp_block_volume(strategy, cfg, shape) -> int:
+    """Closed-form forward all-reduce elements per block (logical payload, no ring factor) that
+    the traced collectives must equal exactly — reference costs.py:28-44: full-rank two [T, d]
+    boundaries, naive TP five [T, d] + two [T, d_ff] full-width partials, BTP seven [T, r]."""
+    from .plan import Strategy
+
+    t = shape.b * shape.s
+    if strategy is Strategy.FULL_RANK:
+        return 2 * t * cfg.d
+    if strategy is Strategy.VANILLA:
+        return 5 * t * cfg.d + 2 * t * cfg.d_ff
+    if strategy is Strategy.BOTTLENECK:
+        if cfg.r is None:
+            raise ValueError("btp volume needs a bottleneck rank r")
+        return 7 * t * cfg.r
+    raise ValueError(f"unknown strategy {strategy!r}")

@@ -76,6 +76,18 @@ def _run_tp2(strategy, grouping, online, ckpt, world=2, cfg_name="SMALL", bs=(2,
     return res
 
 
+def _assert_closed_form_volume(fwd_records, strategy, b, s):
+    """Traced forward block volume == the closed form (reference test_costs.py:129-145)."""
+    from tests.gpu_util import SMALL
+    from paper_2512_12131_b200.model import RunShape
+    from paper_2512_12131_b200.plan import Strategy
+    from paper_2512_12131_b200.trace import tp_block_volume
+
+    # the closed form counts the boundary tensors; sync-norm statistics ([T] each) come on top
+    traced = sum(rec[3] for rec in fwd_records if rec[2] == "block" and not rec[0].endswith("-stat"))
+    assert traced == tp_block_volume(Strategy(strategy), SMALL, RunShape(b, s, 2)), (strategy, traced)
+
+
 @pytest.mark.parametrize("grouping,online,ckpt", [(True, True, False), (False, True, False), (True, False, True)])
 def test_btp_tp2_matches_oracle(grouping, online, ckpt):
     from tests.gpu_util import BF16_TOL, SMALL, inputs, oracle_step, rel
@@ -100,6 +112,7 @@ def test_btp_tp2_matches_oracle(grouping, online, ckpt):
         assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred                      # real collectives == the plan's prediction
+        _assert_closed_form_volume(fwd, "btp", b, s)
         assert sum(rec[3] for rec in bwd) == 7 * b * s * SMALL.r  # backward moves only rank-r tensors
         assert refwd == []                      # checkpoint recompute is collective-free
 
@@ -123,6 +136,7 @@ def test_vanilla_tp2_matches_oracle(strategy):
         for n in O.PROJECTIONS:
             assert rel(grads["B"][n], g_ref["B"][n][idx, :]) < BF16_TOL, (rank, "B", n)
             assert rel(grads["A"][n], g_ref["A"][n][:, idx]) < BF16_TOL, (rank, "A", n)
+        _assert_closed_form_volume(_rest[0], "vanilla", b, s)
 
 
 def test_full_rank_tp2_matches_oracle():
@@ -147,6 +161,7 @@ def test_full_rank_tp2_matches_oracle():
         for n, w in want.items():
             assert rel(grads["W"][n], w) < BF16_TOL, (rank, n)
         assert [r[0] for r in fwd] == ["attn", "mlp"]
+        _assert_closed_form_volume(fwd, "full-rank", b, s)
 
 
 @pytest.mark.parametrize("world", [4, 8])

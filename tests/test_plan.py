@@ -70,3 +70,22 @@ def test_grouping_preserves_volume_and_cuts_collectives():
 def test_cola_pair_indices():
     idx = cola_pair_indices(8, 2, 1)
     assert list(idx) == [2, 3, 6, 7]
+
+
+def test_closed_form_block_volume_matches_plan():
+    """The plan's predicted forward collectives sum to the closed form of reference costs.py:28-44
+    for every strategy, tp and grouping (the device traces are checked against the plan on the GPU)."""
+    from paper_2512_12131_b200.model import ModelConfig, RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, enumerate_collectives, plan
+    from paper_2512_12131_b200.trace import tp_block_volume
+
+    cfg = ModelConfig(layers=2, heads=4, d=16, d_ff=40, r=4)
+    for strategy, var in ((Strategy.FULL_RANK, None), (Strategy.VANILLA, Variant.SVD), (Strategy.BOTTLENECK, Variant.SVD),
+                          (Strategy.BOTTLENECK, Variant.COLA)):
+        for tp in (1, 2, 4):
+            for grouping in (False, True):
+                for b, s in ((1, 4), (2, 8)):
+                    shape = RunShape(b, s, tp)
+                    pl = plan(strategy, cfg, shape, var, online_norm=True, grouping=grouping)
+                    got = sum(p.elements for p in enumerate_collectives(pl) if p.tag == "block")
+                    assert got == tp_block_volume(strategy, cfg, shape), (strategy, tp, grouping, b, s)
