@@ -166,3 +166,40 @@ def test_gemm_scatter_reduce_into_owners(M, N, Kd, nprob, b_mn, tp):
     for i in range(nprob):
         ref = A[i].float() @ (B[i].float() if b_mn else B[i].float().t())
         assert rel(full[:, i * N:(i + 1) * N] / 2, ref) < TOL
+
+
+def test_randomised_shapes_against_torch():
+    """Seeded sweep over problem counts, shapes (multiples of 8, incl. tails of every tile size),
+    operand majors, split-K, residual and row/col scales, against torch fp32 of the same op."""
+    import random
+
+    rng = random.Random(1234)
+    for case in range(40):
+        nprob = rng.choice([1, 1, 2, 3, 4])
+        probs, checks = [], []
+        fp32_split = rng.random() < 0.3
+        for _ in range(nprob):
+            M = rng.choice([8, 96, 128, 200, 256, 1000, 2048])
+            N = 8 * rng.randint(1, 96)
+            Kd = 8 * rng.randint(1, 160)
+            a_mn, b_mn = rng.random() < 0.3, rng.random() < 0.5
+            A, B = _mk(M, Kd), _mk(N, Kd)
+            Aop = A.t().contiguous() if a_mn else A
+            Bop = B.t().contiguous() if b_mn else B
+            ref = A.float() @ B.float().t()
+            if fp32_split:
+                splits = rng.choice([1, 2, 3, 5])
+                C = torch.zeros(M, N, device="cuda")
+                cs = torch.rand(N, device="cuda") + 0.5
+                probs.append(K.Gemm(Aop, Bop, C, a_mn=a_mn, b_mn=b_mn, splits=splits, reduce_add=True, col_scale=cs))
+                checks.append((C, ref * cs[None, :], 1e-5))
+            else:
+                rs = torch.rand(M, device="cuda") + 0.5 if rng.random() < 0.3 else None
+                R = _mk(M, N) if rng.random() < 0.3 else None
+                C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+                probs.append(K.Gemm(Aop, Bop, C, a_mn=a_mn, b_mn=b_mn, row_scale=rs, resid=R))
+                want = ref * (rs[:, None] if rs is not None else 1.0) + (R.float() if R is not None else 0.0)
+                checks.append((C, want, TOL))
+        K.gemm(*probs, bn=rng.choice([0, 0, 128, 192, 256]))
+        for C, want, tol in checks:
+            assert rel(C, want) < tol, (case, tuple(C.shape))
