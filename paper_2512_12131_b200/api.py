@@ -68,14 +68,15 @@ def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
 
 def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
                   device=None, attn_backend: str = "auto", precision: str = "bf16", comm: TPComm | None = None,
-                  boundary: str = "nccl"):
+                  boundary: str = "nccl", peer_provider: str = "symmetric_memory"):
     """Build this rank's executor for the plan's strategy (comm: default = the process group).
 
     boundary="peer" (BTP, tp > 1): the chunk boundaries run as fused reduce-scatter -> fix-up/sigma
     -> all-gather kernels over NVLink peer memory (torch symmetric-memory heap, csrc/peer.cu)
     instead of NCCL all-reduces + a fix-up launch. boundary="nvls": the same kernels' NVLink-SHARP
     form — the switch reduces the partials (multimem.ld_reduce) and replicates the results
-    (multimem.st) through the heap's multicast mapping."""
+    (multimem.st) through the heap's multicast mapping. peer_provider: how the ranks' heaps are
+    mapped — "symmetric_memory" (torch), or "cuda_ipc" (cudaIpc handles over the process group)."""
     if boundary not in ("nccl", "peer", "nvls"):
         raise ValueError(f"boundary must be 'nccl', 'peer' or 'nvls', got {boundary!r}")
     if comm is None:
@@ -85,7 +86,7 @@ def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS
 
             dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
             comm = TPComm(comm.tp, comm.rank, comm.group, comm.trace,
-                          peer=PeerComm(comm.tp, comm.rank, dev, provider="symmetric_memory",
+                          peer=PeerComm(comm.tp, comm.rank, dev, provider=peer_provider,
                                         nvls=boundary == "nvls"))
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:

@@ -13,6 +13,11 @@ Two providers of the per-rank heap bases:
   CUDA stream; the "peer" buffers are plain device allocations of the same GPU. The kernels,
   flags and executor code are exactly those of the multi-GPU path, so the single-GPU box can
   check the multi-rank numerics and the signal/wait protocol.
+* `"cuda_ipc"`: a plain cudaMalloc heap per rank, exported with cudaIpcGetMemHandle and mapped by
+  every other rank (handles exchanged over the process group) — the same heap without torch's
+  symmetric-memory allocator. CUDA IPC also maps between processes on ONE device (where
+  symmetric memory refuses), so the single-GPU box runs the real multi-process protocol: tp rank
+  processes, time-sliced contexts, system-scope flags across address spaces.
 * `"local_multicast"` (tests, tp=1): the heap is a cuMem allocation bound to a ONE-device NVSwitch
   multicast object (`LocalMulticastHeap`), so the NVLS kernels' multimem instructions run for real
   on a single-GPU box (the switch "sum" over one member is the identity).
@@ -117,6 +122,43 @@ class LocalMulticastHeap:
         self._holder = holder
 
 
+class IpcHeap:
+    """`nbytes` of cudaMalloc'd device memory (a whole allocation, so an IPC handle maps its base),
+    wrapped as a torch uint8 tensor, plus the mapped bases of other ranks' heaps."""
+
+    def __init__(self, nbytes: int, device):
+        from cuda.bindings import runtime as rt
+
+        self._rt = rt
+        dev = torch.device(device)
+        torch.empty(1, device=dev)  # context current
+        err, ptr = rt.cudaMalloc(max(int(nbytes), 1))
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"ipc heap: cudaMalloc {err}")
+        self.ptr = int(ptr)
+        holder = type("_IPC", (), {})()
+        holder.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (self.ptr, False),
+                                           "version": 3}
+        self.tensor = torch.as_tensor(holder, device=dev)
+        self._holder = holder
+        self._opened: list[int] = []
+
+    def handle(self) -> bytes:
+        err, h = self._rt.cudaIpcGetMemHandle(self.ptr)
+        if err != self._rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"ipc heap: cudaIpcGetMemHandle {err}")
+        return bytes(h.reserved)
+
+    def open(self, handle: bytes) -> int:
+        h = self._rt.cudaIpcMemHandle_t()
+        h.reserved = list(handle)
+        err, ptr = self._rt.cudaIpcOpenMemHandle(h, self._rt.cudaIpcMemLazyEnablePeerAccess)
+        if err != self._rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"ipc heap: cudaIpcOpenMemHandle {err}")
+        self._opened.append(int(ptr))
+        return int(ptr)
+
+
 class PeerComm:
     """One rank's view of the symmetric heap: named buffers, peer pointer arrays, flags."""
 
@@ -182,6 +224,18 @@ class PeerComm:
                 if not self.mc_base:
                     raise RuntimeError("symmetric memory returned no multicast address (NVLS unavailable)")
             self._symm = hdl
+            dist.barrier(group=group)  # every rank's flags are zero before anyone signals
+        elif self.provider == "cuda_ipc":
+            import torch.distributed as dist
+
+            self._ipc = IpcHeap(total, self.dev)
+            self.heap = self._ipc.tensor
+            self.heap.zero_()
+            torch.cuda.synchronize(self.dev)
+            group = self.group if self.group is not None else dist.group.WORLD
+            handles = [None] * self.tp
+            dist.all_gather_object(handles, self._ipc.handle(), group=group)
+            bases = [self._ipc.ptr if j == self.rank else self._ipc.open(handles[j]) for j in range(self.tp)]
             dist.barrier(group=group)  # every rank's flags are zero before anyone signals
         elif self.provider == "local_multicast":
             self._mc_heap = LocalMulticastHeap(total, self.dev)
