@@ -259,7 +259,8 @@ def run_ours(args, cfg):
         x = seeded_fill((b, s, cfg.d), 10000).values
         G = seeded_fill((b, s, cfg.d), 30000).values
         trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
-                               optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary)
+                               optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary,
+                               peer_provider=args.peer_provider)
         if variant is Variant.LAX:  # a resident previous-layer bundle, like G (the merge runs every step)
             from paper_2512_12131_b200.model import seeded_h_prev
 
@@ -400,6 +401,8 @@ def main(argv=None):
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
     ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
                     help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
+    ap.add_argument("--peer-provider", default="symmetric_memory", choices=["symmetric_memory", "cuda_ipc"],
+                    help="--boundary peer/nvls: how the ranks' heaps are mapped")
     ap.add_argument("--model", action="store_true", help="multi-layer model step (embedding + blocks + LM head)")
     ap.add_argument("--layers", type=int, default=0, help="--model: number of blocks (default: the preset's)")
     ap.add_argument("--vocab", type=int, default=32000, help="--model: vocabulary size")

@@ -250,10 +250,11 @@ class BlockTrainer:
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
                  optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl",
-                 graph_collectives: bool = True):
+                 graph_collectives: bool = True, peer_provider: str = "symmetric_memory"):
         self.pl = pl
         self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
-                                                                      comm=comm, boundary=boundary)
+                                                                      comm=comm, boundary=boundary,
+                                                                      peer_provider=peer_provider)
         # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
         self.adamw = dict(adamw or {}) if optimizer else None
         # A step without live collectives is always graphed. With live NCCL collectives the whole
