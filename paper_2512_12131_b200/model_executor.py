@@ -48,8 +48,8 @@ class ModelExecutor(ExecutorBase):
         self._setup(pl, comm, device, eps, precision)
         self.vocab = mw.vocab
         self.d, self.dl = pl.cfg.d, pl.cfg.d // self.tp
-        self.blocks = [BTPBlockExecutor(pl, blk, self.comm, self.dev, eps, attn_backend, precision)
-                       for blk in mw.blocks]
+        self.blocks = [BTPBlockExecutor(pl, blk, self._block_comm(l), self.dev, eps, attn_backend, precision)
+                       for l, blk in enumerate(mw.blocks)]
         for ex in self.blocks:
             ex.stats = self.stats  # one launch/FLOP count for the whole step
         sl = slice(self.rank * self.dl, (self.rank + 1) * self.dl)
@@ -61,6 +61,20 @@ class ModelExecutor(ExecutorBase):
         self._flatten_params()
         self.final_gamma = self.gamma1
         self._ids = None
+
+    def _block_comm(self, l: int) -> TPComm:
+        """The communicator of block l: the model's own, except that peer-memory boundaries need a
+        symmetric heap (and flag epochs) PER block — block l's boundary buffers hold activations
+        its backward reads after later blocks have run. Same group, same collective log."""
+        pc = getattr(self.comm, "peer", None)
+        if pc is None or l == 0:
+            return self.comm
+        from .peer import PeerComm
+
+        bpc = PeerComm(pc.tp, pc.rank, pc.dev, provider=pc.provider, group=pc.group, scatter=pc.scatter, nvls=pc.nvls)
+        c = TPComm(self.comm.tp, self.comm.rank, self.comm.group, self.comm.trace, emulate=self.comm.emulate, peer=bpc)
+        c.live = self.comm.live
+        return c
 
     # ------------------------------------------------------------------ instrumentation
     @property

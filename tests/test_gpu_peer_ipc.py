@@ -112,3 +112,68 @@ def test_peer_boundaries_across_processes(world, scatter, variant):
         bad = {k: v for k, v in errs.items() if v > BF16_TOL}
         assert not bad, (rank, bad)
         assert o["fwd"][-len(pred):] == pred
+
+
+def _model_rank_main(rank, world, port, q):
+    try:
+        import datetime
+
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=300))
+        from tests.test_gpu_model import B, S, _setup
+        from paper_2512_12131_b200.comm import TPComm
+        from paper_2512_12131_b200.model import RunShape, Variant
+        from paper_2512_12131_b200.model_executor import ModelExecutor, model_train_step
+        from paper_2512_12131_b200.peer import PeerComm
+        from paper_2512_12131_b200.plan import Strategy, plan
+        from paper_2512_12131_b200.trace import Trace
+
+        cfg, mw, ids, tg, _, _ = _setup()
+        pl = plan(Strategy.BOTTLENECK, cfg, RunShape(B, S, world), Variant.COLA, online_norm=True, grouping=True)
+        comm = TPComm(world, rank, dist.group.WORLD, Trace(), peer=PeerComm(world, rank, "cuda:0", provider="cuda_ipc"))
+        ex = ModelExecutor(pl, mw, comm, "cuda:0")
+        loss, ex = model_train_step(pl, mw, ids, tg, executor=ex)
+        q.put((rank, dict(loss=loss, grads=ex.model_grads(), heaps=len({b.peer.heap.data_ptr() for b in ex.blocks})),
+               None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        import traceback
+
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_model_with_peer_boundaries_across_processes():
+    """The multi-layer model over peer boundaries (one symmetric heap per block) at TP = 2."""
+    from tests.test_gpu_model import _check_grads, _setup
+
+    world = 2
+    cfg, _, _, _, loss_ref, g_ref = _setup()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    os.environ["CUDA_MODULE_LOADING"] = "EAGER"
+    try:
+        procs = [ctx.Process(target=_model_rank_main, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+    finally:
+        os.environ.pop("CUDA_MODULE_LOADING", None)
+    res = {}
+    try:
+        for _ in procs:
+            rank, out, err = q.get(timeout=600)
+            assert err is None, f"rank {rank} failed:\n{err}"
+            res[rank] = out
+    finally:
+        for p in procs:
+            p.join(timeout=60 if len(res) == world else 1)
+            if p.is_alive():
+                p.kill()
+    for rank, o in res.items():
+        assert abs(o["loss"] - loss_ref) / abs(loss_ref) < 2e-2
+        _check_grads(o["grads"], g_ref, tp=world, rank=rank, cfg=cfg)
+        assert o["heaps"] == len(g_ref["blocks"])  # one peer heap per block
