@@ -253,7 +253,8 @@ def run_ours(args, cfg):
         mw = build_model(cfg, variant, 0, args.vocab, layers=args.layers or cfg.layers)
         x, G = token_batch(b, s, args.vocab)
         trainer = ModelTrainer(pl, mw, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
-                               optimizer=not args.no_optimizer, comm=comm)
+                               optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary,
+                               peer_provider=args.peer_provider)
     else:
         blk = fan_in_scaled(build_block(cfg, variant, 0))
         x = seeded_fill((b, s, cfg.d), 10000).values

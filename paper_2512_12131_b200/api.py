@@ -461,10 +461,19 @@ class ModelTrainer(BlockTrainer):
 
     def __init__(self, pl: ShardPlan, mw, *, eps: float = EPS_DEFAULT, attn_backend: str = "auto",
                  use_graph: bool = True, adamw: dict | None = None, optimizer: bool = True,
-                 comm: TPComm | None = None):
+                 comm: TPComm | None = None, boundary: str = "nccl", peer_provider: str = "symmetric_memory"):
         from .model_executor import ModelExecutor
 
-        comm = comm if comm is not None else TPComm.from_env(pl.shape.tp, trace=Trace())
+        if boundary not in ("nccl", "peer", "nvls"):
+            raise ValueError(f"boundary must be 'nccl', 'peer' or 'nvls', got {boundary!r}")
+        if comm is None:
+            comm = TPComm.from_env(pl.shape.tp, trace=Trace())
+            if boundary != "nccl" and comm.tp > 1:
+                from .peer import PeerComm
+
+                dev = torch.device("cuda", torch.cuda.current_device())
+                comm = TPComm(comm.tp, comm.rank, comm.group, comm.trace,
+                              peer=PeerComm(comm.tp, comm.rank, dev, provider=peer_provider, nvls=boundary == "nvls"))
         ex = ModelExecutor(pl, mw, comm, torch.device("cuda", torch.cuda.current_device()), eps, attn_backend)
         super().__init__(pl, None, use_graph=use_graph, adamw=adamw, optimizer=optimizer, executor=ex)
 
