@@ -8,6 +8,7 @@ CPU or PyTorch path.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -181,7 +182,8 @@ def load(path: Path | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else _LIB_PATH
+        # BTP_LIB: an alternative build of the same library (in-process A/B of kernel versions)
+        p = Path(path) if path else Path(os.environ.get("BTP_LIB", str(_LIB_PATH)))
         if not p.exists():
             raise NativeUnavailable(
                 f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
