@@ -224,6 +224,10 @@ def run_ours(args, cfg):
         _executor.FUSE_SIGMA = False
     if args.concurrent_wgrad:
         _executor.ExecutorBase.concurrent_wgrad = True
+    if args.gemm_pair >= 0:
+        from paper_2512_12131_b200 import kernels as _K
+
+        _K.set_pair_mode(args.gemm_pair)
     from paper_2512_12131_b200.model import RunShape, Variant, build_block, fan_in_scaled
     from paper_2512_12131_b200.plan import Strategy, plan
     from paper_2512_12131_b200.tensor import seeded_fill
@@ -395,6 +399,8 @@ def main(argv=None):
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-optimizer", action="store_true", help="drop the AdamW update from the step")
     ap.add_argument("--no-fuse-sigma", action="store_true", help="TP=1: separate fix-up/sigma kernel (A/B)")
+    ap.add_argument("--gemm-pair", type=int, default=-1, choices=[-1, 0, 1, 2],
+                    help="CTA-pair GEMM tiles: 0 off, 1 plain/sigma epilogues, 2 also residual epilogues (A/B)")
     ap.add_argument("--concurrent-wgrad", action="store_true", help="weight-gradient GEMMs on a side stream (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)

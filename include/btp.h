@@ -96,11 +96,14 @@ int btp_gemm(const btp_gemm_problem* problems, int n, int bn_hint, void* stream)
 int btp_gemm_scatter(const btp_gemm_problem* problems, int n, int bn_hint, void* const* owners, int n_owners,
                      int rows_per_owner, int width, long long ld, const int* col0, void* stream);
 
-/* Tile mode switch for btp_gemm: 1 (default) = CTA-pair tiles (cluster of 2 CTAs on one TPC,
+/* Tile mode switch for btp_gemm: 1 = CTA-pair tiles (cluster of 2 CTAs on one TPC,
  * tcgen05.mma.cta_group::2, 256 x BN per pair) for launches with plain / sigma epilogues
- * (residual epilogues stay single-CTA); 2 = pair tiles for residual epilogues too;
+ * (residual epilogues stay single-CTA); 2 (default) = pair tiles for residual epilogues too;
  * 0 = single-CTA 128 x BN tiles everywhere. Returns the previous setting. */
 int btp_gemm_set_pair(int enable);
+/* Residual epilogues: 1 (default) stage a tile's whole residual (four 64-column chunk buffers per
+ * epilogue warp, one TMA round trip per tile), 0 = per-chunk prefetch; returns the previous value. */
+int btp_gemm_set_res4(int enable);
 
 /* Online RMSNorm (local form) fused with the residual add, one row per warp.
  *   v = x (+ branch); if x_out: x_out = bf16(v); stats use the rounded v

@@ -86,7 +86,9 @@ struct DevParams {
 };
 
 // kSlots: staging slots per chunk buffer (2 for the two-input / two-output swiglu-bwd epilogue,
-// which trades mainloop stages for epilogue staging).
+// which trades mainloop stages for epilogue staging). kSlots == 4 is the residual layout: four
+// single-slot chunk buffers per warp, so a tile's whole residual (<= 4 x 64 columns) is TMA-loaded
+// in one go and each chunk is added and stored in place.
 // kPair: CTA-pair mode (cluster of 2, tcgen05.mma.cta_group::2): a 256 x BN tile per pair,
 // each CTA holding 128 rows of A and BN/2 rows of B per stage and its own 128 x BN accumulator.
 // Halving the per-CTA B tile buys a deeper smem pipeline (up to 8 stages).
@@ -98,9 +100,9 @@ struct Cfg {
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;  // double-buffered accumulator (pow2 alloc)
-  static constexpr int kEpiWarpBytes = 2 * kSlots * kEpiStageBytes;  // double-buffered chunks
+  static constexpr int kEpiWarpBytes = (kSlots == 4 ? 4 : 2 * kSlots) * kEpiStageBytes;  // chunk buffers
   static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
-  static constexpr int kBarrierBytes = 256;
+  static constexpr int kBarrierBytes = 512;
   static constexpr int kAvail = 232448 - 1024 - kEpiBytes - kBarrierBytes;
   static constexpr int kStages = (kAvail / kStageBytes) > 8 ? 8 : (kAvail / kStageBytes);
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarrierBytes;
@@ -139,8 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar_all = tempty_bar + 2;  // 4 epilogue warps x 2 staging buffers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar_all + 8);
+  uint64_t* aux_bar_all = tempty_bar + 2;  // 4 epilogue warps x (2, or 4 when kSlots == 4) buffers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar_all + 16);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // one arrival per epilogue warp (pair: both CTAs' four warps release the leader's buffer)
       mbar_init(&tempty_bar[b], kPair ? 8 : 4);
     }
-    for (int b = 0; b < 8; ++b) mbar_init(&aux_bar_all[b], 1);
+    for (int b = 0; b < 16; ++b) mbar_init(&aux_bar_all[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -282,7 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     uint8_t* stage_ptr0 = sEpi + q * C::kEpiWarpBytes;
     const uint32_t stage0 = smem_u32(stage_ptr0);
     const uint32_t row_sw = lane & 7;  // 128B swizzle: 16B chunk j of row i lives at chunk j ^ (i % 8)
-    uint64_t* aux_bar = aux_bar_all + q * 2;  // one per staging buffer of this warp
+    uint64_t* aux_bar = aux_bar_all + q * (kSlots == 4 ? 4 : 2);  // one per staging buffer of this warp
+    uint32_t res_phase = 0u;  // kSlots == 4: bit c = parity of the next wait on aux_bar[c]
     uint32_t aux_phase = 0u;  // bit b: parity of the next wait on aux_bar[b]
     // staging slot s of buffer b (each slot = one 32-row x 128 B chunk)
     auto slot_ptr = [&](int b, int s) { return stage_ptr0 + (b * kSlots + s) * kEpiStageBytes; };
@@ -319,13 +322,83 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // aux tiles (residual, or g/u for swiglu-bwd) ride the staging buffers (bf16 out only)
       const bool aux = pr.resid != nullptr;
       const bool swb = pr.epi == kEpiSwigluBwd;
-      if (aux && lane == 0) issue_aux(pr, chunk_seq & 1, n0, out_row0);  // prefetch under the mainloop
+      if constexpr (kSlots == 4) {
+        // the tile's whole residual in flight at once (one latency per tile, not per chunk), as
+        // soon as the previous tile's stores have read the buffers
+        if (lane == 0) {
+          bulk_wait_read<0>();
+          if (aux) {
+            fence_proxy_async_smem();
+            for (int c = 0; c < 4 && c * 64 < n_valid; ++c) {
+              mbar_arrive_expect_tx(&aux_bar[c], kEpiStageBytes);
+              tma_load_2d(stage_ptr0 + c * kEpiStageBytes, &pr.tma_r, &aux_bar[c], n0 + c * 64, out_row0);
+            }
+          }
+        }
+        __syncwarp();
+      } else if (aux && lane == 0) {
+        issue_aux(pr, chunk_seq & 1, n0, out_row0);  // prefetch under the mainloop
+      }
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < pr.M;
       float rscale = pr.alpha;
       if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
+      if constexpr (kSlots == 4) {
+        // bf16 output, 64-column chunks c = 0..3: residual (if any) landed in buffer c; the sum is
+        // written back in place and TMA-stored from there
+#pragma unroll 1
+        for (int c = 0; c * 64 < n_valid; ++c) {
+          const int c0 = c * 64;
+          uint8_t* cb = stage_ptr0 + c * kEpiStageBytes;
+          const uint32_t row_addr = smem_u32(cb) + lane * 128;
+          if (aux) {
+            mbar_wait(&aux_bar[c], (res_phase >> c) & 1u);
+            res_phase ^= 1u << c;
+          }
+          float v[64];
+          {
+            uint32_t r[64];
+            tmem_ld_32x32b_x64(tmem_base + ((q * 32u) << 16) + buf * BN + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(r[j]) * rscale;
+          }
+          if (c0 + 64 >= n_valid) release_tmem(buf);
+          const int col = n0 + c0;
+          if (pr.col_scale != nullptr) {
+            const int lim = min(64, n_valid - c0);
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < lim) v[j] *= __ldg(pr.col_scale + col + j);
+          }
+          if (aux) {
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const uint4 rv = ld_shared_v4(row_addr + ((g ^ row_sw) << 4));
+              const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                v[g * 8 + 2 * h] += bf16_lo(w[h]);
+                v[g * 8 + 2 * h + 1] += bf16_hi(w[h]);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(row_addr + ((j ^ row_sw) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
+                         pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pr.tma_c, cb, col, out_row0);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
       if (kSlots == 2 && pr.epi == kEpiSigma) {  // (launched with two staging slots per buffer)
         // accumulator columns [0, BN/2) = u block, [BN/2, BN) = v block of the same projection.
         // Per 64-column step: z_u, z_v -> C from staging buffer 0 (two slots), then
@@ -573,7 +646,7 @@ template <int BN, int kSlots, bool kPair>
 static int launch(const DevParams& P, int grid, cudaStream_t stream) {
   using C = Cfg<BN, kSlots, kPair>;
   static_assert(C::kSmemBytes <= 232448, "shared memory budget");
-  static_assert(2 * C::kStages * 8 + 12 * 8 + 8 <= C::kBarrierBytes, "barrier region");
+  static_assert(2 * C::kStages * 8 + 20 * 8 + 8 <= C::kBarrierBytes, "barrier region");
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(gemm_kernel<BN, kSlots, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -627,9 +700,18 @@ static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, 
 }
 
 // CTA-pair (cta_group::2) tiles: 0 never, 1 plain / sigma epilogues, 2 also residual epilogues
-static int g_pair_mode = 1;
+// (default: with the whole-tile residual staging the pair tiles win there too)
+static int g_pair_mode = 2;
+// residual epilogues with whole-tile residual staging (kSlots == 4); 0 = per-chunk prefetch (A/B)
+static int g_res4 = 1;
 
 }  // namespace btp
+
+extern "C" int btp_gemm_set_res4(int enable) {
+  const int prev = btp::g_res4;
+  btp::g_res4 = enable ? 1 : 0;
+  return prev;
+}
 
 extern "C" int btp_gemm_set_pair(int enable) {
   const int prev = btp::g_pair_mode;
@@ -680,8 +762,8 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
   int slots = 1;
   for (int i = 0; i < n; ++i) slots = probs[i].epilogue != kEpiStore ? 2 : slots;
   const bool sigma = probs[0].epilogue == kEpiSigma;
-  // pair tiles win on plain epilogues; the residual epilogue measured slower with them (its
-  // 128-row-per-CTA aux prefetch does not overlap as well), so those launches stay single-CTA
+  // pair tiles win on plain epilogues, and on residual ones with the whole-tile residual staging
+  // (the per-chunk residual prefetch did not gain from them: mode 1 keeps those single-CTA)
   bool any_resid = false;
   for (int i = 0; i < n; ++i) any_resid = any_resid || probs[i].resid != nullptr;
   const bool pair = g_pair_mode && (slots == 1 || sigma) && (!any_resid || g_pair_mode == 2) && num_sms_cached() >= 2;
@@ -761,13 +843,22 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
   }
   int grid_units = tiles < units ? tiles : units;
   if (max_ctas > 0 && grid_units > max_ctas) grid_units = max_ctas;
+  // residual launches (bf16 outputs only): the whole-tile residual staging layout
+  bool res4 = g_res4 && slots == 1 && any_resid && sc == nullptr;
+  for (int i = 0; i < n; ++i) res4 = res4 && !probs[i].c_fp32 && !probs[i].reduce_add && probs[i].splits == 1;
   if (pair) {
     const int grid = 2 * grid_units;
+    if (res4) return BN == 256 ? launch<256, 4, true>(P, grid, stream) : launch<128, 4, true>(P, grid, stream);
     if (slots == 2) return BN == 256 ? launch<256, 2, true>(P, grid, stream) : launch<128, 2, true>(P, grid, stream);
     if (BN == 256) return launch<256, 1, true>(P, grid, stream);
     return launch<128, 1, true>(P, grid, stream);
   }
   const int grid = grid_units;
+  if (res4) {
+    if (BN == 256) return launch<256, 4, false>(P, grid, stream);
+    if (BN == 192) return launch<192, 4, false>(P, grid, stream);
+    return launch<128, 4, false>(P, grid, stream);
+  }
   if (slots == 2) {
     if (BN == 256) return launch<256, 2, false>(P, grid, stream);
     if (BN == 192) return launch<192, 2, false>(P, grid, stream);

@@ -162,9 +162,14 @@ def counter_add(ctr, delta: int = 1):
 
 
 def set_pair_mode(mode: int) -> int:
-    """CTA-pair (cta_group::2) GEMM tiles: 0 off, 1 plain/sigma epilogues (default), 2 also residual
-    epilogues; returns the previous setting."""
+    """CTA-pair (cta_group::2) GEMM tiles: 0 off, 1 plain/sigma epilogues, 2 also residual
+    epilogues (default); returns the previous setting."""
     return int(_native.load().btp_gemm_set_pair(int(mode)))
+
+
+def set_res4(enable: bool) -> int:
+    """Residual GEMM epilogues stage the whole tile's residual (default on); returns the previous."""
+    return int(_native.load().btp_gemm_set_res4(int(bool(enable))))
 
 
 def zero(t: torch.Tensor) -> None:

@@ -27,11 +27,14 @@ for M, N, Kd in [(16384, 512, 1024), (16384, 2048, 512), (16384, 1024, 512)]:
     r = torch.randn(M, N, device="cuda").bfloat16()
     o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     fl = 2 * M * N * Kd
-    for pair in (0, 1, 2):
+    for pair in (1, 2):
         K.set_pair_mode(pair)
-        for bn in (0, 128, 256):
+        for bn in (0, 256):
             tp = t(lambda: K.gemm(K.Gemm(a, w, o), bn=bn))
+            K.set_res4(False)
+            tr0 = t(lambda: K.gemm(K.Gemm(a, w, o, resid=r), bn=bn))
+            K.set_res4(True)
             tr = t(lambda: K.gemm(K.Gemm(a, w, o, resid=r), bn=bn))
             print(f"[{M}x{N} K={Kd}] pair={pair} bn={bn or 'auto'}: plain {tp:6.1f} us ({fl / tp / 1e6:5.0f} TF/s)"
-                  f"  resid {tr:6.1f} us ({fl / tr / 1e6:5.0f} TF/s)")
+                  f"  resid/chunk {tr0:6.1f} us  resid/tile {tr:6.1f} us ({fl / tr / 1e6:5.0f} TF/s)")
     K.set_pair_mode(1)
