@@ -464,9 +464,27 @@ __global__ void __launch_bounds__(256) dot_kernel(const T* __restrict__ a, long 
   __shared__ float red[8];
   const int per_row = cols >> 3;
   const long long total = (long long)per_row * rows;
+  // four grid-stride items per round, all eight 16-byte loads issued before any FMA: a thread
+  // otherwise waits one full memory latency per item (the grid is capped at 4 blocks per SM)
   float acc = 0.f;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; idx + 3 * stride < total; idx += 4 * stride) {
+    float fa[4][8], fb[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long it = idx + u * stride;
+      const int row = (int)(it / per_row);
+      const int c = (int)(it - (long long)row * per_row) * 8;
+      load8(a + (long long)row * lda + c, fa[u]);
+      load8(b + (long long)row * ldb + c, fb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = fmaf(fa[u][j], fb[u][j], acc);
+  }
+  for (; idx < total; idx += stride) {
     const int row = (int)(idx / per_row);
     const int c = (int)(idx - (long long)row * per_row) * 8;
     float fa[8], fb[8];
