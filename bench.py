@@ -30,7 +30,6 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-import numpy as np  # noqa: E402
 
 METRIC = "train tokens/s (fwd+bwd) for CoLA block at TP 1/2/4/8; % of bf16 tensor peak"
 UNIT = "tokens/s"

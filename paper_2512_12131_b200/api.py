@@ -18,7 +18,6 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import kernels as K
 from .comm import TPComm
 from .executor import BTPBlockExecutor
 from .model import EPS_DEFAULT, DecoderBlockWeights, Variant

@@ -20,7 +20,7 @@ import torch
 from . import kernels as K
 from .attention import Attention
 from .comm import TPComm
-from .executor import BF16, F32, ExecutorBase
+from .executor import F32, ExecutorBase
 from .model import DecoderBlockWeights, Variant
 from .plan import PlanError, ShardPlan, Strategy, cola_pair_indices, col_shard_bounds
 

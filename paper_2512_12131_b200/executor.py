@@ -30,7 +30,7 @@ import dataclasses
 import functools
 import math
 import os
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
