@@ -8,6 +8,7 @@ from paper_2512_12131_b200.tensor import seeded_fill
 
 SMALL = ModelConfig(layers=1, heads=4, d=256, d_ff=640, r=64)
 C60M = ModelConfig(layers=8, heads=8, d=512, d_ff=1376, r=128)
+P7B = ModelConfig(layers=32, heads=32, d=4096, d_ff=11008, r=1024)  # the paper's CoLA-7B block widths
 BF16_TOL = 2e-2  # north_star: bf16 mode within 2e-2 relative on activations, gradients and loss
 
 
