@@ -223,21 +223,23 @@ def test_btp_tp2_sliced_forward_boundaries():
         assert fwd == pred  # one record per chunk boundary although each is issued in slices
 
 
-def test_btp_tp2_paper_7b_widths():
-    """CoLA-7B block widths (d 4096, d_ff 11008, r 1024) at TP=2, short sequence: each rank's
-    shard is d/2 = 2048 wide with 16 heads and a 5504-wide d_ff slice."""
+@pytest.mark.parametrize("world", [2, 8])
+def test_btp_tp2_paper_7b_widths(world):
+    """CoLA-7B block widths (d 4096, d_ff 11008, r 1024) at TP=2 and TP=8 (BASELINE configs[2]'s
+    sharding), short sequence: a TP=8 rank owns 512 residual columns, 4 heads, 1376 d_ff columns."""
     from tests.gpu_util import BF16_TOL, P7B, inputs, oracle_step, rel
     from oracle import btp_oracle as O
     from paper_2512_12131_b200.model import Variant
 
     b, s = 1, 256
-    res = _run_tp2("btp", True, True, False, cfg_name="P7B", bs=(b, s))
+    res = _run_tp2("btp", True, True, False, world=world, cfg_name="P7B", bs=(b, s))
+    assert len(res) == world
     blk, x, G, oblk = inputs(P7B, Variant.COLA, b, s)
-    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, P7B, b, s, tp=2, sharded=False)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, P7B, b, s, tp=world, sharded=False)
     for rank, (_, y, loss, dx, grads, fwd, bwd, *_r) in res.items():
         assert rel(y.reshape(-1, P7B.d), y_ref) < BF16_TOL
         assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
-        gr = O.grads_for_rank(g_ref, 2, rank, P7B.d, P7B.d_ff)
+        gr = O.grads_for_rank(g_ref, world, rank, P7B.d, P7B.d_ff)
         assert rel(dx, gr["dx"]) < BF16_TOL
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
