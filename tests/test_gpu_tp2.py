@@ -109,6 +109,8 @@ def test_btp_tp2_matches_oracle(grouping, online, ckpt):
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        if ckpt:
+            assert _r[0] == []  # re-forward records no collective
         assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred                      # real collectives == the plan's prediction
@@ -189,6 +191,8 @@ def test_btp_tp4_tp8_c60m_matches_oracle(world):
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        if ckpt:
+            assert _r[0] == []  # re-forward records no collective
         assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred
@@ -220,19 +224,22 @@ def test_btp_tp2_sliced_forward_boundaries():
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        if ckpt:
+            assert _r[0] == []  # re-forward records no collective
         assert fwd == pred  # one record per chunk boundary although each is issued in slices
 
 
-@pytest.mark.parametrize("world", [2, 8])
-def test_btp_tp2_paper_7b_widths(world):
+@pytest.mark.parametrize("world,ckpt", [(2, False), (8, False), (4, True)])
+def test_btp_tp2_paper_7b_widths(world, ckpt):
     """CoLA-7B block widths (d 4096, d_ff 11008, r 1024) at TP=2 and TP=8 (BASELINE configs[2]'s
-    sharding), short sequence: a TP=8 rank owns 512 residual columns, 4 heads, 1376 d_ff columns."""
+    sharding), short sequence: a TP=8 rank owns 512 residual columns, 4 heads, 1376 d_ff columns;
+    TP=4 with the low-rank checkpoint is configs[4]'s path (its re-forward must stay collective-free)."""
     from tests.gpu_util import BF16_TOL, P7B, inputs, oracle_step, rel
     from oracle import btp_oracle as O
     from paper_2512_12131_b200.model import Variant
 
     b, s = 1, 256
-    res = _run_tp2("btp", True, True, False, world=world, cfg_name="P7B", bs=(b, s))
+    res = _run_tp2("btp", True, True, ckpt, world=world, cfg_name="P7B", bs=(b, s))
     assert len(res) == world
     blk, x, G, oblk = inputs(P7B, Variant.COLA, b, s)
     y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, P7B, b, s, tp=world, sharded=False)
@@ -244,3 +251,5 @@ def test_btp_tp2_paper_7b_widths(world):
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
+        if ckpt:
+            assert _r[0] == []  # re-forward records no collective
