@@ -109,8 +109,6 @@ def test_btp_tp2_matches_oracle(grouping, online, ckpt):
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
-        if ckpt:
-            assert _r[0] == []  # re-forward records no collective
         assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred                      # real collectives == the plan's prediction
@@ -191,8 +189,6 @@ def test_btp_tp4_tp8_c60m_matches_oracle(world):
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
-        if ckpt:
-            assert _r[0] == []  # re-forward records no collective
         assert rel(grads["gamma1"], gr["dgamma1"]) < BF16_TOL
         assert rel(grads["gamma2"], gr["dgamma2"]) < BF16_TOL
         assert fwd == pred
@@ -224,8 +220,6 @@ def test_btp_tp2_sliced_forward_boundaries():
         for n in O.PROJECTIONS:
             assert rel(grads["A"][n], gr["A"][n]) < BF16_TOL, (rank, "A", n)
             assert rel(grads["B"][n], gr["B"][n]) < BF16_TOL, (rank, "B", n)
-        if ckpt:
-            assert _r[0] == []  # re-forward records no collective
         assert fwd == pred  # one record per chunk boundary although each is issued in slices
 
 
