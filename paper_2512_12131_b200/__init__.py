@@ -33,6 +33,12 @@ from .api import (BlockTrainer, ModelTrainer, SimResult, StepResult, execute_for
                   reference_forward, train_step)
 from .tensor_ops import batched_matmul, matmul, swiglu
 from .checkpointing import CkptPolicy, CkptReport, eff_ckpt, run_with_ckpt
+from .config import (ConfigError, Scenario, add_config_flags, apply_overrides, build_plan, load_scenario,
+                     run_scenario, scenario_from_dict)
+from . import config as cli  # the reference keeps its config API in `btpsim.cli` (cli.py:55-304)
+import sys as _sys
+
+_sys.modules.setdefault(__name__ + ".cli", cli)   # `import paper_2512_12131_b200.cli as cli` works too
 
 __all__ = [
     "Tensor", "tensor", "zeros", "seeded_fill", "DimensionError", "DivisibilityError",
@@ -44,6 +50,8 @@ __all__ = [
     "CollectiveRecord", "Trace", "trace_volume", "ring_transfer_elements",
     "execute_forward", "reference_forward", "matmul", "batched_matmul", "swiglu", "train_step", "make_executor", "BlockTrainer", "ModelTrainer", "SimResult", "StepResult",
     "CkptPolicy", "CkptReport", "eff_ckpt", "run_with_ckpt",
+    "ConfigError", "Scenario", "scenario_from_dict", "load_scenario", "apply_overrides", "build_plan",
+    "add_config_flags", "run_scenario", "cli",
 ]
 
 __version__ = "0.1.0"

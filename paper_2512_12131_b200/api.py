@@ -20,6 +20,7 @@ import torch.distributed as dist
 
 from .comm import TPComm
 from .executor import BTPBlockExecutor
+from .interop import as_block, as_h_prev, as_plan, element_bytes_of, values_of
 from .model import EPS_DEFAULT, DecoderBlockWeights, Variant
 from .plan import PlanError, ShardPlan, Strategy, plan
 from .tensor import Tensor
@@ -54,10 +55,15 @@ class StepResult:
     dh_prev: dict | None = None   # lax with an h_prev: {projection: dL/dh_prev [b, s, r]} (float64 host)
 
 
+def _normalise(pl, block):
+    """Our plan / block for ours or the reference's own objects (interop.py)."""
+    return as_plan(pl), as_block(block)
+
+
 def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
     if block.variant is not pl.variant:
         raise PlanError(f"plan variant {pl.variant.value} != block variant {block.variant.value}")
-    xv = x.values if isinstance(x, Tensor) else np.asarray(x)
+    xv = values_of(x)
     if xv.ndim != 3 or xv.shape[2] != pl.cfg.d:
         raise PlanError(f"x must be [b, s, d={pl.cfg.d}], got {tuple(xv.shape)}")
     if (xv.shape[0], xv.shape[1]) != (pl.shape.b, pl.shape.s):
@@ -78,6 +84,7 @@ def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS
     mapped — "symmetric_memory" (torch), or "cuda_ipc" (cudaIpc handles over the process group)."""
     if boundary not in ("nccl", "peer", "nvls"):
         raise ValueError(f"boundary must be 'nccl', 'peer' or 'nvls', got {boundary!r}")
+    pl, block = _normalise(pl, block)
     if comm is None:
         comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
         if boundary in ("peer", "nvls") and pl.strategy is Strategy.BOTTLENECK:
@@ -115,7 +122,7 @@ def _gather_y(ex, y_sh: torch.Tensor, model_tail: bool) -> torch.Tensor:
         return y_sh if ex.tp == 1 else y_sh.repeat(1, ex.tp)
     # host-side result assembly (the reference concatenates without a record, simulator.py:713)
     parts = [torch.empty_like(y_sh) for _ in range(ex.tp)]
-    dist.all_gather(parts, y_sh.contiguous())
+    dist.all_gather(parts, y_sh.contiguous(), group=ex.comm.group)
     return torch.cat(parts, dim=1)
 
 
@@ -124,7 +131,8 @@ def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *
                     attn_backend: str = "auto", precision: str = "bf16") -> SimResult:
     """Run one block forward under the plan on the GPU; returns the gathered logical y (and, for
     lax, the h_cur bundle; h_prev is given logically, {projection: Tensor [b, s, r]}, as in the
-    reference simulator.py:268-316)."""
+    reference simulator.py:268-316). pl / block / x / h_prev may be the reference's own objects."""
+    pl, block = _normalise(pl, block)
     xv = _check_inputs(pl, block, x)
     ex = make_executor(pl, block, eps=eps, trace=trace, attn_backend=attn_backend, precision=precision)
     _stage_h_prev(ex, block, h_prev)
@@ -136,7 +144,7 @@ def execute_forward(pl: ShardPlan, block: DecoderBlockWeights, x, h_prev=None, *
         ws[ex.rank] = ex.capture_workspaces()
     b, s, d = xv.shape
     y_host = y.double().cpu().numpy().reshape(b, s, d)
-    eb = x.element_bytes if isinstance(x, Tensor) else 2
+    eb = element_bytes_of(x)
     return SimResult(Tensor(y_host, eb), _h_cur(ex, b, s, eb), ex.comm.trace, ws, pl)
 
 
@@ -148,7 +156,8 @@ def reference_forward(block: DecoderBlockWeights, x, h_prev=None, eps: float = E
     precision="fp32" (default) keeps it within the north_star 1e-4 of the float64 reference."""
     from .model import RunShape
 
-    xv = x.values if isinstance(x, Tensor) else np.asarray(x)
+    block = as_block(block)
+    xv = values_of(x)
     if xv.ndim != 3 or xv.shape[2] != block.cfg.d:
         from .tensor import DimensionError
 
@@ -166,7 +175,7 @@ def _stage_h_prev(ex, block: DecoderBlockWeights, h_prev) -> None:
     if block.variant is not Variant.LAX:
         return  # the reference ignores a bundle handed to a non-lax block (simulator.py:297)
     if h_prev is not None:
-        h_prev = {k: (v.values if isinstance(v, Tensor) else np.asarray(v)) for k, v in h_prev.items()}
+        h_prev = {k: values_of(v) for k, v in h_prev.items()}
     ex.set_h_prev(h_prev)
 
 
@@ -178,7 +187,7 @@ def _bundle_host(ex, views: dict, b, s) -> dict:
         if not getattr(ex, "residual_sharded", True) and ex.tp > 1:
             if ex.comm.live:
                 parts = [torch.empty_like(h.contiguous()) for _ in range(ex.tp)]
-                dist.all_gather(parts, h.contiguous())
+                dist.all_gather(parts, h.contiguous(), group=ex.comm.group)
                 h = torch.cat(parts, dim=1)
             else:
                 h = h.repeat(1, ex.tp)
@@ -203,11 +212,12 @@ def train_step(pl: ShardPlan, block: DecoderBlockWeights, x, G=None, *, eps: flo
     G defaults to the loss projection seeded_fill((b, s, d), 30000)."""
     from .tensor import seeded_fill
 
+    pl, block = _normalise(pl, block)
     xv = _check_inputs(pl, block, x)
     b, s, d = xv.shape
     if G is None:
         G = seeded_fill((b, s, d), 30000).values
-    Gv = G.values if isinstance(G, Tensor) else np.asarray(G)
+    Gv = values_of(G)
     ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
                                                              precision=precision)
     _stage_h_prev(ex, block, h_prev)
@@ -250,6 +260,7 @@ class BlockTrainer:
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
                  optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl",
                  graph_collectives: bool = True, peer_provider: str = "symmetric_memory"):
+        pl, block = _normalise(pl, block)
         self.pl = pl
         self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
                                                                       comm=comm, boundary=boundary,

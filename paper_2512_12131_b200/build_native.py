@@ -55,11 +55,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     ]
     if verbose:
         common += ["-Xptxas", "-v"]
-    for src in SOURCES:
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(src):
         obj = LIB_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc, "-c", str(CSRC / src), "-o", str(obj)] + common
-        subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+        subprocess.run([nvcc, "-c", str(CSRC / src), "-o", str(obj)] + common, check=True)
+        return str(obj)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.run([nvcc, "-shared", "-o", str(tmp)] + objs + ARCH, check=True)
     os.replace(tmp, LIB)

@@ -37,11 +37,14 @@ class CkptPolicy(str, Enum):
 
 @dataclass(frozen=True)
 class CkptReport:
-    """Reference checkpointing.py:45-72, field for field (element counts over this rank's kept
-    activations; the device also reports the bytes, which mix bf16 activations and fp32 stats)."""
+    """Reference checkpointing.py:45-72, field for field, in the reference's all-rank units:
+    stored elements and recompute FLOPs summed over the TP ranks (replicated z charged once per
+    rank), ring elements 2(tp-1) x payload per re-run collective. The device also reports bytes
+    (bf16 activations + fp32 statistics). The kept set is what the device backward reads, not the
+    reference's workspace inventory, so ΔMem / eff are comparable in ordering, not digit for digit."""
 
     policy: CkptPolicy
-    stored_elements_without: int   # activation elements a plain forward keeps for backward (this rank)
+    stored_elements_without: int   # activation elements a plain forward keeps for backward (all ranks)
     stored_elements_with: int      # ... under the low-rank boundary policy
     recompute_flops: int
     reforward_collectives: int
@@ -101,6 +104,21 @@ class CkptRun:
 _RECOMPUTED_BTP = ("x_mid", "gu", "act", "qkv", "attn", "a_o", "a_gu", "a_d", "a_qkv")
 
 
+def _all_ranks(ex, *counts) -> tuple[int, ...]:
+    """Per-rank counts summed over the TP group — the reference's all-rank convention
+    (checkpointing.py:1-8: memory summed over ranks, replicated storage charged once per rank;
+    trace FLOPs summed over ranks). Live group: an all-reduce; record-only: ranks are symmetric."""
+    if ex.tp == 1:
+        return tuple(int(c) for c in counts)
+    if ex.comm.live:
+        import torch.distributed as dist
+
+        t = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=ex.dev)
+        dist.all_reduce(t, group=ex.comm.group)
+        return tuple(int(v) for v in t.tolist())
+    return tuple(int(c) * ex.tp for c in counts)
+
+
 def _snapshot(ex, names) -> dict:
     out = {}
     for name in names:
@@ -113,8 +131,11 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
                   eps: float = EPS_DEFAULT, model_tail: bool = False) -> CkptRun:
     """Device analogue of the reference's run_with_ckpt (checkpointing.py:109-163): BTP re-forwards
     with zero collectives; the naive-TP baseline replays its chunk all-reduces (3 grouped / 6 not)."""
-    from .api import SimResult, _check_inputs, _gather_y, _h_cur, _stage_h_prev, make_executor, shard_input
+    from .api import SimResult, _check_inputs, _gather_y, _h_cur, _normalise, _stage_h_prev, make_executor, shard_input
     from .tensor import Tensor
+
+    pl, block = _normalise(pl, block)
+    policy = CkptPolicy(getattr(policy, "value", policy))
 
     if policy is CkptPolicy.LOWRANK_BOUNDARY and pl.strategy is Strategy.FULL_RANK:
         raise PlanError("lowrank-boundary checkpointing stores rank-r tensors; the full-rank strategy has none")
@@ -129,7 +150,7 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
     y = _gather_y(ex, y_sh, model_tail)
     result = SimResult(Tensor(y.double().cpu().numpy().reshape(b, s, d)), h_cur, ex.comm.trace,
                        [dict() for _ in range(pl.shape.tp)], pl)
-    without_e, without_b = ex.saved_activation_elements(), ex.saved_activation_bytes()
+    without_e, without_b = _all_ranks(ex, ex.saved_activation_elements(), ex.saved_activation_bytes())
     if policy is CkptPolicy.NONE:
         rep = CkptReport(policy, without_e, without_e, 0, 0, 0, without_b, without_b)
         return CkptRun(result, rep, True, {})
@@ -140,7 +161,7 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
     ck = make_executor(ck_pl, block, eps=eps)
     _stage_h_prev(ck, block, h_prev)
     ck.forward(x_sh)
-    with_e, with_b = ck.saved_activation_elements(), ck.saved_activation_bytes()
+    with_e, with_b = _all_ranks(ck, ck.saved_activation_elements(), ck.saved_activation_bytes())
     f0 = ck.stats.gemm_flops
     if pl.strategy is Strategy.BOTTLENECK:
         ck._recompute_mlp_inputs()
@@ -150,7 +171,10 @@ def run_with_ckpt(pl: ShardPlan, block: DecoderBlockWeights, x, policy: CkptPoli
         ck._reforward()
         heads_dim = pl.cfg.d                  # replicated attention
     torch.cuda.synchronize()
-    recompute_flops = ck.stats.gemm_flops - f0 + 4 * b * s * s * heads_dim
+    # GEMM FLOPs + the re-run attention's (4 b s^2 x its width, the reference's sdpa_values
+    # count, model.py:205-230), summed over ranks like the reference's trace; elementwise FLOPs
+    # (the reference's EW_FLOPS, simulator.py:37) are not counted on the device path
+    recompute_flops = _all_ranks(ck, ck.stats.gemm_flops - f0 + 4 * b * s * s * heads_dim)[0]
     checks = {}
     for name, want in reference.items():
         got = ck.saved[name]

@@ -451,8 +451,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           for (int j = 0; j < 32; ++j) {
             const float ul = bf16_lo(zu[j]), uh = bf16_hi(zu[j]);
             const float vl = bf16_lo(zv[j]), vh = bf16_hi(zv[j]);
-            zu[j] = pack_bf16(silu_fast(ul) * vl, silu_fast(uh) * vh);
-            zv[j] = pack_bf16(silu_fast(vl) * ul, silu_fast(vh) * uh);
+            zu[j] = pack_bf16(silu_crossgate<__nv_bfloat16>(ul) * vl, silu_crossgate<__nv_bfloat16>(uh) * vh);
+            zv[j] = pack_bf16(silu_crossgate<__nv_bfloat16>(vl) * ul, silu_crossgate<__nv_bfloat16>(vh) * uh);
           }
           if (lane == 0) bulk_wait_read<1>();  // the a buffer's previous group has been read
           __syncwarp();

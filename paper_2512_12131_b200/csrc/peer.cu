@@ -60,7 +60,6 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
 }
 
-__device__ __forceinline__ float silu_acc(float x) { return x * sigmoidf_safe(x); }
 
 __device__ __forceinline__ float warp_sum32(float v) {
 #pragma unroll
@@ -260,8 +259,8 @@ __global__ void __launch_bounds__(256) peer_boundary_fwd_kernel(Src P, Stat ss, 
         float au[8], av[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          au[e] = silu_acc(zu[e]) * zv[e];
-          av[e] = silu_acc(zv[e]) * zu[e];
+          au[e] = silu_crossgate<__nv_bfloat16>(zu[e]) * zv[e];
+          av[e] = silu_crossgate<__nv_bfloat16>(zv[e]) * zu[e];
         }
         A.store8(row * W + cu, pack8(au));
         A.store8(row * W + cv, pack8(av));

@@ -315,6 +315,19 @@ __device__ __forceinline__ float sigmoidf_safe(float x) {
   return x >= 0.0f ? inv : e * inv;
 }
 
+// The crossgate SiLU of every bf16 site (down-GEMM sigma epilogue, btp_fixup_sigma, the peer
+// boundary kernels) is ONE formula, so a low-rank-checkpoint recompute through btp_fixup_sigma is
+// bitwise the forward that ran in the GEMM epilogue or the boundary kernel. fp32 parity mode keeps
+// the accurate x * sigmoid(x) (tanh.approx's ~2^-11 would eat the 1e-4 budget).
+template <typename T>
+__device__ __forceinline__ float silu_crossgate(float x) {
+  if constexpr (sizeof(T) == 4) {
+    return x * sigmoidf_safe(x);
+  } else {
+    return silu_fast(x);
+  }
+}
+
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 

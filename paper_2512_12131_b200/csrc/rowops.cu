@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(256) fixup_sigma_kernel(const T* P, long long 
       float au[8], av[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        au[j] = silu_f(u[j]) * v[j];
-        av[j] = silu_f(v[j]) * u[j];
+        au[j] = silu_crossgate<T>(u[j]) * v[j];
+        av[j] = silu_crossgate<T>(v[j]) * u[j];
       }
       store8(a_out + (long long)row * lda + cu, au);
       store8(a_out + (long long)row * lda + cv, av);

@@ -130,6 +130,7 @@ class ExecutorBase:
         self.sms = K.num_sms()
         self.stats = StepStats()
         self._buf: dict[str, torch.Tensor] = {}
+        self._scratch: dict[str, torch.Tensor] = self._buf   # see share_scratch
         self.saved: dict = {}
 
     def _dev(self, a, dtype=None) -> torch.Tensor:
@@ -193,6 +194,22 @@ class ExecutorBase:
         self.stats.kernel_launches += 3
 
     # ------------------------------------------------------------------ buffers
+    def share_scratch(self, scratch: dict) -> None:
+        """Home this executor's non-persistent buffers in `scratch`, one dict shared by all blocks
+        of a model: forward temporaries (n1, n2, ...), backward scratch and — under low-rank
+        checkpointing — every activation the backward recomputes. Only `_persistent` names (what
+        the backward reads from the forward, and the block output) stay per block, so an L-block
+        model holds L x (persistent set) + ONE scratch set in HBM."""
+        self._scratch = scratch
+
+    def _persistent(self, name: str) -> bool:
+        return True
+
+    def _store(self, name: str) -> dict:
+        if self._scratch is self._buf or self._persistent(name):
+            return self._buf
+        return self._scratch
+
     def buf(self, name: str, shape, dtype=None) -> torch.Tensor:
         dtype = dtype or self.act
         pc = getattr(self, "peer", None)
@@ -201,17 +218,18 @@ class ExecutorBase:
             if tuple(t.shape) != tuple(shape) or t.dtype != dtype:
                 raise PlanError(f"symmetric buffer {name}: {t.dtype} {tuple(t.shape)} != {dtype} {tuple(shape)}")
             return t
-        t = self._buf.get(name)
+        store = self._store(name)
+        t = store.get(name)
         if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
             t = torch.empty(shape, device=self.dev, dtype=dtype)
-            self._buf[name] = t
+            store[name] = t
         return t
 
     def _wgrad_parts(self, n_elems: int) -> torch.Tensor:
-        t = self._buf.get("_wg_parts")
+        t = self._scratch.get("_wg_parts")
         if t is None or t.numel() < n_elems:
             t = torch.empty(n_elems, device=self.dev, dtype=F32)
-            self._buf["_wg_parts"] = t
+            self._scratch["_wg_parts"] = t
         return t
 
     # ------------------------------------------------------------------ GEMM helpers
@@ -286,7 +304,9 @@ class ExecutorBase:
 
     def _wgrad_now(self, pairs, col_scale=None):
         """pairs: list of (dY [T, M] (MN-major A), X [T, N] (MN-major B), out fp32 [M, N]).
-        out = (dY^T X) (* col_scale) via split-K and a deterministic reduction."""
+        out = (dY^T X) (* col_scale). With split-K every split TMA-reduce-adds its fp32 tile into the
+        zeroed gradient in L2; the order of those adds across CTAs is not fixed, so split weight
+        gradients are reproducible to fp32 rounding, not bitwise, from run to run."""
         T = pairs[0][0].shape[0]
         kb = (T + 63) // 64
         tiles = sum(math.ceil(dy.shape[1] / 256) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
@@ -312,7 +332,7 @@ class ExecutorBase:
         if self.comm.live and self.residual_sharded:
             import torch.distributed as dist
 
-            dist.all_reduce(out)  # loss assembly across d-shards (outside the block's collective log)
+            dist.all_reduce(out, group=self.comm.group)  # loss over the TP group's d-shards (not logged)
         return out
 
     def loss(self, y: torch.Tensor, G: torch.Tensor) -> float:
@@ -402,6 +422,21 @@ class BTPBlockExecutor(ExecutorBase):
         self._load_weights(block)
 
     CHUNKS = (("q", "k", "v"), ("o",), ("gate", "up"), ("down",))
+
+    # per-block buffers when blocks share scratch (share_scratch): the block output, the norm
+    # statistics, the stored z's (= the forward all-reduce buffers), the lax bundle and its
+    # gradient; without low-rank ckpt also every activation the backward reads
+    _KEEP = frozenset({"y", "s1", "s2", "rl1", "rl2"})
+    _KEEP_PREFIX = ("P_", "P3_", "zown_", "hp_", "dPlax_")
+    _KEEP_NO_CKPT = frozenset({"qkv", "attn", "x_mid", "gu", "act"})
+    _KEEP_NO_CKPT_PREFIX = ("a_", "alax_")
+
+    def _persistent(self, name: str) -> bool:
+        if name in self._KEEP or name.startswith(self._KEEP_PREFIX):
+            return True
+        if self.ckpt:
+            return False
+        return name in self._KEEP_NO_CKPT or name.startswith(self._KEEP_NO_CKPT_PREFIX)
 
     def _peer_specs(self):
         """Symmetric buffers of the peer boundaries, identical (names, shapes, order) on every rank:
@@ -543,7 +578,7 @@ class BTPBlockExecutor(ExecutorBase):
         are still recorded, in plan order."""
         T, r, k = self.T, self.r, len(names)
         if norm_chunk and self.online:
-            self._buf[f"s{s_tag}"] = rl
+            self._store(f"s{s_tag}")[f"s{s_tag}"] = rl
         if self.grouping or k == 1:
             P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
             self._gemm(K.Gemm(n_in, W, P, sigma=(a_store, r // 2)))
@@ -746,11 +781,11 @@ class BTPBlockExecutor(ExecutorBase):
         n1, ss1, rl1, s1 = self._norm(x, self.gamma1, 1)
         z_qkv, a_qkv, P_qkv = self._down_boundary(("q", "k", "v"), n1, W["d_qkv"], ss1, rl1, 1, True)
         a_qkv = self._a_input(("q", "k", "v"), z_qkv, a_qkv)
-        S["s1"] = s1 if s1 is not None else self._buf["s1"]
+        S["s1"] = s1 if s1 is not None else self._store("s1")["s1"]
         qkv = self.buf("qkv", (3, T, dl))
         self._up(a_qkv, [W["u_qkv"][i] for i in range(3)], [qkv[i] for i in range(3)])
         attn, actx = self.attn.forward(qkv[0], qkv[1], qkv[2])
-        self._buf["attn"] = attn
+        self._store("attn")["attn"] = attn
         z_o, a_o, P_o = self._down_boundary(("o",), attn, W["d_o"], None, None, 0, False)
         a_o = self._a_input(("o",), z_o, a_o)
         x_mid = self.buf("x_mid", (T, dl))
@@ -759,7 +794,7 @@ class BTPBlockExecutor(ExecutorBase):
         n2, ss2, rl2, s2 = self._norm(x_mid, self.gamma2, 2)
         z_gu, a_gu, P_gu = self._down_boundary(("gate", "up"), n2, W["d_gu"], ss2, rl2, 2, True)
         a_gu = self._a_input(("gate", "up"), z_gu, a_gu)
-        S["s2"] = s2 if s2 is not None else self._buf["s2"]
+        S["s2"] = s2 if s2 is not None else self._store("s2")["s2"]
         gu = self.buf("gu", (2, T, fl))
         self._up(a_gu, [W["u_gu"][0], W["u_gu"][1]], [gu[0], gu[1]])
         act = self.buf("act", (T, fl))
@@ -784,13 +819,14 @@ class BTPBlockExecutor(ExecutorBase):
         S, T, r = self.saved, self.T, self.r
         names3, names2 = ("q", "k", "v"), ("gate", "up")
         ws = {"x": S["x"]}
-        ws["n1"], ws["n2"] = self._buf["n1"], self._buf["n2"]
-        qkv, gu = self._buf["qkv"], self._buf["gu"]
+        get = lambda n: self._store(n)[n]  # noqa: E731
+        ws["n1"], ws["n2"] = get("n1"), get("n2")
+        qkv, gu = get("qkv"), get("gu")
         for i, n in enumerate(names3):
             ws[n] = qkv[i]
         ws["gate"], ws["up"] = gu[0][:, :self.fl], gu[1][:, :self.fl]
-        ws["attn"] = S.get("attn", self._buf.get("attn"))
-        ws["x_mid"], ws["act"], ws["y"] = self._buf["x_mid"], self._buf["act"][:, :self.fl], self._buf["y"]
+        ws["attn"] = S.get("attn", self._store("attn").get("attn"))
+        ws["x_mid"], ws["act"], ws["y"] = get("x_mid"), get("act")[:, :self.fl], get("y")
         zs = {n: S["z_qkv"][i] for i, n in enumerate(names3)}
         zs.update({n: S["z_gu"][i] for i, n in enumerate(names2)})
         zs["o"], zs["down"] = S["z_o"][0], S["z_d"][0]
@@ -800,7 +836,7 @@ class BTPBlockExecutor(ExecutorBase):
             pre = "a_" if self.var == 1 else "alax_"
             for key, names in ((pre + "q_k_v", names3), (pre + "gate_up", names2), (pre + "o", ("o",)),
                                (pre + "down", ("down",))):
-                a = self._buf[key]
+                a = get(key)
                 for i, n in enumerate(names):
                     ws[f"a_in_{n}"] = a[:, i * r:(i + 1) * r]
         if not self.online:

@@ -131,6 +131,9 @@ class DecoderBlockWeights:
 def build_block(cfg: ModelConfig, variant: Variant, seed: int, element_bytes: int = 2) -> DecoderBlockWeights:
     """Deterministic weights: seed+i per full matrix, or seed+2i (B) / seed+2i+1 (A) per factor pair;
     gamma1/gamma2 from seed+101/102 (reference model.py:158-186)."""
+    variant = Variant(getattr(variant, "value", variant))
+    if not isinstance(cfg, ModelConfig):
+        cfg = ModelConfig(layers=cfg.layers, heads=cfg.heads, d=cfg.d, d_ff=cfg.d_ff, r=getattr(cfg, "r", None))
     dims = projection_dims(cfg)
     full: dict[str, Tensor] = {}
     down: dict[str, Tensor] = {}

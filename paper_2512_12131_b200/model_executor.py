@@ -50,8 +50,10 @@ class ModelExecutor(ExecutorBase):
         self.d, self.dl = pl.cfg.d, pl.cfg.d // self.tp
         self.blocks = [BTPBlockExecutor(pl, blk, self._block_comm(l), self.dev, eps, attn_backend, precision)
                        for l, blk in enumerate(mw.blocks)]
+        self._block_scratch: dict = {}
         for ex in self.blocks:
             ex.stats = self.stats  # one launch/FLOP count for the whole step
+            ex.share_scratch(self._block_scratch)  # one set of temporaries / recomputables for all blocks
         sl = slice(self.rank * self.dl, (self.rank + 1) * self.dl)
         self.W = {"embedding": self._dev(mw.embedding.values[:, sl]),   # [V, d/tp] (row-split first layer)
                   "head": self._dev(mw.head.values)}                    # [V, d] replicated

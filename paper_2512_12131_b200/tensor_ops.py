@@ -14,6 +14,7 @@ import numpy as np
 import torch
 
 from . import kernels as K
+from .interop import as_tensor
 from .tensor import DimensionError, Tensor
 
 _MAX_GROUP = 4  # problems per grouped GEMM launch
@@ -63,6 +64,7 @@ def _launch(pairs, precision: str) -> list[Tensor]:
 
 def matmul(a: Tensor, b: Tensor, *, precision: str = "fp32") -> tuple[Tensor, int]:
     """Dense 2-D product on the device; returns (result, flops) with flops = 2*M*N*K."""
+    a, b = as_tensor(a), as_tensor(b)
     _check_pair(a, b)
     m, k = a.shape
     return _launch([(a, b)], precision)[0], 2 * m * b.shape[1] * k
@@ -74,6 +76,7 @@ def batched_matmul(pairs: Sequence[tuple[Tensor, Tensor]], *, precision: str = "
     reference requires of its batched kernel (tensor.py:97-112)."""
     if not pairs:
         raise DimensionError("batched_matmul needs at least one pair")
+    pairs = [(as_tensor(a), as_tensor(b)) for a, b in pairs]
     for a, b in pairs:
         _check_pair(a, b)
     flops = sum(2 * a.shape[0] * b.shape[1] * a.shape[1] for a, b in pairs)
@@ -82,6 +85,7 @@ def batched_matmul(pairs: Sequence[tuple[Tensor, Tensor]], *, precision: str = "
 
 def swiglu(gate: Tensor, up: Tensor, *, precision: str = "fp32") -> Tensor:
     """Elementwise silu(gate) * up on the device; shapes must match exactly."""
+    gate, up = as_tensor(gate), as_tensor(up)
     if gate.shape != up.shape:
         raise DimensionError(f"swiglu operands disagree: {gate.shape} vs {up.shape}")
     dt = torch.float32 if precision == "fp32" else torch.bfloat16

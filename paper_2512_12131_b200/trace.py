@@ -92,6 +92,7 @@ def tp_block_volume(strategy, cfg, shape) -> int:
     boundaries, naive TP five [T, d] + two [T, d_ff] full-width partials, BTP seven [T, r]."""
     from .plan import Strategy
 
+    strategy = Strategy(getattr(strategy, "value", strategy))
     t = shape.b * shape.s
     if strategy is Strategy.FULL_RANK:
         return 2 * t * cfg.d

@@ -115,3 +115,24 @@ def test_ckpt_vanilla_train_step_matches_oracle():
             assert rel(st.grads["A"][n], g_ref["A"][n]) < BF16_TOL, n
             assert rel(st.grads["B"][n], g_ref["B"][n]) < BF16_TOL, n
         assert len(st.trace.record_tuples("reforward")) == (3 if grouping else 6)
+
+
+@pytest.mark.parametrize("variant", ["cola", "svd"])
+@pytest.mark.parametrize("grouping", [True, False])
+def test_ckpt_recompute_bitwise_with_fused_sigma_epilogue(variant, grouping):
+    """TP = 1 at r = 128 (CoLA-60M widths): the forward's crossgate runs in the down-GEMM epilogue
+    while the checkpoint recompute runs btp_fixup_sigma — both must use the same SiLU so the
+    recomputed activations equal the forward's bitwise."""
+    from tests.gpu_util import C60M, inputs
+    from paper_2512_12131_b200 import executor as E
+    from paper_2512_12131_b200.checkpointing import CkptPolicy, run_with_ckpt
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, plan
+
+    assert E.FUSE_SIGMA
+    b, s = 2, 128
+    blk, x, _, _ = inputs(C60M, Variant(variant), b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant(variant), online_norm=True, grouping=grouping)
+    run = run_with_ckpt(pl, blk, x, CkptPolicy.LOWRANK_BOUNDARY)
+    assert run.recompute_bitwise_ok, run.recompute_checks
+    assert run.report.reforward_collectives == 0

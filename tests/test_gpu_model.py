@@ -157,3 +157,38 @@ def test_model_tp2_matches_oracle(variant, layers):
         assert abs(loss - loss_ref) / abs(loss_ref) < 2e-2
         _check_grads(grads, g_ref, tp=2, rank=rank, cfg=cfg)
         assert fwd[-1][:3] == ("final-gather", "all-gather", "boundary")
+
+
+def test_lowrank_ckpt_frees_device_memory():
+    """with low-rank ckpt the recomputable activations of all blocks live in ONE
+    scratch set shared by the blocks, so the model's peak device memory drops (not just the
+    saved-tensor bookkeeping), and the step still matches the non-ckpt step closely."""
+    import gc
+
+    from paper_2512_12131_b200.model import ModelConfig, RunShape, Variant, build_model, token_batch
+    from paper_2512_12131_b200.model_executor import model_train_step
+    from paper_2512_12131_b200.plan import Strategy, plan
+
+    layers, b, s = 6, 2, 512
+    cfg = ModelConfig(layers=layers, heads=8, d=512, d_ff=1376, r=128)
+    mw = build_model(cfg, Variant.COLA, 0, V)
+    ids, tg = token_batch(b, s, V)
+    peaks, losses = {}, {}
+    for ckpt in (False, True):
+        gc.collect()
+        torch.cuda.empty_cache()
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True,
+                  lowrank_ckpt=ckpt)
+        loss, ex = model_train_step(pl, mw, ids, tg)
+        torch.cuda.synchronize()
+        peaks[ckpt] = torch.cuda.max_memory_allocated() - base
+        losses[ckpt] = loss
+        del ex
+    T = b * s
+    # per block, ckpt drops at least qkv + attn + x_mid + 2 x gu + act + a_* (bf16) minus one shared set
+    per_block = 2 * T * (3 * cfg.d + cfg.d + cfg.d + 3 * cfg.d_ff + 7 * cfg.r)
+    assert peaks[False] - peaks[True] > 0.5 * (layers - 1) * per_block, peaks
+    assert abs(losses[True] - losses[False]) <= 1e-3 * abs(losses[False])
