@@ -10,9 +10,18 @@ fan-in-scaled random-init weights. One step = forward + loss + backward (all wei
     python bench.py --impl reference [...]                     # CPU reference arm (oracle port)
     torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: one rank per GPU, NCCL
 
+    python bench.py --gpus N ...                               # same: self-launches N ranks via torch.distributed.run
+
 Timing: W warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
 launching stream, max over ranks. Working set (~1.3 GB of activations) >> L2 (126 MB), so no
-L2 flush is needed. Prints ONE JSON line on rank 0.
+L2 flush is needed. Prints ONE JSON line on rank 0 with, beside the contract keys:
+  roofline      the tcgen05 GEMM family, per-launch CUDA events inside a replayed graph
+  baselines     the same kernels under naive low-rank TP and full-rank Megatron TP (same N, shape,
+                step), and BTP's speed-up over each (north_star targets 1.8x / 1.4x at TP=8)
+  comm          (N > 1) the plan's boundary all-reduces timed standalone: NCCL bus GB/s vs 900
+  cpu_baseline  the oracle port on rank 0's host cores (+ `reference_itself`: btpsim's own
+                forward at config C1 when baseline/_ref is installed)
+`--dry-run` (CPU, gloo) exercises the launch path and the line's schema without a GPU.
 """
 
 from __future__ import annotations
@@ -198,54 +207,100 @@ def run_reference(args, cfg):
                                    "restatement of btpsim (reference itself is forward-only)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.dry_run:
+        line["cpu_baseline"]["reference_itself"] = _reference_itself()
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------------------------- GPU arm
-def run_ours(args, cfg):
+def _reduce_max(dist, world, value, dev):
+    """Max over ranks of a per-rank scalar (device time: max over ranks)."""
+    if world == 1:
+        return value
     import torch
-    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
-    from paper_2512_12131_b200 import executor as _executor
-    from paper_2512_12131_b200.api import BlockTrainer
 
-    if args.no_fuse_sigma:
-        _executor.FUSE_SIGMA = False
-    if args.concurrent_wgrad:
-        _executor.ExecutorBase.concurrent_wgrad = True
-    if args.gemm_pair >= 0:
-        from paper_2512_12131_b200 import kernels as _K
+class _Timer:
+    """CUDA events on the launching (current) stream; perf_counter in --dry-run (no device)."""
 
-        _K.set_pair_mode(args.gemm_pair)
-    from paper_2512_12131_b200.model import RunShape, Variant, build_block, fan_in_scaled
+    def __init__(self, dry: bool):
+        self.dry = dry
+
+    def __enter__(self):
+        if self.dry:
+            self.t0 = time.perf_counter()
+        else:
+            import torch
+
+            self.st = torch.cuda.current_stream()
+            self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            self.e0.record(self.st)
+        return self
+
+    def __exit__(self, *exc):
+        if self.dry:
+            self.ms = (time.perf_counter() - self.t0) * 1e3
+        else:
+            self.e1.record(self.st)
+
+    def elapsed(self) -> float:
+        if self.dry:
+            return self.ms
+        self.e1.synchronize()
+        return self.e0.elapsed_time(self.e1)
+
+
+class _DryTrainer:
+    """--dry-run stand-in for BlockTrainer (CPU, gloo): exercises the launch path, the rendezvous,
+    barriers, max-over-ranks timing and the JSON line without a GPU. Never a measurement."""
+
+    def __init__(self, pl):
+        import torch
+
+        self.pl, self.graphed, self.kernel_launches = pl, False, 0
+        self.w = torch.randn(64, 64)
+
+    def device_inputs(self, x, G):
+        import torch
+
+        return torch.as_tensor(x, dtype=torch.float32), torch.as_tensor(G, dtype=torch.float32)
+
+    def pinned_host_inputs(self, x, G):
+        return self.device_inputs(x, G)
+
+    def step_device(self, x, g):
+        (x.reshape(-1, 64)[:256] @ self.w).sum()
+
+    def fit(self, xs, g):
+        for x in xs:
+            self.step_device(x, g)
+        return [0.0] * len(xs)
+
+    def time_gemms(self, x, g):
+        return {"ms": 0.0, "flops": 0.0, "tflops": 0.0, "launches": 0, "per_launch": []}
+
+
+def _make_trainer(args, cfg, strategy, shape, comm):
+    """The timed object: BlockTrainer (or ModelTrainer with --model) for one TP strategy."""
+    from paper_2512_12131_b200.model import Variant, build_block, fan_in_scaled
     from paper_2512_12131_b200.plan import Strategy, plan
     from paper_2512_12131_b200.tensor import seeded_fill
 
-    b, s, tp = args.b, args.s, world
-    comm = None
-    if args.emulate_tp:
-        if world != 1:
-            raise SystemExit("--emulate-tp runs one rank's share on ONE GPU (no torchrun)")
-        from paper_2512_12131_b200.comm import TPComm
-
-        tp = args.emulate_tp
-        comm = TPComm.emulated(tp, 0)
-    shape = RunShape(b, s, tp)
-    strategy = Strategy(args.strategy)
+    b, s = shape.b, shape.s
     variant = Variant.FULL_RANK if strategy is Strategy.FULL_RANK else Variant(args.variant)
     pl = plan(strategy, cfg, shape, None if variant is Variant.FULL_RANK else variant,
               online_norm=strategy is Strategy.BOTTLENECK, grouping=not args.no_grouping,
-              lowrank_ckpt=args.ckpt)
+              lowrank_ckpt=args.ckpt and strategy is not Strategy.FULL_RANK)
+    if args.dry_run:
+        x = seeded_fill((b, s, cfg.d), 10000).values
+        return _DryTrainer(pl), pl, variant, x, x
+    from paper_2512_12131_b200.api import BlockTrainer
+
     if args.model:
         # the multi-layer model (SURVEY §8f row 1): embedding shard + L blocks + LM head + cross-entropy
         from paper_2512_12131_b200.api import ModelTrainer
@@ -258,61 +313,198 @@ def run_ours(args, cfg):
         trainer = ModelTrainer(pl, mw, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
                                optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary,
                                peer_provider=args.peer_provider)
-    else:
-        blk = fan_in_scaled(build_block(cfg, variant, 0))
-        x = seeded_fill((b, s, cfg.d), 10000).values
-        G = seeded_fill((b, s, cfg.d), 30000).values
-        trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
-                               optimizer=not args.no_optimizer, comm=comm, boundary=args.boundary,
-                               peer_provider=args.peer_provider)
-        if variant is Variant.LAX:  # a resident previous-layer bundle, like G (the merge runs every step)
-            from paper_2512_12131_b200.model import seeded_h_prev
+        return trainer, pl, variant, x, G
+    blk = fan_in_scaled(build_block(cfg, variant, 0))
+    x = seeded_fill((b, s, cfg.d), 10000).values
+    G = seeded_fill((b, s, cfg.d), 30000).values
+    boundary = args.boundary if strategy is Strategy.BOTTLENECK else "nccl"
+    trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
+                           optimizer=not args.no_optimizer, comm=comm, boundary=boundary,
+                           peer_provider=args.peer_provider)
+    if variant is Variant.LAX:  # a resident previous-layer bundle, like G (the merge runs every step)
+        from paper_2512_12131_b200.model import seeded_h_prev
 
-            trainer.ex.set_h_prev({n: h.values for n, h in seeded_h_prev(cfg, shape, 20000).items()})
-    x_dev, g_dev = trainer.device_inputs(x, G)
+        trainer.ex.set_h_prev({n: h.values for n, h in seeded_h_prev(cfg, shape, 20000).items()})
+    return trainer, pl, variant, x, G
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
 
+def _time_steps(args, trainer, x_dev, g_dev, barrier, clk=None):
+    """W untimed warm-up steps, then exactly K steps between barrier + synchronize; ms per step
+    on this rank (the caller takes the max over ranks) and the launches counted in the region."""
     for _ in range(args.warmup):
         trainer.step_device(x_dev, g_dev)
     barrier()
     launches0 = trainer.kernel_launches
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(st)
-        for _ in range(args.steps):
-            trainer.step_device(x_dev, g_dev)
-        e1.record(st)
+    tm = _Timer(args.dry_run)
+    if clk is not None:
+        clk.__enter__()
+    try:
+        with tm:
+            for _ in range(args.steps):
+                trainer.step_device(x_dev, g_dev)
         barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    launches = (trainer.kernel_launches - launches0)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    finally:
+        if clk is not None:
+            clk.__exit__(None, None, None)
+    return tm.elapsed() / args.steps, trainer.kernel_launches - launches0
+
+
+def _comm_profile(args, pl, comm_tp, world, dist, dev, ms_step):
+    """TP > 1: every forward chunk-boundary collective of the plan (`enumerate_collectives`, the
+    reference's SimGroup calls simulator.py:123-186) timed standalone through TPComm — the bf16
+    [T, k*r] payload and, where the plan has one, its fp32 rider in the same NCCL group — with CUDA
+    events, max over ranks. Bus bandwidth = payload bytes * 2(n-1)/n / time (ring all-reduce
+    convention, nccl-tests busbw) against NVLink 5's 900 GB/s per direction. The backward mirrors
+    each forward boundary (same payload), so per step = 2 x the forward sum; `share_of_step` is
+    that un-overlapped sum over the measured step (an upper bound: backward reductions overlap the
+    weight-gradient GEMMs)."""
+    import torch
+
+    from paper_2512_12131_b200.comm import TPComm
+    from paper_2512_12131_b200.plan import enumerate_collectives
+
+    comm = TPComm.from_env()
+    dt = torch.float32 if args.dry_run else torch.bfloat16
+    rows, reps = [], 20
+    for pc in enumerate_collectives(pl):
+        if pc.tag != "block" or pc.chunk_id.endswith("-stat"):
+            continue
+        main = torch.ones(pc.elements, dtype=dt, device=dev)
+        rider = torch.ones(dict(pc.extras).get("fused-stat", 0), dtype=torch.float32, device=dev) \
+            if pc.extras else None
+
+        def once():
+            if rider is not None:
+                comm.wait(comm.all_reduce_coalesced_start(main, rider, pc.chunk_id, record=False))
+            else:
+                comm.wait(comm.all_reduce_start(main, pc.chunk_id, record=False))
+
+        for _ in range(5):
+            once()
+        if not args.dry_run:
+            torch.cuda.synchronize()
+        dist.barrier()
+        tm = _Timer(args.dry_run)
+        with tm:
+            for _ in range(reps):
+                once()
+        ms = _reduce_max(dist, world, tm.elapsed() / reps, dev)
+        nbytes = pc.elements * main.element_size() + (0 if rider is None else rider.numel() * 4)
+        bus = nbytes * 2 * (world - 1) / world / (ms / 1e3) / 1e9
+        rows.append({"chunk": pc.chunk_id, "elements": pc.elements, "rider": 0 if rider is None else rider.numel(),
+                     "bytes": nbytes, "us": ms * 1e3, "bus_gbs": bus})
+        del main, rider
+    fwd_ms = sum(r["us"] for r in rows) / 1e3
+    tot_bytes = sum(r["bytes"] for r in rows)
+    bus = tot_bytes * 2 * (world - 1) / world / (fwd_ms / 1e3) / 1e9 if fwd_ms else None
+    return {"backend": dist.get_backend(), "boundary": args.boundary, "per_boundary_fwd": rows,
+            "boundary_ms_per_step": 2 * fwd_ms, "share_of_step": 2 * fwd_ms / ms_step,
+            "bus_gbs": bus, "peak_gbs": 900.0, "frac": None if bus is None else bus / 900.0,
+            "payload_bytes_per_step": 2 * tot_bytes,
+            "note": "standalone NCCL all-reduces of the plan's boundary payloads (bf16 + fp32 rider), "
+                    "busbw = bytes*2(n-1)/n/t; share is un-overlapped (upper bound)"}
+
+
+def _reference_itself():
+    """The reference's own forward (btpsim, installed unmodified in baseline/_ref) on config C1:
+    execute_forward(plan(BOTTLENECK, CoLA-60M, RunShape(8, 256, 1), COLA, online, grouped),
+    build_block(.., 0), x) — SURVEY §8(d). Forward-only: the reference has no backward."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "btpsim").is_dir():
+        return {"unavailable": "baseline/_ref (pip --target install of the reference) not present"}
+    sys.path.insert(0, str(ref))
+    try:
+        import btpsim  # noqa: F401
+        from btpsim.model import ModelConfig, RunShape, Variant, build_block
+        from btpsim.plan import Strategy, plan
+        from btpsim.simulator import execute_forward
+        from btpsim.tensor import seeded_fill
+    finally:
+        sys.path.remove(str(ref))
+    cfg = ModelConfig(layers=8, heads=8, d=512, d_ff=1376, r=128)
+    b, s = 8, 256
+    pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    blk = build_block(cfg, Variant.COLA, 0)
+    x = seeded_fill((b, s, cfg.d), 10000)
+    t0 = time.perf_counter()
+    execute_forward(pl, blk, x)
+    sec = time.perf_counter() - t0
+    return {"value": b * s / sec, "unit": UNIT, "seconds": sec, "nproc": os.cpu_count(),
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS"), "cores": 1,
+            "label": "fwd-only; reference has no backward (btpsim.execute_forward, elementwise NumPy)",
+            "config": "C1 CoLA-60M block (d512 d_ff1376 r128 h8) b=8 s=256 TP=1, BTP online grouped"}
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        dev = torch.device("cpu")
+        if world > 1:
+            dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+
+    if not args.dry_run:
+        from paper_2512_12131_b200 import executor as _executor
+
+        if args.no_fuse_sigma:
+            _executor.FUSE_SIGMA = False
+        if args.concurrent_wgrad:
+            _executor.ExecutorBase.concurrent_wgrad = True
+        if args.gemm_pair >= 0:
+            from paper_2512_12131_b200 import kernels as _K
+
+            _K.set_pair_mode(args.gemm_pair)
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy
+
+    b, s, tp = args.b, args.s, world
+    comm = None
+    if args.emulate_tp:
+        if world != 1:
+            raise SystemExit("--emulate-tp runs one rank's share on ONE GPU (no torchrun)")
+        from paper_2512_12131_b200.comm import TPComm
+
+        tp = args.emulate_tp
+        comm = TPComm.emulated(tp, 0)
+    shape = RunShape(b, s, tp)
+    strategy = Strategy(args.strategy)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        if not args.dry_run:
+            torch.cuda.synchronize()
+
+    trainer, pl, variant, x, G = _make_trainer(args, cfg, strategy, shape, comm)
+    x_dev, g_dev = trainer.device_inputs(x, G)
+    clk = None if args.dry_run else ClockSampler(local)
+    ms, launches = _time_steps(args, trainer, x_dev, g_dev, barrier, clk)
+    ms = _reduce_max(dist, world, ms, dev)
     value = b * s / (ms / 1e3)
 
     # ---- end to end through the public API: pinned host inputs -> H2D -> step -> loss D2H
     # x is the per-step data (two distinct pinned host batches, alternating); G, the fixed loss
     # projection, is copied once per fit() call. Batch i+1's H2D overlaps step i on a side stream.
     xh, gh = trainer.pinned_host_inputs(x, G)
-    xh2 = xh.clone().pin_memory()
+    xh2 = xh.clone().pin_memory() if not args.dry_run else xh.clone()
     trainer.fit([xh, xh2, xh], gh)
     barrier()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(st)
-    losses = trainer.fit([xh if i % 2 == 0 else xh2 for i in range(args.steps)], gh)
-    e3.record(st)
+    tm = _Timer(args.dry_run)
+    with tm:
+        losses = trainer.fit([xh if i % 2 == 0 else xh2 for i in range(args.steps)], gh)
     barrier()
-    ms_e2e = e2.elapsed_time(e3) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = _reduce_max(dist, world, tm.elapsed() / args.steps, dev)
     e2e = {"value": b * s / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
            "d2h_bytes_per_step": 4, "loss": losses[-1], "api": "BlockTrainer.fit (pinned host batches H2D per step on a copy stream; each step's loss copied D2H behind it and read by the host one step later)",
            "h2d_once_per_call_bytes": int(gh.numel() * gh.element_size())}
@@ -326,24 +518,61 @@ def run_ours(args, cfg):
     if args.model:  # L blocks (sharded) + the replicated head: 3 * 2 T d V on every rank
         flops = flops * trainer.ex.blocks.__len__() + 3 * 2 * b * s * cfg.d * args.vocab
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "r01_gemm_traffic_summary.json"
+    tfile = ROOT / "profiles" / "r02_gemm_traffic_summary.json"
+    if not tfile.exists():
+        tfile = ROOT / "profiles" / "r01_gemm_traffic_summary.json"
     if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model:
         t = json.loads(tfile.read_text())
         traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
+    g_ms = gemm["ms"] or float("nan")
     roof = {"bound": "tensor", "kernel": "btp gemm_kernel (all tcgen05 GEMM launches of one step)",
             "achieved": gemm["tflops"], "peak": peak_sus, "unit": "TFLOP/s", "frac": gemm["tflops"] / peak_sus,
             "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write, ncu)", "traffic_source": traffic_src,
             "algorithmic_flops_per_launch": gemm["flops"] / max(gemm["launches"], 1),
-            "avg_launch_us": gemm["ms"] * 1e3 / max(gemm["launches"], 1),
+            "avg_launch_us": g_ms * 1e3 / max(gemm["launches"], 1),
             "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
-            "gemm_share_of_step": gemm["ms"] / ms, "gemm_launches_per_step": gemm["launches"],
+            "gemm_share_of_step": g_ms / ms, "gemm_launches_per_step": gemm["launches"],
             "step_frac_of_peak": flops / (ms / 1e3) / 1e12 / peak_sus}
+    graphed = trainer.graphed
+    del trainer, x_dev, g_dev, xh, xh2, gh
+    if not args.dry_run:
+        torch.cuda.empty_cache()
+
+    # ---- the boundary collectives (TP > 1): NCCL bus bandwidth vs NVLink, share of the step
+    comm_prof = None
+    if world > 1 and not args.emulate_tp and strategy is Strategy.BOTTLENECK and args.boundary == "nccl":
+        comm_prof = _comm_profile(args, pl, tp, world, dist, dev, ms)
+
+    # ---- same-box baselines (north_star): the same kernels under naive low-rank TP and under
+    # full-rank Megatron TP, same N, same block shape, same step (fwd+bwd+AdamW)
+    baselines = None
+    if not args.no_baselines and not args.model and strategy is Strategy.BOTTLENECK:
+        baselines = {}
+        for key, strat in (("naive_tp", Strategy.VANILLA), ("full_rank", Strategy.FULL_RANK)):
+            if args.emulate_tp:
+                from paper_2512_12131_b200.comm import TPComm
+
+                comm = TPComm.emulated(tp, 0)
+            tr, bpl, bvar, bx, bG = _make_trainer(args, cfg, strat, shape, comm)
+            bxd, bgd = tr.device_inputs(bx, bG)
+            bms, _ = _time_steps(args, tr, bxd, bgd, barrier)
+            bms = _reduce_max(dist, world, bms, dev)
+            lowrank = bvar is not Variant.FULL_RANK
+            baselines[key] = {"value": b * s / (bms / 1e3), "unit": UNIT, "ms_per_step": bms,
+                              "strategy": strat.value, "variant": bvar.value, "grouping": bpl.grouping,
+                              "algorithmic_tflops_per_gpu": flops_per_step(cfg, b, s, lowrank=lowrank) / tp / (bms / 1e3) / 1e12}
+            del tr, bxd, bgd
+            if not args.dry_run:
+                torch.cuda.empty_cache()
+        baselines["btp_over_naive_tp"] = value / baselines["naive_tp"]["value"]
+        baselines["btp_over_full_rank"] = value / baselines["full_rank"]["value"]
+        baselines["targets"] = {"btp_over_naive_tp": 1.8, "btp_over_full_rank": 1.4, "at": "TP=8 (north_star)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded uniform inputs, fan-in-scaled random init)",
-        "config": {"workload": (f"CoLA-{args.config} model ({len(trainer.ex.blocks)} blocks + d-sharded embedding + "
+        "config": {"workload": (f"CoLA-{args.config} model ({args.layers or cfg.layers} blocks + d-sharded embedding + "
                                 f"replicated LM head V={args.vocab} + cross-entropy) " if args.model else
                                 f"CoLA-{args.config} decoder block ")
                                + (f"[{variant.value} variant] " if variant not in (Variant.COLA, Variant.FULL_RANK)
@@ -353,32 +582,61 @@ def run_ours(args, cfg):
                                f"TP={tp}{' lowrank-ckpt' if pl.lowrank_ckpt else ''}",
                    "d": cfg.d, "d_ff": cfg.d_ff, "r": cfg.r, "heads": cfg.heads, "global_batch": b, "seq_len": s,
                    "tokens_per_step": b * s, "parallelism": f"tp{tp}", "l2": "inputs larger than L2 (no flush)",
-                   "cuda_graph": trainer.graphed,
+                   "cuda_graph": graphed,
                    "boundary": args.boundary if tp > 1 else "none (tp=1)",
                    "optimizer": None if args.no_optimizer else dict(ADAMW, kind="AdamW fp32 master+moments, fused"),
                    "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
-        "clocks": clk.summary(),
+        "clocks": clk.summary() if clk is not None else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry-run"]},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": roof,
         "algorithmic_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
     }
+    if comm_prof is not None:
+        line["comm"] = comm_prof
+    if baselines is not None:
+        line["baselines"] = baselines
+    if args.dry_run:
+        line["dry_run"] = True
+        line["data"] = "dry run (CPU, gloo): launch path and line schema only, NOT a measurement"
     if args.emulate_tp:
         line["metric"] = (f"EMULATED per-rank compute of a TP={tp} step on one GPU (collectives not executed; "
                           "value = tokens/s if comm were free; not the bench metric)")
         line["emulated_tp"] = tp
         line["scaling"] = None
         args.no_cpu_baseline = True
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, times, threads = cpu_oracle_rate(cfg, s, seconds_budget=args.cpu_seconds)
+    if rank == 0 and not args.no_cpu_baseline:
+        # the CPU arm runs on rank 0 only, after the timed work (other ranks wait at the barrier)
+        rate, times, threads = cpu_oracle_rate(cfg, s, seconds_budget=args.cpu_seconds,
+                                               max_steps=1 if args.dry_run else None)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"b=1 s={s} (1 of {b} sequences) CoLA-{args.config} block fwd+bwd, float64 "
                                           f"NumPy/BLAS oracle + AdamW, {len(times)} steps"}
+        if not args.dry_run:
+            line["cpu_baseline"]["reference_itself"] = _reference_itself()
+    if world > 1:
+        dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def _self_launch(argv, gpus):
+    """`python bench.py --gpus N` without torchrun: re-launch this script as N ranks (one process
+    per GPU) through torch.distributed.run on 127.0.0.1; rank 0's line is the output."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    # torchrun's own parser would take the short "--s" for an abbreviation of its options
+    argv = ["--seq-len" if a == "--s" else "--batch" if a == "--b" else a for a in argv]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
 
 
 def main(argv=None):
@@ -388,8 +646,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="1b")
-    ap.add_argument("--b", type=int, default=4)
-    ap.add_argument("--s", type=int, default=4096)
+    ap.add_argument("--b", "--batch", dest="b", type=int, default=4)
+    ap.add_argument("--s", "--seq-len", dest="s", type=int, default=4096)
     ap.add_argument("--strategy", default="btp", choices=["btp", "vanilla", "full-rank"])
     ap.add_argument("--variant", default="cola", choices=["cola", "svd", "lax"],
                     help="low-rank block variant (lax: merges a resident seeded h bundle every step)")
@@ -402,6 +660,9 @@ def main(argv=None):
                     help="CTA-pair GEMM tiles: 0 off, 1 plain/sigma epilogues, 2 also residual epilogues (A/B)")
     ap.add_argument("--concurrent-wgrad", action="store_true", help="weight-gradient GEMMs on a side stream (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the naive-TP / full-rank same-box arms")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU + gloo: launch path, rendezvous and JSON schema only (contract test; no measurement)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
@@ -415,7 +676,10 @@ def main(argv=None):
     ap.add_argument("--emulate-tp", type=int, default=0,
                     help="time ONE rank's compute of a TP=N plan on one GPU, collectives not executed "
                          "(compute-only; NOT the bench metric)")
-    args = ap.parse_args(argv)
+    raw = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(raw, args.gpus)
     from paper_2512_12131_b200.model import COLA_60M, preset
 
     cfg = COLA_60M if args.config == "60m" else preset(args.config)

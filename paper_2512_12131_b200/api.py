@@ -56,8 +56,9 @@ class StepResult:
 
 
 def _normalise(pl, block):
-    """Our plan / block for ours or the reference's own objects (interop.py)."""
-    return as_plan(pl), as_block(block)
+    """Our plan / block for ours or the reference's own objects (interop.py). block=None: the
+    caller supplies its own executor (ModelTrainer)."""
+    return as_plan(pl), None if block is None else as_block(block)
 
 
 def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
@@ -299,7 +300,7 @@ class BlockTrainer:
 
     def _tail(self, g):
         self.loss_buf = self.ex.loss_device(self._y, g)
-        self.ex.backward(g)
+        self._dx = self.ex.backward(g)
         if self.adamw is not None:
             self.ex.optimizer_step(**self.adamw)
 
@@ -435,18 +436,24 @@ class BlockTrainer:
         self.ex.gemm_timer = []
         self._eager(x, g)  # allocate every buffer outside the capture
         torch.cuda.synchronize()
-        if self.ex.comm.live:  # collectives stay eager; timings then include host gaps
+        if self.ex.comm.live and not self.use_graph:  # collectives eager; timings then include host gaps
             rec, self.ex.gemm_timer = self.ex.gemm_timer, None
             return self._gemm_summary(rec)
+        # live NCCL collectives are captured with the step (as in step_device), so every
+        # interval is device time only at TP > 1 too
         graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         saved = self.ex.stats.kernel_launches
-        with torch.cuda.stream(side):
-            self.ex.gemm_timer = []
-            with torch.cuda.graph(graph, stream=side):
-                self._eager(x, g)
-        self.ex.stats.kernel_launches = saved
+        n_rec = len(self.ex.comm.trace.records)
+        try:
+            with torch.cuda.stream(side):
+                self.ex.gemm_timer = []
+                with torch.cuda.graph(graph, stream=side):
+                    self._eager(x, g)
+        finally:
+            self.ex.stats.kernel_launches = saved
+            del self.ex.comm.trace.records[n_rec:]
         torch.cuda.current_stream().wait_stream(side)
         for _ in range(2):
             graph.replay()

@@ -171,15 +171,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int b = 0; b < 16; ++b) mbar_init(&aux_bar_all[b], 1);
     fence_barrier_init();
   }
+  // CTA pair: each CTA's allocating warp names its OWN result word (slot[rank]) — the pair
+  // allocation may report the address into both CTAs' shared memory, and two writers of one word
+  // (same value) were racecheck hazards; with distinct words every word has one writer.
+  uint32_t* my_slot = tmem_slot + (kPair ? cluster_ctarank() : 0u);
   if (warp == 2) {
-    if constexpr (kPair) tmem_alloc_pair<C::kTmemCols>(tmem_slot);
-    else tmem_alloc<C::kTmemCols>(tmem_slot);
+    if constexpr (kPair) tmem_alloc_pair<C::kTmemCols>(my_slot);
+    else tmem_alloc<C::kTmemCols>(my_slot);
   }
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all();  // peer barriers must exist before any remote arrive
   else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = *my_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)

@@ -434,6 +434,10 @@ class BTPBlockExecutor(ExecutorBase):
     def _persistent(self, name: str) -> bool:
         if name in self._KEEP or name.startswith(self._KEEP_PREFIX):
             return True
+        # lax: dL/dh_prev are views of the reduced dA, read by the PREVIOUS block's backward
+        # (its dL/dh_cur) after this block's backward returned — they must outlive the scratch
+        if self.lax and name.startswith(("dA_", "dA3_")):
+            return True
         if self.ckpt:
             return False
         return name in self._KEEP_NO_CKPT or name.startswith(self._KEEP_NO_CKPT_PREFIX)

@@ -2,17 +2,22 @@
 gloo ranks sharing the GPU), mirroring the reference's test_ckpt.py:79-125: the BTP re-forward is
 collective-free, the vanilla one replays its chunk all-reduces (3 grouped / 6 ungrouped; the down
 chunk's output feeds nothing backward needs), both rebuild every tensor BITWISE, BTP frees less
-memory per rank but at a far better memory-per-recompute efficiency — and the checkpointed
-training step still matches the oracle."""
+memory, and ΔMem / eff_ckpt order the two strategies as the reference itself does at this shape
+(tests/golden/ckpt_small.json) — and the checkpointed training step still matches the oracle."""
 
+import json
 import os
 import socket
+
+from pathlib import Path
 
 import pytest
 import torch
 import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
+
+REF_CKPT = json.loads((Path(__file__).resolve().parent / "golden" / "ckpt_small.json").read_text())
 
 
 def _port():
@@ -88,10 +93,18 @@ def test_ckpt_btp_vs_vanilla_tp2():
                 assert o["calls"] == 0 and o["ring"] == 0, key
             else:
                 assert o["calls"] == (3 if grouping else 6) and o["ring"] > 0, key
-        for variant in ("svd", "lax"):
+        # the reference itself at this shape (tests/golden/ckpt_small.json, make_ckpt_golden.py):
+        # same collective counts and ring elements; ΔMem and eff_ckpt in the reference's ORDER
+        for (strategy, variant, grouping), o in out.items():
+            ref = REF_CKPT[f"{strategy}/{variant}/{int(grouping)}"]
+            assert o["calls"] == ref["reforward_collectives"], (strategy, variant, grouping)
+            assert o["ring"] == ref["reforward_ring_elements"], (strategy, variant, grouping, o["ring"])
+        for variant in ("svd", "lax", "cola"):
             van, btp = out[("vanilla", variant, True)], out[("btp", variant, True)]
+            rv, rb = REF_CKPT[f"vanilla/{variant}/1"], REF_CKPT[f"btp/{variant}/1"]
             assert van["dmem"] > btp["dmem"] > 0, (rank, variant)
-            assert btp["eff"] > van["eff"], (rank, variant)
+            assert rv["delta_mem_elements"] > rb["delta_mem_elements"]
+            assert (btp["eff"] > van["eff"]) == (rb["eff_ckpt"] > rv["eff_ckpt"]), (rank, variant, btp, van)
 
 
 def test_ckpt_vanilla_train_step_matches_oracle():
