@@ -282,7 +282,8 @@ class _DryTrainer:
         return [0.0] * len(xs)
 
     def time_gemms(self, x, g):
-        return {"ms": 0.0, "flops": 0.0, "tflops": 0.0, "launches": 0, "per_launch": []}
+        return {"ms": 0.0, "flops": 0.0, "tflops": 0.0, "launches": 0, "per_launch": [],
+                "attention_ms": {"fwd": 0.0, "bwd": 0.0}}
 
 
 def _make_trainer(args, cfg, strategy, shape, comm):
@@ -465,6 +466,14 @@ def run_ours(args, cfg):
             from paper_2512_12131_b200 import kernels as _K
 
             _K.set_pair_mode(args.gemm_pair)
+        if args.gemm_st_global >= 0:
+            from paper_2512_12131_b200 import kernels as _K
+
+            _K.set_st_global(bool(args.gemm_st_global))
+        if args.gemm_res >= 0:
+            from paper_2512_12131_b200 import kernels as _K
+
+            _K.set_res4(args.gemm_res)
     from paper_2512_12131_b200.model import RunShape, Variant
     from paper_2512_12131_b200.plan import Strategy
 
@@ -533,6 +542,12 @@ def run_ours(args, cfg):
             "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
             "gemm_share_of_step": g_ms / ms, "gemm_launches_per_step": gemm["launches"],
             "step_frac_of_peak": flops / (ms / 1e3) / 1e12 / peak_sus}
+    att = gemm.get("attention_ms", {})
+    # where the step goes (device time of one graph-replayed step, kernels serialised): the
+    # tcgen05 GEMMs, cuDNN attention (not a changed subsystem), everything else (row kernels, AdamW,
+    # collectives, gaps) — a slow run's line says which part moved
+    breakdown = {"gemm_ms": gemm["ms"], "attention_fwd_ms": att.get("fwd"), "attention_bwd_ms": att.get("bwd"),
+                 "other_ms": ms - gemm["ms"] - sum(v for v in att.values() if v)}
     graphed = trainer.graphed
     del trainer, x_dev, g_dev, xh, xh2, gh
     if not args.dry_run:
@@ -591,6 +606,7 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "roofline": roof,
         "algorithmic_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
+        "breakdown": breakdown,
     }
     if comm_prof is not None:
         line["comm"] = comm_prof
@@ -658,6 +674,11 @@ def main(argv=None):
     ap.add_argument("--no-fuse-sigma", action="store_true", help="TP=1: separate fix-up/sigma kernel (A/B)")
     ap.add_argument("--gemm-pair", type=int, default=-1, choices=[-1, 0, 1, 2],
                     help="CTA-pair GEMM tiles: 0 off, 1 plain/sigma epilogues, 2 also residual epilogues (A/B)")
+    ap.add_argument("--gemm-st-global", type=int, default=-1, choices=[-1, 0, 1],
+                    help="GEMM epilogue stores: 1 coalesced st.global, 0 TMA bulk stores (A/B)")
+    ap.add_argument("--gemm-res", type=int, default=-1, choices=[-1, 0, 1, 2, 3],
+                    help="residual-epilogue layout: 0 per-chunk, 1 whole tile, 2 producer-warp pipeline, "
+                         "3 by width (default) (A/B)")
     ap.add_argument("--concurrent-wgrad", action="store_true", help="weight-gradient GEMMs on a side stream (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true", help="skip the naive-TP / full-rank same-box arms")

@@ -101,9 +101,16 @@ int btp_gemm_scatter(const btp_gemm_problem* problems, int n, int bn_hint, void*
  * (residual epilogues stay single-CTA); 2 (default) = pair tiles for residual epilogues too;
  * 0 = single-CTA 128 x BN tiles everywhere. Returns the previous setting. */
 int btp_gemm_set_pair(int enable);
-/* Residual epilogues: 1 (default) stage a tile's whole residual (four 64-column chunk buffers per
- * epilogue warp, one TMA round trip per tile), 0 = per-chunk prefetch; returns the previous value. */
+/* Residual epilogues: 3 (default) by output width — every residual problem N <= 1024 (the TP >= 2
+ * o / down up-projections): pipelined residual slots refilled one tile ahead by a producer warp,
+ * with st.global stores; wider: stage a tile's whole residual. 2 = always the pipeline (CTA-pair
+ * launches), 1 = always whole-tile staging (four 64-column chunk buffers per epilogue warp, one TMA
+ * round trip per tile), 0 = per-chunk prefetch. Returns the previous value. */
 int btp_gemm_set_res4(int enable);
+/* Epilogue stores: 0 (default) TMA bulk-tensor stores, 1 = coalesced st.global from the swizzled
+ * staging chunk (4 rows x 128 B per warp instruction) for every launch. Split-K reduce-adds and the
+ * scatter mode always use the TMA reduce. Returns the previous value. */
+int btp_gemm_set_st_global(int enable);
 
 /* Online RMSNorm (local form) fused with the residual add, one row per warp.
  *   v = x (+ branch); if x_out: x_out = bf16(v); stats use the rounded v

@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "btp_gemm_scatter",
     "btp_gemm_set_pair",
     "btp_gemm_set_res4",
+    "btp_gemm_set_st_global",
     "btp_rmsnorm_residual",
     "btp_rmsnorm_apply",
     "btp_fixup_sigma",
@@ -148,6 +149,7 @@ _SIGNATURES = {
     "btp_gemm_f32": [ctypes.POINTER(GemmProblem), _I, _P],
     "btp_gemm_set_pair": [_I],
     "btp_gemm_set_res4": [_I],
+    "btp_gemm_set_st_global": [_I],
     "btp_adamw": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
     "btp_adamw_f32": [_P, _P, _P, _P, _P, _LL, _F, _F, _F, _F, _F, _I, _P, _P],
     "btp_counter_add": [_P, _I, _P],

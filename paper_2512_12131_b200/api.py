@@ -432,8 +432,13 @@ class BlockTrainer:
             for e, c in zip(execs, saved_cc):
                 e.concurrent_wgrad = c
 
+    def _attns(self):
+        return [e.attn for e in [self.ex] + list(getattr(self.ex, "blocks", [])) if getattr(e, "attn", None) is not None]
+
     def _time_gemms(self, x: torch.Tensor, g: torch.Tensor) -> dict:
         self.ex.gemm_timer = []
+        for a in self._attns():
+            a.timer = None
         self._eager(x, g)  # allocate every buffer outside the capture
         torch.cuda.synchronize()
         if self.ex.comm.live and not self.use_graph:  # collectives eager; timings then include host gaps
@@ -449,17 +454,24 @@ class BlockTrainer:
         try:
             with torch.cuda.stream(side):
                 self.ex.gemm_timer = []
+                attn_rec: list = []
+                for a in self._attns():
+                    a.timer = attn_rec
                 with torch.cuda.graph(graph, stream=side):
                     self._eager(x, g)
         finally:
             self.ex.stats.kernel_launches = saved
             del self.ex.comm.trace.records[n_rec:]
+            for a in self._attns():
+                a.timer = None
         torch.cuda.current_stream().wait_stream(side)
         for _ in range(2):
             graph.replay()
         torch.cuda.synchronize()
         rec, self.ex.gemm_timer = self.ex.gemm_timer, None
-        return self._gemm_summary(rec)
+        out = self._gemm_summary(rec)
+        out["attention_ms"] = {k: sum(a.elapsed_time(b) for a, b, kind in attn_rec if kind == k) for k in ("fwd", "bwd")}
+        return out
 
     @staticmethod
     def _gemm_summary(rec) -> dict:

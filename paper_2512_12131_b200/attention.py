@@ -24,7 +24,28 @@ _BACKENDS = {
 }
 
 
+class _Timed:
+    """CUDA events around one SDPA call when the owner's timer list is armed (bench breakdown;
+    external events become record nodes inside a graph capture)."""
+
+    def __init__(self, timer, kind):
+        self.timer, self.kind = timer, kind
+
+    def __enter__(self):
+        if self.timer is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True, external=True)
+            self.e0.record()
+
+    def __exit__(self, *exc):
+        if self.timer is not None:
+            e1 = torch.cuda.Event(enable_timing=True, external=True)
+            e1.record()
+            self.timer.append((self.e0, e1, self.kind))
+
+
 class Attention:
+    timer: list | None = None  # bench instrumentation: (start_event, end_event, "fwd"|"bwd")
+
     def __init__(self, b: int, s: int, heads: int, head_dim: int, backend: str = "auto"):
         self.b, self.s, self.h, self.hd = b, s, heads, head_dim
         self.scale = 1.0 / head_dim**0.5
@@ -42,13 +63,14 @@ class Attention:
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, need_grad: bool = True):
         q4, k4, v4 = (self._view4(t).detach().requires_grad_(need_grad) for t in (q, k, v))
-        with torch.enable_grad() if need_grad else torch.no_grad(), sdpa_kernel(self.backends, set_priority=True):
+        with torch.enable_grad() if need_grad else torch.no_grad(), sdpa_kernel(self.backends, set_priority=True), \
+                _Timed(self.timer, "fwd"):
             out = F.scaled_dot_product_attention(q4, k4, v4, scale=self.scale)
         return self._as2d(out.detach()), (q4, k4, v4, out)
 
     def backward(self, dout: torch.Tensor, ctx):
         q4, k4, v4, out = ctx
         do4 = self._view4(dout)
-        with sdpa_kernel(self.backends, set_priority=True):
+        with sdpa_kernel(self.backends, set_priority=True), _Timed(self.timer, "bwd"):
             dq, dk, dv = torch.autograd.grad(out, (q4, k4, v4), do4)
         return self._as2d(dq), self._as2d(dk), self._as2d(dv)

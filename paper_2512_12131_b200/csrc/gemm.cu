@@ -65,6 +65,9 @@ struct alignas(64) DevProblem {
   float alpha;
   int sig_half;     // kEpiSigma: r/2; an N tile = BN/2 "u" columns + the BN/2 "v" columns r/2 later
   int scatter_col0; // scatter mode: this problem's first column in the owners' buffers
+  char* c_ptr;      // st.global epilogue stores: outputs and row strides (elements)
+  char* c2_ptr;
+  long long ldc, ldc2;
 };
 
 constexpr int kMaxOwners = 8;
@@ -82,6 +85,10 @@ struct DevParams {
   // (per-row register red.add was 3.6x slower: one row per lane is uncoalesced).
   int scatter_n;
   int scatter_rows;
+  // 1: plain stores leave the epilogue as coalesced st.global (4 rows x 128 B per warp instruction)
+  // from the swizzled staging chunk instead of TMA bulk-tensor stores — the TMA unit then only moves
+  // operands (and the residual), which is what bounds the K = 512 GEMMs (TMA bytes per tile).
+  int st_global;
   CUtensorMap scatter[kMaxOwners];
 };
 
@@ -89,6 +96,11 @@ struct DevParams {
 // which trades mainloop stages for epilogue staging). kSlots == 4 is the residual layout: four
 // single-slot chunk buffers per warp, so a tile's whole residual (<= 4 x 64 columns) is TMA-loaded
 // in one go and each chunk is added and stored in place.
+// kSlots == 5 is the pipelined residual layout (kResPipe, CTA pairs): per epilogue warp four
+// residual chunk slots owned by a dedicated residual-producer warp (warp 3) plus two output
+// staging buffers. The producer refills a slot with the NEXT tile's residual chunk as soon as the
+// epilogue has read it into registers, so a tile's residual is in flight for a whole tile period
+// instead of being issued when the tile's epilogue starts (the kSlots == 4 layout's exposed latency).
 // kPair: CTA-pair mode (cluster of 2, tcgen05.mma.cta_group::2): a 256 x BN tile per pair,
 // each CTA holding 128 rows of A and BN/2 rows of B per stage and its own 128 x BN accumulator.
 // Halving the per-CTA B tile buys a deeper smem pipeline (up to 8 stages).
@@ -100,9 +112,11 @@ struct Cfg {
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = (2 * BN <= 256) ? 256 : 512;  // double-buffered accumulator (pow2 alloc)
-  static constexpr int kEpiWarpBytes = (kSlots == 4 ? 4 : 2 * kSlots) * kEpiStageBytes;  // chunk buffers
+  static constexpr bool kResPipe = kSlots == 5;
+  static constexpr int kEpiWarpBytes =
+      (kResPipe ? 6 : (kSlots == 4 ? 4 : 2 * kSlots)) * kEpiStageBytes;  // chunk buffers
   static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
-  static constexpr int kBarrierBytes = 512;
+  static constexpr int kBarrierBytes = kResPipe ? 1024 : 512;
   static constexpr int kAvail = 232448 - 1024 - kEpiBytes - kBarrierBytes;
   static constexpr int kStages = (kAvail / kStageBytes) > 8 ? 8 : (kAvail / kStageBytes);
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + kBarrierBytes;
@@ -142,7 +156,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar_all = tempty_bar + 2;  // 4 epilogue warps x (2, or 4 when kSlots == 4) buffers
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar_all + 16);
+  // kResPipe: residual slot (warp q, chunk c) -> full / empty barriers at index q * 4 + c
+  uint64_t* res_full = aux_bar_all + 16;
+  uint64_t* res_empty = res_full + (C::kResPipe ? 16 : 0);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_empty + (C::kResPipe ? 16 : 0));
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -169,21 +186,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       mbar_init(&tempty_bar[b], kPair ? 8 : 4);
     }
     for (int b = 0; b < 16; ++b) mbar_init(&aux_bar_all[b], 1);
+    if constexpr (C::kResPipe) {
+      for (int b = 0; b < 16; ++b) {
+        mbar_init(&res_full[b], 1);
+        mbar_init(&res_empty[b], 1);  // the owning epilogue warp's lane 0
+      }
+    }
     fence_barrier_init();
   }
-  // CTA pair: each CTA's allocating warp names its OWN result word (slot[rank]) — the pair
-  // allocation may report the address into both CTAs' shared memory, and two writers of one word
-  // (same value) were racecheck hazards; with distinct words every word has one writer.
-  uint32_t* my_slot = tmem_slot + (kPair ? cluster_ctarank() : 0u);
   if (warp == 2) {
-    if constexpr (kPair) tmem_alloc_pair<C::kTmemCols>(my_slot);
-    else tmem_alloc<C::kTmemCols>(my_slot);
+    if constexpr (kPair) tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
   tc_fence_before();
   if constexpr (kPair) cluster_sync_all();  // peer barriers must exist before any remote arrive
   else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *my_slot;
+  const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -282,6 +301,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       __syncwarp();
     }
+  } else if (C::kResPipe && warp == 3) {
+    // ------------------------------------------------------------ residual producer (kResPipe)
+    // Walks the same tile sequence as the epilogue; slot (q, c) of the next residual tile is
+    // refilled as soon as epilogue warp q has read chunk c of the previous one.
+    if (elect_one()) {
+      uint32_t ph = 0u;  // bit s: parity flips per use of slot s
+      for (int tile = unit; tile < P.total_tiles; tile += n_units) {
+        const TileCoord tc = decode_tile(P, tile);
+        const DevProblem& pr = P.prob[tc.p];
+        if (pr.resid == nullptr) continue;
+        const int m0 = tc.m_blk * C::kTileM + (int)rank * kBM, n0 = tc.n_blk * BN;
+        const int n_valid = min(BN, pr.N - n0);
+        for (int c = 0; c < 4 && c * 64 < n_valid; ++c) {
+#pragma unroll 1
+          for (int qq = 0; qq < 4; ++qq) {
+            const int sl = qq * 4 + c;
+            mbar_wait(&res_empty[sl], ((ph >> sl) & 1u) ^ 1u);
+            ph ^= 1u << sl;
+            mbar_arrive_expect_tx(&res_full[sl], kEpiStageBytes);
+            tma_load_2d(sEpi + qq * C::kEpiWarpBytes + c * kEpiStageBytes, &pr.tma_r, &res_full[sl], n0 + c * 64,
+                        m0 + qq * 32);
+          }
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter == rows [32q, 32q+32) of the tile
@@ -293,6 +337,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     uint32_t aux_phase = 0u;  // bit b: parity of the next wait on aux_bar[b]
     // staging slot s of buffer b (each slot = one 32-row x 128 B chunk)
     auto slot_ptr = [&](int b, int s) { return stage_ptr0 + (b * kSlots + s) * kEpiStageBytes; };
+    // coalesced store of one staged 32-row x 128 B chunk (128B-swizzled) at (row0, col0) of an
+    // output with row stride ld elements of esz bytes; rows >= M and columns >= N are skipped (N % 8
+    // == 0, so a 16-byte segment never straddles N). The warp reads the staging synchronously, so
+    // the buffer is free again after the following __syncwarp.
+    auto store_chunk = [&](const uint8_t* sbuf, char* base, long long ld, int esz, int M, int N, int row0, int col0) {
+      const uint32_t sa = smem_u32(sbuf);
+      const int seg = (int)(lane & 7);
+      const int cpos = col0 + seg * (16 / esz);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = j * 4 + (int)(lane >> 3);
+        const uint4 v = ld_shared_v4(sa + i * 128 + ((seg ^ (i & 7)) << 4));
+        const int row = row0 + i;
+        if (row < M && cpos < N) st_global_v4(base + ((long long)row * ld + cpos) * esz, v);
+      }
+      __syncwarp();
+    };
     // lane 0: TMA-load the aux chunk(s) for output column `col` into buffer b
     auto issue_aux = [&](const DevProblem& pr, int b, int col, int row0) {
       const int naux = pr.epi == kEpiSwigluBwd ? 2 : 1;
@@ -326,7 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       // aux tiles (residual, or g/u for swiglu-bwd) ride the staging buffers (bf16 out only)
       const bool aux = pr.resid != nullptr;
       const bool swb = pr.epi == kEpiSwigluBwd;
-      if constexpr (kSlots == 4) {
+      if constexpr (C::kResPipe) {
+        // residual chunks arrive through the producer warp's slots
+      } else if constexpr (kSlots == 4) {
         // the tile's whole residual in flight at once (one latency per tile, not per chunk), as
         // soon as the previous tile's stores have read the buffers
         if (lane == 0) {
@@ -349,7 +412,69 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const bool row_ok = row < pr.M;
       float rscale = pr.alpha;
       if (pr.row_scale != nullptr && row_ok) rscale *= pr.row_scale[row];
-      if constexpr (kSlots == 4) {
+      if constexpr (C::kResPipe) {
+        // bf16 output, 64-column chunks c = 0..3: TMEM -> registers (+ residual slot c, released to
+        // the producer right after the read) -> output staging buffer (double-buffered) -> TMA store
+#pragma unroll 1
+        for (int c = 0; c * 64 < n_valid; ++c, ++chunk_seq) {
+          const int c0 = c * 64;
+          float v[64];
+          {
+            uint32_t r[64];
+            tmem_ld_32x32b_x64(tmem_base + ((q * 32u) << 16) + buf * BN + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(r[j]) * rscale;
+          }
+          if (c0 + 64 >= n_valid) release_tmem(buf);
+          const int col = n0 + c0;
+          if (pr.col_scale != nullptr) {
+            const int lim = min(64, n_valid - c0);
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < lim) v[j] *= __ldg(pr.col_scale + col + j);
+          }
+          if (aux) {
+            const int sl = (int)q * 4 + c;
+            mbar_wait(&res_full[sl], (res_phase >> c) & 1u);
+            res_phase ^= 1u << c;
+            const uint32_t raddr = smem_u32(stage_ptr0 + c * kEpiStageBytes) + lane * 128;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const uint4 rv = ld_shared_v4(raddr + ((g ^ row_sw) << 4));
+              const uint32_t w[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                v[g * 8 + 2 * h] += bf16_lo(w[h]);
+                v[g * 8 + 2 * h + 1] += bf16_hi(w[h]);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&res_empty[sl]);  // every lane has its residual in registers
+          }
+          uint8_t* ob = stage_ptr0 + (4 + (chunk_seq & 1)) * kEpiStageBytes;
+          const uint32_t row_addr = smem_u32(ob) + lane * 128;
+          if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read this buffer
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(row_addr + ((j ^ row_sw) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
+                         pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          if (P.st_global) {
+            __syncwarp();
+            store_chunk(ob, pr.c_ptr, pr.ldc, 2, pr.M, pr.N, out_row0, col);
+            continue;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&pr.tma_c, ob, col, out_row0);
+            bulk_commit();
+          }
+        }
+        continue;
+      } else if constexpr (kSlots == 4) {
         // bf16 output, 64-column chunks c = 0..3: residual (if any) landed in buffer c; the sum is
         // written back in place and TMA-stored from there
 #pragma unroll 1
@@ -394,6 +519,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             st_shared_v4(row_addr + ((j ^ row_sw) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
                          pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
                          pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          if (P.st_global) {
+            __syncwarp();
+            store_chunk(cb, pr.c_ptr, pr.ldc, 2, pr.M, pr.N, out_row0, col);
+            continue;
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -444,12 +574,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             st_shared_v4(rz0 + ((g ^ row_sw) << 4), zu[4 * g], zu[4 * g + 1], zu[4 * g + 2], zu[4 * g + 3]);
             st_shared_v4(rz1 + ((g ^ row_sw) << 4), zv[4 * g], zv[4 * g + 1], zv[4 * g + 2], zv[4 * g + 3]);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&pr.tma_c, sz0, u0 + c0, out_row0);
-            tma_store_2d(&pr.tma_c, sz1, v0 + c0, out_row0);
-            bulk_commit();
+          if (P.st_global) {
+            __syncwarp();
+            store_chunk(sz0, pr.c_ptr, pr.ldc, 2, pr.M, pr.N, out_row0, u0 + c0);
+            store_chunk(sz1, pr.c_ptr, pr.ldc, 2, pr.M, pr.N, out_row0, v0 + c0);
+          } else {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&pr.tma_c, sz0, u0 + c0, out_row0);
+              tma_store_2d(&pr.tma_c, sz1, v0 + c0, out_row0);
+              bulk_commit();
+            }
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -465,12 +601,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             st_shared_v4(ra0 + ((g ^ row_sw) << 4), zu[4 * g], zu[4 * g + 1], zu[4 * g + 2], zu[4 * g + 3]);
             st_shared_v4(ra1 + ((g ^ row_sw) << 4), zv[4 * g], zv[4 * g + 1], zv[4 * g + 2], zv[4 * g + 3]);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&pr.tma_c2, sa0, u0 + c0, out_row0);
-            tma_store_2d(&pr.tma_c2, sa1, v0 + c0, out_row0);
-            bulk_commit();
+          if (P.st_global) {
+            __syncwarp();
+            store_chunk(sa0, pr.c2_ptr, pr.ldc2, 2, pr.M, pr.N, out_row0, u0 + c0);
+            store_chunk(sa1, pr.c2_ptr, pr.ldc2, 2, pr.M, pr.N, out_row0, v0 + c0);
+          } else {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&pr.tma_c2, sa0, u0 + c0, out_row0);
+              tma_store_2d(&pr.tma_c2, sa1, v0 + c0, out_row0);
+              bulk_commit();
+            }
           }
         }
         continue;
@@ -544,6 +686,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             st_shared_v4(row_addr + off, dgw[0], dgw[1], dgw[2], dgw[3]);
             st_shared_v4(row_addr2 + off, duw[0], duw[1], duw[2], duw[3]);
           }
+          if (P.st_global) {
+            __syncwarp();
+            store_chunk(slot_ptr(b, 0), pr.c_ptr, pr.ldc, 2, pr.M, pr.N, out_row0, col);
+            store_chunk(slot_ptr(b, 1), pr.c2_ptr, pr.ldc2, 2, pr.M, pr.N, out_row0, col);
+            continue;
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -577,6 +725,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             st_shared_v4(row_addr + ((j ^ row_sw) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
                          pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
                          pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+        }
+        if (P.st_global && P.scatter_n == 0 && !pr.reduce_add) {
+          __syncwarp();
+          store_chunk(slot_ptr(b, 0), pr.c_ptr, pr.ldc, pr.out_fp32 ? 4 : 2, pr.M, pr.N, out_row0, col);
+          continue;
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -706,14 +859,29 @@ static int pick_bn(const btp_gemm_problem* probs, int n, int units, int tile_m, 
 // CTA-pair (cta_group::2) tiles: 0 never, 1 plain / sigma epilogues, 2 also residual epilogues
 // (default: with the whole-tile residual staging the pair tiles win there too)
 static int g_pair_mode = 2;
-// residual epilogues with whole-tile residual staging (kSlots == 4); 0 = per-chunk prefetch (A/B)
-static int g_res4 = 1;
+// residual epilogues: 3 (default) = by width: narrow outputs (every residual problem N <= 1024,
+// e.g. the TP >= 2 o / down up-projections) take the producer-warp pipeline with st.global stores,
+// wide ones the whole-tile staging (measured on B200, tests/gpu_gemm_resid_ab.py: [16384 x 512,
+// K = 1024] 24.6 -> 19.2 us; [16384 x 2048, K = 512] 37.8 us tile vs 39.4 us pipeline);
+// 2 = always the pipeline (kSlots == 5, CTA pairs; single-CTA launches fall back to 1),
+// 1 = whole-tile residual staging (kSlots == 4), 0 = per-chunk prefetch (A/B)
+static int g_res4 = 3;
+// epilogue stores: 0 (default) = TMA bulk-tensor stores, 1 = coalesced st.global from the staging
+// chunk for every launch (measured slower for plain epilogues: [16384 x 2048, K = 512] 29.4 ->
+// 33.3 us); mode 3 above turns st.global on for the narrow residual launches only
+static int g_st_global = 0;
 
 }  // namespace btp
 
 extern "C" int btp_gemm_set_res4(int enable) {
   const int prev = btp::g_res4;
-  btp::g_res4 = enable ? 1 : 0;
+  btp::g_res4 = enable < 0 ? 0 : (enable > 3 ? 3 : enable);
+  return prev;
+}
+
+extern "C" int btp_gemm_set_st_global(int enable) {
+  const int prev = btp::g_st_global;
+  btp::g_st_global = enable ? 1 : 0;
   return prev;
 }
 
@@ -819,6 +987,10 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
     }
     d.row_scale = q.row_scale;
     d.col_scale = q.col_scale;
+    d.c_ptr = reinterpret_cast<char*>(q.c);
+    d.ldc = q.ldc;
+    d.c2_ptr = reinterpret_cast<char*>(q.c2);
+    d.ldc2 = q.ldc2;
     d.resid = reinterpret_cast<const __nv_bfloat16*>(q.resid);
     d.ld_resid = q.ld_resid;
     d.M = q.M; d.N = q.N; d.K = q.K;
@@ -837,6 +1009,10 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
   }
   P.num_problems = n;
   P.total_tiles = tiles;
+  P.st_global = g_st_global;
+  int max_resid_n = 0;
+  for (int i = 0; i < n; ++i)
+    if (probs[i].resid) max_resid_n = probs[i].N > max_resid_n ? probs[i].N : max_resid_n;
   if (sc != nullptr) {
     P.scatter_n = sc->n_owners;
     P.scatter_rows = sc->rows_per_owner;
@@ -852,6 +1028,11 @@ int gemm_launch_scatter(const btp_gemm_problem* probs, int n, int bn_hint, int m
   for (int i = 0; i < n; ++i) res4 = res4 && !probs[i].c_fp32 && !probs[i].reduce_add && probs[i].splits == 1;
   if (pair) {
     const int grid = 2 * grid_units;
+    const bool narrow = btp::g_res4 == 3 && max_resid_n <= 1024;
+    if (res4 && (btp::g_res4 == 2 || narrow)) {
+      if (narrow) P.st_global = 1;
+      return BN == 256 ? launch<256, 5, true>(P, grid, stream) : launch<128, 5, true>(P, grid, stream);
+    }
     if (res4) return BN == 256 ? launch<256, 4, true>(P, grid, stream) : launch<128, 4, true>(P, grid, stream);
     if (slots == 2) return BN == 256 ? launch<256, 2, true>(P, grid, stream) : launch<128, 2, true>(P, grid, stream);
     if (BN == 256) return launch<256, 1, true>(P, grid, stream);

@@ -167,9 +167,17 @@ def set_pair_mode(mode: int) -> int:
     return int(_native.load().btp_gemm_set_pair(int(mode)))
 
 
-def set_res4(enable: bool) -> int:
-    """Residual GEMM epilogues stage the whole tile's residual (default on); returns the previous."""
-    return int(_native.load().btp_gemm_set_res4(int(bool(enable))))
+def set_res4(mode) -> int:
+    """Residual GEMM epilogue layout: 3 (default) by width (pipeline + st.global for N <= 1024,
+    whole-tile staging above), 2 pipelined residual slots fed by a producer warp (CTA pairs),
+    1 whole-tile residual staging, 0 per-chunk prefetch; True/False map to 1/0. Returns the
+    previous mode."""
+    return int(_native.load().btp_gemm_set_res4(int(mode)))
+
+
+def set_st_global(enable: bool) -> int:
+    """GEMM epilogue stores via coalesced st.global, or TMA bulk stores (default); returns previous."""
+    return int(_native.load().btp_gemm_set_st_global(int(bool(enable))))
 
 
 def zero(t: torch.Tensor) -> None:

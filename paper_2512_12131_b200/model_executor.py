@@ -90,6 +90,7 @@ class ModelExecutor(ExecutorBase):
             ex.gemm_timer = value
 
     _gemm_timer = None
+    loss_scale = 1.0
 
     # ------------------------------------------------------------------ step pieces
     def forward(self, ids: torch.Tensor) -> torch.Tensor:
@@ -134,7 +135,8 @@ class ModelExecutor(ExecutorBase):
         logits = self.buf("logits", (T, V))
         self._gemm(K.Gemm(hn, self.W["head"], logits))
         rows = self.buf("loss_rows", (T,), F32)
-        K.cross_entropy(logits, targets, rows, dlogits=logits, scale=1.0 / T)
+        # dlogits = (softmax - onehot) * loss_scale / T (loss_scale: 1/m for m pipeline micro-batches)
+        K.cross_entropy(logits, targets, rows, dlogits=logits, scale=self.loss_scale / T)
         out = self.buf("loss", (1,), F32)
         inv_t = self._buf.get("inv_T")
         if inv_t is None:
@@ -146,6 +148,13 @@ class ModelExecutor(ExecutorBase):
     def backward(self, targets: torch.Tensor | None = None) -> torch.Tensor:
         """Backward of the whole model for the loss computed by loss_device. Returns dx of the
         embedding output shard and fills every gradient (blocks: ex.grad; here: self.grad)."""
+        dy_sh = self._blocks_backward(self._head_backward())
+        self._embedding_backward(dy_sh)
+        self._join_side()
+        return dy_sh
+
+    def _head_backward(self) -> torch.Tensor:
+        """LM head + final norm backward: this rank's column slice of dL/dy (no collective)."""
         T, d = self.T, self.d
         dlogits, hn, y = self._buf["logits"], self._buf["hn"], self._y_full
         self.comm.pass_tag = "backward"
@@ -159,18 +168,22 @@ class ModelExecutor(ExecutorBase):
         nb = K.rmsnorm_bwd(dhn, y, self.final_gamma, dss, dy, gparts)
         K.reduce_rows(gparts[:nb].view(nb, 1, d), self.grad["gamma1"].view(1, d))
         self.stats.kernel_launches += 3
-        dy_sh = dy[:, self.rank * self.dl:(self.rank + 1) * self.dl]            # replicated head: local slice
+        return dy[:, self.rank * self.dl:(self.rank + 1) * self.dl]            # replicated head: local slice
+
+    def _blocks_backward(self, dy_sh: torch.Tensor) -> torch.Tensor:
+        self.comm.pass_tag = "backward"
         dh = None
         for ex in reversed(self.blocks):
             if ex.lax:
                 ex.dh_cur_in = dh
             dy_sh = ex.backward(dy_sh)
             dh = ex.dh_prev if ex.lax else None
+        return dy_sh
+
+    def _embedding_backward(self, dy_sh: torch.Tensor) -> None:
         K.zero(self.grad["embedding"])
         K.embedding_bwd(self._ids, dy_sh, self.grad["embedding"])
         self.stats.kernel_launches += 2
-        self._join_side()
-        return dy_sh
 
     def optimizer_step(self, **hp) -> None:
         for ex in self.blocks:

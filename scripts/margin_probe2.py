@@ -71,14 +71,14 @@ def rank_main(mode, *args):
     T._rank_main(*args)
 
 
-def run(mode, world, b, s):
+def run(mode, world, b, s, cfg_name="C60M"):
     import torch.multiprocessing as mp
     from tests import test_gpu_tp2 as T
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = T._port()
-    procs = [ctx.Process(target=rank_main, args=(mode, r, world, port, "btp", True, True, False, q, "C60M", (b, s)))
+    procs = [ctx.Process(target=rank_main, args=(mode, r, world, port, "btp", True, True, False, q, cfg_name, (b, s)))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -93,20 +93,30 @@ def run(mode, world, b, s):
 
 
 def main():
+    import argparse
+
     from oracle import btp_oracle as O
-    from tests.gpu_util import C60M, inputs, oracle_step, rel
+    from tests import gpu_util
+    from tests.gpu_util import inputs, oracle_step, rel
     from paper_2512_12131_b200.model import Variant
 
-    b, s = 2, 128
-    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
-    y_ref, g_ref, _, _ = oracle_step(oblk, x, G, C60M, b, s, sharded=False)
-    for world in (1, 8):
-        for mode in (("none",) if world == 1 else ("none", "fwd", "bwd", "both")):
-            res = run(mode, world, b, s)
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="C60M")
+    ap.add_argument("--bs", default="2,128")
+    ap.add_argument("--worlds", default="1,8")
+    ap.add_argument("--modes", default="none,fwd,bwd,both")
+    a = ap.parse_args()
+    cfg = getattr(gpu_util, a.cfg)
+    b, s = (int(v) for v in a.bs.split(","))
+    blk, x, G, oblk = inputs(cfg, Variant.COLA, b, s)
+    y_ref, g_ref, _, _ = oracle_step(oblk, x, G, cfg, b, s, sharded=False)
+    for world in (int(w) for w in a.worlds.split(",")):
+        for mode in (("none",) if world == 1 else a.modes.split(",")):
+            res = run(mode, world, b, s, a.cfg)
             worst = {}
             for rank, (_, y, loss, dx, grads, *_r) in res.items():
-                gr = O.grads_for_rank(g_ref, world, rank, C60M.d, C60M.d_ff)
-                errs = {"y": rel(y.reshape(-1, C60M.d), y_ref), "dx": rel(dx, gr["dx"]),
+                gr = O.grads_for_rank(g_ref, world, rank, cfg.d, cfg.d_ff)
+                errs = {"y": rel(y.reshape(-1, cfg.d), y_ref), "dx": rel(dx, gr["dx"]),
                         "g1": rel(grads["gamma1"], gr["dgamma1"]), "g2": rel(grads["gamma2"], gr["dgamma2"])}
                 for n in O.PROJECTIONS:
                     errs["A_" + n] = rel(grads["A"][n], gr["A"][n])
@@ -114,7 +124,8 @@ def main():
                 for k, v in errs.items():
                     worst[k] = max(worst.get(k, 0), v)
             top = sorted(worst.items(), key=lambda kv: -kv[1])[:5]
-            print(f"world={world} mode={mode}: " + ", ".join(f"{k}={v:.3e}" for k, v in top), flush=True)
+            print(f"{a.cfg} b{b} s{s} world={world} mode={mode}: " + ", ".join(f"{k}={v:.3e}" for k, v in top),
+                  flush=True)
 
 
 if __name__ == "__main__":

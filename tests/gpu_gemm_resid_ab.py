@@ -1,5 +1,7 @@
-"""A/B of the residual-epilogue GEMM against the plain one at the TP=8 / TP=1 up-projection
-shapes (not a pytest module):  python tests/gpu_gemm_resid_ab.py"""
+"""A/B of the residual-epilogue GEMM layouts against the plain epilogue at the TP=8 / TP=1
+up-projection shapes (not a pytest module):  python tests/gpu_gemm_resid_ab.py
+Residual modes (btp_gemm_set_res4): 0 per-chunk prefetch, 1 whole-tile staging, 2 pipelined
+residual slots fed by a producer warp (pair tiles)."""
 import sys
 
 sys.path.insert(0, ".")
@@ -21,20 +23,25 @@ def t(fn, reps=30):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-for M, N, Kd in [(16384, 512, 1024), (16384, 2048, 512), (16384, 1024, 512)]:
+for M, N, Kd in [(16384, 512, 1024), (16384, 2048, 512), (16384, 1024, 512), (16384, 4096, 1024)]:
     a = torch.randn(M, Kd, device="cuda").bfloat16()
     w = torch.randn(N, Kd, device="cuda").bfloat16()
     r = torch.randn(M, N, device="cuda").bfloat16()
     o = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ref = (a.float() @ w.float().t() + r.float())
     fl = 2 * M * N * Kd
-    for pair in (1, 2):
-        K.set_pair_mode(pair)
-        for bn in (0, 256):
-            tp = t(lambda: K.gemm(K.Gemm(a, w, o), bn=bn))
-            K.set_res4(False)
-            tr0 = t(lambda: K.gemm(K.Gemm(a, w, o, resid=r), bn=bn))
-            K.set_res4(True)
-            tr = t(lambda: K.gemm(K.Gemm(a, w, o, resid=r), bn=bn))
-            print(f"[{M}x{N} K={Kd}] pair={pair} bn={bn or 'auto'}: plain {tp:6.1f} us ({fl / tp / 1e6:5.0f} TF/s)"
-                  f"  resid/chunk {tr0:6.1f} us  resid/tile {tr:6.1f} us ({fl / tr / 1e6:5.0f} TF/s)")
-    K.set_pair_mode(1)
+    K.set_pair_mode(2)
+    for st in (0, 1):
+        K.set_st_global(st)
+        tp = t(lambda: K.gemm(K.Gemm(a, w, o)))
+        res = {}
+        for mode in (0, 1, 2, 3):
+            K.set_res4(mode)
+            res[mode] = t(lambda: K.gemm(K.Gemm(a, w, o, resid=r)))
+            err = float((o.float() - ref).norm() / ref.norm())
+            assert err < 1e-2, (mode, err)
+        K.set_res4(3)
+        print(f"[{M}x{N} K={Kd}] st_global={st} plain {tp:6.1f} us ({fl / tp / 1e6:5.0f} TF/s) | resid chunk "
+              f"{res[0]:6.1f}  tile {res[1]:6.1f}  pipe {res[2]:6.1f}  auto {res[3]:6.1f} us "
+              f"({fl / res[3] / 1e6:5.0f} TF/s)", flush=True)
+    K.set_st_global(0)

@@ -77,6 +77,26 @@ def _main(port, q):
             xh, gh = tr.pinned_host_inputs(x.values, G.values)
             losses = tr.fit([xh, xh, xh, xh], gh)
             runs[graphs] = (tr.graphed, losses)
+        # a backend that refuses the capture: the trainer warns once and keeps running eagerly
+        import warnings
+
+        orig_graph = torch.cuda.graph
+
+        def _refuse(*a, **k):
+            raise RuntimeError("capture refused (test)")
+
+        torch.cuda.graph = _refuse
+        try:
+            with warnings.catch_warnings(record=True) as caught:
+                warnings.simplefilter("always")
+                tr = BlockTrainer(pl, blk, comm=TPComm(1, 0, trace=Trace(), force=True), adamw=dict(lr=1e-3),
+                                  graph_collectives=True)
+                xh, gh = tr.pinned_host_inputs(x.values, G.values)
+                losses = tr.fit([xh, xh, xh, xh], gh)
+        finally:
+            torch.cuda.graph = orig_graph
+        runs["refused"] = (tr.graphed, tr.use_graph, losses,
+                           sum("capture" in str(w.message) for w in caught))
         gathered = tr.ex.comm.all_gather_cols(torch.ones(4, 8, device="cuda"), "final-gather")
         out["trainer"] = (runs, tuple(gathered.shape))
         dist.destroy_process_group()
@@ -111,4 +131,7 @@ def test_nccl_one_rank_step_is_bit_identical():
     # replay == eager up to the split-K fp32 reduce order, which AdamW can amplify where a gradient
     # element is ~0 (its normalised update flips sign): a loose relative bar
     np.testing.assert_allclose(losses, eager_losses, rtol=5e-3)
+    r_graphed, r_use_graph, r_losses, n_warn = runs["refused"]
+    assert not r_graphed and not r_use_graph and n_warn == 1  # fell back to eager launches, warned once
+    np.testing.assert_allclose(r_losses, eager_losses, rtol=5e-3)
     assert gshape == (4, 8)
