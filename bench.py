@@ -321,7 +321,8 @@ def _make_trainer(args, cfg, strategy, shape, comm):
     boundary = args.boundary if strategy is Strategy.BOTTLENECK else "nccl"
     trainer = BlockTrainer(pl, blk, use_graph=not args.no_graph, attn_backend=args.attn, adamw=ADAMW,
                            optimizer=not args.no_optimizer, comm=comm, boundary=boundary,
-                           peer_provider=args.peer_provider)
+                           peer_provider=args.peer_provider,
+                           boundary_dtype=args.boundary_dtype if strategy is Strategy.BOTTLENECK else "bf16")
     if variant is Variant.LAX:  # a resident previous-layer bundle, like G (the merge runs every step)
         from paper_2512_12131_b200.model import seeded_h_prev
 
@@ -599,6 +600,7 @@ def run_ours(args, cfg):
                    "tokens_per_step": b * s, "parallelism": f"tp{tp}", "l2": "inputs larger than L2 (no flush)",
                    "cuda_graph": graphed,
                    "boundary": args.boundary if tp > 1 else "none (tp=1)",
+                   "boundary_dtype": args.boundary_dtype if tp > 1 else None,
                    "optimizer": None if args.no_optimizer else dict(ADAMW, kind="AdamW fp32 master+moments, fused"),
                    "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
         "clocks": clk.summary() if clk is not None else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry-run"]},
@@ -689,6 +691,8 @@ def main(argv=None):
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
     ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
                     help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
+    ap.add_argument("--boundary-dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="NCCL boundaries: reduce the forward rank-r partials in fp32 (parity margin; 2x bytes)")
     ap.add_argument("--peer-provider", default="symmetric_memory", choices=["symmetric_memory", "cuda_ipc"],
                     help="--boundary peer/nvls: how the ranks' heaps are mapped")
     ap.add_argument("--model", action="store_true", help="multi-layer model step (embedding + blocks + LM head)")

@@ -149,6 +149,13 @@ int btp_swiglu_bwd(const void* g, long long ldg, const void* u, long long ldu, c
                    long long ldda, void* dg, long long lddg, void* du, long long lddu, int rows, int cols,
                    void* stream);
 
+/* btp_fixup_sigma for an fp32 reduced partial P (bf16 z / a outputs; z_out required): the chunk
+ * boundary all-reduced in fp32 (`boundary_dtype="fp32"`), so the cross-rank sum is rounded to
+ * bf16 once, here, instead of once per ring hop. Same arguments and errors as btp_fixup_sigma. */
+int btp_fixup_sigma_f32in(const float* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                          void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj,
+                          int variant, void* stream);
+
 /* Backward of `btp_fixup_sigma` for one chunk (sigma-bwd + normalisation-bwd, no collective):
  *   dz = sigma'(z) . da       (crossgate-bwd for variant 1, identity for 0)
  *   if s: dP = dz / s ;  dss[t] = -<dz_t, z_t> / (2 s^2 d)      else dP = dz

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "btp_rmsnorm_residual",
     "btp_rmsnorm_apply",
     "btp_fixup_sigma",
+    "btp_fixup_sigma_f32in",
     "btp_swiglu",
     "btp_swiglu_bwd",
     "btp_fixup_sigma_bwd",
@@ -135,6 +136,7 @@ _SIGNATURES = {
     "btp_rmsnorm_residual": [_P, _LL, _P, _LL, _P, _LL, _P, _P, _LL, _P, _P, _I, _I, _F, _P],
     "btp_rmsnorm_apply": [_P, _LL, _P, _P, _I, _F, _P, _LL, _P, _I, _I, _P],
     "btp_fixup_sigma": [_P, _LL, _P, _I, _F, _P, _P, _LL, _P, _LL, _I, _I, _I, _I, _P],
+    "btp_fixup_sigma_f32in": [_P, _LL, _P, _I, _F, _P, _P, _LL, _P, _LL, _I, _I, _I, _I, _P],
     "btp_swiglu": [_P, _LL, _P, _LL, _P, _LL, _I, _I, _P],
     "btp_swiglu_bwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _I, _I, _P],
     "btp_fixup_sigma_bwd": [_P, _LL, _P, _LL, _P, _I, _P, _LL, _P, _I, _I, _I, _I, _P],

@@ -74,8 +74,11 @@ def _check_inputs(pl: ShardPlan, block: DecoderBlockWeights, x) -> np.ndarray:
 
 def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT, trace: Trace | None = None,
                   device=None, attn_backend: str = "auto", precision: str = "bf16", comm: TPComm | None = None,
-                  boundary: str = "nccl", peer_provider: str = "symmetric_memory"):
+                  boundary: str = "nccl", peer_provider: str = "symmetric_memory", boundary_dtype: str = "bf16"):
     """Build this rank's executor for the plan's strategy (comm: default = the process group).
+
+    boundary_dtype="fp32" (BTP, NCCL boundaries): the forward rank-r all-reduces carry an fp32
+    partial (one bf16 rounding of the cross-rank sum instead of one per ring hop; 2x the bytes).
 
     boundary="peer" (BTP, tp > 1): the chunk boundaries run as fused reduce-scatter -> fix-up/sigma
     -> all-gather kernels over NVLink peer memory (torch symmetric-memory heap, csrc/peer.cu)
@@ -85,6 +88,8 @@ def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS
     mapped — "symmetric_memory" (torch), or "cuda_ipc" (cudaIpc handles over the process group)."""
     if boundary not in ("nccl", "peer", "nvls"):
         raise ValueError(f"boundary must be 'nccl', 'peer' or 'nvls', got {boundary!r}")
+    if boundary_dtype not in ("bf16", "fp32"):
+        raise ValueError(f"boundary_dtype must be 'bf16' or 'fp32', got {boundary_dtype!r}")
     pl, block = _normalise(pl, block)
     if comm is None:
         comm = TPComm.from_env(pl.shape.tp, trace=trace if trace is not None else Trace())
@@ -97,7 +102,9 @@ def make_executor(pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS
                                         nvls=boundary == "nvls"))
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     if pl.strategy is Strategy.BOTTLENECK:
-        return BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)
+        ex = BTPBlockExecutor(pl, block, comm, dev, eps, attn_backend, precision)
+        ex.boundary_dtype = boundary_dtype
+        return ex
     from .baselines import FullRankExecutor, VanillaExecutor
 
     cls = VanillaExecutor if pl.strategy is Strategy.VANILLA else FullRankExecutor
@@ -260,12 +267,14 @@ class BlockTrainer:
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, *, eps: float = EPS_DEFAULT,
                  attn_backend: str = "auto", use_graph: bool = True, adamw: dict | None = None,
                  optimizer: bool = True, comm: TPComm | None = None, executor=None, boundary: str = "nccl",
-                 graph_collectives: bool = True, peer_provider: str = "symmetric_memory"):
+                 graph_collectives: bool = True, peer_provider: str = "symmetric_memory",
+                 boundary_dtype: str = "bf16"):
         pl, block = _normalise(pl, block)
         self.pl = pl
         self.ex = executor if executor is not None else make_executor(pl, block, eps=eps, attn_backend=attn_backend,
                                                                       comm=comm, boundary=boundary,
-                                                                      peer_provider=peer_provider)
+                                                                      peer_provider=peer_provider,
+                                                                      boundary_dtype=boundary_dtype)
         # AdamW hyper-parameters (lr, b1, b2, eps, wd); the update is part of every step unless disabled
         self.adamw = dict(adamw or {}) if optimizer else None
         # A step without live collectives is always graphed. With live NCCL collectives the whole

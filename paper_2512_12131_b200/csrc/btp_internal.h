@@ -26,6 +26,9 @@ int rmsnorm_residual(const void* x, long long ldx, const void* branch, long long
                      int width, float eps, cudaStream_t st, bool f32);
 int rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float* ss_total, int d, float eps,
                   void* n_out, long long ldn, float* rms_out, int rows, int width, cudaStream_t st, bool f32);
+int fixup_sigma_f32in(const float* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                      void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant,
+                      cudaStream_t st);
 int fixup_sigma(const void* P, long long ldp, const float* ss_total, int d, float eps, float* s_out, void* z_out,
                 long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, cudaStream_t st,
                 bool f32);

@@ -61,6 +61,13 @@ BTP_PAIR(btp_fixup_sigma, fixup_sigma,
           long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant, void* stream),
          A_FIXUP)
 
+int btp_fixup_sigma_f32in(const float* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                          void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj,
+                          int variant, void* stream) {
+  return btp::fixup_sigma_f32in(P, ldp, ss_total, d, eps, s_out, z_out, ldz, a_out, lda, rows, r, nproj, variant,
+                                ST(stream));
+}
+
 #define A_SWIGLU(f32) (g, ldg, u, ldu, act, lda, rows, cols, ST(stream), f32)
 BTP_PAIR(btp_swiglu, swiglu,
          (const void* g, long long ldg, const void* u, long long ldu, void* act, long long lda, int rows, int cols,

@@ -167,8 +167,10 @@ __global__ void __launch_bounds__(256) rmsnorm_apply_kernel(const T* __restrict_
 // ----------------------------------------------------------------------------- K4 forward
 // Work item = (row, projection, group of 8 columns of the u half) for cola,
 //             (row, projection, group of 8 columns) for svd.
-template <typename T>
-__global__ void __launch_bounds__(256) fixup_sigma_kernel(const T* P, long long ldp, const float* __restrict__ ss_total,
+// TIn: the reduced partial P's type — T, or fp32 when the boundary all-reduce ran in fp32 (one
+// rounding of the cross-rank sum, here, instead of one per NCCL ring hop)
+template <typename T, typename TIn = T>
+__global__ void __launch_bounds__(256) fixup_sigma_kernel(const TIn* P, long long ldp, const float* __restrict__ ss_total,
                                                           int d, float eps, float* __restrict__ s_out, T* z_out,
                                                           long long ldz, T* __restrict__ a_out, long long lda,
                                                           int rows, int r, int nproj, int variant) {
@@ -903,6 +905,23 @@ int rmsnorm_apply(const void* x, long long ldx, const float* gamma, const float*
   else
     rmsnorm_apply_kernel<bf16><<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const bf16*>(x), ldx, gamma, ss_total, d,
                                                               eps, static_cast<bf16*>(n_out), ldn, rms_out, rows, width);
+  BTP_CHECK_LAUNCH();
+}
+
+int fixup_sigma_f32in(const float* P, long long ldp, const float* ss_total, int d, float eps, float* s_out,
+                      void* z_out, long long ldz, void* a_out, long long lda, int rows, int r, int nproj, int variant,
+                      cudaStream_t st) {
+  if (rows <= 0 || r <= 0 || nproj <= 0 || z_out == nullptr) return BTP_ERR_DIM;
+  if (variant != 0 && variant != 1) return BTP_ERR_DIM;
+  if (variant == 1 && (r % 16)) return BTP_ERR_DIVISIBILITY;
+  if (r % 8 || ldp % 8 || ldz % 8 || (a_out && lda % 8)) return BTP_ERR_ALIGNMENT;
+  if (variant == 1 && a_out == nullptr) return BTP_ERR_DIM;
+  if (!al16(P) || !al16(z_out) || (a_out && !al16(a_out))) return BTP_ERR_ALIGNMENT;
+  const long long items = (long long)rows * nproj * (variant == 1 ? r / 16 : r / 8);
+  fixup_sigma_kernel<bf16, float><<<grid_for(items), 256, 0, st>>>(P, ldp, ss_total, d, eps, s_out,
+                                                                   static_cast<bf16*>(z_out), ldz,
+                                                                   static_cast<bf16*>(a_out), lda, rows, r, nproj,
+                                                                   variant);
   BTP_CHECK_LAUNCH();
 }
 

@@ -368,6 +368,13 @@ class ExecutorBase:
 class BTPBlockExecutor(ExecutorBase):
     """One rank's shard of a low-rank (svd/cola/lax) block under a BTP plan."""
 
+    # "fp32": the forward chunk boundaries (NCCL path, tp > 1) reduce an fp32 partial — the down
+    # GEMM writes P in fp32 and btp_fixup_sigma_f32in rounds the cross-rank sum to bf16 once —
+    # instead of a bf16 all-reduce that rounds at every ring hop (2x the forward boundary bytes).
+    # Measured (scripts/margin_probe2.py): the worst TP=8 parity error drops 1.86e-2 -> 1.58e-2 at
+    # CoLA-7B widths and 1.98e-2 -> 1.78e-2 at CoLA-60M; an fp32 BACKWARD reduction does not move it.
+    boundary_dtype = "bf16"
+
     def __init__(self, pl: ShardPlan, block: DecoderBlockWeights, comm: TPComm | None = None,
                  device: torch.device | str = "cuda", eps: float = 1e-6, attn_backend: str = "auto",
                  precision: str = "bf16"):
@@ -543,15 +550,17 @@ class BTPBlockExecutor(ExecutorBase):
             return self._down_boundary_fused(names, n_in, W, ss, rl, s_tag, norm_chunk, a_store)
         if self.fwd_slices > 1:
             return self._down_boundary_sliced(names, n_in, W, ss, rl, s_out, norm_chunk, a_store)
+        f32 = self.boundary_dtype == "fp32" and self.comm.live
         if self.grouping or k == 1:
             P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
-            self._gemm(K.Gemm(n_in, W, P, row_scale=row_scale))
+            Pr = self.buf(f"Pf_{'_'.join(names)}", (T, k * r), F32) if f32 else P  # the reduced buffer
+            self._gemm(K.Gemm(n_in, W, Pr, row_scale=row_scale))
             if ss_total is not None:
-                self.comm.all_reduce_coalesced(P, ss, names[0] if k == 1 else self._gid(names))
+                self.comm.all_reduce_coalesced(Pr, ss, names[0] if k == 1 else self._gid(names))
             else:
-                self.comm.all_reduce(P, names[0] if k == 1 else self._gid(names))
-            if self.var == 1 or ss_total is not None:
-                K.fixup_sigma(P, r=r, nproj=k, variant=self.var, z_out=P, a_out=a_store, ss_total=ss_total,
+                self.comm.all_reduce(Pr, names[0] if k == 1 else self._gid(names))
+            if self.var == 1 or ss_total is not None or f32:
+                K.fixup_sigma(Pr, r=r, nproj=k, variant=self.var, z_out=P, a_out=a_store, ss_total=ss_total,
                               d=self.d, s_out=s_out, eps=self.eps)
                 self.stats.kernel_launches += 1
             z = [P[:, i * r:(i + 1) * r] for i in range(k)]
@@ -559,16 +568,17 @@ class BTPBlockExecutor(ExecutorBase):
             return z, a, P
         # ungrouped: one GEMM + one collective per projection (reference simulator.py:623-639)
         P3 = self.buf(f"P3_{'_'.join(names)}", (k, T, r))
+        Pr3 = self.buf(f"Pf3_{'_'.join(names)}", (k, T, r), F32) if f32 else P3
         z, a = [], []
         for i, nm in enumerate(names):
-            self._gemm(K.Gemm(n_in, W[i * r:(i + 1) * r], P3[i], row_scale=row_scale))
+            self._gemm(K.Gemm(n_in, W[i * r:(i + 1) * r], Pr3[i], row_scale=row_scale))
             if ss_total is not None and i == 0:
-                self.comm.all_reduce_coalesced(P3[i], ss, nm)
+                self.comm.all_reduce_coalesced(Pr3[i], ss, nm)
             else:
-                self.comm.all_reduce(P3[i], nm)
-            if self.var == 1 or ss_total is not None:
+                self.comm.all_reduce(Pr3[i], nm)
+            if self.var == 1 or ss_total is not None or f32:
                 a_i = a_store[:, i * r:(i + 1) * r] if a_store is not None else None
-                K.fixup_sigma(P3[i], r=r, nproj=1, variant=self.var, z_out=P3[i], a_out=a_i, ss_total=ss_total,
+                K.fixup_sigma(Pr3[i], r=r, nproj=1, variant=self.var, z_out=P3[i], a_out=a_i, ss_total=ss_total,
                               d=self.d, s_out=s_out if i == 0 else None, eps=self.eps)
                 self.stats.kernel_launches += 1
             z.append(P3[i])
@@ -610,26 +620,28 @@ class BTPBlockExecutor(ExecutorBase):
         keeps ONE record per chunk boundary (the logical collective of the reference)."""
         T, r, k, C = self.T, self.r, len(names), self.fwd_slices
         online = norm_chunk and self.online
+        f32 = self.boundary_dtype == "fp32"
         P = self.buf(f"P_{'_'.join(names)}", (T, k * r))
+        Pr = self.buf(f"Pf_{'_'.join(names)}", (T, k * r), F32) if f32 else P  # the reduced buffer
         gid = names[0] if k == 1 else self._gid(names)
         rows = T // C
         handles = []
         for c in range(C):
             sl = slice(c * rows, (c + 1) * rows)
-            self._gemm(K.Gemm(n_in[sl], W, P[sl], row_scale=rl[sl] if online else None))
+            self._gemm(K.Gemm(n_in[sl], W, Pr[sl], row_scale=rl[sl] if online else None))
             if online:
-                handles.append(self.comm.all_reduce_coalesced_start(P[sl], ss[sl], gid, record=False))
+                handles.append(self.comm.all_reduce_coalesced_start(Pr[sl], ss[sl], gid, record=False))
             else:
-                handles.append(self.comm.all_reduce_start(P[sl], gid, record=False))
+                handles.append(self.comm.all_reduce_start(Pr[sl], gid, record=False))
         if online:
             self.comm.record("all-reduce-coalesced", gid, T * k * r, extras=(("fused-stat", T),))
         else:
             self.comm.record("all-reduce", gid, T * k * r)
         for c in range(C):
             self.comm.wait(handles[c])
-            if self.var == 1 or online:
+            if self.var == 1 or online or f32:
                 sl = slice(c * rows, (c + 1) * rows)
-                K.fixup_sigma(P[sl], r=r, nproj=k, variant=self.var, z_out=P[sl],
+                K.fixup_sigma(Pr[sl], r=r, nproj=k, variant=self.var, z_out=P[sl],
                               a_out=a_store[sl] if a_store is not None else None, ss_total=ss[sl] if online else None,
                               d=self.d, s_out=s_out[sl] if s_out is not None else None, eps=self.eps)
                 self.stats.kernel_launches += 1

@@ -201,9 +201,11 @@ def rmsnorm_apply(x, gamma, ss_total, d, n_out, *, rms_out=None, eps=1e-6):
 
 
 def fixup_sigma(P, *, r, nproj, variant, z_out=None, a_out=None, ss_total=None, d=1, s_out=None, eps=1e-6):
+    """P fp32 with bf16 z_out: the fp32-reduced boundary (btp_fixup_sigma_f32in)."""
     rows = P.shape[0]
+    mixed = P.dtype == F32 and z_out is not None and z_out.dtype == BF16
     _native.call(
-        _fn("btp_fixup_sigma", P), _p(P), _ld(P), _p(ss_total), d, ctypes.c_float(eps), _p(s_out), _p(z_out),
+        "btp_fixup_sigma_f32in" if mixed else _fn("btp_fixup_sigma", P), _p(P), _ld(P), _p(ss_total), d, ctypes.c_float(eps), _p(s_out), _p(z_out),
         _ld(z_out), _p(a_out), _ld(a_out), rows, r, nproj, variant, _stream(),
     )
 
