@@ -534,21 +534,28 @@ def run_ours(args, cfg):
     if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model:
         t = json.loads(tfile.read_text())
         traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
-    g_ms = gemm["ms"] or float("nan")
+    b2b = gemm.get("back_to_back") or gemm
+    g_ms = b2b["ms"] or float("nan")
+    # achieved = the step's GEMM launches replayed back to back (one graph, two CUDA events): each
+    # kernel's own device time plus the graph's inter-kernel gap; the per-launch event brackets
+    # inside the step graph (event nodes add their own gaps) are reported beside it
     roof = {"bound": "tensor", "kernel": "btp gemm_kernel (all tcgen05 GEMM launches of one step)",
-            "achieved": gemm["tflops"], "peak": peak_sus, "unit": "TFLOP/s", "frac": gemm["tflops"] / peak_sus,
+            "achieved": b2b["tflops"], "peak": peak_sus, "unit": "TFLOP/s", "frac": b2b["tflops"] / peak_sus,
             "traffic": traffic, "traffic_unit": "bytes per launch (dram read+write, ncu)", "traffic_source": traffic_src,
-            "algorithmic_flops_per_launch": gemm["flops"] / max(gemm["launches"], 1),
-            "avg_launch_us": g_ms * 1e3 / max(gemm["launches"], 1),
+            "algorithmic_flops_per_launch": b2b["flops"] / max(b2b["launches"], 1),
+            "avg_launch_us": g_ms * 1e3 / max(b2b["launches"], 1),
+            "timing": "the step's GEMM launches as one back-to-back graph replay, CUDA events around it",
+            "achieved_event_bracketed": gemm["tflops"],
             "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
-            "gemm_share_of_step": g_ms / ms, "gemm_launches_per_step": gemm["launches"],
+            "gemm_share_of_step": g_ms / ms, "gemm_launches_per_step": b2b["launches"],
             "step_frac_of_peak": flops / (ms / 1e3) / 1e12 / peak_sus}
     att = gemm.get("attention_ms", {})
     # where the step goes (device time of one graph-replayed step, kernels serialised): the
     # tcgen05 GEMMs, cuDNN attention (not a changed subsystem), everything else (row kernels, AdamW,
     # collectives, gaps) — a slow run's line says which part moved
-    breakdown = {"gemm_ms": gemm["ms"], "attention_fwd_ms": att.get("fwd"), "attention_bwd_ms": att.get("bwd"),
-                 "other_ms": ms - gemm["ms"] - sum(v for v in att.values() if v)}
+    gms = (gemm.get("back_to_back") or gemm)["ms"]
+    breakdown = {"gemm_ms": gms, "attention_fwd_ms": att.get("fwd"), "attention_bwd_ms": att.get("bwd"),
+                 "other_ms": ms - gms - sum(v for v in att.values() if v)}
     graphed = trainer.graphed
     del trainer, x_dev, g_dev, xh, xh2, gh
     if not args.dry_run:

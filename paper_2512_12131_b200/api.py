@@ -18,6 +18,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import kernels as K
 from .comm import TPComm
 from .executor import BTPBlockExecutor
 from .interop import as_block, as_h_prev, as_plan, element_bytes_of, values_of
@@ -480,7 +481,39 @@ class BlockTrainer:
         rec, self.ex.gemm_timer = self.ex.gemm_timer, None
         out = self._gemm_summary(rec)
         out["attention_ms"] = {k: sum(a.elapsed_time(b) for a, b, kind in attn_rec if kind == k) for k in ("fwd", "bwd")}
+        out["back_to_back"] = self._time_gemm_sequence(x, g)
         return out
+
+    def _time_gemm_sequence(self, x: torch.Tensor, g: torch.Tensor, reps: int = 5) -> dict:
+        """The step's GEMM launches alone, in step order on the step's own buffers, captured into
+        one graph and replayed back to back between two CUDA events: each launch's device time
+        without the per-launch event nodes (which add their own gaps inside a graph). Overwrites
+        activations / gradients of the last step — instrumentation only, after the timed region."""
+        self.ex.gemm_log = []
+        try:
+            self._eager(x, g)
+        finally:
+            log, self.ex.gemm_log = self.ex.gemm_log, None
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                for probs, _ in log:
+                    K.gemm(*probs)
+        torch.cuda.current_stream().wait_stream(side)
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = sum(f for _, f in log)
+        return {"ms": ms, "flops": fl, "tflops": fl / (ms / 1e3) / 1e12 if ms else 0.0, "launches": len(log)}
 
     @staticmethod
     def _gemm_summary(rec) -> dict:

@@ -112,6 +112,7 @@ class ExecutorBase:
 
     residual_sharded = True
     gemm_timer: list | None = None  # bench instrumentation: (start_event, end_event, flops) per launch
+    gemm_log: list | None = None    # bench instrumentation: (problems, flops) of every launch, in order
     fuse_swiglu_bwd = False         # SwiGLU backward in the dgrad GEMM epilogue (False: separate kernel)
 
     def _setup(self, pl: ShardPlan, comm: TPComm | None, device, eps: float, precision: str = "bf16"):
@@ -242,6 +243,8 @@ class ExecutorBase:
             N = p.b.shape[1] if p.b_mn else p.b.shape[0]
             flops += 2 * M * N * Kd
             shapes.append((M, N, Kd, int(p.a_mn), int(p.b_mn), p.splits))
+        if self.gemm_log is not None:
+            self.gemm_log.append((probs, flops))
         if self.gemm_timer is not None:
             # external=True: inside a CUDA-graph capture these become event-record nodes, so the
             # timings are pure device time (no host launch gaps)

@@ -90,6 +90,18 @@ class ModelExecutor(ExecutorBase):
             ex.gemm_timer = value
 
     _gemm_timer = None
+
+    @property
+    def gemm_log(self):
+        return self._gemm_log
+
+    @gemm_log.setter
+    def gemm_log(self, value):
+        self._gemm_log = value
+        for ex in getattr(self, "blocks", ()):
+            ex.gemm_log = value
+
+    _gemm_log = None
     loss_scale = 1.0
 
     # ------------------------------------------------------------------ step pieces
