@@ -84,7 +84,7 @@ def _pick_splits(tiles: int, k_blocks: int, units: int) -> int:
     """Split-K factor for a weight-gradient GEMM (the reduction runs over the T tokens).
 
     tiles: 256 x 256 CTA-pair output tiles of one split; units: CTA pairs (SMs / 2). Cost model,
-    fitted to measured B200 sweeps (tests/gpu_gemm_ab.py, tests/gpu_gemm_ab2.py): a launch takes
+    fitted to measured B200 sweeps (scripts/microbench/gpu_gemm_ab.py, scripts/microbench/gpu_gemm_ab2.py): a launch takes
     waves x (k-blocks per split + ~5 k-blocks of per-tile epilogue / pipeline fill), with
     waves = ceil(tiles * splits / units). Keeps >= 4 k-blocks (256 tokens) per split; ties go to
     fewer splits (less reduce-add traffic)."""

@@ -5,7 +5,7 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 
 from paper_2512_12131_b200 import kernels as K  # noqa: E402
-from tests.gpu_gemm_ab import flops, mk, timeit  # noqa: E402
+from scripts.microbench.gpu_gemm_ab import flops, mk, timeit  # noqa: E402
 
 T = 16384
 for (M, N, n) in ((5472, 512, 2), (2048, 512, 3), (5472, 512, 1), (512, 5472, 1), (1024, 2048, 1), (512, 2048, 1)):

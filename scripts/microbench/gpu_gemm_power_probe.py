@@ -1,5 +1,5 @@
 """Why do the step's GEMMs take longer back to back (67.7 us / launch) than in ncu's isolated
-replay (59.7 us at a LOWER clock)? Probe (not a pytest module):  python tests/gpu_gemm_power_probe.py
+replay (59.7 us at a LOWER clock)? Probe (not a pytest module):  python scripts/microbench/gpu_gemm_power_probe.py
 
 (a) the step's 24 GEMM launches as one graph, replayed hot back to back;
 (b) the same graph replayed once after the GPU idled 0.5 s (cool);

@@ -1,5 +1,5 @@
 """A/B of the residual-epilogue GEMM layouts against the plain epilogue at the TP=8 / TP=1
-up-projection shapes (not a pytest module):  python tests/gpu_gemm_resid_ab.py
+up-projection shapes (not a pytest module):  python scripts/microbench/gpu_gemm_resid_ab.py
 Residual modes (btp_gemm_set_res4): 0 per-chunk prefetch, 1 whole-tile staging, 2 pipelined
 residual slots fed by a producer warp (pair tiles)."""
 import sys

@@ -1,5 +1,5 @@
 """Worst relative error (vs the float64 oracle) of the virtual-rank peer-boundary step, repeated:
-python tests/gpu_peer_margin.py TP SCATTER REPS  (not a pytest module)."""
+python scripts/microbench/gpu_peer_margin.py TP SCATTER REPS  (not a pytest module)."""
 import sys
 
 sys.path.insert(0, ".")

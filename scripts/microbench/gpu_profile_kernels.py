@@ -1,6 +1,6 @@
 """Standalone launches of the step's kernels at CoLA-1B (b4 s4096, TP=1) shapes — and of the
 peer-memory boundary at CoLA-7B TP=8 shapes (tp virtual peer buffers on one GPU) — for ncu
-captures on the box:  python tests/gpu_profile_kernels.py <name> [reps]   (not a pytest module)."""
+captures on the box:  python scripts/microbench/gpu_profile_kernels.py <name> [reps]   (not a pytest module)."""
 import ctypes
 import sys
 

@@ -203,3 +203,49 @@ def test_randomised_shapes_against_torch():
         K.gemm(*probs, bn=rng.choice([0, 0, 128, 192, 256]))
         for C, want, tol in checks:
             assert rel(C, want) < tol, (case, tuple(C.shape))
+
+
+@pytest.mark.parametrize("res_mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("st_global", [0, 1])
+def test_residual_layouts_and_store_paths(res_mode, st_global):
+    """Every residual-epilogue layout (0 per-chunk, 1 whole tile, 2 producer-warp pipeline, 3 by
+    width) x both store paths (TMA bulk / coalesced st.global), incl. M / N tails, a grouped launch
+    mixing residual and plain problems, in-place accumulation (resid aliasing C, the chained dgrads)
+    and the sigma / fp32 / split-K epilogues that must ignore the store switch."""
+    prev_r, prev_s = K.set_res4(res_mode), K.set_st_global(bool(st_global))
+    try:
+        for M, N, Kd in [(1000, 640, 512), (16384, 512, 1024), (2048, 2048, 512), (296, 1000, 72)]:
+            A, B, R = _mk(M, Kd), _mk(N, Kd), _mk(M, N)
+            C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            K.gemm(K.Gemm(A, B, C, resid=R))
+            ref = A.float() @ B.float().t()
+            assert rel(C, ref + R.float()) < TOL, (M, N, Kd)
+            K.gemm(K.Gemm(A, B, C, resid=C))                      # in place: C = A B^T + C
+            assert rel(C, 2 * ref + R.float()) < TOL, (M, N, Kd, "in-place")
+        # grouped: residual + plain problems in one launch
+        A1, B1, R1 = _mk(1024, 512), _mk(768, 512), _mk(1024, 768)
+        A2, B2 = _mk(1024, 512), _mk(512, 512)
+        C1 = torch.empty(1024, 768, device="cuda", dtype=torch.bfloat16)
+        C2 = torch.empty(1024, 512, device="cuda", dtype=torch.bfloat16)
+        K.gemm(K.Gemm(A1, B1, C1, resid=R1), K.Gemm(A2, B2, C2))
+        assert rel(C1, A1.float() @ B1.float().t() + R1.float()) < TOL
+        assert rel(C2, A2.float() @ B2.float().t()) < TOL
+        # fp32 output and split-K reduce-add (TMA reduce regardless of the store switch)
+        Cf = torch.zeros(512, 640, device="cuda")
+        dY, X = _mk(4096, 512), _mk(4096, 640)
+        K.gemm(K.Gemm(dY, X, Cf, a_mn=True, b_mn=True, splits=4))
+        assert rel(Cf, dY.float().t() @ X.float()) < 1e-5
+        Cp = torch.empty(1000, 640, device="cuda")
+        A3, B3 = _mk(1000, 256), _mk(640, 256)
+        K.gemm(K.Gemm(A3, B3, Cp))
+        assert rel(Cp, A3.float() @ B3.float().t()) < 1e-5
+        # sigma epilogue (TP = 1 boundary): z and crossgate(z) both through the store path
+        n_in, W = _mk(2048, 512), _mk(1024, 512) * 0.05
+        z = torch.empty(2048, 1024, device="cuda", dtype=torch.bfloat16)
+        a = torch.empty_like(z)
+        K.gemm(K.Gemm(n_in, W, z, sigma=(a, 256)))
+        assert rel(z, n_in.float() @ W.float().t()) < TOL
+        assert rel(a, _crossgate_ref(z, 512)) < TOL
+    finally:
+        K.set_res4(prev_r)
+        K.set_st_global(bool(prev_s))

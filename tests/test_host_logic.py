@@ -9,7 +9,7 @@ from paper_2512_12131_b200.executor import _pick_splits
 
 @pytest.mark.parametrize("shapes,best", [
     # weight-gradient launches of the CoLA-1B step (T = 16384 tokens, 256 k-blocks); `best` is the
-    # fastest split count of the measured B200 sweeps (tests/gpu_gemm_ab.py, tests/gpu_gemm_ab2.py)
+    # fastest split count of the measured B200 sweeps (scripts/microbench/gpu_gemm_ab.py, scripts/microbench/gpu_gemm_ab2.py)
     ([(1024, 2048)], 2),
     ([(512, 2048)], 9),
     ([(5472, 512)], 5),
