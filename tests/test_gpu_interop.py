@@ -43,11 +43,18 @@ def test_hook_with_reference_objects_matches_btpsim(variant, online, grouping, p
     pl = bs.plan(bs.Strategy.BOTTLENECK, cfg, bs.RunShape(b, s, 1), bs.Variant(variant), online_norm=online,
                  grouping=grouping)
     want = bs.execute_forward(pl, blk, x, model_tail=True)
-    got = btp.execute_forward(pl, blk, x, model_tail=True, precision=precision)
+    got = btp.execute_forward(pl, blk, x, model_tail=True, precision=precision, capture_workspaces=True)
     assert isinstance(got.y, btp.Tensor)
     assert rel(got.y.values, want.y.values) < tol
-    # the y ≈ x residual path hides errors in the branches: compare the block's update too
-    assert rel(got.y.values - x.values, want.y.values - x.values) < tol
+    # the y ≈ x residual path hides errors in the branches: compare the branch outputs too. In
+    # fp32 mode that is the block's update y - x itself; in bf16 the update of this block is ~1 bf16
+    # ulp of y (|y - x| ~ 1e-3 |x| for the raw reference gains), so the rounding of y alone exceeds
+    # 2e-2 of it — the attention / MLP branch outputs are compared directly, as the reference's
+    # workspace tensors (simulator.py:672-706)
+    if precision == "fp32":
+        assert rel(got.y.values - x.values, want.y.values - x.values) < tol
+    for name in ("o", "mlp"):
+        assert rel(got.workspaces[0][name], want.workspaces[0][name]) < tol, name
     # the routing is BTP: our collective log is the reference's own trace, record for record
     assert got.trace.record_tuples("forward") == [
         (r.chunk_id, r.kind, r.tag, r.elements, tuple((t, e) for t, e, _ in r.extras))
