@@ -320,6 +320,26 @@ int btp_peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int
 int btp_peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
                                const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, void* stream);
 
+/* ---- attention (reference model.py:205-230 `sdpa_values`, simulator.py:221-233) ----------------
+ * Unmasked softmax(q k^T / sqrt(hd)) v per (batch, head) on tcgen05 / TMEM. q, k, v, o are bf16
+ * row-major [b*s, >= h*hd] with row strides ld* (elements, multiple of 8) and head j at columns
+ * [j*hd, (j+1)*hd): the reference's heads-as-contiguous-feature-slices layout. s % 128 == 0,
+ * hd in {64, 128}. lse (fp32 [b, h, s]) receives the log2-domain log-sum-exp of the scaled scores,
+ * log2(sum_k exp2(q.k * log2(e)/sqrt(hd))), the statistics the backward recomputes P from. */
+int btp_attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, void* o,
+                 long long ldo, float* lse, int b, int s, int h, int hd, void* stream);
+
+/* Attention backward for btp_attn_fwd's output o and lse: dq, dk, dv (bf16, same layout as q/k/v)
+ * from dO. Workspaces: D fp32 [b, h, s] (rowsum(dO o O)), dq_acc fp32 [b*s, >= h*hd] (row stride
+ * ldacc, zeroed and summed over the key tiles inside the call). Three launches: the D / zero pass,
+ * the tcgen05 kernel (one CTA per key tile walking every query tile; dK / dV in TMEM, dQ reduced
+ * into dq_acc), the dq conversion. Replaces the reference's (absent) attention backward: the
+ * analytic derivative of model.py:205-230. */
+int btp_attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv,
+                 const void* o, long long ldo, const void* dO, long long lddo, const float* lse, float* D,
+                 float* dq_acc, long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv,
+                 long long lddv, int b, int s, int h, int hd, void* stream);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

@@ -80,6 +80,9 @@ EXPORTED_SYMBOLS = (
     "btp_peer_boundary_bwd_local",
     "btp_peer_boundary_fwd_nvls",
     "btp_peer_boundary_bwd_nvls",
+    # attention
+    "btp_attn_fwd",
+    "btp_attn_bwd",
 )
 
 
@@ -166,6 +169,9 @@ _SIGNATURES = {
     "btp_peer_boundary_bwd_local": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "btp_peer_boundary_fwd_nvls": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P, _P, _P],
     "btp_peer_boundary_bwd_nvls": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
+    "btp_attn_fwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _I, _I, _I, _I, _P],
+    "btp_attn_bwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _LL, _P, _LL,
+                     _I, _I, _I, _I, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",

@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libbtp.so"
-SOURCES = ("gemm.cu", "gemm_f32.cu", "rowops.cu", "modelops.cu", "peer.cu", "capi.cu")
+SOURCES = ("gemm.cu", "gemm_f32.cu", "rowops.cu", "modelops.cu", "peer.cu", "attn.cu", "capi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,795 @@
+// Unmasked multi-head attention on tcgen05 / TMEM for sm_100a (bf16 in, fp32 softmax statistics).
+//
+// The reference runs, per (batch, head), scores = q k^T / sqrt(hd), a row softmax and probs @ v,
+// with heads as contiguous feature slices of the [T, heads*hd] activations (model.py:205-230,
+// simulator.py:221-233). Here q / k / v / o stay in that [T, width] layout: a head's 128-row tile is
+// one TMA box (64 columns = 128 B, 128B swizzle) per 64 head-dim columns, so no transposes or
+// per-head copies are ever materialised.
+//
+// Forward (one CTA per 128-query tile of one (batch, head); two CTAs per SM):
+//   w0      TMA producer: Q once, then K_j / V_j into a 2-stage ring
+//   w1      TMEM allocator + MMA issuer:  S = Q K_j^T (SS, M128 N128) -> TMEM;
+//           after the softmax warps publish P_j:  O += P_j V_j (TS: A = P_j straight from TMEM)
+//   w2..w5  softmax: thread i owns query row i == TMEM lane i, so a row's max / sum never leave
+//           the thread (no shuffles). exp2 on the MUFU; P_j is written back as packed bf16 over the
+//           first 64 columns of S (the MMA reads it as the A operand: no shared-memory round trip).
+//           The running max is updated lazily (only when it grows by > 2^8), so the O accumulator
+//           in TMEM is rescaled only on those rare tiles; the final 1/l and the log2-domain
+//           log-sum-exp (the backward's statistics) are applied in the epilogue.
+// The S buffer is single: the next S MMA is issued after P_j is consumed (tcgen05 MMAs of one
+// thread execute in order), and the second resident CTA on the SM fills the gap.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "btp_internal.h"
+#include "ptx.cuh"
+
+namespace btp {
+namespace {
+
+constexpr int kTile = 128;  // query rows per CTA and key/value rows per step
+
+template <int HD, int ST>
+struct FwdCfg {
+  static constexpr int kTileBytes = kTile * HD * 2;
+  static constexpr int kChunks = HD / 64;  // 128-byte-wide TMA boxes per tile
+  static constexpr int kTmemCols = (kTile + HD) <= 256 ? 256 : 512;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmem = 1024 + kTileBytes * (1 + 2 * ST) + kBarBytes;
+  static constexpr int kThreads = 192;
+};
+
+struct FwdParams {
+  CUtensorMap tq, tk, tv;
+  __nv_bfloat16* o;
+  long long ldo;
+  float* lse;  // [b, h, s]: log2-domain log-sum-exp of the scaled scores (m + log2 l)
+  int s, h, n_kv;
+  float c;  // log2(e) / sqrt(hd)
+};
+
+template <int HD, int ST>
+__global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ FwdParams P) {
+  using C = FwdCfg<HD, ST>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::kTileBytes;
+  uint8_t* sV = sK + ST * C::kTileBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * C::kTileBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + ST;
+  uint64_t* s_full = kv_empty + ST;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* o_bar = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 1);
+
+  const int qt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int row0 = bi * P.s + qt * kTile;
+  const int kv0 = bi * P.s;
+  const int col0 = head * HD;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(q_full, 1);
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&kv_full[s], 1);
+        mbar_init(&kv_empty[s], 1);
+      }
+      mbar_init(s_full, 1);
+      mbar_init(p_full, 4);
+      mbar_init(o_bar, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tO = tmem + kTile;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, C::kTileBytes);
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c) tma_load_2d(sQ + c * kTile * 128, &P.tq, q_full, col0 + 64 * c, row0);
+      for (int j = 0; j < P.n_kv; ++j) {
+        const int st = j % ST;
+        const uint32_t ph = (j / ST) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kTileBytes);
+        uint8_t* k_dst = sK + st * C::kTileBytes;
+        uint8_t* v_dst = sV + st * C::kTileBytes;
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(k_dst + c * kTile * 128, &P.tk, &kv_full[st], col0 + 64 * c, kv0 + j * kTile);
+          tma_load_2d(v_dst + c * kTile * 128, &P.tv, &kv_full[st], col0 + 64 * c, kv0 + j * kTile);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_bf16_f32(kTile, kTile, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16_f32(kTile, HD, false, true);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint32_t q_base = smem_u32(sQ);
+    for (int j = 0; j < P.n_kv; ++j) {
+      const int st = j % ST;
+      const uint32_t ph = (j / ST) & 1;
+      mbar_wait(&kv_full[st], ph);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sK + st * C::kTileBytes);
+      const uint32_t v_base = smem_u32(sV + st * C::kTileBytes);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * kTile * 128 + (k & 3) * 32;  // K-major: 32 B per 16 elements
+          umma_bf16(tS, make_sw128_desc(q_base + off, 16, 1024), make_sw128_desc(k_base + off, 16, 1024), idesc_s,
+                    k > 0 ? 1u : 0u);
+        }
+        umma_commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        // P_j (bf16 pairs in S columns [0, 64)) x V_j: V is MN-major ([kv, hd] rows of 128 B);
+        // 16 kv rows = 2 KB per K step, 64-column chunks kTile * 128 B apart (LBO).
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k) {
+          umma_bf16_ts(tO, tS + k * 8, make_sw128_desc(v_base + k * 2048, kTile * 128, 1024), idesc_o,
+                       (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[st]);
+        umma_commit(o_bar);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax (warps 2..5)
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const float c = P.c;
+    float m_used = 0.f, l = 0.f;
+    for (int j = 0; j < P.n_kv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint32_t s[128];
+      tmem_ld_32x32b_x64(tS + lane_addr, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
+      tmem_ld_32x32b_x64(tS + lane_addr + 64, *reinterpret_cast<uint32_t(*)[64]>(&s[64]));
+      tmem_ld_wait();
+      float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
+#pragma unroll
+      for (int i = 2; i < 128; i += 2) {
+        mx0 = fmaxf(mx0, __uint_as_float(s[i]));
+        mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+      }
+      const float m_new = fmaxf(mx0, mx1) * c;
+      if (j == 0) {
+        m_used = m_new;
+      } else {
+        const bool need = m_new > m_used + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          // rescale this row's O accumulator once PV_{j-1} has landed
+          mbar_wait(o_bar, (j - 1) & 1);
+          tc_fence_after();
+          const float alpha = need ? ex2_approx(m_used - m_new) : 1.f;
+#pragma unroll
+          for (int cc = 0; cc < HD / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + lane_addr + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(tO + lane_addr + cc * 32, o);
+          }
+          tmem_st_wait();
+          if (need) {
+            l *= alpha;
+            m_used = m_new;
+          }
+        }
+      }
+      float l0 = 0.f, l1 = 0.f;
+      uint32_t p[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float a = ex2_approx(fmaf(__uint_as_float(s[2 * i]), c, -m_used));
+        const float b = ex2_approx(fmaf(__uint_as_float(s[2 * i + 1]), c, -m_used));
+        l0 += a;
+        l1 += b;
+        p[i] = pack_bf16(a, b);
+      }
+      l += l0 + l1;
+      tmem_st_32x32b_x32(tS + lane_addr, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
+      tmem_st_32x32b_x32(tS + lane_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---------------------------------------------------------------- epilogue: O / l, lse
+    mbar_wait(o_bar, (P.n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = P.o + (long long)(row0 + row) * P.ldo + col0;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tO + lane_addr + cc * 32, o);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        st_global_v4(orow + cc * 32 + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+    }
+    P.lse[((long long)bi * P.h + head) * P.s + qt * kTile + row] = m_used + __log2f(l);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+}
+
+// ============================================================================ backward
+//
+// One CTA per 128-row key/value tile of one (batch, head) (one CTA per SM: 512 TMEM columns);
+// the CTA walks every 128-row query tile i:
+//   [1] S^T_i  = K Q_i^T        (SS)  -> tS     lane = key row n, column = query m
+//   [2] dP^T_i = V dO_i^T       (SS)  -> tdP
+//   compute warps: P^T = exp2(S^T c - lse[m]) -> bf16 over tS;  dS^T = P^T (dP^T - D[m]) -> bf16 over
+//                  tdP and, MN-major 128B-swizzled, into shared memory (the A operand of [5])
+//   [3] dV += P^T_i dO_i        (TS: A = P^T from TMEM)
+//   [4] dK += dS^T_i Q_i        (TS: A = dS^T from TMEM)
+//   [5] dQ_i = dS_i K           (SS: A = dS from shared memory) -> tdQ; four reduce warps add it
+//       into the fp32 dQ accumulator in global memory (vector red.add; summed over the key tiles)
+// dK / dV stay in TMEM for the whole walk and are written once (dK scaled by 1/sqrt(hd)).
+// MMA issue order [1]_0 [2]_0 | [3]_i [1]_{i+1} [4]_i [5]_i [2]_{i+1} | ... lets the tensor core run
+// the next tile's S^T while the compute warps form dS of this one (tcgen05 MMAs of one thread
+// execute in issue order, which is what makes the TMEM aliasing safe).
+// D = rowsum(dO o O) and the zeroed dQ accumulator come from attn_bwd_prep; attn_bwd_dq converts the
+// accumulator to bf16 with the 1/sqrt(hd) scale.
+template <int HD, int ST>
+struct BwdCfg {
+  static constexpr int kTileBytes = kTile * HD * 2;
+  static constexpr int kChunks = HD / 64;
+  static constexpr int kDsBytes = kTile * kTile * 2;  // dS (bf16) MN-major: 2 chunks of 64 queries
+  static constexpr int kStageBytes = 2 * kTileBytes + 2 * kTile * 4;  // Q, dO, lse, D
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmem = 1024 + 2 * kTileBytes + ST * kStageBytes + kDsBytes + kBarBytes;
+  static constexpr int kThreads = 320;
+  // TMEM columns
+  static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 256 + HD;
+  static constexpr uint32_t tdQ = (HD == 64) ? 384 : tdP;  // hd 128: dQ reuses the dP / dS columns
+};
+
+struct BwdParams {
+  CUtensorMap tq, tk, tv, tdo;
+  const float* lse;  // [b, h, s] log2 domain (attn_fwd)
+  const float* D;    // [b, h, s] rowsum(dO o O)
+  float* dq_acc;     // fp32 [b*s, ldacc]
+  long long ldacc;
+  __nv_bfloat16* dk;
+  long long lddk;
+  __nv_bfloat16* dv;
+  long long lddv;
+  int s, h, n_q;
+  float c;         // log2(e) / sqrt(hd)
+  float dk_scale;  // 1 / sqrt(hd)
+};
+
+__device__ __forceinline__ void red_add_v4(float* ptr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+template <int HD, int ST>
+__global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant__ BwdParams P) {
+  using C = BwdCfg<HD, ST>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::kTileBytes;
+  uint8_t* sStage = sV + C::kTileBytes;  // ST x {Q, dO, lse[128], D[128]}
+  uint8_t* sdS = sStage + ST * C::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + C::kDsBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;
+  uint64_t* qdo_empty = qdo_full + ST;
+  uint64_t* s_full = qdo_empty + ST;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* dp_full = p_full + 1;
+  uint64_t* ds_full = dp_full + 1;
+  uint64_t* sds_empty = ds_full + 1;
+  uint64_t* dq_full = sds_empty + 1;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* acc_full = dq_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int kt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int kv_row0 = bi * P.s + kt * kTile;
+  const int q_row_base = bi * P.s;
+  const int col0 = head * HD;
+  const long long stat0 = ((long long)bi * P.h + head) * P.s;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  auto sQ = [&](int st) { return sStage + st * C::kStageBytes; };
+  auto sdO = [&](int st) { return sStage + st * C::kStageBytes + C::kTileBytes; };
+  auto sLse = [&](int st) { return reinterpret_cast<float*>(sStage + st * C::kStageBytes + 2 * C::kTileBytes); };
+  auto sD = [&](int st) { return sLse(st) + kTile; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+    tma_prefetch_desc(&P.tdo);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(kv_full, 1);
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&qdo_full[s], 1);
+        mbar_init(&qdo_empty[s], 1);
+      }
+      mbar_init(s_full, 1);
+      mbar_init(p_full, 4);
+      mbar_init(dp_full, 1);
+      mbar_init(ds_full, 4);
+      mbar_init(sds_empty, 1);
+      mbar_init(dq_full, 1);
+      mbar_init(dq_empty, 4);
+      mbar_init(acc_full, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c) {
+        tma_load_2d(sK + c * kTile * 128, &P.tk, kv_full, col0 + 64 * c, kv_row0);
+        tma_load_2d(sV + c * kTile * 128, &P.tv, kv_full, col0 + 64 * c, kv_row0);
+      }
+      for (int i = 0; i < P.n_q; ++i) {
+        const int st = i % ST;
+        const uint32_t ph = (i / ST) & 1;
+        mbar_wait(&qdo_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(sQ(st) + c * kTile * 128, &P.tq, &qdo_full[st], col0 + 64 * c, q_row_base + i * kTile);
+          tma_load_2d(sdO(st) + c * kTile * 128, &P.tdo, &qdo_full[st], col0 + 64 * c, q_row_base + i * kTile);
+        }
+        bulk_load_1d(sLse(st), P.lse + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+        bulk_load_1d(sD(st), P.D + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_ss = make_idesc_bf16_f32(kTile, kTile, false, false);  // [1], [2]
+    constexpr uint32_t idesc_ts = make_idesc_bf16_f32(kTile, HD, false, true);      // [3], [4]
+    constexpr uint32_t idesc_dq = make_idesc_bf16_f32(kTile, HD, true, true);       // [5]
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), ds_base = smem_u32(sdS);
+    auto mma_ss = [&](uint32_t d, uint32_t a_base, uint32_t b_base) {  // K-major x K-major over hd
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k) {
+        const uint32_t off = (k >> 2) * kTile * 128 + (k & 3) * 32;
+        umma_bf16(d, make_sw128_desc(a_base + off, 16, 1024), make_sw128_desc(b_base + off, 16, 1024), idesc_ss,
+                  k > 0 ? 1u : 0u);
+      }
+    };
+    auto mma_ts = [&](uint32_t d, uint32_t a_tmem, uint32_t b_base, bool acc) {  // over 128 query rows
+#pragma unroll
+      for (int k = 0; k < kTile / 16; ++k)
+        umma_bf16_ts(d, a_tmem + k * 8, make_sw128_desc(b_base + k * 2048, kTile * 128, 1024), idesc_ts,
+                     (acc || k > 0) ? 1u : 0u);
+    };
+    mbar_wait(kv_full, 0);
+    mbar_wait(&qdo_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) {
+      mma_ss(tmem + C::tS, k_base, smem_u32(sQ(0)));
+      umma_commit(s_full);
+      mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(0)));
+      umma_commit(dp_full);
+    }
+    __syncwarp();
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i % ST;
+      const uint32_t ph = i & 1;
+      mbar_wait(p_full, ph);
+      tc_fence_after();
+      if (elect_one()) mma_ts(tmem + C::tdV, tmem + C::tS, smem_u32(sdO(st)), i > 0);  // [3]
+      __syncwarp();
+      const bool more = i + 1 < P.n_q;
+      const int st1 = (i + 1) % ST;
+      if (more) {
+        mbar_wait(&qdo_full[st1], ((i + 1) / ST) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss(tmem + C::tS, k_base, smem_u32(sQ(st1)));  // [1]_{i+1}
+          umma_commit(s_full);
+        }
+        __syncwarp();
+      }
+      mbar_wait(ds_full, ph);
+      tc_fence_after();
+      if (elect_one()) {
+        mma_ts(tmem + C::tdK, tmem + C::tdP, smem_u32(sQ(st)), i > 0);  // [4]
+        umma_commit(&qdo_empty[st]);
+      }
+      __syncwarp();
+      if (i > 0) {
+        mbar_wait(dq_empty, (i - 1) & 1);
+        tc_fence_after();
+      }
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)  // [5]: A = dS (MN-major, 2 chunks of 64 queries), B = K (MN-major)
+          umma_bf16(tmem + C::tdQ, make_sw128_desc(ds_base + k * 2048, kTile * 128, 1024),
+                    make_sw128_desc(k_base + k * 2048, kTile * 128, 1024), idesc_dq, k > 0 ? 1u : 0u);
+        umma_commit(dq_full);
+        umma_commit(sds_empty);
+      }
+      __syncwarp();
+      if (more) {
+        if constexpr (C::tdQ == C::tdP) {
+          mbar_wait(dq_empty, i & 1);  // dQ_i must be drained before dP^T_{i+1} overwrites it
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(st1)));  // [2]_{i+1}
+          umma_commit(dp_full);
+        }
+        __syncwarp();
+      }
+    }
+    if (elect_one()) umma_commit(acc_full);
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---------------------------------------------------------------- compute warps 2..5
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // key row within the tile == TMEM lane
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const float c = P.c;
+    const uint32_t ds_row = smem_u32(sdS) + row * 128;
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i % ST;
+      const uint32_t ph = i & 1;
+      const uint32_t lse_a = smem_u32(sLse(st)), d_a = smem_u32(sD(st));
+      mbar_wait(&qdo_full[st], (i / ST) & 1);  // lse / D of this query tile are resident
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      // P^T kept as packed bf16 pairs (the values the dV MMA consumes) for dS below
+      uint32_t pk[64];
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        float sv[64];
+        tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + h2 * 64, *reinterpret_cast<uint32_t(*)[64]>(&sv[0]));
+        tmem_ld_wait();
+#pragma unroll
+        for (int m = 0; m < 64; m += 4) {
+          const float4 l4 = ld_shared_f4(lse_a + (h2 * 64 + m) * 4);
+          pk[h2 * 32 + m / 2] = pack_bf16(ex2_approx(fmaf(sv[m], c, -l4.x)), ex2_approx(fmaf(sv[m + 1], c, -l4.y)));
+          pk[h2 * 32 + m / 2 + 1] =
+              pack_bf16(ex2_approx(fmaf(sv[m + 2], c, -l4.z)), ex2_approx(fmaf(sv[m + 3], c, -l4.w)));
+        }
+        // S^T columns [0, 64) were read in the first half: P^T columns [32 h2, 32 h2 + 32) go there
+        tmem_st_32x32b_x32(tmem + C::tS + lane_addr + h2 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[h2 * 32]));
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // dS^T = P^T (dP^T - D)
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      if (i > 0) mbar_wait(sds_empty, (i - 1) & 1);  // dQ_{i-1} has read the previous dS
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {  // 32 query columns per step
+        uint32_t dp[32];
+        tmem_ld_32x32b_x32(tmem + C::tdP + lane_addr + cc * 32, dp);
+        tmem_ld_wait();
+        uint32_t ds[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 d4 = ld_shared_f4(d_a + (cc * 32 + j) * 4);
+          const int m = cc * 32 + j;
+          const uint32_t p01 = pk[m / 2], p23 = pk[m / 2 + 1];
+          ds[j / 2] = pack_bf16(bf16_lo(p01) * (__uint_as_float(dp[j]) - d4.x),
+                                bf16_hi(p01) * (__uint_as_float(dp[j + 1]) - d4.y));
+          ds[j / 2 + 1] = pack_bf16(bf16_lo(p23) * (__uint_as_float(dp[j + 2]) - d4.z),
+                                    bf16_hi(p23) * (__uint_as_float(dp[j + 3]) - d4.w));
+        }
+        // TMEM columns [16cc, 16cc + 16) of the dP block (already read) take dS^T
+        tmem_st_32x32b_x32(tmem + C::tdP + lane_addr + cc * 16, *reinterpret_cast<uint32_t(*)[32]>(&ds[0]));
+        // shared: chunk cc/2 (64 queries), row = key, 16-byte units (cc%2)*4 .. +3, 128B swizzle
+        const uint32_t base = ds_row + (cc >> 1) * (kTile * 128);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t unit = (cc & 1) * 4 + u;
+          st_shared_v4(base + ((unit ^ (row & 7)) << 4), ds[4 * u], ds[4 * u + 1], ds[4 * u + 2], ds[4 * u + 3]);
+        }
+      }
+      tmem_st_wait();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    // ---------------------------------------------------------------- dK / dV epilogue
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    __nv_bfloat16* dvrow = P.dv + (long long)(kv_row0 + row) * P.lddv + col0;
+    __nv_bfloat16* dkrow = P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t tcol = which == 0 ? C::tdV : C::tdK;
+      const float sc = which == 0 ? 1.f : P.dk_scale;
+      __nv_bfloat16* out = which == 0 ? dvrow : dkrow;
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          st_global_v4(out + cc * 32 + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- dQ reduce warps 6..9
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // query row within the tile
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    for (int i = 0; i < P.n_q; ++i) {
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      float* dst = P.dq_acc + (long long)(q_row_base + i * kTile + row) * P.ldacc + col0;
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + C::tdQ + lane_addr + cc * 32, o);
+        tmem_ld_wait();
+        if (cc == HD / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);  // TMEM drained; the adds below only touch registers
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          red_add_v4(dst + cc * 32 + j, __uint_as_float(o[j]), __uint_as_float(o[j + 1]), __uint_as_float(o[j + 2]),
+                     __uint_as_float(o[j + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// D[b, h, s] = sum_hd dO o O (fp32) per (row, head); zero the fp32 dQ accumulator. One warp per row.
+template <int HD>
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, long long ldo,
+                                     const __nv_bfloat16* __restrict__ dO, long long lddo, float* __restrict__ D,
+                                     float* __restrict__ dq_acc, long long ldacc, int rows, int s, int h) {
+  const int warps = blockDim.x / 32;
+  const int lane = threadIdx.x & 31;
+  constexpr int kLanesPerHead = HD / 8;
+  for (int r = blockIdx.x * warps + threadIdx.x / 32; r < rows; r += gridDim.x * warps) {
+    const int bi = r / s, si = r - bi * s;
+    for (int c = lane * 8; c < h * HD; c += 32 * 8) {
+      const uint4 a = *reinterpret_cast<const uint4*>(o + (long long)r * ldo + c);
+      const uint4 g = *reinterpret_cast<const uint4*>(dO + (long long)r * lddo + c);
+      float acc = bf16_lo(a.x) * bf16_lo(g.x) + bf16_hi(a.x) * bf16_hi(g.x);
+      acc = fmaf(bf16_lo(a.y), bf16_lo(g.y), acc);
+      acc = fmaf(bf16_hi(a.y), bf16_hi(g.y), acc);
+      acc = fmaf(bf16_lo(a.z), bf16_lo(g.z), acc);
+      acc = fmaf(bf16_hi(a.z), bf16_hi(g.z), acc);
+      acc = fmaf(bf16_lo(a.w), bf16_lo(g.w), acc);
+      acc = fmaf(bf16_hi(a.w), bf16_hi(g.w), acc);
+#pragma unroll
+      for (int off = kLanesPerHead / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if ((lane % kLanesPerHead) == 0) D[((long long)bi * h + c / HD) * s + si] = acc;
+      float4* z = reinterpret_cast<float4*>(dq_acc + (long long)r * ldacc + c);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+// dq = bf16(scale * dq_acc)
+__global__ void attn_bwd_dq_kernel(const float* __restrict__ acc, long long ldacc, __nv_bfloat16* __restrict__ dq,
+                                   long long lddq, int rows, int width, float scale) {
+  const int per_row = width / 8;
+  const long long n = (long long)rows * per_row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / per_row), c = (int)(i - (long long)r * per_row) * 8;
+    const float4 a = *reinterpret_cast<const float4*>(acc + (long long)r * ldacc + c);
+    const float4 b = *reinterpret_cast<const float4*>(acc + (long long)r * ldacc + c + 4);
+    *reinterpret_cast<uint4*>(dq + (long long)r * lddq + c) =
+        make_uint4(pack_bf16(a.x * scale, a.y * scale), pack_bf16(a.z * scale, a.w * scale),
+                   pack_bf16(b.x * scale, b.y * scale), pack_bf16(b.z * scale, b.w * scale));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [rows, width] bf16 row-major with row stride ld elements; 64 x 128 boxes, 128B swizzle.
+int head_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long ld) {
+  auto enc = encode_fn();
+  if (!enc) return BTP_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, kTile};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
+}
+
+template <int HD, int ST>
+int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
+  using C = FwdCfg<HD, ST>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / kTile, P.h, b);
+  attn_fwd_kernel<HD, ST><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+template <int HD, int ST>
+int launch_bwd(const BwdParams& P, int b, cudaStream_t stream) {
+  using C = BwdCfg<HD, ST>;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_bwd_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / kTile, P.h, b);
+  attn_bwd_kernel<HD, ST><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+}  // namespace
+
+int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, void* o,
+             long long ldo, float* lse, int b, int s, int h, int hd, cudaStream_t stream) {
+  if (b <= 0 || s <= 0 || h <= 0) return BTP_ERR_DIM;
+  if (s % kTile != 0 || (hd != 64 && hd != 128)) return BTP_ERR_DIM;
+  const long long width = (long long)h * hd;
+  if (ldq < width || ldk < width || ldv < width || ldo < width) return BTP_ERR_DIM;
+  auto mis = [](const void* p, long long ld) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) != 0 || (ld * 2) % 16 != 0;
+  };
+  if (mis(q, ldq) || mis(k, ldk) || mis(v, ldv) || mis(o, ldo) || lse == nullptr) return BTP_ERR_ALIGNMENT;
+  FwdParams P{};
+  const int rows = b * s;
+  int rc;
+  if ((rc = head_tile_map(&P.tq, q, rows, (int)width, ldq)) != BTP_OK) return rc;
+  if ((rc = head_tile_map(&P.tk, k, rows, (int)width, ldk)) != BTP_OK) return rc;
+  if ((rc = head_tile_map(&P.tv, v, rows, (int)width, ldv)) != BTP_OK) return rc;
+  P.o = static_cast<__nv_bfloat16*>(o);
+  P.ldo = ldo;
+  P.lse = lse;
+  P.s = s;
+  P.h = h;
+  P.n_kv = s / kTile;
+  P.c = 1.4426950408889634f / sqrtf((float)hd);
+  return hd == 64 ? launch_fwd<64, 2>(P, b, stream) : launch_fwd<128, 1>(P, b, stream);
+}
+
+int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, const void* o,
+             long long ldo, const void* dO, long long lddo, const float* lse, float* D, float* dq_acc,
+             long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv, long long lddv, int b,
+             int s, int h, int hd, cudaStream_t stream) {
+  if (b <= 0 || s <= 0 || h <= 0) return BTP_ERR_DIM;
+  if (s % kTile != 0 || (hd != 64 && hd != 128)) return BTP_ERR_DIM;
+  const long long width = (long long)h * hd;
+  if (ldq < width || ldk < width || ldv < width || ldo < width || lddo < width || ldacc < width || lddq < width ||
+      lddk < width || lddv < width)
+    return BTP_ERR_DIM;
+  auto mis = [](const void* p, long long ld) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) != 0 || (ld * 2) % 16 != 0;
+  };
+  if (mis(q, ldq) || mis(k, ldk) || mis(v, ldv) || mis(o, ldo) || mis(dO, lddo) || mis(dq, lddq) || mis(dk, lddk) ||
+      mis(dv, lddv) || mis(dq_acc, 2 * ldacc) || lse == nullptr || D == nullptr)
+    return BTP_ERR_ALIGNMENT;
+  if ((reinterpret_cast<uintptr_t>(lse) & 15) || (reinterpret_cast<uintptr_t>(D) & 15)) return BTP_ERR_ALIGNMENT;
+  const int rows = b * s;
+  const int nsm = num_sms_cached();
+  if (hd == 64)
+    attn_bwd_prep_kernel<64><<<nsm * 8, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(o), ldo,
+                                                          static_cast<const __nv_bfloat16*>(dO), lddo, D, dq_acc,
+                                                          ldacc, rows, s, h);
+  else
+    attn_bwd_prep_kernel<128><<<nsm * 8, 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(o), ldo,
+                                                           static_cast<const __nv_bfloat16*>(dO), lddo, D, dq_acc,
+                                                           ldacc, rows, s, h);
+  BwdParams P{};
+  int rc;
+  if ((rc = head_tile_map(&P.tq, q, rows, (int)width, ldq)) != BTP_OK) return rc;
+  if ((rc = head_tile_map(&P.tk, k, rows, (int)width, ldk)) != BTP_OK) return rc;
+  if ((rc = head_tile_map(&P.tv, v, rows, (int)width, ldv)) != BTP_OK) return rc;
+  if ((rc = head_tile_map(&P.tdo, dO, rows, (int)width, lddo)) != BTP_OK) return rc;
+  P.lse = lse;
+  P.D = D;
+  P.dq_acc = dq_acc;
+  P.ldacc = ldacc;
+  P.dk = static_cast<__nv_bfloat16*>(dk);
+  P.lddk = lddk;
+  P.dv = static_cast<__nv_bfloat16*>(dv);
+  P.lddv = lddv;
+  P.s = s;
+  P.h = h;
+  P.n_q = s / kTile;
+  P.dk_scale = 1.f / sqrtf((float)hd);
+  P.c = 1.4426950408889634f * P.dk_scale;
+  rc = hd == 64 ? launch_bwd<64, 2>(P, b, stream) : launch_bwd<128, 1>(P, b, stream);
+  if (rc != BTP_OK) return rc;
+  attn_bwd_dq_kernel<<<nsm * 8, 256, 0, stream>>>(dq_acc, ldacc, static_cast<__nv_bfloat16*>(dq), lddq, rows,
+                                                  (int)width, P.dk_scale);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+}  // namespace btp

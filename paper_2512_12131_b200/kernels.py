@@ -301,3 +301,25 @@ def cross_entropy(logits, targets, loss_rows, *, dlogits=None, scale=1.0):
 
 def num_sms() -> int:
     return _native.load().btp_num_sms()
+
+
+def attn_fwd(q, k, v, o, lse, *, b: int, s: int, heads: int, head_dim: int) -> None:
+    """o = softmax(q k^T / sqrt(hd)) v per (batch, head) on [b*s, heads*hd] row-major bf16 views;
+    lse fp32 [b, heads, s] gets the log2-domain log-sum-exp (btp_attn_fwd)."""
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o)):
+        _check(t, BF16, name)
+    _check(lse, F32, "lse")
+    _native.call("btp_attn_fwd", _p(q), _ld(q), _p(k), _ld(k), _p(v), _ld(v), _p(o), _ld(o), _p(lse),
+                 b, s, heads, head_dim, _stream())
+
+
+def attn_bwd(q, k, v, o, dO, lse, D, dq_acc, dq, dk, dv, *, b: int, s: int, heads: int, head_dim: int) -> None:
+    """dq, dk, dv of attn_fwd's o for upstream dO (btp_attn_bwd); D fp32 [b, heads, s] and dq_acc fp32
+    [b*s, heads*hd] are workspaces."""
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("dO", dO), ("dq", dq), ("dk", dk), ("dv", dv)):
+        _check(t, BF16, name)
+    for name, t in (("lse", lse), ("D", D), ("dq_acc", dq_acc)):
+        _check(t, F32, name)
+    _native.call("btp_attn_bwd", _p(q), _ld(q), _p(k), _ld(k), _p(v), _ld(v), _p(o), _ld(o), _p(dO), _ld(dO),
+                 _p(lse), _p(D), _p(dq_acc), _ld(dq_acc), _p(dq), _ld(dq), _p(dk), _ld(dk), _p(dv), _ld(dv),
+                 b, s, heads, head_dim, _stream())

@@ -1,0 +1,107 @@
+"""The tcgen05 / TMEM attention kernels (csrc/attn.cu) against a plain PyTorch fp32 reference of the
+reference's unmasked per-head SDPA (model.py:205-230 `sdpa_values`: heads as contiguous feature
+slices of [T, heads*hd]).
+
+Tolerances: bf16 inputs, fp32 statistics, P rounded to bf16 before the PV MMA (as every
+flash-attention kernel does) -> 1e-2 relative Frobenius on o (measured ~3e-3), 1e-5 absolute on the
+log-sum-exp."""
+
+import math
+
+import pytest
+import torch
+
+from paper_2512_12131_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    return float((a.float() - b.float()).norm() / b.float().norm())
+
+
+def _ref(q, k, v, b, s, h, hd):
+    def v4(t):
+        return t.float().view(b, s, h, hd).transpose(1, 2)
+
+    sc = v4(q) @ v4(k).transpose(-1, -2) / math.sqrt(hd)
+    lse = torch.logsumexp(sc, dim=-1)  # natural log, [b, h, s]
+    o = torch.softmax(sc, dim=-1) @ v4(v)
+    return o.transpose(1, 2).reshape(b * s, h * hd), lse
+
+
+def _inputs(b, s, h, hd, scale=1.0, ld_pad=0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    w = h * hd
+    out = []
+    for _ in range(3):
+        t = torch.randn(b * s, w + ld_pad, device="cuda", generator=g) * scale
+        out.append(t.bfloat16()[:, :w])
+    return out
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+@pytest.mark.parametrize("b,s,h", [(1, 128, 1), (2, 256, 3), (1, 1024, 4), (2, 512, 2)])
+def test_attn_fwd_matches_fp32(b, s, h, hd):
+    q, k, v = _inputs(b, s, h, hd, seed=b * 1000 + s + h)
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
+    assert _rel(o, o_ref) < 1e-2
+    assert torch.allclose(lse * math.log(2.0), lse_ref, atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_attn_fwd_large_scores_rescale_and_strided_views(hd):
+    """Scores spread over ~+-60 so the running max grows by more than 2^8 across key tiles (the lazy
+    O rescale path), on q/k/v/o views with padded row strides (the [T, width] column slices)."""
+    b, s, h = 2, 512, 2
+    q, k, v = _inputs(b, s, h, hd, scale=3.0, ld_pad=64, seed=7)
+    # a key tile late in the sequence carries the largest scores for half the queries
+    k[b * s // 2 - 128 : b * s // 2] *= 2.0
+    obuf = torch.zeros(b * s, h * hd + 32, device="cuda", dtype=torch.bfloat16)
+    o = obuf[:, : h * hd]
+    lse = torch.empty(b, h, s, device="cuda")
+    K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
+    assert _rel(o, o_ref) < 1e-2
+    assert torch.allclose(lse * math.log(2.0), lse_ref, atol=1e-3, rtol=1e-5)
+    assert torch.count_nonzero(obuf[:, h * hd :]) == 0  # nothing written past the view
+
+
+def test_attn_fwd_rejects_bad_shapes():
+    q, k, v = _inputs(1, 128, 1, 64)
+    o = torch.empty_like(q)
+    lse = torch.empty(1, 1, 128, device="cuda")
+    with pytest.raises(Exception):
+        K.attn_fwd(q, k, v, o, lse, b=1, s=100, heads=1, head_dim=64)
+    with pytest.raises(Exception):
+        K.attn_fwd(q, k, v, o, lse, b=1, s=128, heads=1, head_dim=32)
+
+
+def _ref_bwd(q, k, v, do, b, s, h, hd):
+    qf, kf, vf = (t.float().detach().requires_grad_(True) for t in (q, k, v))
+    o, _ = _ref(qf, kf, vf, b, s, h, hd)
+    o.backward(do.float())
+    return qf.grad, kf.grad, vf.grad
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+@pytest.mark.parametrize("b,s,h", [(1, 128, 1), (2, 256, 3), (1, 1024, 2)])
+def test_attn_bwd_matches_fp32(b, s, h, hd):
+    q, k, v = _inputs(b, s, h, hd, seed=11 * s + h)
+    do = torch.randn(b * s, h * hd, device="cuda").bfloat16()
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+    D = torch.empty(b, h, s, device="cuda")
+    acc = torch.empty(b * s, h * hd, device="cuda")
+    dq, dk, dv = (torch.empty_like(o) for _ in range(3))
+    K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd)
+    torch.cuda.synchronize()
+    rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
+    errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
+    assert max(errs.values()) < 2e-2, errs
