@@ -275,8 +275,12 @@ struct BwdCfg {
   static constexpr int kChunks = HD / 64;
   static constexpr int kDsBytes = kTile * kTile * 2;  // dS (bf16) MN-major: 2 chunks of 64 queries
   static constexpr int kStageBytes = 2 * kTileBytes + 2 * kTile * 4;  // Q, dO, lse, D
-  static constexpr int kBarBytes = 256;
-  static constexpr int kSmem = 1024 + 2 * kTileBytes + ST * kStageBytes + kDsBytes + kBarBytes;
+  static constexpr int kBarBytes = 128;
+  static constexpr int kBody = 2 * kTileBytes + ST * kStageBytes + kDsBytes + kBarBytes;
+  // 1 KB of slack for aligning the dynamic window to the 128B-swizzle atom, when it fits; without
+  // it (hd 128, two stages) the kernel checks that the window is already 1 KB aligned.
+  static constexpr int kSlack = (kBody + 1024 <= 232448) ? 1024 : 0;
+  static constexpr int kSmem = kSlack + kBody;
   static constexpr int kThreads = 320;
   // TMEM columns
   static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 256 + HD;
@@ -312,7 +316,11 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
 template <int HD, int ST>
 __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant__ BwdParams P) {
   using C = BwdCfg<HD, ST>;
+  static_assert(ST >= 2, "S^T of the next query tile is issued before this tile's dK MMA releases its stage");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if constexpr (C::kSlack == 0) {
+    if (smem_u32(smem_raw) & 1023) __trap();
+  }
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + C::kTileBytes;
@@ -785,7 +793,7 @@ int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const v
   P.n_q = s / kTile;
   P.dk_scale = 1.f / sqrtf((float)hd);
   P.c = 1.4426950408889634f * P.dk_scale;
-  rc = hd == 64 ? launch_bwd<64, 2>(P, b, stream) : launch_bwd<128, 1>(P, b, stream);
+  rc = hd == 64 ? launch_bwd<64, 2>(P, b, stream) : launch_bwd<128, 2>(P, b, stream);
   if (rc != BTP_OK) return rc;
   attn_bwd_dq_kernel<<<nsm * 8, 256, 0, stream>>>(dq_acc, ldacc, static_cast<__nv_bfloat16*>(dq), lddq, rows,
                                                   (int)width, P.dk_scale);

@@ -35,13 +35,29 @@ def main():
         lse = torch.empty(b, h, s, device="cuda")
         flops = 4 * b * h * s * s * hd
         t_own = timeit(lambda: K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd))
-        v4 = lambda t: t.view(b, s, h, hd).transpose(1, 2)
+        view4 = lambda t: t.view(b, s, h, hd).transpose(1, 2)
         with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
-            t_cud = timeit(lambda: F.scaled_dot_product_attention(v4(q), v4(k), v4(v), scale=1 / math.sqrt(hd)))
-            ref = F.scaled_dot_product_attention(v4(q), v4(k), v4(v), scale=1 / math.sqrt(hd))
+            t_cud = timeit(lambda: F.scaled_dot_product_attention(view4(q), view4(k), view4(v), scale=1 / math.sqrt(hd)))
+            ref = F.scaled_dot_product_attention(view4(q), view4(k), view4(v), scale=1 / math.sqrt(hd))
         err = float((o.float() - ref.transpose(1, 2).reshape(b * s, w).float()).norm() / ref.float().norm())
         print(f"b{b} s{s} h{h} hd{hd}: own fwd {t_own*1e3:.1f} us ({flops/t_own/1e9:.0f} TF/s)  "
               f"cudnn fwd {t_cud*1e3:.1f} us ({flops/t_cud/1e9:.0f} TF/s)  rel err vs cudnn {err:.2e}", flush=True)
+        # backward: 2.5x the forward FLOPs (5 GEMMs)
+        do = torch.randn(b * s, w, device="cuda").bfloat16()
+        D = torch.empty(b, h, s, device="cuda")
+        acc = torch.empty(b * s, w, device="cuda")
+        dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+        t_ob = timeit(lambda: K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd))
+        q4, k4, v4 = (view4(t).detach().requires_grad_() for t in (q, k, v))
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            out = F.scaled_dot_product_attention(q4, k4, v4, scale=1 / math.sqrt(hd))
+            t_cb = timeit(lambda: torch.autograd.grad(out, (q4, k4, v4), view4(do), retain_graph=True))
+            gq, gk, gv = torch.autograd.grad(out, (q4, k4, v4), view4(do), retain_graph=True)
+        e = [float((a.float() - g_.transpose(1, 2).reshape(b * s, w).float()).norm() / g_.float().norm())
+             for a, g_ in ((dq, gq), (dk, gk), (dv, gv))]
+        bfl = 2.5 * flops
+        print(f"    own bwd {t_ob*1e3:.1f} us ({bfl/t_ob/1e9:.0f} TF/s)  cudnn bwd {t_cb*1e3:.1f} us ({bfl/t_cb/1e9:.0f} TF/s)"
+              f"  rel err dq/dk/dv vs cudnn {e[0]:.2e}/{e[1]:.2e}/{e[2]:.2e}", flush=True)
 
 
 if __name__ == "__main__":
