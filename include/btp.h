@@ -340,6 +340,13 @@ int btp_attn_bwd(const void* q, long long ldq, const void* k, long long ldk, con
                  float* dq_acc, long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv,
                  long long lddv, int b, int s, int h, int hd, void* stream);
 
+/* btp_attn_bwd with pipeline diagnostics: the CTA of key tile 0 / head 0 / batch 0 writes clock64()
+ * stamps of its warp roles into trace (int64 [s/128, 16], device memory) per query tile. */
+int btp_attn_bwd_trace(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv,
+                       const void* o, long long ldo, const void* dO, long long lddo, const float* lse, float* D,
+                       float* dq_acc, long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv,
+                       long long lddv, int b, int s, int h, int hd, long long* trace, void* stream);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

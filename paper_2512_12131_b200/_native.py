@@ -83,6 +83,7 @@ EXPORTED_SYMBOLS = (
     # attention
     "btp_attn_fwd",
     "btp_attn_bwd",
+    "btp_attn_bwd_trace",
 )
 
 
@@ -172,6 +173,8 @@ _SIGNATURES = {
     "btp_attn_fwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _I, _I, _I, _I, _P],
     "btp_attn_bwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _LL, _P, _LL,
                      _I, _I, _I, _I, _P],
+    "btp_attn_bwd_trace": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _LL, _P, _LL,
+                           _I, _I, _I, _I, _P, _P],
 }
 for _name in ("btp_rmsnorm_residual", "btp_rmsnorm_apply", "btp_fixup_sigma", "btp_swiglu", "btp_swiglu_bwd",
               "btp_fixup_sigma_bwd", "btp_rmsnorm_bwd", "btp_rmsnorm_bwd_prep", "btp_add", "btp_dot",

@@ -281,7 +281,7 @@ struct BwdCfg {
   // it (hd 128, two stages) the kernel checks that the window is already 1 KB aligned.
   static constexpr int kSlack = (kBody + 1024 <= 232448) ? 1024 : 0;
   static constexpr int kSmem = kSlack + kBody;
-  static constexpr int kThreads = 320;
+  static constexpr int kThreads = 448;
   // TMEM columns
   static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 256 + HD;
   static constexpr uint32_t tdQ = (HD == 64) ? 384 : tdP;  // hd 128: dQ reuses the dP / dS columns
@@ -289,6 +289,7 @@ struct BwdCfg {
 
 struct BwdParams {
   CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tdq;  // fp32 dq_acc, 32-column x 128-row boxes, 128B swizzle (hd-64 kernel's TMA reduce)
   const float* lse;  // [b, h, s] log2 domain (attn_fwd)
   const float* D;    // [b, h, s] rowsum(dO o O)
   float* dq_acc;     // fp32 [b*s, ldacc]
@@ -300,7 +301,20 @@ struct BwdParams {
   int s, h, n_q;
   float c;         // log2(e) / sqrt(hd)
   float dk_scale;  // 1 / sqrt(hd)
+  long long* trace;  // optional: per-iteration clock64 stamps of CTA (0, 0, 0) (pipeline diagnostics)
 };
+
+#define BTP_STAMP64(e)                                                                            \
+  do {                                                                                            \
+    if constexpr (kTrace) {                                                                       \
+      if (tr != nullptr && lane == 0) tr[i * 16 + (e)] = clock64();                               \
+    }                                                                                             \
+  } while (0)
+
+#define BTP_STAMP(e)                                                                              \
+  do {                                                                                            \
+    if (tr != nullptr && lane == 0) tr[i * 16 + (e)] = clock64();                                 \
+  } while (0)
 
 __device__ __forceinline__ void red_add_v4(float* ptr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "f"(a), "f"(b), "f"(c), "f"(d)
@@ -314,7 +328,7 @@ __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
 }
 
 template <int HD, int ST>
-__global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant__ BwdParams P) {
+__global__ void __launch_bounds__(448, 1) attn_bwd_kernel(const __grid_constant__ BwdParams P) {
   using C = BwdCfg<HD, ST>;
   static_assert(ST >= 2, "S^T of the next query tile is issued before this tile's dK MMA releases its stage");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -345,6 +359,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
   const int q_row_base = bi * P.s;
   const int col0 = head * HD;
   const long long stat0 = ((long long)bi * P.h + head) * P.s;
+  long long* const tr = (kt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
   auto sQ = [&](int st) { return sStage + st * C::kStageBytes; };
@@ -366,9 +381,9 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
         mbar_init(&qdo_empty[s], 1);
       }
       mbar_init(s_full, 1);
-      mbar_init(p_full, 4);
+      mbar_init(p_full, 8);
       mbar_init(dp_full, 1);
-      mbar_init(ds_full, 4);
+      mbar_init(ds_full, 8);
       mbar_init(sds_empty, 1);
       mbar_init(dq_full, 1);
       mbar_init(dq_empty, 4);
@@ -420,10 +435,12 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
                   k > 0 ? 1u : 0u);
       }
     };
-    auto mma_ts = [&](uint32_t d, uint32_t a_tmem, uint32_t b_base, bool acc) {  // over 128 query rows
+    // over 128 query rows; A = P^T / dS^T bf16 pairs: queries [64g, 64g + 64) at TMEM columns [64g, 64g + 32)
+    auto mma_ts = [&](uint32_t d, uint32_t a_tmem, uint32_t b_base, bool acc) {
 #pragma unroll
       for (int k = 0; k < kTile / 16; ++k)
-        umma_bf16_ts(d, a_tmem + k * 8, make_sw128_desc(b_base + k * 2048, kTile * 128, 1024), idesc_ts,
+        umma_bf16_ts(d, a_tmem + (k >> 2) * 64 + (k & 3) * 8, make_sw128_desc(b_base + k * 2048, kTile * 128, 1024),
+                     idesc_ts,
                      (acc || k > 0) ? 1u : 0u);
     };
     mbar_wait(kv_full, 0);
@@ -440,6 +457,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
       const int st = i % ST;
       const uint32_t ph = i & 1;
       mbar_wait(p_full, ph);
+      BTP_STAMP(8);
       tc_fence_after();
       if (elect_one()) mma_ts(tmem + C::tdV, tmem + C::tS, smem_u32(sdO(st)), i > 0);  // [3]
       __syncwarp();
@@ -454,7 +472,9 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
         }
         __syncwarp();
       }
+      BTP_STAMP(9);
       mbar_wait(ds_full, ph);
+      BTP_STAMP(10);
       tc_fence_after();
       if (elect_one()) {
         mma_ts(tmem + C::tdK, tmem + C::tdP, smem_u32(sQ(st)), i > 0);  // [4]
@@ -465,6 +485,7 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
         mbar_wait(dq_empty, (i - 1) & 1);
         tc_fence_after();
       }
+      BTP_STAMP(11);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < kTile / 16; ++k)  // [5]: A = dS (MN-major, 2 chunks of 64 queries), B = K (MN-major)
@@ -484,73 +505,82 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
           umma_commit(dp_full);
         }
         __syncwarp();
+        BTP_STAMP(12);
       }
     }
     if (elect_one()) umma_commit(acc_full);
     __syncwarp();
-  } else if (warp < 6) {
-    // ---------------------------------------------------------------- compute warps 2..5
+  } else if (warp < 10) {
+    // ---------------------------------------------------------------- compute warps 2..9
+    // Two warps per TMEM lane quarter: group g handles query columns [64g, 64g + 64) of the tile and
+    // writes its bf16 P^T / dS^T pairs over TMEM columns [64g, 64g + 32) of the S / dP blocks, which
+    // only it reads (the MMA A-operand addresses follow that split).
+    const uint32_t g = (warp - 2) >> 2;
     const uint32_t q4 = warp & 3;
     const uint32_t row = q4 * 32 + lane;  // key row within the tile == TMEM lane
     const uint32_t lane_addr = (q4 * 32) << 16;
-    const float c = P.c;
-    const uint32_t ds_row = smem_u32(sdS) + row * 128;
+    const float2 c2 = make_float2(P.c, P.c);
+    const uint32_t ds_row = smem_u32(sdS) + g * (kTile * 128) + row * 128;
     for (int i = 0; i < P.n_q; ++i) {
       const int st = i % ST;
       const uint32_t ph = i & 1;
-      const uint32_t lse_a = smem_u32(sLse(st)), d_a = smem_u32(sD(st));
+      const uint32_t lse_a = smem_u32(sLse(st)) + g * 256, d_a = smem_u32(sD(st)) + g * 256;
       mbar_wait(&qdo_full[st], (i / ST) & 1);  // lse / D of this query tile are resident
       mbar_wait(s_full, ph);
+      if (q4 == 2) BTP_STAMP(4 * g);
       tc_fence_after();
       // P^T kept as packed bf16 pairs (the values the dV MMA consumes) for dS below
-      uint32_t pk[64];
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
+      uint32_t pk[32];
+      {
         float sv[64];
-        tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + h2 * 64, *reinterpret_cast<uint32_t(*)[64]>(&sv[0]));
+        tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + g * 64, *reinterpret_cast<uint32_t(*)[64]>(&sv[0]));
         tmem_ld_wait();
 #pragma unroll
         for (int m = 0; m < 64; m += 4) {
-          const float4 l4 = ld_shared_f4(lse_a + (h2 * 64 + m) * 4);
-          pk[h2 * 32 + m / 2] = pack_bf16(ex2_approx(fmaf(sv[m], c, -l4.x)), ex2_approx(fmaf(sv[m + 1], c, -l4.y)));
-          pk[h2 * 32 + m / 2 + 1] =
-              pack_bf16(ex2_approx(fmaf(sv[m + 2], c, -l4.z)), ex2_approx(fmaf(sv[m + 3], c, -l4.w)));
+          const float4 l4 = ld_shared_f4(lse_a + m * 4);
+          const float2 x01 = ffma2(make_float2(sv[m], sv[m + 1]), c2, make_float2(-l4.x, -l4.y));
+          const float2 x23 = ffma2(make_float2(sv[m + 2], sv[m + 3]), c2, make_float2(-l4.z, -l4.w));
+          pk[m / 2] = pack_bf16(ex2_approx(x01.x), ex2_approx(x01.y));
+          pk[m / 2 + 1] = pack_bf16(ex2_approx(x23.x), ex2_approx(x23.y));
         }
-        // S^T columns [0, 64) were read in the first half: P^T columns [32 h2, 32 h2 + 32) go there
-        tmem_st_32x32b_x32(tmem + C::tS + lane_addr + h2 * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[h2 * 32]));
       }
+      tmem_st_32x32b_x32(tmem + C::tS + lane_addr + g * 64, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (q4 == 2) BTP_STAMP(4 * g + 1);
       // dS^T = P^T (dP^T - D)
       mbar_wait(dp_full, ph);
       tc_fence_after();
       if (i > 0) mbar_wait(sds_empty, (i - 1) & 1);  // dQ_{i-1} has read the previous dS
+      if (q4 == 2) BTP_STAMP(4 * g + 2);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // 32 query columns per step
+      for (int cc = 0; cc < 2; ++cc) {  // 32 query columns per step
         uint32_t dp[32];
-        tmem_ld_32x32b_x32(tmem + C::tdP + lane_addr + cc * 32, dp);
+        tmem_ld_32x32b_x32(tmem + C::tdP + lane_addr + g * 64 + cc * 32, dp);
         tmem_ld_wait();
         uint32_t ds[16];
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const float4 d4 = ld_shared_f4(d_a + (cc * 32 + j) * 4);
-          const int m = cc * 32 + j;
-          const uint32_t p01 = pk[m / 2], p23 = pk[m / 2 + 1];
-          ds[j / 2] = pack_bf16(bf16_lo(p01) * (__uint_as_float(dp[j]) - d4.x),
-                                bf16_hi(p01) * (__uint_as_float(dp[j + 1]) - d4.y));
-          ds[j / 2 + 1] = pack_bf16(bf16_lo(p23) * (__uint_as_float(dp[j + 2]) - d4.z),
-                                    bf16_hi(p23) * (__uint_as_float(dp[j + 3]) - d4.w));
+          const uint32_t p01 = pk[(cc * 32 + j) / 2], p23 = pk[(cc * 32 + j) / 2 + 1];
+          const float2 a01 = fmul2(make_float2(bf16_lo(p01), bf16_hi(p01)),
+                                   fadd2(make_float2(__uint_as_float(dp[j]), __uint_as_float(dp[j + 1])),
+                                         make_float2(-d4.x, -d4.y)));
+          const float2 a23 = fmul2(make_float2(bf16_lo(p23), bf16_hi(p23)),
+                                   fadd2(make_float2(__uint_as_float(dp[j + 2]), __uint_as_float(dp[j + 3])),
+                                         make_float2(-d4.z, -d4.w)));
+          ds[j / 2] = pack_bf16(a01.x, a01.y);
+          ds[j / 2 + 1] = pack_bf16(a23.x, a23.y);
         }
-        // TMEM columns [16cc, 16cc + 16) of the dP block (already read) take dS^T
-        tmem_st_32x32b_x32(tmem + C::tdP + lane_addr + cc * 16, *reinterpret_cast<uint32_t(*)[32]>(&ds[0]));
-        // shared: chunk cc/2 (64 queries), row = key, 16-byte units (cc%2)*4 .. +3, 128B swizzle
-        const uint32_t base = ds_row + (cc >> 1) * (kTile * 128);
+        // TMEM columns [64g + 16cc, +16) of the dP block (already read) take dS^T
+        tmem_st_32x32b_x16(tmem + C::tdP + lane_addr + g * 64 + cc * 16, ds);
+        // shared: chunk g (64 queries), row = key, 16-byte units 4cc .. 4cc + 3, 128B swizzle
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t unit = (cc & 1) * 4 + u;
-          st_shared_v4(base + ((unit ^ (row & 7)) << 4), ds[4 * u], ds[4 * u + 1], ds[4 * u + 2], ds[4 * u + 3]);
+          const uint32_t unit = cc * 4 + u;
+          st_shared_v4(ds_row + ((unit ^ (row & 7)) << 4), ds[4 * u], ds[4 * u + 1], ds[4 * u + 2], ds[4 * u + 3]);
         }
       }
       tmem_st_wait();
@@ -558,37 +588,35 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (q4 == 2) BTP_STAMP(4 * g + 3);
     }
-    // ---------------------------------------------------------------- dK / dV epilogue
+    // ---------------------------------------------------------------- dK / dV epilogue (group 0: dV, 1: dK)
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    __nv_bfloat16* dvrow = P.dv + (long long)(kv_row0 + row) * P.lddv + col0;
-    __nv_bfloat16* dkrow = P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
+    const uint32_t tcol = g == 0 ? C::tdV : C::tdK;
+    const float sc = g == 0 ? 1.f : P.dk_scale;
+    __nv_bfloat16* out = g == 0 ? P.dv + (long long)(kv_row0 + row) * P.lddv + col0
+                                : P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tcol = which == 0 ? C::tdV : C::tdK;
-      const float sc = which == 0 ? 1.f : P.dk_scale;
-      __nv_bfloat16* out = which == 0 ? dvrow : dkrow;
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
+      tmem_ld_wait();
+      uint32_t ok[16];
 #pragma unroll
-      for (int cc = 0; cc < HD / 32; ++cc) {
-        uint32_t o[32];
-        tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
-        tmem_ld_wait();
-        uint32_t pk[16];
+      for (int j = 0; j < 16; ++j) ok[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-          st_global_v4(out + cc * 32 + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
-      }
+      for (int v = 0; v < 4; ++v)
+        st_global_v4(out + cc * 32 + v * 8, make_uint4(ok[4 * v], ok[4 * v + 1], ok[4 * v + 2], ok[4 * v + 3]));
     }
   } else {
-    // ---------------------------------------------------------------- dQ reduce warps 6..9
+    // ---------------------------------------------------------------- dQ reduce warps 10..13
     const uint32_t q4 = warp & 3;
     const uint32_t row = q4 * 32 + lane;  // query row within the tile
     const uint32_t lane_addr = (q4 * 32) << 16;
     for (int i = 0; i < P.n_q; ++i) {
       mbar_wait(dq_full, i & 1);
+      if (q4 == 2) BTP_STAMP(13);
       tc_fence_after();
       float* dst = P.dq_acc + (long long)(q_row_base + i * kTile + row) * P.ldacc + col0;
 #pragma unroll
@@ -607,6 +635,351 @@ __global__ void __launch_bounds__(320, 1) attn_bwd_kernel(const __grid_constant_
                      __uint_as_float(o[j + 3]));
       }
     }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------- backward, hd 64
+// At hd = 64 the three N = hd products (dV, dK, dQ) run at half the tensor rate (an M128 x N64 x K16
+// tcgen05.mma costs the same ~64 cycles as N128: scripts/microbench/mma_rates.cu), so the tensor pipe
+// is the bound and must never wait. Differences from the generic kernel above:
+//   * dS^T is NOT written back to TMEM: the dK MMA reads it from the same shared-memory tile the dQ
+//     MMA uses (rows = key, 128 B of queries per row: K-major for A = dS^T, MN-major for A = dS);
+//   * so the dP^T block is free as soon as the compute warps hold dP^T in registers (dp_read), and
+//     dP^T of the next query tile is issued BEFORE this tile's dK / dQ MMAs;
+//   * dS (shared) and dQ (TMEM, columns 384 / 448) are double-buffered, so neither the compute warps
+//     nor the MMA issuer wait on the previous tile's dQ MMA or its reduction.
+// Tensor order per tile:  [3]_i dV  [1]_{i+1} S^T  [2]_{i+1} dP^T  [4]_i dK  [5]_i dQ.
+struct Bwd64Cfg {
+  static constexpr int HD = 64;
+  static constexpr int ST = 2;
+  static constexpr int kTileBytes = kTile * HD * 2;                 // 16 KB
+  static constexpr int kStageBytes = 2 * kTileBytes + 2 * kTile * 4;  // Q, dO, lse, D
+  static constexpr int kDsBytes = kTile * kTile * 2;                  // 32 KB per buffer
+  static constexpr int kBarBytes = 256;
+  static constexpr int kDqBytes = kTile * HD * 4;                    // fp32 dQ staging for the TMA reduce
+  static constexpr int kSmem = 1024 + 2 * kTileBytes + ST * kStageBytes + 2 * kDsBytes + kDqBytes + kBarBytes;
+  static constexpr int kThreads = 448;
+  static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 320, tdQ = 384;  // dQ: 384 / 448
+};
+
+template <bool kTrace>
+__global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constant__ BwdParams P) {
+  using C = Bwd64Cfg;
+  constexpr int HD = 64, ST = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::kTileBytes;
+  uint8_t* sStage = sV + C::kTileBytes;
+  uint8_t* sdS = sStage + ST * C::kStageBytes;  // 2 buffers
+  float* sdQ = reinterpret_cast<float*>(sdS + 2 * C::kDsBytes);  // fp32 [128][64] staging, two 32-col boxes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sdQ) + C::kDqBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;       // [2]
+  uint64_t* qdo_empty = qdo_full + 2;  // [2]
+  uint64_t* s_full = qdo_empty + 2;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* dp_full = p_full + 1;
+  uint64_t* dp_read = dp_full + 1;
+  uint64_t* ds_full = dp_read + 1;
+  uint64_t* sds_empty = ds_full + 1;   // [2]
+  uint64_t* dq_full = sds_empty + 2;   // [2]
+  uint64_t* dq_empty = dq_full + 2;    // [2]
+  uint64_t* acc_full = dq_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int kt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int kv_row0 = bi * P.s + kt * kTile;
+  const int q_row_base = bi * P.s;
+  const int col0 = head * HD;
+  const long long stat0 = ((long long)bi * P.h + head) * P.s;
+  long long* const tr = (kTrace && kt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  auto sQ = [&](int st) { return sStage + st * C::kStageBytes; };
+  auto sdO = [&](int st) { return sStage + st * C::kStageBytes + C::kTileBytes; };
+  auto sLse = [&](int st) { return reinterpret_cast<float*>(sStage + st * C::kStageBytes + 2 * C::kTileBytes); };
+  auto sD = [&](int st) { return sLse(st) + kTile; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+    tma_prefetch_desc(&P.tdo);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(kv_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        mbar_init(&qdo_full[s], 1);
+        mbar_init(&qdo_empty[s], 1);
+        mbar_init(&sds_empty[s], 1);
+        mbar_init(&dq_full[s], 1);
+        mbar_init(&dq_empty[s], 4);
+      }
+      mbar_init(s_full, 1);
+      mbar_init(p_full, 8);
+      mbar_init(dp_full, 1);
+      mbar_init(dp_read, 8);
+      mbar_init(ds_full, 8);
+      mbar_init(acc_full, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
+      tma_load_2d(sK, &P.tk, kv_full, col0, kv_row0);
+      tma_load_2d(sV, &P.tv, kv_full, col0, kv_row0);
+      for (int i = 0; i < P.n_q; ++i) {
+        const int st = i & 1;
+        mbar_wait(&qdo_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
+        tma_load_2d(sQ(st), &P.tq, &qdo_full[st], col0, q_row_base + i * kTile);
+        tma_load_2d(sdO(st), &P.tdo, &qdo_full[st], col0, q_row_base + i * kTile);
+        bulk_load_1d(sLse(st), P.lse + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+        bulk_load_1d(sD(st), P.D + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_ss = make_idesc_bf16_f32(kTile, kTile, false, false);  // [1], [2]
+    constexpr uint32_t idesc_ts = make_idesc_bf16_f32(kTile, HD, false, true);      // [3], [4]
+    constexpr uint32_t idesc_dq = make_idesc_bf16_f32(kTile, HD, true, true);       // [5]
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+    auto mma_ss = [&](uint32_t d, uint32_t a_base, uint32_t b_base) {  // K-major x K-major over hd = 64
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_bf16(d, make_sw128_desc(a_base + k * 32, 16, 1024), make_sw128_desc(b_base + k * 32, 16, 1024), idesc_ss,
+                  k > 0 ? 1u : 0u);
+    };
+    mbar_wait(kv_full, 0);
+    mbar_wait(&qdo_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) {
+      mma_ss(tmem + C::tS, k_base, smem_u32(sQ(0)));
+      umma_commit(s_full);
+      mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(0)));
+      umma_commit(dp_full);
+    }
+    __syncwarp();
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i & 1;
+      const uint32_t ph = i & 1;
+      const bool more = i + 1 < P.n_q;
+      const int st1 = st ^ 1;
+      mbar_wait(p_full, ph);
+      BTP_STAMP64(8);
+      tc_fence_after();
+      if (elect_one()) {  // [3] dV += P^T dO: A = P^T pairs, queries [64g, +64) at TMEM columns [64g, +32)
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + C::tdV, tmem + C::tS + (k >> 2) * 64 + (k & 3) * 8,
+                       make_sw128_desc(smem_u32(sdO(st)) + k * 2048, kTile * 128, 1024), idesc_ts,
+                       (i > 0 || k > 0) ? 1u : 0u);
+      }
+      __syncwarp();
+      if (more) {
+        mbar_wait(&qdo_full[st1], ((i + 1) >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss(tmem + C::tS, k_base, smem_u32(sQ(st1)));  // [1]_{i+1}
+          umma_commit(s_full);
+        }
+        __syncwarp();
+        mbar_wait(dp_read, ph);  // the compute warps hold dP^T_i in registers
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(st1)));  // [2]_{i+1}
+          umma_commit(dp_full);
+        }
+        __syncwarp();
+      }
+      BTP_STAMP64(9);
+      mbar_wait(ds_full, ph);
+      BTP_STAMP64(10);
+      tc_fence_after();
+      const uint32_t ds_base = smem_u32(sdS + st * C::kDsBytes);
+      if (elect_one()) {
+        // [4] dK += dS^T Q: A = dS^T K-major in shared memory (chunk g = queries [64g, +64), 128 B rows)
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16(tmem + C::tdK, make_sw128_desc(ds_base + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024),
+                    make_sw128_desc(smem_u32(sQ(st)) + k * 2048, kTile * 128, 1024), idesc_ts,
+                    (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&qdo_empty[st]);
+      }
+      __syncwarp();
+      if (i >= 2) {
+        mbar_wait(&dq_empty[st], ((i >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      BTP_STAMP64(11);
+      if (elect_one()) {
+        // [5] dQ_i = dS K: A = dS MN-major (the same tile), B = K MN-major
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16(tmem + C::tdQ + st * 64, make_sw128_desc(ds_base + k * 2048, kTile * 128, 1024),
+                    make_sw128_desc(k_base + k * 2048, kTile * 128, 1024), idesc_dq, k > 0 ? 1u : 0u);
+        umma_commit(&dq_full[st]);
+        umma_commit(&sds_empty[st]);
+      }
+      __syncwarp();
+      BTP_STAMP64(12);
+    }
+    if (elect_one()) umma_commit(acc_full);
+    __syncwarp();
+  } else if (warp < 10) {
+    // ---------------------------------------------------------------- compute warps 2..9
+    const uint32_t g = (warp - 2) >> 2;
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // key row within the tile == TMEM lane
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const float2 c2 = make_float2(P.c, P.c);
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i & 1;
+      const uint32_t ph = i & 1;
+      const uint32_t lse_a = smem_u32(sLse(st)) + g * 256, d_a = smem_u32(sD(st)) + g * 256;
+      mbar_wait(&qdo_full[st], (i >> 1) & 1);  // lse / D of this query tile are resident
+      mbar_wait(s_full, ph);
+      if (q4 == 2) BTP_STAMP64(4 * g);
+      tc_fence_after();
+      // P^T in fp32 registers for dS below; its bf16 pairs go to TMEM for the dV MMA
+      float pv[64];
+      tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + g * 64, *reinterpret_cast<uint32_t(*)[64]>(&pv[0]));
+      tmem_ld_wait();
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int m = 0; m < 64; m += 4) {
+          const float4 l4 = ld_shared_f4(lse_a + m * 4);
+          const float2 x01 = ffma2(make_float2(pv[m], pv[m + 1]), c2, make_float2(-l4.x, -l4.y));
+          const float2 x23 = ffma2(make_float2(pv[m + 2], pv[m + 3]), c2, make_float2(-l4.z, -l4.w));
+          pv[m] = ex2_approx(x01.x);
+          pv[m + 1] = ex2_approx(x01.y);
+          pv[m + 2] = ex2_approx(x23.x);
+          pv[m + 3] = ex2_approx(x23.y);
+          pk[m / 2] = pack_bf16(pv[m], pv[m + 1]);
+          pk[m / 2 + 1] = pack_bf16(pv[m + 2], pv[m + 3]);
+        }
+        tmem_st_32x32b_x32(tmem + C::tS + lane_addr + g * 64, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      if (q4 == 2) BTP_STAMP64(4 * g + 1);
+      mbar_wait(dp_full, ph);
+      tc_fence_after();
+      if (i >= 2) mbar_wait(&sds_empty[st], ((i >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
+      if (q4 == 2) BTP_STAMP64(4 * g + 2);
+      const uint32_t ds_row = smem_u32(sdS + st * C::kDsBytes) + g * (kTile * 128) + row * 128;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {  // 32 queries per half
+        uint32_t dp[32];
+        tmem_ld_32x32b_x32(tmem + C::tdP + lane_addr + g * 64 + hh * 32, dp);
+        tmem_ld_wait();
+        if (hh == 1) {  // dP^T of this tile is in registers: the next tile's dP^T MMA may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_read);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // 8 queries per 16-byte unit
+          uint32_t ds[4];
+#pragma unroll
+          for (int j = 0; j < 8; j += 4) {
+            const int mm = u * 8 + j, m = hh * 32 + mm;
+            const float4 d4 = ld_shared_f4(d_a + m * 4);
+            const float2 a01 = fmul2(make_float2(pv[m], pv[m + 1]),
+                                     fadd2(make_float2(__uint_as_float(dp[mm]), __uint_as_float(dp[mm + 1])),
+                                           make_float2(-d4.x, -d4.y)));
+            const float2 a23 = fmul2(make_float2(pv[m + 2], pv[m + 3]),
+                                     fadd2(make_float2(__uint_as_float(dp[mm + 2]), __uint_as_float(dp[mm + 3])),
+                                           make_float2(-d4.z, -d4.w)));
+            ds[j / 2] = pack_bf16(a01.x, a01.y);
+            ds[j / 2 + 1] = pack_bf16(a23.x, a23.y);
+          }
+          const uint32_t unit = hh * 4 + u;
+          st_shared_v4(ds_row + ((unit ^ (row & 7)) << 4), ds[0], ds[1], ds[2], ds[3]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (q4 == 2) BTP_STAMP64(4 * g + 3);
+    }
+    // ---------------------------------------------------------------- dK / dV epilogue (group 0: dV, 1: dK)
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t tcol = g == 0 ? C::tdV : C::tdK;
+    const float sc = g == 0 ? 1.f : P.dk_scale;
+    __nv_bfloat16* out = g == 0 ? P.dv + (long long)(kv_row0 + row) * P.lddv + col0
+                                : P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
+      tmem_ld_wait();
+      uint32_t ok[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) ok[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        st_global_v4(out + cc * 32 + v * 8, make_uint4(ok[4 * v], ok[4 * v + 1], ok[4 * v + 2], ok[4 * v + 3]));
+    }
+  } else {
+    // ---------------------------------------------------------------- dQ reduce warps 10..13
+    // TMEM -> registers -> 128B-swizzled fp32 smem tile -> TMA reduce-add into the fp32 accumulator
+    // (the add happens in L2; no per-thread red.global traffic in the LSU queue the compute warps use)
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // query row within the tile
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const bool issuer = (warp == 10 && lane == 0);
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i & 1;
+      mbar_wait(&dq_full[st], (i >> 1) & 1);
+      if (q4 == 2) BTP_STAMP64(13);
+      tc_fence_after();
+      uint32_t o[64];
+      tmem_ld_32x32b_x64(tmem + C::tdQ + st * 64 + lane_addr, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[st]);
+      if (issuer) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
+      named_bar_sync(1, 128);
+#pragma unroll
+      for (int bx = 0; bx < 2; ++bx) {  // box bx: columns [32 bx, 32 bx + 32) = 8 units of 16 B per row
+        const uint32_t base = smem_u32(sdQ) + bx * (kTile * 128) + row * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          st_shared_v4(base + ((u ^ (row & 7)) << 4), o[bx * 32 + 4 * u], o[bx * 32 + 4 * u + 1],
+                       o[bx * 32 + 4 * u + 2], o[bx * 32 + 4 * u + 3]);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (issuer) {
+        tma_reduce_add_2d(&P.tdq, sdQ, col0, q_row_base + i * kTile);
+        tma_reduce_add_2d(&P.tdq, reinterpret_cast<uint8_t*>(sdQ) + kTile * 128, col0 + 32, q_row_base + i * kTile);
+        bulk_commit();
+      }
+    }
+    if (issuer) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -688,6 +1061,20 @@ int head_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long lon
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
+// fp32 [rows, width] with row stride ld elements; 32 x 128 boxes (128 B rows), 128B swizzle.
+int f32_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long ld) {
+  auto enc = encode_fn();
+  if (!enc) return BTP_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, kTile};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
+}
+
 template <int HD, int ST>
 int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
   using C = FwdCfg<HD, ST>;
@@ -716,6 +1103,26 @@ int launch_bwd(const BwdParams& P, int b, cudaStream_t stream) {
   }
   dim3 grid(P.s / kTile, P.h, b);
   attn_bwd_kernel<HD, ST><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
+  using C = Bwd64Cfg;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_bwd64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(attn_bwd64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+            cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / kTile, P.h, b);
+  if (P.trace != nullptr)
+    attn_bwd64_kernel<true><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  else
+    attn_bwd64_kernel<false><<<grid, C::kThreads, C::kSmem, stream>>>(P);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
@@ -750,7 +1157,7 @@ int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const v
 int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, const void* o,
              long long ldo, const void* dO, long long lddo, const float* lse, float* D, float* dq_acc,
              long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv, long long lddv, int b,
-             int s, int h, int hd, cudaStream_t stream) {
+             int s, int h, int hd, cudaStream_t stream, long long* trace) {
   if (b <= 0 || s <= 0 || h <= 0) return BTP_ERR_DIM;
   if (s % kTile != 0 || (hd != 64 && hd != 128)) return BTP_ERR_DIM;
   const long long width = (long long)h * hd;
@@ -780,6 +1187,7 @@ int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const v
   if ((rc = head_tile_map(&P.tk, k, rows, (int)width, ldk)) != BTP_OK) return rc;
   if ((rc = head_tile_map(&P.tv, v, rows, (int)width, ldv)) != BTP_OK) return rc;
   if ((rc = head_tile_map(&P.tdo, dO, rows, (int)width, lddo)) != BTP_OK) return rc;
+  if ((rc = f32_tile_map(&P.tdq, dq_acc, rows, (int)width, ldacc)) != BTP_OK) return rc;
   P.lse = lse;
   P.D = D;
   P.dq_acc = dq_acc;
@@ -793,7 +1201,8 @@ int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const v
   P.n_q = s / kTile;
   P.dk_scale = 1.f / sqrtf((float)hd);
   P.c = 1.4426950408889634f * P.dk_scale;
-  rc = hd == 64 ? launch_bwd<64, 2>(P, b, stream) : launch_bwd<128, 2>(P, b, stream);
+  P.trace = trace;
+  rc = hd == 64 ? launch_bwd64(P, b, stream) : launch_bwd<128, 2>(P, b, stream);
   if (rc != BTP_OK) return rc;
   attn_bwd_dq_kernel<<<nsm * 8, 256, 0, stream>>>(dq_acc, ldacc, static_cast<__nv_bfloat16*>(dq), lddq, rows,
                                                   (int)width, P.dk_scale);

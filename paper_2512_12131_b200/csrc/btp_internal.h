@@ -79,5 +79,5 @@ int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const v
 int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, const void* o,
              long long ldo, const void* dO, long long lddo, const float* lse, float* D, float* dq_acc,
              long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv, long long lddv, int b,
-             int s, int h, int hd, cudaStream_t stream);
+             int s, int h, int hd, cudaStream_t stream, long long* trace = nullptr);
 }  // namespace btp

@@ -50,6 +50,14 @@ int btp_attn_bwd(const void* q, long long ldq, const void* k, long long ldk, con
                        b, s, h, hd, ST(stream));
 }
 
+int btp_attn_bwd_trace(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv,
+                       const void* o, long long ldo, const void* dO, long long lddo, const float* lse, float* D,
+                       float* dq_acc, long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv,
+                       long long lddv, int b, int s, int h, int hd, long long* trace, void* stream) {
+  return btp::attn_bwd(q, ldq, k, ldk, v, ldv, o, ldo, dO, lddo, lse, D, dq_acc, ldacc, dq, lddq, dk, lddk, dv, lddv,
+                       b, s, h, hd, ST(stream), trace);
+}
+
 int btp_gemm_f32(const btp_gemm_problem* problems, int n, void* stream) {
   return btp::gemm_f32_launch(problems, n, ST(stream));
 }
