@@ -148,6 +148,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------- CPU arm
+def attention_label(attn: str, cfg, args) -> str:
+    from paper_2512_12131_b200 import attention as A
+
+    hl = cfg.heads // max(1, getattr(args, "gpus", 1))
+    native = attn == "native" or (attn == "auto" and A.AUTO_NATIVE and A.native_supported(args.s, cfg.d // cfg.heads))
+    if native:
+        return "own tcgen05/TMEM flash kernels (btp_attn_fwd / btp_attn_bwd; not a changed subsystem)"
+    return "cuDNN SDPA via torch (not a changed subsystem)"
+
+
 def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True, optimizer=True):
     """Oracle port (float64 NumPy, BLAS) fwd+bwd+AdamW on a bounded sample: ONE sequence (b=1) of the
     workload's length s. Returns (tokens_per_s, per-step seconds list, threads)."""
@@ -609,7 +619,7 @@ def run_ours(args, cfg):
                    "boundary": args.boundary if tp > 1 else "none (tp=1)",
                    "boundary_dtype": args.boundary_dtype if tp > 1 else None,
                    "optimizer": None if args.no_optimizer else dict(ADAMW, kind="AdamW fp32 master+moments, fused"),
-                   "attention": "cuDNN SDPA via torch (not a changed subsystem)"},
+                   "attention": attention_label(args.attn, cfg, args)},
         "clocks": clk.summary() if clk is not None else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry-run"]},
         "e2e": e2e,
         "gpu_launches": launches,
@@ -695,7 +705,7 @@ def main(argv=None):
                     help="CPU + gloo: launch path, rendezvous and JSON schema only (contract test; no measurement)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
-    ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash"])
+    ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native"])
     ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
                     help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
     ap.add_argument("--boundary-dtype", default="bf16", choices=["bf16", "fp32"],

@@ -347,6 +347,18 @@ int btp_attn_bwd_trace(const void* q, long long ldq, const void* k, long long ld
                        float* dq_acc, long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv,
                        long long lddv, int b, int s, int h, int hd, long long* trace, void* stream);
 
+/* btp_attn_fwd with pipeline diagnostics (split-row kernel): the CTA of query tile 0 / head 0 / batch 0
+ * writes clock64() stamps of its warp roles into trace (int64 [s/128, 16], device memory) per key tile. */
+int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv,
+                       void* o, long long ldo, float* lse, int b, int s, int h, int hd, long long* trace, void* stream);
+
+/* Attention tuning knobs (host-side state read at launch; graph captures keep their choice). key 0: every
+ * n-th exp2 pair of the forward softmax on the FMA pipe (polynomial) instead of the MUFU (n in {0 = none,
+ * 2, 3, 4, 5}, default 4); key 1: forward kernel (1 = split-row double-buffered, default; 0 = single S
+ * buffer, two CTAs per SM); key 2: in the hd-64 backward's P phase, every n-th group of four exp2s has two
+ * on the FMA pipe (n in {0 = none, 1, 2, 4}). value < 0 only queries. Returns the previous value (-1: unknown key). */
+int btp_attn_tune(int key, int value);
+
 /* *ctr += delta on the stream (device-side step counters). */
 int btp_counter_add(int* ctr, int delta, void* stream);
 

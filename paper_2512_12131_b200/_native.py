@@ -84,6 +84,8 @@ EXPORTED_SYMBOLS = (
     "btp_attn_fwd",
     "btp_attn_bwd",
     "btp_attn_bwd_trace",
+    "btp_attn_tune",
+    "btp_attn_fwd_trace",
 )
 
 
@@ -173,6 +175,8 @@ _SIGNATURES = {
     "btp_attn_fwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _I, _I, _I, _I, _P],
     "btp_attn_bwd": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _LL, _P, _LL,
                      _I, _I, _I, _I, _P],
+    "btp_attn_tune": [_I, _I],
+    "btp_attn_fwd_trace": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _I, _I, _I, _I, _P, _P],
     "btp_attn_bwd_trace": [_P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _LL, _P, _P, _P, _LL, _P, _LL, _P, _LL, _P, _LL,
                            _I, _I, _I, _I, _P, _P],
 }

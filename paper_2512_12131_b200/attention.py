@@ -2,11 +2,16 @@
 
 Attention is NOT one of the subsystems BTP changes: the reference runs an
 unmasked softmax(q k^T / sqrt(hd)) v per head with heads as contiguous feature slices
-(model.py:205-230, simulator.py:221-233). Here it is delegated, like a cuBLAS GEMM, to the
-cuDNN (Blackwell) or FlashAttention SDPA kernels through torch's SDPA dispatcher, with the
-backend pinned by `sdpa_kernel` (cuDNN first). q/k/v are passed as strided [b, h, s, hd] views
-of the [T, d] buffers, so no transposes are materialised; the backward is one
-`torch.autograd.grad` over the recorded SDPA node (no Python autograd elsewhere in the block).
+(model.py:205-230, simulator.py:221-233). Two implementations behind one interface:
+
+* "native": this package's tcgen05 / TMEM kernels (csrc/attn.cu, `btp_attn_fwd` / `btp_attn_bwd`)
+  straight on the [T, width] buffers (head j = columns [j*hd, (j+1)*hd)), hd 64 / 128, s % 128 == 0;
+  the forward keeps the log2-domain log-sum-exp for the backward.
+* "cudnn" / "flash": torch's SDPA dispatcher (cuDNN's Blackwell kernels first), with q/k/v passed as
+  strided [b, h, s, hd] views of the [T, d] buffers; the backward is one `torch.autograd.grad` over
+  the recorded SDPA node.
+"auto" picks "native" where it applies (measured per shape in scripts/microbench/gpu_attn_bench.py),
+else cuDNN. "fp32" is the parity mode (fp32 q/k/v through the exact SDPA kernels).
 """
 
 from __future__ import annotations
@@ -14,6 +19,8 @@ from __future__ import annotations
 import torch
 import torch.nn.functional as F
 from torch.nn.attention import SDPBackend, sdpa_kernel
+
+from . import kernels as K
 
 _BACKENDS = {
     "auto": [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION],
@@ -43,13 +50,29 @@ class _Timed:
             self.timer.append((self.e0, e1, self.kind))
 
 
+def native_supported(s: int, head_dim: int) -> bool:
+    return s % 128 == 0 and head_dim in (64, 128)
+
+
+# "auto" resolution: the native kernels where they apply and are the faster choice (set from the
+# measured A/B; scripts/microbench/gpu_attn_bench.py, profiles/README.md)
+AUTO_NATIVE = False
+
+
 class Attention:
     timer: list | None = None  # bench instrumentation: (start_event, end_event, "fwd"|"bwd")
 
     def __init__(self, b: int, s: int, heads: int, head_dim: int, backend: str = "auto"):
         self.b, self.s, self.h, self.hd = b, s, heads, head_dim
         self.scale = 1.0 / head_dim**0.5
-        self.backends = _BACKENDS[backend]
+        if backend == "auto" and AUTO_NATIVE and native_supported(s, head_dim):
+            backend = "native"
+        if backend == "native" and not native_supported(s, head_dim):
+            raise ValueError(f"native attention needs s % 128 == 0 and head_dim in (64, 128); got s={s}, "
+                             f"head_dim={head_dim}")
+        self.native = backend == "native"
+        self.backends = None if self.native else _BACKENDS[backend]
+        self.stats = None  # the owning executor's ExecStats: native launches are counted there
 
     def _view4(self, t2d: torch.Tensor) -> torch.Tensor:
         # [T, h*hd] -> [b, h, s, hd] view (heads are contiguous feature slices)
@@ -62,6 +85,15 @@ class Attention:
         return t.reshape(self.b * self.s, self.h * self.hd)
 
     def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, need_grad: bool = True):
+        if self.native:
+            T = self.b * self.s
+            out = torch.empty(T, self.h * self.hd, device=q.device, dtype=torch.bfloat16)
+            lse = torch.empty(self.b, self.h, self.s, device=q.device, dtype=torch.float32)
+            with _Timed(self.timer, "fwd"):
+                K.attn_fwd(q, k, v, out, lse, b=self.b, s=self.s, heads=self.h, head_dim=self.hd)
+            if self.stats is not None:
+                self.stats.kernel_launches += 1
+            return out, (q, k, v, out, lse)
         q4, k4, v4 = (self._view4(t).detach().requires_grad_(need_grad) for t in (q, k, v))
         with torch.enable_grad() if need_grad else torch.no_grad(), sdpa_kernel(self.backends, set_priority=True), \
                 _Timed(self.timer, "fwd"):
@@ -69,6 +101,20 @@ class Attention:
         return self._as2d(out.detach()), (q4, k4, v4, out)
 
     def backward(self, dout: torch.Tensor, ctx):
+        if self.native:
+            q, k, v, out, lse = ctx
+            T, W = self.b * self.s, self.h * self.hd
+            dq, dk, dv = (torch.empty(T, W, device=q.device, dtype=torch.bfloat16) for _ in range(3))
+            D = torch.empty(self.b, self.h, self.s, device=q.device, dtype=torch.float32)
+            acc = torch.empty(T, W, device=q.device, dtype=torch.float32)
+            if dout.stride(-1) != 1:
+                dout = dout.contiguous()
+            with _Timed(self.timer, "bwd"):
+                K.attn_bwd(q, k, v, out, dout, lse, D, acc, dq, dk, dv, b=self.b, s=self.s, heads=self.h,
+                           head_dim=self.hd)
+            if self.stats is not None:
+                self.stats.kernel_launches += 3  # D / zero pass, the tcgen05 kernel, dq conversion
+            return dq, dk, dv
         q4, k4, v4, out = ctx
         do4 = self._view4(dout)
         with sdpa_kernel(self.backends, set_priority=True), _Timed(self.timer, "bwd"):

@@ -72,6 +72,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.dl = cfg.d  # replicated residual
         self.attn = Attention(pl.shape.b, pl.shape.s, cfg.heads, cfg.head_dim,
                               "fp32" if precision == "fp32" else attn_backend)
+        self.attn.stats = self.stats
         if pl.variant is Variant.COLA:
             idx = cola_pair_indices(cfg.r, self.tp, self.rank)
         else:
@@ -343,6 +344,7 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
         self.dl, self.fl, self.hl = cfg.d // tp, cfg.d_ff // tp, cfg.heads // tp
         self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
                               "fp32" if precision == "fp32" else attn_backend)
+        self.attn.stats = self.stats
         sl, fsl = slice(rk * self.dl, (rk + 1) * self.dl), slice(rk * self.fl, (rk + 1) * self.fl)
         Wf = {n: t.values for n, t in block.full.items()}
         # d_ff shard padded to a multiple of 8 for 16-byte TMA strides (exact: zero rows / columns)

@@ -49,9 +49,10 @@ struct FwdParams {
   float* lse;  // [b, h, s]: log2-domain log-sum-exp of the scaled scores (m + log2 l)
   int s, h, n_kv;
   float c;  // log2(e) / sqrt(hd)
+  long long* trace;  // optional clock64 stamps of CTA (0, 0, 0), [n_kv][16] (pipeline diagnostics)
 };
 
-template <int HD, int ST>
+template <int HD, int ST, int kPoly>
 __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ FwdParams P) {
   using C = FwdCfg<HD, ST>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -174,13 +175,17 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
       tmem_ld_32x32b_x64(tS + lane_addr, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
       tmem_ld_32x32b_x64(tS + lane_addr + 64, *reinterpret_cast<uint32_t(*)[64]>(&s[64]));
       tmem_ld_wait();
-      float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
+      float mx[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
 #pragma unroll
-      for (int i = 2; i < 128; i += 2) {
-        mx0 = fmaxf(mx0, __uint_as_float(s[i]));
-        mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+      for (int i = 4; i < 128; i += 8) {
+        mx[0] = fmax3(mx[0], __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+        mx[1] = fmax3(mx[1], __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+        if (i + 4 < 128) {
+          mx[2] = fmax3(mx[2], __uint_as_float(s[i + 4]), __uint_as_float(s[i + 5]));
+          mx[3] = fmax3(mx[3], __uint_as_float(s[i + 6]), __uint_as_float(s[i + 7]));
+        }
       }
-      const float m_new = fmaxf(mx0, mx1) * c;
+      const float m_new = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;
       if (j == 0) {
         m_used = m_new;
       } else {
@@ -206,19 +211,28 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
           }
         }
       }
-      float l0 = 0.f, l1 = 0.f;
-      uint32_t p[64];
+      // exp2 on the MUFU, except every kPoly-th pair on the FMA pipe (ex2_poly2): the MUFU's 16 / clk / SM
+      // is this loop's bound
+      float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
+      const float2 c2 = make_float2(c, c), nm = make_float2(-m_used, -m_used);
+      // P pair i is packed into s[i] (s[2i], s[2i+1] are consumed by then): no second 64-register array
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        const float a = ex2_approx(fmaf(__uint_as_float(s[2 * i]), c, -m_used));
-        const float b = ex2_approx(fmaf(__uint_as_float(s[2 * i + 1]), c, -m_used));
-        l0 += a;
-        l1 += b;
-        p[i] = pack_bf16(a, b);
+        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nm);
+        float2 e;
+        if (kPoly > 0 && (i % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
+          e = ex2_poly2(x);
+        } else {
+          e.x = ex2_approx(x.x);
+          e.y = ex2_approx(x.y);
+        }
+        if (i & 1) l2b = fadd2(l2b, e);
+        else l2a = fadd2(l2a, e);
+        s[i] = pack_bf16(e.x, e.y);
       }
-      l += l0 + l1;
-      tmem_st_32x32b_x32(tS + lane_addr, *reinterpret_cast<uint32_t(*)[32]>(&p[0]));
-      tmem_st_32x32b_x32(tS + lane_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&p[32]));
+      l += (l2a.x + l2a.y) + (l2b.x + l2b.y);
+      tmem_st_32x32b_x32(tS + lane_addr, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_st_32x32b_x32(tS + lane_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -249,6 +263,296 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
+}
+
+// ---------------------------------------------------------------------------- forward, split rows
+// The kernel above alternates, per query tile, softmax and the PV + next-S MMAs on one S buffer, so
+// each CTA's softmax waits ~800 tensor cycles per key tile (2 CTAs / SM only partly hide it). This one
+// (one CTA / SM, 512 TMEM columns):
+//   * double-buffers S (columns 0 / 128): S_{j+1} is computed while the softmax works on S_j;
+//   * splits every query row's 128 keys over two warps (group g = keys [64g, 64g + 64)), each with its
+//     OWN running max m_g, sum l_g and O accumulator O_g (columns 256 + g*hd): no cross-warp exchange
+//     inside the loop, 8 softmax warps (two per scheduler); PV is two K = 64 MMA chains (O_g += P_g V_g);
+//   * combines once at the end: O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) / (l_0 2^(m_0-m) + l_1 2^(m_1-m)).
+// kSplit key groups per row (2, or 4 at hd 64: 2 S buffers + 4 O accumulators fill the 512 columns).
+template <int HD, int ST, int kSplit>
+struct Fwd2Cfg {
+  static constexpr int kTileBytes = kTile * HD * 2;
+  static constexpr int kChunks = HD / 64;
+  static constexpr int kKG = kTile / kSplit;              // keys per group
+  static constexpr int kMlBytes = kSplit * 2 * kTile * 4;  // (m, l) per group and row
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmem = 1024 + kTileBytes * (1 + 2 * ST) + kMlBytes + kBarBytes;
+  static constexpr int kSoftWarps = 4 * kSplit;
+  static constexpr int kThreads = 64 + 32 * kSoftWarps;
+  static constexpr uint32_t tO = 256;  // O_g at 256 + g * HD
+  static_assert(256 + kSplit * HD <= 512, "TMEM budget");
+};
+
+template <int HD, int ST, int kPoly, int kSplit>
+__global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
+    attn_fwd2_kernel(const __grid_constant__ FwdParams P) {
+  using C = Fwd2Cfg<HD, ST, kSplit>;
+  constexpr int kKG = C::kKG;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + C::kTileBytes;
+  uint8_t* sV = sK + ST * C::kTileBytes;
+  float* sML = reinterpret_cast<float*>(sV + ST * C::kTileBytes);  // [kSplit groups][m | l][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sML) + C::kMlBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + ST;
+  uint64_t* s_full = kv_empty + ST;  // [2]
+  uint64_t* p_full = s_full + 2;     // [2]
+  uint64_t* o_bar = p_full + 2;      // one phase per PV pair
+  uint64_t* o_final = o_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
+
+  const int qt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int row0 = bi * P.s + qt * kTile;
+  const int kv0 = bi * P.s;
+  const int col0 = head * HD;
+  const int n = P.n_kv;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  long long* const tr = (qt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
+#define FSTAMP(jj, e)                                               \
+  do {                                                              \
+    if (tr != nullptr && lane == 0) tr[(jj) * 16 + (e)] = clock64(); \
+  } while (0)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(q_full, 1);
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&kv_full[s], 1);
+        mbar_init(&kv_empty[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_full[b], 1);
+        mbar_init(&p_full[b], C::kSoftWarps);
+      }
+      mbar_init(o_bar, 1);
+      mbar_init(o_final, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, C::kTileBytes);
+#pragma unroll
+      for (int c = 0; c < C::kChunks; ++c) tma_load_2d(sQ + c * kTile * 128, &P.tq, q_full, col0 + 64 * c, row0);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % ST;
+        mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_2d(sK + st * C::kTileBytes + c * kTile * 128, &P.tk, &kv_full[st], col0 + 64 * c, kv0 + j * kTile);
+          tma_load_2d(sV + st * C::kTileBytes + c * kTile * 128, &P.tv, &kv_full[st], col0 + 64 * c, kv0 + j * kTile);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_bf16_f32(kTile, kTile, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16_f32(kTile, HD, false, true);
+    const uint32_t q_base = smem_u32(sQ);
+    auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j & 1
+      const int st = j % ST;
+      mbar_wait(&kv_full[st], (j / ST) & 1);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sK + st * C::kTileBytes);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t off = (k >> 2) * kTile * 128 + (k & 3) * 32;
+          umma_bf16(tmem + (j & 1) * 128, make_sw128_desc(q_base + off, 16, 1024),
+                    make_sw128_desc(k_base + off, 16, 1024), idesc_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    issue_s(0);
+    if (n > 1) issue_s(1);
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1, st = j % ST;
+      mbar_wait(&p_full[b], (j >> 1) & 1);
+      FSTAMP(j, 8);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sV + st * C::kTileBytes);
+      if (elect_one()) {
+        // O_g += P_g V[kKG g, kKG (g + 1)): A = P_g (bf16 pairs at S columns kKG g ..), B = V rows (MN-major)
+#pragma unroll
+        for (int g = 0; g < kSplit; ++g) {
+#pragma unroll
+          for (int k = 0; k < kKG / 16; ++k)
+            umma_bf16_ts(tmem + C::tO + g * HD, tmem + b * 128 + g * kKG + k * 8,
+                         make_sw128_desc(v_base + (g * kKG + 16 * k) * 128, kTile * 128, 1024), idesc_o,
+                         (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[st]);
+        umma_commit(o_bar);
+        if (j == n - 1) umma_commit(o_final);
+      }
+      __syncwarp();
+      FSTAMP(j, 9);
+      if (j + 2 < n) issue_s(j + 2);  // into buffer b, which P_j (just consumed) aliased
+      FSTAMP(j, 10);
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax warps 2 .. 2 + 4 kSplit
+    const uint32_t g = (warp - 2) >> 2;  // key group
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const uint32_t tOg = tmem + C::tO + g * HD + lane_addr;
+    const float c = P.c;
+    float m_used = 0.f, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const int b = j & 1;
+      const uint32_t tSg = tmem + b * 128 + g * kKG + lane_addr;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      if (q4 == 2) FSTAMP(j, 4 * g);
+      tc_fence_after();
+      uint32_t s[kKG];
+      if constexpr (kKG == 64) tmem_ld_32x32b_x64(tSg, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
+      else tmem_ld_32x32b_x32(tSg, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      tmem_ld_wait();
+      float mx[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
+#pragma unroll
+      for (int i = 4; i < kKG; i += 8) {
+        mx[0] = fmax3(mx[0], __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+        mx[1] = fmax3(mx[1], __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+        if (i + 4 < kKG) {
+          mx[2] = fmax3(mx[2], __uint_as_float(s[i + 4]), __uint_as_float(s[i + 5]));
+          mx[3] = fmax3(mx[3], __uint_as_float(s[i + 6]), __uint_as_float(s[i + 7]));
+        }
+      }
+      const float m_new = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;
+      if (q4 == 2) FSTAMP(j, 4 * g + 1);
+      if (j == 0) {
+        m_used = m_new;
+      } else {
+        const bool need = m_new > m_used + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          // O_g must hold PV_{j-1} before it is rescaled (S_j was issued after PV_{j-2}: the barrier is at
+          // phase j-1 or j, so the parity wait is unambiguous)
+          mbar_wait(o_bar, (j - 1) & 1);
+          tc_fence_after();
+          const float alpha = need ? ex2_approx(m_used - m_new) : 1.f;
+#pragma unroll
+          for (int cc = 0; cc < HD / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tOg + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(tOg + cc * 32, o);
+          }
+          tmem_st_wait();
+          if (need) {
+            l *= alpha;
+            m_used = m_new;
+          }
+        }
+      }
+      float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
+      const float2 c2 = make_float2(c, c), nm = make_float2(-m_used, -m_used);
+#pragma unroll
+      for (int i = 0; i < kKG / 2; ++i) {
+        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nm);
+        float2 e;
+        if (kPoly > 0 && (i % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
+          e = ex2_poly2(x);
+        } else {
+          e.x = ex2_approx(x.x);
+          e.y = ex2_approx(x.y);
+        }
+        if (i & 1) l2b = fadd2(l2b, e);
+        else l2a = fadd2(l2a, e);
+        s[i] = pack_bf16(e.x, e.y);
+      }
+      l += (l2a.x + l2a.y) + (l2b.x + l2b.y);
+      if constexpr (kKG == 64) tmem_st_32x32b_x32(tSg, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      else tmem_st_32x32b_x16(tSg, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (q4 == 2) FSTAMP(j, 4 * g + 2);
+    }
+    // ---------------------------------------------------------------- epilogue: combine the groups
+    sML[(g * 2 + 0) * kTile + row] = m_used;
+    sML[(g * 2 + 1) * kTile + row] = l;
+    named_bar_sync(1, 32 * C::kSoftWarps);
+    float mg[kSplit], lg[kSplit];
+    float m = -3.0e38f;
+#pragma unroll
+    for (int x = 0; x < kSplit; ++x) {
+      mg[x] = sML[(x * 2) * kTile + row];
+      lg[x] = sML[(x * 2 + 1) * kTile + row];
+      m = fmaxf(m, mg[x]);
+    }
+    float L = 0.f;
+#pragma unroll
+    for (int x = 0; x < kSplit; ++x) {
+      mg[x] = ex2_approx(mg[x] - m);  // group weight before normalisation
+      L = fmaf(lg[x], mg[x], L);
+    }
+    const float inv = 1.f / L;
+    mbar_wait(o_final, 0);
+    tc_fence_after();
+    __nv_bfloat16* orow = P.o + (long long)(row0 + row) * P.ldo + col0;
+    constexpr int kOC = HD / kSplit;  // output columns of this warp: [g kOC, (g + 1) kOC)
+#pragma unroll
+    for (int cc = 0; cc < kOC / 16; ++cc) {
+      const int oc = g * kOC + cc * 16;
+      float acc[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int x = 0; x < kSplit; ++x) {
+        uint32_t ox[16];
+        tmem_ld_32x32b_x16(tmem + C::tO + x * HD + oc + lane_addr, ox);
+        tmem_ld_wait();
+        const float w = mg[x] * inv;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fmaf(__uint_as_float(ox[i]), w, acc[i]);
+      }
+      uint32_t pk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(acc[2 * i], acc[2 * i + 1]);
+      st_global_v4(orow + oc, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+      st_global_v4(orow + oc + 8, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+    }
+    if (g == 0) P.lse[((long long)bi * P.h + head) * P.s + qt * kTile + row] = m + __log2f(L);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+#undef FSTAMP
 }
 
 // ============================================================================ backward
@@ -668,7 +972,7 @@ struct Bwd64Cfg {
   static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 320, tdQ = 384;  // dQ: 384 / 448
 };
 
-template <bool kTrace>
+template <bool kTrace, int kPoly>
 __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constant__ BwdParams P) {
   using C = Bwd64Cfg;
   constexpr int HD = 64, ST = 2;
@@ -862,6 +1166,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       float pv[64];
       tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + g * 64, *reinterpret_cast<uint32_t(*)[64]>(&pv[0]));
       tmem_ld_wait();
+      if (q4 == 2 && g == 0) BTP_STAMP64(14);
       {
         uint32_t pk[32];
 #pragma unroll
@@ -869,13 +1174,23 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
           const float4 l4 = ld_shared_f4(lse_a + m * 4);
           const float2 x01 = ffma2(make_float2(pv[m], pv[m + 1]), c2, make_float2(-l4.x, -l4.y));
           const float2 x23 = ffma2(make_float2(pv[m + 2], pv[m + 3]), c2, make_float2(-l4.z, -l4.w));
-          pv[m] = ex2_approx(x01.x);
-          pv[m + 1] = ex2_approx(x01.y);
-          pv[m + 2] = ex2_approx(x23.x);
-          pv[m + 3] = ex2_approx(x23.y);
-          pk[m / 2] = pack_bf16(pv[m], pv[m + 1]);
-          pk[m / 2 + 1] = pack_bf16(pv[m + 2], pv[m + 3]);
+          float2 e01, e23;
+          e01.x = ex2_approx(x01.x);
+          e01.y = ex2_approx(x01.y);
+          if (kPoly > 0 && ((m / 4) % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
+            e23 = ex2_poly2(x23);  // a share of the exp2s on the FMA pipe (the MUFU bounds this phase)
+          } else {
+            e23.x = ex2_approx(x23.x);
+            e23.y = ex2_approx(x23.y);
+          }
+          pv[m] = e01.x;
+          pv[m + 1] = e01.y;
+          pv[m + 2] = e23.x;
+          pv[m + 3] = e23.y;
+          pk[m / 2] = pack_bf16(e01.x, e01.y);
+          pk[m / 2 + 1] = pack_bf16(e23.x, e23.y);
         }
+        if (q4 == 2 && g == 0) BTP_STAMP64(15);
         tmem_st_32x32b_x32(tmem + C::tS + lane_addr + g * 64, pk);
       }
       tmem_st_wait();
@@ -1075,18 +1390,21 @@ int f32_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
-template <int HD, int ST>
-int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
+static int g_fwd_poly = 0;     // every n-th exp2 pair on the FMA pipe (0: all on the MUFU)
+static int g_fwd_variant = 0;  // 2 / 1: split-row double-buffered kernel with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel
+
+template <int HD, int ST, int kPoly>
+int launch_fwd_poly(const FwdParams& P, int b, cudaStream_t stream) {
   using C = FwdCfg<HD, ST>;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attn_fwd_kernel<HD, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(attn_fwd_kernel<HD, ST, kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmem) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
   }
   dim3 grid(P.s / kTile, P.h, b);
-  attn_fwd_kernel<HD, ST><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  attn_fwd_kernel<HD, ST, kPoly><<<grid, C::kThreads, C::kSmem, stream>>>(P);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
@@ -1106,30 +1424,88 @@ int launch_bwd(const BwdParams& P, int b, cudaStream_t stream) {
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
-int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
+static int g_bwd_poly = 0;  // every n-th group of 4 exp2s in the backward's P phase: 2 on the FMA pipe (0: none)
+
+template <bool kTrace, int kPoly>
+int launch_bwd64_t(const BwdParams& P, int b, cudaStream_t stream) {
   using C = Bwd64Cfg;
   static_assert(C::kSmem <= 232448, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attn_bwd64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(attn_bwd64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
-            cudaSuccess)
+    if (cudaFuncSetAttribute(attn_bwd64_kernel<kTrace, kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmem) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
   }
   dim3 grid(P.s / kTile, P.h, b);
-  if (P.trace != nullptr)
-    attn_bwd64_kernel<true><<<grid, C::kThreads, C::kSmem, stream>>>(P);
-  else
-    attn_bwd64_kernel<false><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  attn_bwd64_kernel<kTrace, kPoly><<<grid, C::kThreads, C::kSmem, stream>>>(P);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+template <bool kTrace>
+int launch_bwd64_p(const BwdParams& P, int b, cudaStream_t stream) {
+  switch (g_bwd_poly) {
+    case 1: return launch_bwd64_t<kTrace, 1>(P, b, stream);
+    case 2: return launch_bwd64_t<kTrace, 2>(P, b, stream);
+    case 4: return launch_bwd64_t<kTrace, 4>(P, b, stream);
+    default: return launch_bwd64_t<kTrace, 0>(P, b, stream);
+  }
+}
+
+int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
+  return P.trace != nullptr ? launch_bwd64_p<true>(P, b, stream) : launch_bwd64_p<false>(P, b, stream);
+}
+
+template <int HD, int ST, int kPoly, int kSplit>
+int launch_fwd2_poly(const FwdParams& P, int b, cudaStream_t stream) {
+  using C = Fwd2Cfg<HD, ST, kSplit>;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd2_kernel<HD, ST, kPoly, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmem) != cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / kTile, P.h, b);
+  attn_fwd2_kernel<HD, ST, kPoly, kSplit><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+template <int HD, int ST, int kSplit>
+int launch_fwd2(const FwdParams& P, int b, cudaStream_t stream) {
+  switch (g_fwd_poly) {
+    case 0: return launch_fwd2_poly<HD, ST, 0, kSplit>(P, b, stream);
+    case 2: return launch_fwd2_poly<HD, ST, 2, kSplit>(P, b, stream);
+    case 3: return launch_fwd2_poly<HD, ST, 3, kSplit>(P, b, stream);
+    case 5: return launch_fwd2_poly<HD, ST, 5, kSplit>(P, b, stream);
+    default: return launch_fwd2_poly<HD, ST, 4, kSplit>(P, b, stream);
+  }
+}
+
+template <int HD, int ST>
+int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
+  switch (g_fwd_poly) {
+    case 0: return launch_fwd_poly<HD, ST, 0>(P, b, stream);
+    case 2: return launch_fwd_poly<HD, ST, 2>(P, b, stream);
+    case 3: return launch_fwd_poly<HD, ST, 3>(P, b, stream);
+    case 5: return launch_fwd_poly<HD, ST, 5>(P, b, stream);
+    default: return launch_fwd_poly<HD, ST, 4>(P, b, stream);
+  }
 }
 
 }  // namespace
 
+int attn_tune(int key, int value) {
+  int* slot = key == 0 ? &g_fwd_poly : key == 1 ? &g_fwd_variant : key == 2 ? &g_bwd_poly : nullptr;
+  if (slot == nullptr) return -1;
+  const int prev = *slot;
+  if (value >= 0) *slot = value;
+  return prev;
+}
+
 int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, void* o,
-             long long ldo, float* lse, int b, int s, int h, int hd, cudaStream_t stream) {
+             long long ldo, float* lse, int b, int s, int h, int hd, cudaStream_t stream, long long* trace) {
   if (b <= 0 || s <= 0 || h <= 0) return BTP_ERR_DIM;
   if (s % kTile != 0 || (hd != 64 && hd != 128)) return BTP_ERR_DIM;
   const long long width = (long long)h * hd;
@@ -1151,6 +1527,9 @@ int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const v
   P.h = h;
   P.n_kv = s / kTile;
   P.c = 1.4426950408889634f / sqrtf((float)hd);
+  P.trace = trace;
+  if (g_fwd_variant == 2 && hd == 64) return launch_fwd2<64, 3, 4>(P, b, stream);
+  if (g_fwd_variant >= 1) return hd == 64 ? launch_fwd2<64, 3, 2>(P, b, stream) : launch_fwd2<128, 2, 2>(P, b, stream);
   return hd == 64 ? launch_fwd<64, 2>(P, b, stream) : launch_fwd<128, 1>(P, b, stream);
 }
 

@@ -74,8 +74,9 @@ int peer_boundary_fwd_nvls(const void* P_mc, const float* ss_mc, int tp, int ran
 int peer_boundary_bwd_nvls(const void* dA_mc, int tp, int rank, int T, int W, int r, int variant, int d,
                            const void* z_own, const float* s_own, void* dP_mc, float* dss_mc, cudaStream_t st);
 // attention (attn.cu)
+int attn_tune(int key, int value);
 int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, void* o,
-             long long ldo, float* lse, int b, int s, int h, int hd, cudaStream_t stream);
+             long long ldo, float* lse, int b, int s, int h, int hd, cudaStream_t stream, long long* trace = nullptr);
 int attn_bwd(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv, const void* o,
              long long ldo, const void* dO, long long lddo, const float* lse, float* D, float* dq_acc,
              long long ldacc, void* dq, long long lddq, void* dk, long long lddk, void* dv, long long lddv, int b,

@@ -58,6 +58,13 @@ int btp_attn_bwd_trace(const void* q, long long ldq, const void* k, long long ld
                        b, s, h, hd, ST(stream), trace);
 }
 
+int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ldk, const void* v, long long ldv,
+                       void* o, long long ldo, float* lse, int b, int s, int h, int hd, long long* trace, void* stream) {
+  return btp::attn_fwd(q, ldq, k, ldk, v, ldv, o, ldo, lse, b, s, h, hd, ST(stream), trace);
+}
+
+int btp_attn_tune(int key, int value) { return btp::attn_tune(key, value); }
+
 int btp_gemm_f32(const btp_gemm_problem* problems, int n, void* stream) {
   return btp::gemm_f32_launch(problems, n, ST(stream));
 }

@@ -408,6 +408,7 @@ class BTPBlockExecutor(ExecutorBase):
         self.flp = -(-self.fl // 8) * 8
         self.attn = Attention(pl.shape.b, pl.shape.s, self.hl, cfg.head_dim,
                               "fp32" if precision == "fp32" else attn_backend)
+        self.attn.stats = self.stats
         # sigma in the down-GEMM epilogue (GEMM kernel epilogue 1): TP = 1 only (at TP > 1 the
         # all-reduce sits between GEMM and sigma), cola, bf16, crossgate halves in 64-column blocks
         self.fuse_sigma = (FUSE_SIGMA and precision == "bf16" and tp == 1 and self.var == 1 and self.r % 128 == 0

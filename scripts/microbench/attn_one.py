@@ -14,6 +14,10 @@ lse = torch.empty(b, h, s, device="cuda")
 D = torch.empty(b, h, s, device="cuda")
 acc = torch.empty(b * s, w, device="cuda")
 dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+import os
+from paper_2512_12131_b200 import _native  # noqa: E402
+if os.environ.get("FWD_VARIANT"):
+    _native.load().btp_attn_tune(1, int(os.environ["FWD_VARIANT"]))
 for _ in range(2):
     K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
     K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd)

@@ -27,7 +27,7 @@ t = tr.cpu()
 t0 = int(t[t > 0].min())
 names = {0: "g0 S ready", 1: "g0 P done", 2: "g0 dP ready", 3: "g0 dS done", 4: "g1 S ready", 5: "g1 P done",
          6: "g1 dP ready", 7: "g1 dS done", 8: "mma P seen", 9: "mma [3][1] issued", 10: "mma dS seen",
-         11: "mma dq free", 12: "mma [2] issued", 13: "red dQ ready"}
+         11: "mma dq free", 12: "mma [2] issued", 13: "red dQ ready", 14: "g0 S in regs", 15: "g0 P computed"}
 print("iter " + " ".join(f"{names[e][:12]:>12}" for e in sorted(names)))
 for i in range(t.shape[0]):
     print(f"{i:4d} " + " ".join(f"{(int(t[i, e]) - t0) if t[i, e] else 0:12d}" for e in sorted(names)))

@@ -26,7 +26,37 @@ def timeit(fn, n=20):
     return sorted(res)[1]
 
 
+def poly_sweep():
+    from paper_2512_12131_b200 import _native
+    lib = _native.load()
+    b, s, h, hd = 4, 4096, 32, 64
+    w = h * hd
+    q, k, v = (torch.randn(b * s, w, device="cuda").bfloat16() for _ in range(3))
+    o = torch.empty_like(q)
+    lse = torch.empty(b, h, s, device="cuda")
+    flops = 4 * b * h * s * s * hd
+    for var in (0, 1, 2):
+        lib.btp_attn_tune(1, var)
+        for n in (0, 2, 3, 4, 5):
+            lib.btp_attn_tune(0, n)
+            t_own = timeit(lambda: K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd))
+            print(f"  fwd variant {var} poly every {n}: {t_own*1e3:.1f} us ({flops/t_own/1e9:.0f} TF/s)", flush=True)
+    lib.btp_attn_tune(0, 0)
+    lib.btp_attn_tune(1, 0)
+    do = torch.randn(b * s, w, device="cuda").bfloat16()
+    D = torch.empty(b, h, s, device="cuda")
+    acc = torch.empty(b * s, w, device="cuda")
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    prev = lib.btp_attn_tune(2, -1)
+    for n in (0, 1, 2, 4):
+        lib.btp_attn_tune(2, n)
+        t_b = timeit(lambda: K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd))
+        print(f"  bwd poly {n}: {t_b*1e3:.1f} us ({2.5*flops/t_b/1e9:.0f} TF/s)", flush=True)
+    lib.btp_attn_tune(2, prev)
+
+
 def main():
+    poly_sweep()
     shapes = [(4, 4096, 32, 64), (4, 4096, 4, 128), (4, 4096, 16, 64), (1, 8192, 8, 128)]
     for b, s, h, hd in shapes:
         w = h * hd

@@ -105,3 +105,37 @@ def test_attn_bwd_matches_fp32(b, s, h, hd):
     rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
     errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
     assert max(errs.values()) < 2e-2, errs
+
+
+@pytest.mark.parametrize("grouping", [True, False])
+def test_block_step_native_attention_vs_oracle(grouping):
+    """The BTP CoLA-60M block (8 heads of 64) fwd+bwd with the native attention kernels inside the
+    executor, against the float64 oracle (reference model.py:205-230 attention inside
+    simulator.py:550-714), at the north_star bf16 bar."""
+    from paper_2512_12131_b200.api import train_step
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, plan
+    from tests.gpu_util import BF16_TOL, C60M, inputs, oracle_step, rel
+
+    b, s = 2, 256
+    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=grouping)
+    st = train_step(pl, blk, x, G, attn_backend="native")
+    torch.cuda.synchronize()
+    assert st.executor.attn.native
+    y_ref, g_ref, _, _ = oracle_step(oblk, x, G, C60M, b, s)
+    errs = {"y": rel(st.y.values, y_ref), "dx": rel(st.dx, g_ref["dx"])}
+    for n in g_ref["A"]:
+        errs[f"A_{n}"] = rel(st.grads["A"][n], g_ref["A"][n])
+        errs[f"B_{n}"] = rel(st.grads["B"][n], g_ref["B"][n])
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < BF16_TOL, errs
+
+
+def test_native_attention_rejects_unsupported_shapes():
+    from paper_2512_12131_b200.attention import Attention
+
+    with pytest.raises(ValueError):
+        Attention(1, 100, 2, 64, "native")
+    with pytest.raises(ValueError):
+        Attention(1, 128, 2, 32, "native")

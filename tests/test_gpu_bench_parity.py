@@ -21,13 +21,14 @@ from tests.gpu_util import BF16_TOL, inputs, rel
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("attn", ["auto", "native"])
 @pytest.mark.parametrize("b,s", [(4, 4096)])
-def test_bench_config_block_vs_oracle(b, s):
+def test_bench_config_block_vs_oracle(b, s, attn):
     cfg = preset("1b")
     T = b * s
     blk, x, G, oblk = inputs(cfg, Variant.COLA, b, s)
     pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
-    tr = BlockTrainer(pl, blk, optimizer=False)
+    tr = BlockTrainer(pl, blk, optimizer=False, attn_backend=attn)
     xd, gd = tr.device_inputs(x.values, G.values)
     tr.step_device(xd, gd)          # eager step (allocates), then capture
     tr.step_device(xd, gd)          # first replay
@@ -53,7 +54,7 @@ def test_bench_config_block_vs_oracle(b, s):
     errs["gamma1"] = rel(grads["gamma1"], g_ref["dgamma1"])
     errs["gamma2"] = rel(grads["gamma2"], g_ref["dgamma2"])
     worst = max(errs, key=errs.get)
-    print(f"bench-config parity (1b b{b} s{s}): worst {worst} = {errs[worst]:.3e}; "
+    print(f"bench-config parity (1b b{b} s{s}, attention {attn}): worst {worst} = {errs[worst]:.3e}; "
           + ", ".join(f"{k}={v:.2e}" for k, v in sorted(errs.items())))
     bad = {k: v for k, v in errs.items() if v > BF16_TOL}
     assert not bad, bad
