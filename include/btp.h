@@ -354,8 +354,9 @@ int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ld
 
 /* Attention tuning knobs (host-side state read at launch; graph captures keep their choice). key 0: every
  * n-th exp2 pair of the forward softmax on the FMA pipe (polynomial) instead of the MUFU (n in {0 = none,
- * 2, 3, 4, 5}, default 4); key 1: forward kernel (1 = split-row double-buffered, default; 0 = single S
- * buffer, two CTAs per SM); key 2: in the hd-64 backward's P phase, every n-th group of four exp2s has two
+ * 2, 3, 4, 5}, default 2); key 1: forward kernel (4 = two query tiles per CTA sharing K / V, default when
+ * s % 256 == 0; 3 = split rows, one S buffer, two CTAs per SM; 2 / 1 = split rows, double-buffered S, 4 / 2
+ * key groups; 0 = single S buffer, two CTAs per SM); key 2: in the hd-64 backward's P phase, every n-th group of four exp2s has two
  * on the FMA pipe (n in {0 = none, 1, 2, 4}). value < 0 only queries. Returns the previous value (-1: unknown key). */
 int btp_attn_tune(int key, int value);
 

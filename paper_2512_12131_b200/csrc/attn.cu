@@ -275,43 +275,53 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
 //     inside the loop, 8 softmax warps (two per scheduler); PV is two K = 64 MMA chains (O_g += P_g V_g);
 //   * combines once at the end: O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) / (l_0 2^(m_0-m) + l_1 2^(m_1-m)).
 // kSplit key groups per row (2, or 4 at hd 64: 2 S buffers + 4 O accumulators fill the 512 columns).
-template <int HD, int ST, int kSplit>
+// kSBuf = 1: one S buffer (S_{j+1} issued after PV_j, like attn_fwd_kernel) so that at hd 64 / kSplit 2
+// the CTA needs 256 TMEM columns and two CTAs share an SM (16 softmax warps per SM).
+// kQT = 2: two 128-row query tiles per CTA share every K / V tile (half the K / V traffic from L2 per
+// query row); each has its own S buffer, softmax warps and O accumulators, and the two softmax groups
+// ping-pong with the tensor core (S / PV of one tile run while the other's softmax does).
+template <int HD, int ST, int kSplit, int kSBuf = 2, int kQT = 1>
 struct Fwd2Cfg {
   static constexpr int kTileBytes = kTile * HD * 2;
   static constexpr int kChunks = HD / 64;
   static constexpr int kKG = kTile / kSplit;              // keys per group
-  static constexpr int kMlBytes = kSplit * 2 * kTile * 4;  // (m, l) per group and row
+  static constexpr int kNS = kQT * kSBuf;                 // S buffers
+  static constexpr int kMlBytes = kQT * kSplit * 2 * kTile * 4;  // (m, l) per tile, group and row
   static constexpr int kBarBytes = 256;
-  static constexpr int kSmem = 1024 + kTileBytes * (1 + 2 * ST) + kMlBytes + kBarBytes;
-  static constexpr int kSoftWarps = 4 * kSplit;
+  static constexpr int kSmem = 1024 + kTileBytes * (kQT + 2 * ST) + kMlBytes + kBarBytes;
+  static constexpr int kSoftWarps = 4 * kSplit * kQT;
   static constexpr int kThreads = 64 + 32 * kSoftWarps;
-  static constexpr uint32_t tO = 256;  // O_g at 256 + g * HD
-  static_assert(256 + kSplit * HD <= 512, "TMEM budget");
+  static constexpr uint32_t tO = 128 * kNS;  // O_(u,g) at tO + (u * kSplit + g) * HD
+  static constexpr uint32_t kCols = (tO + kQT * kSplit * HD <= 256) ? 256 : 512;
+  static constexpr int kCtasPerSm = kCols == 256 ? 2 : 1;
+  static_assert(tO + kQT * kSplit * HD <= 512, "TMEM budget");
+  static_assert(kQT == 1 || kSBuf == 1, "two query tiles use one S buffer each");
 };
 
-template <int HD, int ST, int kPoly, int kSplit>
-__global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
+template <int HD, int ST, int kPoly, int kSplit, int kSBuf, int kQT>
+__global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>::kThreads,
+                                  Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>::kCtasPerSm)
     attn_fwd2_kernel(const __grid_constant__ FwdParams P) {
-  using C = Fwd2Cfg<HD, ST, kSplit>;
+  using C = Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>;
   constexpr int kKG = C::kKG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + C::kTileBytes;
+  uint8_t* sK = sQ + kQT * C::kTileBytes;
   uint8_t* sV = sK + ST * C::kTileBytes;
   float* sML = reinterpret_cast<float*>(sV + ST * C::kTileBytes);  // [kSplit groups][m | l][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sML) + C::kMlBytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + ST;
-  uint64_t* s_full = kv_empty + ST;  // [2]
-  uint64_t* p_full = s_full + 2;     // [2]
-  uint64_t* o_bar = p_full + 2;      // one phase per PV pair
-  uint64_t* o_final = o_bar + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
+  uint64_t* s_full = kv_empty + ST;  // [kNS]
+  uint64_t* p_full = s_full + 2 * kQT;  // [kNS]
+  uint64_t* o_bar = p_full + 2 * kQT;   // [kQT], one phase per PV
+  uint64_t* o_final = o_bar + kQT;      // [kQT]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + kQT);
 
   const int qt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
-  const int row0 = bi * P.s + qt * kTile;
+  const int row0 = bi * P.s + qt * kTile * kQT;
   const int kv0 = bi * P.s;
   const int col0 = head * HD;
   const int n = P.n_kv;
@@ -335,16 +345,18 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
         mbar_init(&kv_full[s], 1);
         mbar_init(&kv_empty[s], 1);
       }
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < C::kNS; ++b) {
         mbar_init(&s_full[b], 1);
-        mbar_init(&p_full[b], C::kSoftWarps);
+        mbar_init(&p_full[b], 4 * kSplit);
       }
-      mbar_init(o_bar, 1);
-      mbar_init(o_final, 1);
+      for (int u = 0; u < kQT; ++u) {
+        mbar_init(&o_bar[u], 1);
+        mbar_init(&o_final[u], 1);
+      }
       fence_barrier_init();
     }
     __syncwarp();
-    tmem_alloc<512>(tmem_slot);
+    tmem_alloc<C::kCols>(tmem_slot);
   }
   tc_fence_before();
   __syncthreads();
@@ -354,9 +366,12 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, C::kTileBytes);
+      mbar_arrive_expect_tx(q_full, kQT * C::kTileBytes);
 #pragma unroll
-      for (int c = 0; c < C::kChunks; ++c) tma_load_2d(sQ + c * kTile * 128, &P.tq, q_full, col0 + 64 * c, row0);
+      for (int u = 0; u < kQT; ++u)
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_2d(sQ + u * C::kTileBytes + c * kTile * 128, &P.tq, q_full, col0 + 64 * c, row0 + u * kTile);
       for (int j = 0; j < n; ++j) {
         const int st = j % ST;
         mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
@@ -372,91 +387,100 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = make_idesc_bf16_f32(kTile, kTile, false, false);
     constexpr uint32_t idesc_o = make_idesc_bf16_f32(kTile, HD, false, true);
-    const uint32_t q_base = smem_u32(sQ);
-    auto issue_s = [&](int j) {  // S_j = Q K_j^T into buffer j & 1
+    auto issue_s = [&](int u, int j) {  // S_(u,j) = Q_u K_j^T into buffer u * kSBuf + j % kSBuf
       const int st = j % ST;
       mbar_wait(&kv_full[st], (j / ST) & 1);
       tc_fence_after();
       const uint32_t k_base = smem_u32(sK + st * C::kTileBytes);
+      const uint32_t q_base = smem_u32(sQ + u * C::kTileBytes);
+      const int b = u * kSBuf + j % kSBuf;
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * kTile * 128 + (k & 3) * 32;
-          umma_bf16(tmem + (j & 1) * 128, make_sw128_desc(q_base + off, 16, 1024),
+          umma_bf16(tmem + b * 128, make_sw128_desc(q_base + off, 16, 1024),
                     make_sw128_desc(k_base + off, 16, 1024), idesc_s, k > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[j & 1]);
+        umma_commit(&s_full[b]);
       }
       __syncwarp();
     };
     mbar_wait(q_full, 0);
     tc_fence_after();
-    issue_s(0);
-    if (n > 1) issue_s(1);
+    for (int u = 0; u < kQT; ++u) issue_s(u, 0);
+    if (kSBuf == 2 && n > 1) issue_s(0, 1);
     for (int j = 0; j < n; ++j) {
-      const int b = j & 1, st = j % ST;
-      mbar_wait(&p_full[b], (j >> 1) & 1);
-      FSTAMP(j, 8);
-      tc_fence_after();
+      const int st = j % ST;
       const uint32_t v_base = smem_u32(sV + st * C::kTileBytes);
-      if (elect_one()) {
-        // O_g += P_g V[kKG g, kKG (g + 1)): A = P_g (bf16 pairs at S columns kKG g ..), B = V rows (MN-major)
 #pragma unroll
-        for (int g = 0; g < kSplit; ++g) {
+      for (int u = 0; u < kQT; ++u) {
+        const int b = u * kSBuf + j % kSBuf;
+        mbar_wait(&p_full[b], (j / kSBuf) & 1);
+        if (u == 0) FSTAMP(j, 8);
+        tc_fence_after();
+        if (elect_one()) {
+          // O_(u,g) += P_g V[kKG g, kKG (g + 1)): A = P_g (bf16 pairs at S columns kKG g ..), B = V (MN-major)
 #pragma unroll
-          for (int k = 0; k < kKG / 16; ++k)
-            umma_bf16_ts(tmem + C::tO + g * HD, tmem + b * 128 + g * kKG + k * 8,
-                         make_sw128_desc(v_base + (g * kKG + 16 * k) * 128, kTile * 128, 1024), idesc_o,
-                         (j > 0 || k > 0) ? 1u : 0u);
+          for (int g = 0; g < kSplit; ++g) {
+#pragma unroll
+            for (int k = 0; k < kKG / 16; ++k)
+              umma_bf16_ts(tmem + C::tO + (u * kSplit + g) * HD, tmem + b * 128 + g * kKG + k * 8,
+                           make_sw128_desc(v_base + (g * kKG + 16 * k) * 128, kTile * 128, 1024), idesc_o,
+                           (j > 0 || k > 0) ? 1u : 0u);
+          }
+          if (u == kQT - 1) umma_commit(&kv_empty[st]);
+          umma_commit(&o_bar[u]);
+          if (j == n - 1) umma_commit(&o_final[u]);
         }
-        umma_commit(&kv_empty[st]);
-        umma_commit(o_bar);
-        if (j == n - 1) umma_commit(o_final);
+        __syncwarp();
+        if (u == 0) FSTAMP(j, 9);
+        if (j + kSBuf < n) issue_s(u, j + kSBuf);  // into buffer b, which P_(u,j) (just consumed) aliased
+        if (u == 0) FSTAMP(j, 10);
       }
-      __syncwarp();
-      FSTAMP(j, 9);
-      if (j + 2 < n) issue_s(j + 2);  // into buffer b, which P_j (just consumed) aliased
-      FSTAMP(j, 10);
     }
   } else {
     // ---------------------------------------------------------------- softmax warps 2 .. 2 + 4 kSplit
-    const uint32_t g = (warp - 2) >> 2;  // key group
+    const uint32_t sw = (warp - 2) >> 2;
+    const uint32_t g = sw % kSplit;  // key group
+    const uint32_t u = sw / kSplit;  // query tile
     const uint32_t q4 = warp & 3;
     const uint32_t row = q4 * 32 + lane;
     const uint32_t lane_addr = (q4 * 32) << 16;
-    const uint32_t tOg = tmem + C::tO + g * HD + lane_addr;
+    const uint32_t tOg = tmem + C::tO + (u * kSplit + g) * HD + lane_addr;
     const float c = P.c;
     float m_used = 0.f, l = 0.f;
     for (int j = 0; j < n; ++j) {
-      const int b = j & 1;
+      const int b = u * kSBuf + j % kSBuf;
       const uint32_t tSg = tmem + b * 128 + g * kKG + lane_addr;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      if (q4 == 2) FSTAMP(j, 4 * g);
+      mbar_wait(&s_full[b], (j / kSBuf) & 1);
+      if (q4 == 2 && u == 0) FSTAMP(j, 4 * g);
       tc_fence_after();
-      uint32_t s[kKG];
-      if constexpr (kKG == 64) tmem_ld_32x32b_x64(tSg, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
-      else tmem_ld_32x32b_x32(tSg, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      tmem_ld_wait();
-      float mx[4] = {__uint_as_float(s[0]), __uint_as_float(s[1]), __uint_as_float(s[2]), __uint_as_float(s[3])};
+      // two passes over the group's kKG columns in 32-column chunks (registers: one chunk at a time;
+      // TMEM reads are cheap): max, then exp2 / sum / bf16 pairs written back over the consumed columns
+      float mx[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f};
 #pragma unroll
-      for (int i = 4; i < kKG; i += 8) {
-        mx[0] = fmax3(mx[0], __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
-        mx[1] = fmax3(mx[1], __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-        if (i + 4 < kKG) {
+      for (int ch = 0; ch < kKG / 32; ++ch) {
+        uint32_t s[32];
+        tmem_ld_32x32b_x32(tSg + ch * 32, s);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          mx[0] = fmax3(mx[0], __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+          mx[1] = fmax3(mx[1], __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
           mx[2] = fmax3(mx[2], __uint_as_float(s[i + 4]), __uint_as_float(s[i + 5]));
           mx[3] = fmax3(mx[3], __uint_as_float(s[i + 6]), __uint_as_float(s[i + 7]));
         }
       }
       const float m_new = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;
-      if (q4 == 2) FSTAMP(j, 4 * g + 1);
+      if (q4 == 2 && u == 0) FSTAMP(j, 4 * g + 1);
       if (j == 0) {
         m_used = m_new;
       } else {
         const bool need = m_new > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
-          // O_g must hold PV_{j-1} before it is rescaled (S_j was issued after PV_{j-2}: the barrier is at
-          // phase j-1 or j, so the parity wait is unambiguous)
-          mbar_wait(o_bar, (j - 1) & 1);
+          // O_g must hold PV_{j-1} before it is rescaled (S_j was issued after PV_{j-kSBuf}: the barrier
+          // is at phase j-1 or j, so the parity wait is unambiguous)
+          mbar_wait(&o_bar[u], (j - 1) & 1);
           tc_fence_after();
           const float alpha = need ? ex2_approx(m_used - m_new) : 1.f;
 #pragma unroll
@@ -478,38 +502,44 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
       float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
       const float2 c2 = make_float2(c, c), nm = make_float2(-m_used, -m_used);
 #pragma unroll
-      for (int i = 0; i < kKG / 2; ++i) {
-        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nm);
-        float2 e;
-        if (kPoly > 0 && (i % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
-          e = ex2_poly2(x);
-        } else {
-          e.x = ex2_approx(x.x);
-          e.y = ex2_approx(x.y);
+      for (int ch = 0; ch < kKG / 32; ++ch) {
+        uint32_t s[32];
+        tmem_ld_32x32b_x32(tSg + ch * 32, s);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nm);
+          float2 e;
+          if (kPoly > 0 && ((ch * 16 + i) % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
+            e = ex2_poly2(x);
+          } else {
+            e.x = ex2_approx(x.x);
+            e.y = ex2_approx(x.y);
+          }
+          if (i & 1) l2b = fadd2(l2b, e);
+          else l2a = fadd2(l2a, e);
+          s[i] = pack_bf16(e.x, e.y);
         }
-        if (i & 1) l2b = fadd2(l2b, e);
-        else l2a = fadd2(l2a, e);
-        s[i] = pack_bf16(e.x, e.y);
+        tmem_st_32x32b_x16(tSg + ch * 16, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
       }
       l += (l2a.x + l2a.y) + (l2b.x + l2b.y);
-      if constexpr (kKG == 64) tmem_st_32x32b_x32(tSg, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      else tmem_st_32x32b_x16(tSg, *reinterpret_cast<uint32_t(*)[16]>(&s[0]));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
-      if (q4 == 2) FSTAMP(j, 4 * g + 2);
+      if (q4 == 2 && u == 0) FSTAMP(j, 4 * g + 2);
     }
     // ---------------------------------------------------------------- epilogue: combine the groups
-    sML[(g * 2 + 0) * kTile + row] = m_used;
-    sML[(g * 2 + 1) * kTile + row] = l;
-    named_bar_sync(1, 32 * C::kSoftWarps);
+    float* ml = sML + u * (kSplit * 2 * kTile);
+    ml[(g * 2 + 0) * kTile + row] = m_used;
+    ml[(g * 2 + 1) * kTile + row] = l;
+    named_bar_sync(1 + u, 32 * 4 * kSplit);
     float mg[kSplit], lg[kSplit];
     float m = -3.0e38f;
 #pragma unroll
     for (int x = 0; x < kSplit; ++x) {
-      mg[x] = sML[(x * 2) * kTile + row];
-      lg[x] = sML[(x * 2 + 1) * kTile + row];
+      mg[x] = ml[(x * 2) * kTile + row];
+      lg[x] = ml[(x * 2 + 1) * kTile + row];
       m = fmaxf(m, mg[x]);
     }
     float L = 0.f;
@@ -519,9 +549,9 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
       L = fmaf(lg[x], mg[x], L);
     }
     const float inv = 1.f / L;
-    mbar_wait(o_final, 0);
+    mbar_wait(&o_final[u], 0);
     tc_fence_after();
-    __nv_bfloat16* orow = P.o + (long long)(row0 + row) * P.ldo + col0;
+    __nv_bfloat16* orow = P.o + (long long)(row0 + u * kTile + row) * P.ldo + col0;
     constexpr int kOC = HD / kSplit;  // output columns of this warp: [g kOC, (g + 1) kOC)
 #pragma unroll
     for (int cc = 0; cc < kOC / 16; ++cc) {
@@ -532,7 +562,7 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
 #pragma unroll
       for (int x = 0; x < kSplit; ++x) {
         uint32_t ox[16];
-        tmem_ld_32x32b_x16(tmem + C::tO + x * HD + oc + lane_addr, ox);
+        tmem_ld_32x32b_x16(tmem + C::tO + (u * kSplit + x) * HD + oc + lane_addr, ox);
         tmem_ld_wait();
         const float w = mg[x] * inv;
 #pragma unroll
@@ -544,13 +574,13 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit>::kThreads, 1)
       st_global_v4(orow + oc, make_uint4(pk[0], pk[1], pk[2], pk[3]));
       st_global_v4(orow + oc + 8, make_uint4(pk[4], pk[5], pk[6], pk[7]));
     }
-    if (g == 0) P.lse[((long long)bi * P.h + head) * P.s + qt * kTile + row] = m + __log2f(L);
+    if (g == 0) P.lse[((long long)bi * P.h + head) * P.s + (qt * kQT + u) * kTile + row] = m + __log2f(L);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<C::kCols>(tmem);
   }
 #undef FSTAMP
 }
@@ -1390,8 +1420,9 @@ int f32_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long
   return r == CUDA_SUCCESS ? BTP_OK : BTP_ERR_ALIGNMENT;
 }
 
-static int g_fwd_poly = 0;     // every n-th exp2 pair on the FMA pipe (0: all on the MUFU)
-static int g_fwd_variant = 0;  // 2 / 1: split-row double-buffered kernel with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel
+static int g_fwd_poly = 2;     // every n-th exp2 pair on the FMA pipe (0: all on the MUFU)
+static int g_fwd_variant = 4;  // 4: two query tiles per CTA (s % 256), 3: split rows single S, 2 / 1: split rows
+                               // double-buffered with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel
 
 template <int HD, int ST, int kPoly>
 int launch_fwd_poly(const FwdParams& P, int b, cudaStream_t stream) {
@@ -1456,30 +1487,30 @@ int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
   return P.trace != nullptr ? launch_bwd64_p<true>(P, b, stream) : launch_bwd64_p<false>(P, b, stream);
 }
 
-template <int HD, int ST, int kPoly, int kSplit>
+template <int HD, int ST, int kPoly, int kSplit, int kSBuf = 2, int kQT = 1>
 int launch_fwd2_poly(const FwdParams& P, int b, cudaStream_t stream) {
-  using C = Fwd2Cfg<HD, ST, kSplit>;
-  static_assert(C::kSmem <= 232448, "shared memory budget");
+  using C = Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>;
+  static_assert(C::kSmem <= 232448 / C::kCtasPerSm, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attn_fwd2_kernel<HD, ST, kPoly, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kSmem) != cudaSuccess)
+    if (cudaFuncSetAttribute(attn_fwd2_kernel<HD, ST, kPoly, kSplit, kSBuf, kQT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
   }
-  dim3 grid(P.s / kTile, P.h, b);
-  attn_fwd2_kernel<HD, ST, kPoly, kSplit><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  dim3 grid(P.s / (kTile * kQT), P.h, b);
+  attn_fwd2_kernel<HD, ST, kPoly, kSplit, kSBuf, kQT><<<grid, C::kThreads, C::kSmem, stream>>>(P);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
-template <int HD, int ST, int kSplit>
+template <int HD, int ST, int kSplit, int kSBuf = 2, int kQT = 1>
 int launch_fwd2(const FwdParams& P, int b, cudaStream_t stream) {
   switch (g_fwd_poly) {
-    case 0: return launch_fwd2_poly<HD, ST, 0, kSplit>(P, b, stream);
-    case 2: return launch_fwd2_poly<HD, ST, 2, kSplit>(P, b, stream);
-    case 3: return launch_fwd2_poly<HD, ST, 3, kSplit>(P, b, stream);
-    case 5: return launch_fwd2_poly<HD, ST, 5, kSplit>(P, b, stream);
-    default: return launch_fwd2_poly<HD, ST, 4, kSplit>(P, b, stream);
+    case 0: return launch_fwd2_poly<HD, ST, 0, kSplit, kSBuf, kQT>(P, b, stream);
+    case 2: return launch_fwd2_poly<HD, ST, 2, kSplit, kSBuf, kQT>(P, b, stream);
+    case 3: return launch_fwd2_poly<HD, ST, 3, kSplit, kSBuf, kQT>(P, b, stream);
+    case 5: return launch_fwd2_poly<HD, ST, 5, kSplit, kSBuf, kQT>(P, b, stream);
+    default: return launch_fwd2_poly<HD, ST, 4, kSplit, kSBuf, kQT>(P, b, stream);
   }
 }
 
@@ -1528,6 +1559,9 @@ int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const v
   P.n_kv = s / kTile;
   P.c = 1.4426950408889634f / sqrtf((float)hd);
   P.trace = trace;
+  if (g_fwd_variant == 4 && s % 256 == 0)
+    return hd == 64 ? launch_fwd2<64, 3, 2, 1, 2>(P, b, stream) : launch_fwd2<128, 2, 1, 1, 2>(P, b, stream);
+  if (g_fwd_variant == 3 && hd == 64) return launch_fwd2<64, 2, 2, 1>(P, b, stream);
   if (g_fwd_variant == 2 && hd == 64) return launch_fwd2<64, 3, 4>(P, b, stream);
   if (g_fwd_variant >= 1) return hd == 64 ? launch_fwd2<64, 3, 2>(P, b, stream) : launch_fwd2<128, 2, 2>(P, b, stream);
   return hd == 64 ? launch_fwd<64, 2>(P, b, stream) : launch_fwd<128, 1>(P, b, stream);

@@ -35,7 +35,7 @@ def poly_sweep():
     o = torch.empty_like(q)
     lse = torch.empty(b, h, s, device="cuda")
     flops = 4 * b * h * s * s * hd
-    for var in (0, 1, 2):
+    for var in (0, 1, 3, 4):
         lib.btp_attn_tune(1, var)
         for n in (0, 2, 3, 4, 5):
             lib.btp_attn_tune(0, n)

@@ -139,3 +139,29 @@ def test_native_attention_rejects_unsupported_shapes():
         Attention(1, 100, 2, 64, "native")
     with pytest.raises(ValueError):
         Attention(1, 128, 2, 32, "native")
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("poly", [0, 3])
+@pytest.mark.parametrize("hd", [64, 128])
+def test_attn_fwd_kernel_variants(variant, poly, hd):
+    """Every forward kernel variant behind btp_attn_tune (single S buffer / split rows double-buffered /
+    4 key groups / split rows single-buffered / two query tiles per CTA) and the polynomial exp2
+    share, against torch fp32."""
+    from paper_2512_12131_b200 import _native
+
+    lib = _native.load()
+    b, s, h = 2, 512, 2
+    q, k, v = _inputs(b, s, h, hd, scale=2.0, seed=variant * 10 + poly)
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    prev_v, prev_p = lib.btp_attn_tune(1, variant), lib.btp_attn_tune(0, poly)
+    try:
+        K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+        torch.cuda.synchronize()
+    finally:
+        lib.btp_attn_tune(1, prev_v)
+        lib.btp_attn_tune(0, prev_p)
+    o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
+    assert _rel(o, o_ref) < 1e-2
+    assert torch.allclose(lse * math.log(2.0), lse_ref, atol=2e-3, rtol=1e-5)
