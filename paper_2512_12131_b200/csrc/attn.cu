@@ -636,6 +636,9 @@ struct BwdParams {
   float c;         // log2(e) / sqrt(hd)
   float dk_scale;  // 1 / sqrt(hd)
   long long* trace;  // optional: per-iteration clock64 stamps of CTA (0, 0, 0) (pipeline diagnostics)
+  int dry;           // diagnostics (split-role kernel): 1 = P / dS / reduce warps only do the handshakes
+  int diag;          // diagnostics (split-role kernel, wrong results): bit0 no dS st.shared, bit1 no proxy
+                     // fence after them, bit2 no lse / D shared loads
 };
 
 #define BTP_STAMP64(e)                                                                            \
@@ -1334,6 +1337,427 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------- backward, hd 64, split roles
+// The kernel above runs the P phase (MUFU-bound: exp2) and the dS phase (FMA / ALU: P (dP - D), pack,
+// store) on the SAME 8 warps, one after the other, so each pipe idles half the time and the loop is
+// ~3100 cycles per query tile against a ~2160-cycle tensor floor (profiles/attention). Here the roles
+// are split so P of tile i+1 overlaps dS of tile i:
+//   w2..w9   P warps (two per scheduler, 64 query columns each): S^T -> P^T = exp2(S^T c - lse) ->
+//            bf16 pairs into their own TMEM block (tP), read by the dV MMA and by the dS warps
+//   w10..w17 dS warps, two groups of four alternating query tiles (group = tile parity; one warp per
+//            scheduler per group, a key row's 128 queries each, in 32-column chunks): dP^T and P^T from
+//            TMEM -> dS^T = P^T (dP^T - D) -> bf16, swizzled into shared memory (the A operand of the dK
+//            MMA, K-major, and of the dQ MMA, MN-major). The stores must be made visible to the tensor
+//            core (fence.proxy.async per writing thread), which under the MMAs' shared-memory traffic
+//            costs ~1000 cycles per tile (measured: 1.85 ms with vs 1.28 ms without); alternating groups
+//            give each group two tile periods, so one group's fence drains while the other computes.
+//            Barriers between the dS groups and the other roles are per tile parity.
+//   w18..w21 dQ reduce warps (TMEM -> swizzled fp32 smem tile -> TMA reduce-add)
+// TMEM: S^T 0..127, P^T 128..191, dP^T 192..319, dV 320..383, dK 384..447, dQ 448..511.
+// Tensor order per tile: [1]_{i+1} S^T  [3]_i dV  [2]_{i+1} dP^T  [4]_i dK  [5]_i dQ.
+struct Bwd64sCfg {
+  static constexpr int HD = 64;
+  static constexpr int kTileBytes = kTile * HD * 2;                   // 16 KB
+  static constexpr int kStageBytes = 2 * kTileBytes + 2 * kTile * 4;  // Q, dO, lse, D
+  static constexpr int kDsBytes = kTile * kTile * 2;                  // 32 KB per buffer
+  static constexpr int ST = 3;                                        // Q / dO / lse / D ring
+  static constexpr int kDqBytes = kTile * 32 * 4;                     // one 32-column fp32 box of dQ
+  static constexpr int kBarBytes = 256;
+  static constexpr int kSmem = 1024 + 2 * kTileBytes + ST * kStageBytes + 2 * kDsBytes + kDqBytes + kBarBytes;
+  static constexpr int kThreads = 704;
+  static constexpr uint32_t tS = 0, tP = 128, tdP = 192, tdV = 320, tdK = 384, tdQ = 448;
+};
+
+__global__ void __launch_bounds__(704, 1) attn_bwd64s_kernel(const __grid_constant__ BwdParams P) {
+  using C = Bwd64sCfg;
+  constexpr int HD = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::kTileBytes;
+  uint8_t* sStage = sV + C::kTileBytes;
+  uint8_t* sdS = sStage + C::ST * C::kStageBytes;  // 2 buffers
+  float* sdQ = reinterpret_cast<float*>(sdS + 2 * C::kDsBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sdQ) + C::kDqBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;           // [ST]
+  uint64_t* qdo_empty = qdo_full + C::ST;  // [ST]
+  uint64_t* sds_empty = qdo_empty + C::ST; // [2]
+  uint64_t* s_full = sds_empty + 2;
+  uint64_t* s_read = s_full + 1;
+  uint64_t* p_full = s_read + 1;    // [2] by tile parity
+  uint64_t* p_empty = p_full + 2;   // [2]
+  uint64_t* dp_full = p_empty + 2;  // [2]
+  uint64_t* dp_read = dp_full + 2;  // [2]
+  uint64_t* ds_full = dp_read + 2;  // [2]
+  uint64_t* dq_full = ds_full + 2;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* acc_full = dq_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int kt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int kv_row0 = bi * P.s + kt * kTile;
+  const int q_row_base = bi * P.s;
+  const int col0 = head * HD;
+  const long long stat0 = ((long long)bi * P.h + head) * P.s;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  long long* const tr = (kt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
+#define SSTAMP(e)                                                   \
+  do {                                                              \
+    if (tr != nullptr && lane == 0) tr[i * 16 + (e)] = clock64();   \
+  } while (0)
+  auto sQ = [&](int st) { return sStage + st * C::kStageBytes; };
+  auto sdO = [&](int st) { return sStage + st * C::kStageBytes + C::kTileBytes; };
+  auto sLse = [&](int st) { return reinterpret_cast<float*>(sStage + st * C::kStageBytes + 2 * C::kTileBytes); };
+  auto sD = [&](int st) { return sLse(st) + kTile; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+    tma_prefetch_desc(&P.tdo);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(kv_full, 1);
+      for (int s = 0; s < C::ST; ++s) {
+        mbar_init(&qdo_full[s], 1);
+        mbar_init(&qdo_empty[s], 1);
+      }
+      for (int s = 0; s < 2; ++s) mbar_init(&sds_empty[s], 1);
+      mbar_init(s_full, 1);
+      mbar_init(s_read, 8);
+      for (int q = 0; q < 2; ++q) {
+        mbar_init(&p_full[q], 8);
+        mbar_init(&p_empty[q], 1 + 4);  // the dV MMA (commit) + the tile's four dS warps (P^T in registers)
+        mbar_init(&dp_full[q], 1);
+        mbar_init(&dp_read[q], 4);
+        mbar_init(&ds_full[q], 4);
+      }
+      mbar_init(dq_full, 1);
+      mbar_init(dq_empty, 4);
+      mbar_init(acc_full, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
+      tma_load_2d(sK, &P.tk, kv_full, col0, kv_row0);
+      tma_load_2d(sV, &P.tv, kv_full, col0, kv_row0);
+      for (int i = 0; i < (P.dry == 2 ? 2 : P.n_q); ++i) {
+        const int st = i % C::ST;
+        mbar_wait(&qdo_empty[st], ((i / C::ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
+        tma_load_2d(sQ(st), &P.tq, &qdo_full[st], col0, q_row_base + i * kTile);
+        tma_load_2d(sdO(st), &P.tdo, &qdo_full[st], col0, q_row_base + i * kTile);
+        bulk_load_1d(sLse(st), P.lse + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+        bulk_load_1d(sD(st), P.D + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_ss = make_idesc_bf16_f32(kTile, kTile, false, false);  // [1], [2]
+    constexpr uint32_t idesc_ts = make_idesc_bf16_f32(kTile, HD, false, true);      // [3], [4]
+    constexpr uint32_t idesc_dq = make_idesc_bf16_f32(kTile, HD, true, true);       // [5]
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+    auto mma_ss = [&](uint32_t d, uint32_t a_base, uint32_t b_base) {  // K-major x K-major over hd = 64
+#pragma unroll
+      for (int k = 0; k < HD / 16; ++k)
+        umma_bf16(d, make_sw128_desc(a_base + k * 32, 16, 1024), make_sw128_desc(b_base + k * 32, 16, 1024), idesc_ss,
+                  k > 0 ? 1u : 0u);
+    };
+    mbar_wait(kv_full, 0);
+    mbar_wait(&qdo_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) {
+      mma_ss(tmem + C::tS, k_base, smem_u32(sQ(0)));
+      umma_commit(s_full);
+      mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(0)));
+      umma_commit(&dp_full[0]);
+    }
+    __syncwarp();
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i % C::ST;
+      const uint32_t ph = i & 1;
+      const bool more = i + 1 < P.n_q;
+      const int st1 = (i + 1) % C::ST;
+      if (more) {
+        mbar_wait(s_read, ph);  // the P warps hold S^T_i: the block may take S^T_{i+1}
+        if (P.dry != 2 || i + 1 < 2) mbar_wait(&qdo_full[st1], ((i + 1) / C::ST) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss(tmem + C::tS, k_base, smem_u32(sQ(st1)));  // [1]_{i+1}
+          umma_commit(s_full);
+        }
+        __syncwarp();
+      }
+      const int par = i & 1;
+      const uint32_t ph2 = (i >> 1) & 1;
+      SSTAMP(7);
+      mbar_wait(&p_full[par], ph2);
+      SSTAMP(8);
+      tc_fence_after();
+      if (elect_one()) {  // [3] dV += P^T dO: A = P^T pairs, queries [64g, +64) at tP + [32g, +32)
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + C::tdV, tmem + C::tP + (k >> 2) * 32 + (k & 3) * 8,
+                       make_sw128_desc(smem_u32(sdO(st)) + k * 2048, kTile * 128, 1024), idesc_ts,
+                       (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&p_empty[par]);
+      }
+      __syncwarp();
+      if (more) {
+        mbar_wait(&dp_read[par], ph2);  // the dS warps hold dP^T_i
+        SSTAMP(9);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(st1)));  // [2]_{i+1}
+          umma_commit(&dp_full[par ^ 1]);
+        }
+        __syncwarp();
+      }
+      mbar_wait(&ds_full[par], ph2);
+      SSTAMP(10);
+      tc_fence_after();
+      const uint32_t ds_base = smem_u32(sdS + (i & 1) * C::kDsBytes);
+      if (elect_one()) {
+        // [4] dK += dS^T Q: A = dS^T K-major in shared memory (chunk g = queries [64g, +64), 128 B rows)
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16(tmem + C::tdK, make_sw128_desc(ds_base + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024),
+                    make_sw128_desc(smem_u32(sQ(st)) + k * 2048, kTile * 128, 1024), idesc_ts,
+                    (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&qdo_empty[st]);
+      }
+      __syncwarp();
+      if (i >= 1) {
+        mbar_wait(dq_empty, (i - 1) & 1);  // the reduce warps have drained dQ_{i-1}
+        tc_fence_after();
+      }
+      SSTAMP(11);
+      if (elect_one()) {
+        // [5] dQ_i = dS K: A = dS MN-major (the same tile), B = K MN-major
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16(tmem + C::tdQ, make_sw128_desc(ds_base + k * 2048, kTile * 128, 1024),
+                    make_sw128_desc(k_base + k * 2048, kTile * 128, 1024), idesc_dq, k > 0 ? 1u : 0u);
+        umma_commit(dq_full);
+        umma_commit(&sds_empty[i & 1]);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) umma_commit(acc_full);
+    __syncwarp();
+  } else if (warp < 10) {
+    // ---------------------------------------------------------------- P warps 2..9
+    const uint32_t g = (warp - 2) >> 2;
+    const uint32_t q4 = warp & 3;
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const float2 c2 = make_float2(P.c, P.c);
+    for (int i = 0; i < P.n_q; ++i) {
+      const int st = i % C::ST;
+      const uint32_t lse_a = smem_u32(sLse(st)) + g * 256;
+      if (P.dry != 2 || i < 2) mbar_wait(&qdo_full[st], (i / C::ST) & 1);  // lse of this query tile is resident
+      mbar_wait(s_full, i & 1);
+      if (q4 == 2) SSTAMP(g);
+      tc_fence_after();
+      if (P.dry) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_read);
+        if (i >= 1) mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i & 1]);
+        continue;
+      }
+      // two 32-column halves (register budget: 22 warps share the register file)
+      uint32_t pk[2][16];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sv[32];
+        tmem_ld_32x32b_x32(tmem + C::tS + lane_addr + g * 64 + hh * 32, sv);
+        tmem_ld_wait();
+        if (hh == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_read);
+        }
+#pragma unroll
+        for (int m = 0; m < 32; m += 4) {
+          const float4 l4 = (P.diag & 4) ? make_float4(__int_as_float(lse_a), 1.f, 2.f, 3.f)
+                                         : ld_shared_f4(lse_a + (hh * 32 + m) * 4);
+          const float2 x01 = ffma2(make_float2(__uint_as_float(sv[m]), __uint_as_float(sv[m + 1])), c2,
+                                   make_float2(-l4.x, -l4.y));
+          const float2 x23 = ffma2(make_float2(__uint_as_float(sv[m + 2]), __uint_as_float(sv[m + 3])), c2,
+                                   make_float2(-l4.z, -l4.w));
+          pk[hh][m / 2] = pack_bf16(ex2_approx(x01.x), ex2_approx(x01.y));
+          pk[hh][m / 2 + 1] = pack_bf16(ex2_approx(x23.x), ex2_approx(x23.y));
+        }
+      }
+      if (i >= 1) {
+        mbar_wait(&p_empty[(i - 1) & 1], ((i - 1) >> 1) & 1);  // the dV MMA and the dS warps are done with P^T_{i-1}
+        tc_fence_after();
+      }
+      tmem_st_32x32b_x16(tmem + C::tP + lane_addr + g * 32, pk[0]);
+      tmem_st_32x32b_x16(tmem + C::tP + lane_addr + g * 32 + 16, pk[1]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i & 1]);
+      if (q4 == 2) SSTAMP(2 + g);
+    }
+    // ---------------------------------------------------------------- dK / dV epilogue (group 0: dV, 1: dK)
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const uint32_t row = q4 * 32 + lane;
+    const uint32_t tcol = g == 0 ? C::tdV : C::tdK;
+    const float sc = g == 0 ? 1.f : P.dk_scale;
+    __nv_bfloat16* out = g == 0 ? P.dv + (long long)(kv_row0 + row) * P.lddv + col0
+                                : P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
+#pragma unroll
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
+      tmem_ld_wait();
+      uint32_t ok[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) ok[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        st_global_v4(out + cc * 32 + v * 8, make_uint4(ok[4 * v], ok[4 * v + 1], ok[4 * v + 2], ok[4 * v + 3]));
+    }
+  } else if (warp < 18) {
+    // ---------------------------------------------------------------- dS warps 10..17 (group = tile parity)
+    const int grp = (int)(warp - 10) >> 2;
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // key row within the tile == TMEM lane
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    for (int i = grp; i < P.n_q; i += 2) {
+      const int st = i % C::ST;
+      const int par = i & 1;  // == grp
+      const uint32_t ph2 = (i >> 1) & 1;
+      const uint32_t d_a = smem_u32(sD(st));
+      if (P.dry != 2 || i < 2) mbar_wait(&qdo_full[st], (i / C::ST) & 1);  // D of this query tile is resident
+      mbar_wait(&dp_full[par], ph2);
+      mbar_wait(&p_full[par], ph2);
+      tc_fence_after();
+      if (i >= 2) mbar_wait(&sds_empty[par], ((i >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
+      if (q4 == 2 && grp == 0) SSTAMP(4);
+      if (P.dry) {
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&dp_read[par]);
+          mbar_arrive(&p_empty[par]);
+          mbar_arrive(&ds_full[par]);
+        }
+        continue;
+      }
+      const uint32_t ds_row0 = smem_u32(sdS + par * C::kDsBytes) + row * 128;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {  // 32 queries per chunk
+        uint32_t dp[32], pp[16];
+        tmem_ld_32x32b_x32(tmem + C::tdP + lane_addr + cc * 32, dp);
+        tmem_ld_32x32b_x16(tmem + C::tP + lane_addr + cc * 16, pp);
+        tmem_ld_wait();
+        if (cc == 3) {  // dP^T_i and P^T_i are in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&dp_read[par]);
+            mbar_arrive(&p_empty[par]);
+          }
+        }
+        const uint32_t base = ds_row0 + (cc >> 1) * (kTile * 128);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // 8 queries per 16-byte unit
+          uint32_t ds[4];
+#pragma unroll
+          for (int j = 0; j < 8; j += 4) {
+            const int mm = u * 8 + j;  // column within the chunk
+            const float4 d4 = (P.diag & 4) ? make_float4(__int_as_float(d_a), 1.f, 2.f, 3.f)
+                                           : ld_shared_f4(d_a + (cc * 32 + mm) * 4);
+            const uint32_t p01 = pp[mm / 2], p23 = pp[mm / 2 + 1];
+            const float2 a01 = fmul2(make_float2(bf16_lo(p01), bf16_hi(p01)),
+                                     fadd2(make_float2(__uint_as_float(dp[mm]), __uint_as_float(dp[mm + 1])),
+                                           make_float2(-d4.x, -d4.y)));
+            const float2 a23 = fmul2(make_float2(bf16_lo(p23), bf16_hi(p23)),
+                                     fadd2(make_float2(__uint_as_float(dp[mm + 2]), __uint_as_float(dp[mm + 3])),
+                                           make_float2(-d4.z, -d4.w)));
+            ds[j / 2] = pack_bf16(a01.x, a01.y);
+            ds[j / 2 + 1] = pack_bf16(a23.x, a23.y);
+          }
+          const uint32_t unit = (cc & 1) * 4 + u;
+          if (P.diag & 1) {
+            if ((ds[0] ^ ds[1] ^ ds[2] ^ ds[3]) == 0x12345678u) st_shared_v4(base, 0, 0, 0, 0);
+          } else {
+            st_shared_v4(base + ((unit ^ (row & 7)) << 4), ds[0], ds[1], ds[2], ds[3]);
+          }
+        }
+      }
+      if (!(P.diag & 2)) fence_proxy_async_smem();  // the stores, for the dK / dQ MMAs (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[par]);
+      if (q4 == 2 && grp == 0) SSTAMP(5);
+    }
+  } else {
+    // ---------------------------------------------------------------- dQ reduce warps 18..21
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;  // query row within the tile
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const bool issuer = (warp == 18 && lane == 0);
+    for (int i = 0; i < P.n_q; ++i) {
+      mbar_wait(dq_full, i & 1);
+      if (q4 == 2) SSTAMP(13);
+      tc_fence_after();
+      if (P.dry) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_empty);
+        continue;
+      }
+#pragma unroll
+      for (int bx = 0; bx < 2; ++bx) {  // one 32-column box at a time through the 16 KB staging tile
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + C::tdQ + lane_addr + bx * 32, o);
+        tmem_ld_wait();
+        if (bx == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_empty);
+        }
+        if (issuer) bulk_wait_read<0>();  // the previous box's reduce has read the staging tile
+        named_bar_sync(1, 128);
+        const uint32_t base = smem_u32(sdQ) + row * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          st_shared_v4(base + ((u ^ (row & 7)) << 4), o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (issuer) {
+          tma_reduce_add_2d(&P.tdq, sdQ, col0 + 32 * bx, q_row_base + i * kTile);
+          bulk_commit();
+        }
+      }
+    }
+    if (issuer) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+#undef SSTAMP
+}
+
 // D[b, h, s] = sum_hd dO o O (fp32) per (row, head); zero the fp32 dQ accumulator. One warp per row.
 template <int HD>
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, long long ldo,
@@ -1483,7 +1907,30 @@ int launch_bwd64_p(const BwdParams& P, int b, cudaStream_t stream) {
   }
 }
 
+static int g_bwd_variant = 0;  // 1: split-role hd-64 kernel (attn_bwd64s_kernel), 0: attn_bwd64_kernel (default)
+static int g_bwd_dry = 0;      // diagnostics: handshakes only in the split-role kernel (wrong results)
+static int g_bwd_diag = 0;     // diagnostics: BwdParams::diag bits (wrong results)
+
+int launch_bwd64s(const BwdParams& P, int b, cudaStream_t stream) {
+  using C = Bwd64sCfg;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_bwd64s_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / kTile, P.h, b);
+  BwdParams Q = P;
+  Q.dry = g_bwd_dry;
+  Q.diag = g_bwd_diag;
+  attn_bwd64s_kernel<<<grid, C::kThreads, C::kSmem, stream>>>(Q);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
 int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
+  if (g_bwd_variant == 1) return launch_bwd64s(P, b, stream);
   return P.trace != nullptr ? launch_bwd64_p<true>(P, b, stream) : launch_bwd64_p<false>(P, b, stream);
 }
 
@@ -1528,7 +1975,13 @@ int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
 }  // namespace
 
 int attn_tune(int key, int value) {
-  int* slot = key == 0 ? &g_fwd_poly : key == 1 ? &g_fwd_variant : key == 2 ? &g_bwd_poly : nullptr;
+  int* slot = key == 0   ? &g_fwd_poly
+              : key == 1 ? &g_fwd_variant
+              : key == 2 ? &g_bwd_poly
+              : key == 3 ? &g_bwd_variant
+              : key == 4 ? &g_bwd_dry
+              : key == 5 ? &g_bwd_diag
+                         : nullptr;
   if (slot == nullptr) return -1;
   const int prev = *slot;
   if (value >= 0) *slot = value;

@@ -25,11 +25,16 @@ for _ in range(3):
 torch.cuda.synchronize()
 t = tr.cpu()
 t0 = int(t[t > 0].min())
-names = {0: "g0 S ready", 1: "g0 P done", 2: "g0 dP ready", 3: "g0 dS done", 4: "g1 S ready", 5: "g1 P done",
-         6: "g1 dP ready", 7: "g1 dS done", 8: "mma P seen", 9: "mma [3][1] issued", 10: "mma dS seen",
-         11: "mma dq free", 12: "mma [2] issued", 13: "red dQ ready", 14: "g0 S in regs", 15: "g0 P computed"}
+from paper_2512_12131_b200 import _native as N2  # noqa: E402
+if N2.load().btp_attn_tune(3, -1) == 1:  # split-role kernel
+    names = {0: "P0 S seen", 2: "P0 P done", 4: "dS dP,P seen", 6: "dS ld0", 14: "dS c0 done", 12: "dS ld1",
+             15: "dS c1 done", 5: "dS done", 8: "mma P seen", 10: "mma dS seen", 11: "mma dq free", 13: "red dQ"}
+else:
+    names = {0: "g0 S ready", 1: "g0 P done", 2: "g0 dP ready", 3: "g0 dS done", 4: "g1 S ready", 5: "g1 P done",
+             6: "g1 dP ready", 7: "g1 dS done", 8: "mma P seen", 9: "mma [3][1] issued", 10: "mma dS seen",
+             11: "mma dq free", 12: "mma [2] issued", 13: "red dQ ready", 14: "g0 S in regs", 15: "g0 P computed"}
 print("iter " + " ".join(f"{names[e][:12]:>12}" for e in sorted(names)))
 for i in range(t.shape[0]):
     print(f"{i:4d} " + " ".join(f"{(int(t[i, e]) - t0) if t[i, e] else 0:12d}" for e in sorted(names)))
-per = [(int(t[i + 1, 3]) - int(t[i, 3])) for i in range(4, t.shape[0] - 2)]
-print("clk per query tile (g0 dS done deltas):", sorted(per)[len(per) // 2])
+per = [(int(t[i + 1, 8]) - int(t[i, 8])) for i in range(4, t.shape[0] - 2)]
+print("clk per query tile (mma P seen deltas):", sorted(per)[len(per) // 2])

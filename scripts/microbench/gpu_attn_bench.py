@@ -35,9 +35,9 @@ def poly_sweep():
     o = torch.empty_like(q)
     lse = torch.empty(b, h, s, device="cuda")
     flops = 4 * b * h * s * s * hd
-    for var in (0, 1, 3, 4):
+    for var in (0, 4):
         lib.btp_attn_tune(1, var)
-        for n in (0, 2, 3, 4, 5):
+        for n in (0, 2):
             lib.btp_attn_tune(0, n)
             t_own = timeit(lambda: K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd))
             print(f"  fwd variant {var} poly every {n}: {t_own*1e3:.1f} us ({flops/t_own/1e9:.0f} TF/s)", flush=True)
@@ -47,12 +47,12 @@ def poly_sweep():
     D = torch.empty(b, h, s, device="cuda")
     acc = torch.empty(b * s, w, device="cuda")
     dq, dk, dv = (torch.empty_like(q) for _ in range(3))
-    prev = lib.btp_attn_tune(2, -1)
-    for n in (0, 1, 2, 4):
-        lib.btp_attn_tune(2, n)
+    prev = lib.btp_attn_tune(3, -1)
+    for var in (0, 1, 0, 1):
+        lib.btp_attn_tune(3, var)
         t_b = timeit(lambda: K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd))
-        print(f"  bwd poly {n}: {t_b*1e3:.1f} us ({2.5*flops/t_b/1e9:.0f} TF/s)", flush=True)
-    lib.btp_attn_tune(2, prev)
+        print(f"  bwd variant {var}: {t_b*1e3:.1f} us ({2.5*flops/t_b/1e9:.0f} TF/s)", flush=True)
+    lib.btp_attn_tune(3, prev)
 
 
 def main():

@@ -165,3 +165,30 @@ def test_attn_fwd_kernel_variants(variant, poly, hd):
     o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
     assert _rel(o, o_ref) < 1e-2
     assert torch.allclose(lse * math.log(2.0), lse_ref, atol=2e-3, rtol=1e-5)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("b,s,h", [(1, 256, 2), (2, 1024, 2)])
+def test_attn_bwd_hd64_kernel_variants(variant, b, s, h):
+    """Both hd-64 backward kernels behind btp_attn_tune(3, v) (shared P/dS warps, split roles) vs torch fp32."""
+    from paper_2512_12131_b200 import _native
+
+    lib = _native.load()
+    hd = 64
+    q, k, v = _inputs(b, s, h, hd, seed=3 * s + variant)
+    do = torch.randn(b * s, h * hd, device="cuda").bfloat16()
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+    D = torch.empty(b, h, s, device="cuda")
+    acc = torch.empty(b * s, h * hd, device="cuda")
+    dq, dk, dv = (torch.empty_like(o) for _ in range(3))
+    prev = lib.btp_attn_tune(3, variant)
+    try:
+        K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd)
+        torch.cuda.synchronize()
+    finally:
+        lib.btp_attn_tune(3, prev)
+    rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
+    errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
+    assert max(errs.values()) < 2e-2, errs
