@@ -167,20 +167,41 @@ def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True, opti
     x = O.seeded_fill((s, cfg.d), 10000)
     G = O.loss_projection((s, cfg.d), 30000)
     times, state = [], {}
-    t_start = time.perf_counter()
-    while True:
-        t0 = time.perf_counter()
-        y, cache = O.block_forward(blk, x, 1, s, cfg.heads, lean=lean)
-        grads = O.block_backward(blk, cache, G, 1, s, cfg.heads)
-        if optimizer:
-            O.adamw_step(blk, grads, state, **ADAMW)
-        times.append(time.perf_counter() - t0)
-        if max_steps is not None and len(times) >= max_steps:
-            break
-        if max_steps is None and time.perf_counter() - t_start > seconds_budget:
-            break
-    threads = _blas_threads()
+    with _all_host_threads():
+        t_start = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            y, cache = O.block_forward(blk, x, 1, s, cfg.heads, lean=lean)
+            grads = O.block_backward(blk, cache, G, 1, s, cfg.heads)
+            if optimizer:
+                O.adamw_step(blk, grads, state, **ADAMW)
+            times.append(time.perf_counter() - t0)
+            if max_steps is not None and len(times) >= max_steps:
+                break
+            if max_steps is None and time.perf_counter() - t_start > seconds_budget:
+                break
+        threads = _blas_threads()
     return s / statistics.median(times), times, threads
+
+
+class _all_host_threads:
+    """BLAS on every host thread for the CPU arm, also under torchrun (which exports
+    OMP_NUM_THREADS=1 to each rank): the same core count at every N. The CPU arm runs on rank 0
+    after the timed GPU work, while the other ranks wait."""
+
+    def __enter__(self):
+        self._ctl = None
+        try:
+            from threadpoolctl import threadpool_limits
+
+            self._ctl = threadpool_limits(limits=os.cpu_count(), user_api="blas")
+        except Exception:
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self._ctl is not None:
+            self._ctl.restore_original_limits()
 
 
 def _blas_threads():
@@ -460,6 +481,14 @@ def run_ours(args, cfg):
         dev = torch.device("cpu")
         if world > 1:
             dist.init_process_group("gloo")
+    elif args.share_gpu:
+        # debug: every rank on cuda:0, collectives over gloo (the N > 1 code path on a one-GPU box;
+        # timings are NOT measurements: the ranks share one GPU and gloo stages through the host)
+        local = 0
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        if world > 1:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(local)
         dev = torch.device("cuda", local)
@@ -634,6 +663,9 @@ def run_ours(args, cfg):
     if args.dry_run:
         line["dry_run"] = True
         line["data"] = "dry run (CPU, gloo): launch path and line schema only, NOT a measurement"
+    if args.share_gpu:
+        line["share_gpu"] = True
+        line["data"] = "debug: all ranks on one GPU over gloo (N>1 code path only), NOT a measurement"
     if args.emulate_tp:
         line["metric"] = (f"EMULATED per-rank compute of a TP={tp} step on one GPU (collectives not executed; "
                           "value = tokens/s if comm were free; not the bench metric)")
@@ -706,6 +738,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native"])
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="debug: all ranks on cuda:0 over gloo (exercises the N>1 path on one GPU; not a measurement)")
     ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
                     help="TP>1 BTP chunk boundaries: NCCL all-reduce + fix-up, or the fused peer-memory kernels")
     ap.add_argument("--boundary-dtype", default="bf16", choices=["bf16", "fp32"],
