@@ -360,7 +360,8 @@ int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ld
  * on the FMA pipe (n in {0 = none, 1, 2, 4}); key 3: hd-64 backward kernel (0 = the same 8 warps for P
  * and dS, default; 1 = split roles: P warps, alternating dS warp groups, dQ-reduce warps); keys 4 / 5:
  * diagnostics of the split-role kernel (WRONG results; 4: handshakes only, 5: bit 0 no dS stores, bit 1
- * no proxy fence, bit 2 no lse / D loads). value < 0 only queries. Returns the previous value (-1: unknown key). */
+ * no proxy fence, bit 2 no lse / D loads); key 6: forward diagnostics (split-row variants, WRONG results:
+ * softmax warps only do the handshakes). value < 0 only queries. Returns the previous value (-1: unknown key). */
 int btp_attn_tune(int key, int value);
 
 /* *ctr += delta on the stream (device-side step counters). */

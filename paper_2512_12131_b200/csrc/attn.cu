@@ -50,6 +50,7 @@ struct FwdParams {
   int s, h, n_kv;
   float c;  // log2(e) / sqrt(hd)
   long long* trace;  // optional clock64 stamps of CTA (0, 0, 0), [n_kv][16] (pipeline diagnostics)
+  int dry;           // diagnostics (split-row kernels, wrong results): softmax warps only do the handshakes
 };
 
 template <int HD, int ST, int kPoly>
@@ -455,6 +456,11 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>::kThreads,
       mbar_wait(&s_full[b], (j / kSBuf) & 1);
       if (q4 == 2 && u == 0) FSTAMP(j, 4 * g);
       tc_fence_after();
+      if (P.dry) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b]);
+        continue;
+      }
       // two passes over the group's kKG columns in 32-column chunks (registers: one chunk at a time;
       // TMEM reads are cheap): max, then exp2 / sum / bf16 pairs written back over the consumed columns
       float mx[4] = {-3.0e38f, -3.0e38f, -3.0e38f, -3.0e38f};
@@ -1845,6 +1851,7 @@ int f32_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long
 }
 
 static int g_fwd_poly = 2;     // every n-th exp2 pair on the FMA pipe (0: all on the MUFU)
+static int g_fwd_dry = 0;      // diagnostics: handshake-only softmax in the split-row kernels (wrong results)
 static int g_fwd_variant = 4;  // 4: two query tiles per CTA (s % 256), 3: split rows single S, 2 / 1: split rows
                                // double-buffered with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel
 
@@ -1946,7 +1953,9 @@ int launch_fwd2_poly(const FwdParams& P, int b, cudaStream_t stream) {
     configured = true;
   }
   dim3 grid(P.s / (kTile * kQT), P.h, b);
-  attn_fwd2_kernel<HD, ST, kPoly, kSplit, kSBuf, kQT><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  FwdParams Q = P;
+  Q.dry = g_fwd_dry;
+  attn_fwd2_kernel<HD, ST, kPoly, kSplit, kSBuf, kQT><<<grid, C::kThreads, C::kSmem, stream>>>(Q);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
@@ -1981,6 +1990,7 @@ int attn_tune(int key, int value) {
               : key == 3 ? &g_bwd_variant
               : key == 4 ? &g_bwd_dry
               : key == 5 ? &g_bwd_diag
+              : key == 6 ? &g_fwd_dry
                          : nullptr;
   if (slot == nullptr) return -1;
   const int prev = *slot;
