@@ -151,7 +151,6 @@ class ClockSampler:
 def attention_label(attn: str, cfg, args) -> str:
     from paper_2512_12131_b200 import attention as A
 
-    hl = cfg.heads // max(1, getattr(args, "gpus", 1))
     native = attn == "native" or (attn == "auto" and A.AUTO_NATIVE and A.native_supported(args.s, cfg.d // cfg.heads))
     if native:
         return "own tcgen05/TMEM flash kernels (btp_attn_fwd / btp_attn_bwd; not a changed subsystem)"
