@@ -157,6 +157,61 @@ def attention_label(attn: str, cfg, args) -> str:
     return "cuDNN SDPA via torch (not a changed subsystem)"
 
 
+def _attention_ab(b, s, h, hd, reps=10):
+    """Forward / backward device time of the attention at the step's shape: our kernels
+    (btp_attn_fwd / btp_attn_bwd on the [T, h*hd] buffers) vs cuDNN SDPA (the step's default path),
+    median of 3 x `reps` back-to-back calls between CUDA events."""
+    import math
+
+    import torch
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    from paper_2512_12131_b200 import attention as A
+    from paper_2512_12131_b200 import kernels as K
+
+    if not A.native_supported(s, hd):
+        return {"skipped": f"native kernels need s % 128 == 0 and hd in (64, 128); s={s}, hd={hd}"}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        out = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1) / reps)
+        return sorted(out)[1]
+
+    T, W = b * s, h * hd
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    q, k, v, do = (torch.randn(T, W, device="cuda", generator=gen).bfloat16() for _ in range(4))
+    o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+    lse, D = (torch.empty(b, h, s, device="cuda") for _ in range(2))
+    acc = torch.empty(T, W, device="cuda")
+    nat_f = timed(lambda: K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd))
+    nat_b = timed(lambda: K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd))
+    v4 = [t.view(b, s, h, hd).transpose(1, 2).detach().requires_grad_() for t in (q, k, v)]
+    with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+        cud_f = timed(lambda: F.scaled_dot_product_attention(*v4, scale=1 / math.sqrt(hd)))
+        ref = F.scaled_dot_product_attention(*v4, scale=1 / math.sqrt(hd))
+        do4 = do.view(b, s, h, hd).transpose(1, 2)
+        cud_b = timed(lambda: torch.autograd.grad(ref, v4, do4, retain_graph=True))
+    err = float((o.float() - ref.detach().transpose(1, 2).reshape(T, W).float()).norm() / ref.float().norm())
+    flops = 4 * b * h * s * s * hd
+    return {"shape": {"b": b, "s": s, "heads": h, "head_dim": hd},
+            "native": {"fwd_ms": nat_f, "bwd_ms": nat_b, "fwd_tflops": flops / nat_f / 1e9,
+                       "bwd_tflops": 2.5 * flops / nat_b / 1e9, "kernels": "btp_attn_fwd / btp_attn_bwd (csrc/attn.cu)"},
+            "cudnn": {"fwd_ms": cud_f, "bwd_ms": cud_b, "fwd_tflops": flops / cud_f / 1e9,
+                      "bwd_tflops": 2.5 * flops / cud_b / 1e9},
+            "native_vs_cudnn_out_rel_err": err,
+            "note": "the step runs cuDNN (--attn native runs ours); profiles/attention/README.md"}
+
+
 def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True, optimizer=True):
     """Oracle port (float64 NumPy, BLAS) fwd+bwd+AdamW on a bounded sample: ONE sequence (b=1) of the
     workload's length s. Returns (tokens_per_s, per-step seconds list, threads)."""
@@ -629,6 +684,12 @@ def run_ours(args, cfg):
         baselines["btp_over_full_rank"] = value / baselines["full_rank"]["value"]
         baselines["targets"] = {"btp_over_naive_tp": 1.8, "btp_over_full_rank": 1.4, "at": "TP=8 (north_star)"}
 
+    # ---- attention A/B at the step's attention shape (this rank's heads): our tcgen05 kernels vs the
+    # cuDNN SDPA path the step uses, same process, CUDA events (evidence for profiles/attention)
+    attention_ab = None
+    if not args.dry_run and not args.no_attention_ab and not args.model and (world == 1 or args.share_gpu):
+        attention_ab = _attention_ab(b, s, cfg.heads // tp, cfg.d // cfg.heads)
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -659,6 +720,8 @@ def run_ours(args, cfg):
         line["comm"] = comm_prof
     if baselines is not None:
         line["baselines"] = baselines
+    if attention_ab is not None:
+        line["attention_ab"] = attention_ab
     if args.dry_run:
         line["dry_run"] = True
         line["data"] = "dry run (CPU, gloo): launch path and line schema only, NOT a measurement"
@@ -737,6 +800,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native"])
+    ap.add_argument("--no-attention-ab", action="store_true",
+                    help="skip the in-process attention A/B (own kernels vs cuDNN) in the bench line")
     ap.add_argument("--share-gpu", action="store_true",
                     help="debug: all ranks on cuda:0 over gloo (exercises the N>1 path on one GPU; not a measurement)")
     ap.add_argument("--boundary", default="nccl", choices=["nccl", "peer", "nvls"],
