@@ -192,3 +192,61 @@ def test_attn_bwd_hd64_kernel_variants(variant, b, s, h):
     rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
     errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
     assert max(errs.values()) < 2e-2, errs
+
+
+def test_paper_7b_width_block_native_attention_vs_oracle():
+    """CoLA-7B block widths (32 heads of hd 128: the hd-128 forward / backward kernels) with native
+    attention inside the BTP block, fwd + bwd vs the float64 oracle."""
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.api import train_step
+    from paper_2512_12131_b200.model import RunShape, Variant, preset
+    from paper_2512_12131_b200.plan import Strategy, plan
+    from tests.gpu_util import BF16_TOL, inputs, oracle_step, rel
+
+    cfg = preset("7b")
+    b, s = 1, 256
+    blk, x, G, oblk = inputs(cfg, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True)
+    st = train_step(pl, blk, x, G, attn_backend="native")
+    assert st.executor.attn.native and st.executor.attn.hd == 128
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, cfg, b, s, sharded=False)
+    errs = {"y": rel(st.y.values.reshape(-1, cfg.d), y_ref), "loss": abs(st.loss - loss_ref) / abs(loss_ref),
+            "dx": rel(st.dx, g_ref["dx"])}
+    for n in O.PROJECTIONS:
+        errs[f"A_{n}"] = rel(st.grads["A"][n], g_ref["A"][n])
+        errs[f"B_{n}"] = rel(st.grads["B"][n], g_ref["B"][n])
+    bad = {k: v for k, v in errs.items() if v > BF16_TOL}
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("ckpt", [False, True])
+def test_model_step_native_attention_vs_oracle(ckpt):
+    """The 2-layer model step (embedding -> BTP blocks -> head -> cross-entropy) with native attention
+    in every block (and with low-rank checkpointing: the recompute runs the native forward again),
+    fwd + bwd vs the float64 oracle model."""
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import ModelConfig, RunShape, Variant, build_model, token_batch
+    from paper_2512_12131_b200.model_executor import model_train_step
+    from paper_2512_12131_b200.plan import Strategy, plan
+    from tests.gpu_util import BF16_TOL, SMALL, rel
+
+    layers, V, b, s = 2, 256, 2, 128
+    cfg = ModelConfig(layers=layers, heads=SMALL.heads, d=SMALL.d, d_ff=SMALL.d_ff, r=SMALL.r)
+    mw = build_model(cfg, Variant.COLA, 0, V)
+    om = O.build_model(cfg.d, cfg.d_ff, cfg.r, "cola", 0, V, layers)
+    ids, tg = token_batch(b, s, V)
+    loss_ref, cache = O.model_forward(om, ids, tg, b, s, cfg.heads)
+    g_ref = O.model_backward(om, cache, b, s, cfg.heads)
+    pl = plan(Strategy.BOTTLENECK, cfg, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=True,
+              lowrank_ckpt=ckpt)
+    loss, ex = model_train_step(pl, mw, ids, tg, attn_backend="native")
+    assert all(blk.attn.native for blk in ex.blocks)
+    assert abs(loss - loss_ref) / abs(loss_ref) < BF16_TOL
+    got = ex.model_grads()
+    assert rel(got["dhead"], g_ref["dhead"]) < BF16_TOL
+    assert rel(got["dembedding"], g_ref["dembedding"]) < BF16_TOL
+    for l in range(layers):
+        gr, gb = g_ref["blocks"][l], got["blocks"][l]
+        for n in O.PROJECTIONS:
+            assert rel(gb["A"][n], gr["A"][n]) < BF16_TOL, (l, "A", n)
+            assert rel(gb["B"][n], gr["B"][n]) < BF16_TOL, (l, "B", n)
