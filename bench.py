@@ -603,12 +603,16 @@ def run_ours(args, cfg):
     xh2 = xh.clone().pin_memory() if not args.dry_run else xh.clone()
     trainer.fit([xh, xh2, xh], gh)
     barrier()
+    # K steps like the device-timed loop (a longer e2e run measures a hotter GPU: sustained load
+    # lowers the SM clock under the power cap; scripts/probe_h2d_interference.py)
+    e2e_steps = args.steps
     tm = _Timer(args.dry_run)
     with tm:
-        losses = trainer.fit([xh if i % 2 == 0 else xh2 for i in range(args.steps)], gh)
+        losses = trainer.fit([xh if i % 2 == 0 else xh2 for i in range(e2e_steps)], gh)
     barrier()
-    ms_e2e = _reduce_max(dist, world, tm.elapsed() / args.steps, dev)
-    e2e = {"value": b * s / (ms_e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+    ms_e2e = _reduce_max(dist, world, tm.elapsed() / e2e_steps, dev)
+    e2e = {"value": b * s / (ms_e2e / 1e3), "unit": UNIT, "steps": e2e_steps,
+           "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
            "d2h_bytes_per_step": 4, "loss": losses[-1], "api": "BlockTrainer.fit (pinned host batches H2D per step on a copy stream; each step's loss copied D2H behind it and read by the host one step later)",
            "h2d_once_per_call_bytes": int(gh.numel() * gh.element_size())}
 
