@@ -1000,12 +1000,12 @@ __global__ void __launch_bounds__(448, 1) attn_bwd_kernel(const __grid_constant_
 // Tensor order per tile:  [3]_i dV  [1]_{i+1} S^T  [2]_{i+1} dP^T  [4]_i dK  [5]_i dQ.
 struct Bwd64Cfg {
   static constexpr int HD = 64;
-  static constexpr int ST = 2;
+  static constexpr int ST = 3;                                       // Q / dO / lse / D ring
   static constexpr int kTileBytes = kTile * HD * 2;                 // 16 KB
   static constexpr int kStageBytes = 2 * kTileBytes + 2 * kTile * 4;  // Q, dO, lse, D
   static constexpr int kDsBytes = kTile * kTile * 2;                  // 32 KB per buffer
   static constexpr int kBarBytes = 256;
-  static constexpr int kDqBytes = kTile * HD * 4;                    // fp32 dQ staging for the TMA reduce
+  static constexpr int kDqBytes = kTile * 32 * 4;                    // fp32 dQ staging: one 32-column box
   static constexpr int kSmem = 1024 + 2 * kTileBytes + ST * kStageBytes + 2 * kDsBytes + kDqBytes + kBarBytes;
   static constexpr int kThreads = 448;
   static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 320, tdQ = 384;  // dQ: 384 / 448
@@ -1014,19 +1014,19 @@ struct Bwd64Cfg {
 template <bool kTrace, int kPoly>
 __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constant__ BwdParams P) {
   using C = Bwd64Cfg;
-  constexpr int HD = 64, ST = 2;
+  constexpr int HD = 64, ST = C::ST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = sK + C::kTileBytes;
   uint8_t* sStage = sV + C::kTileBytes;
   uint8_t* sdS = sStage + ST * C::kStageBytes;  // 2 buffers
-  float* sdQ = reinterpret_cast<float*>(sdS + 2 * C::kDsBytes);  // fp32 [128][64] staging, two 32-col boxes
+  float* sdQ = reinterpret_cast<float*>(sdS + 2 * C::kDsBytes);  // fp32 [128][32] staging (one box at a time)
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sdQ) + C::kDqBytes);
   uint64_t* kv_full = bars;
-  uint64_t* qdo_full = bars + 1;       // [2]
-  uint64_t* qdo_empty = qdo_full + 2;  // [2]
-  uint64_t* s_full = qdo_empty + 2;
+  uint64_t* qdo_full = bars + 1;        // [ST]
+  uint64_t* qdo_empty = qdo_full + ST;  // [ST]
+  uint64_t* s_full = qdo_empty + ST;
   uint64_t* p_full = s_full + 1;
   uint64_t* dp_full = p_full + 1;
   uint64_t* dp_read = dp_full + 1;
@@ -1059,9 +1059,11 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
   if (warp == 1) {
     if (lane == 0) {
       mbar_init(kv_full, 1);
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < ST; ++s) {
         mbar_init(&qdo_full[s], 1);
         mbar_init(&qdo_empty[s], 1);
+      }
+      for (int s = 0; s < 2; ++s) {
         mbar_init(&sds_empty[s], 1);
         mbar_init(&dq_full[s], 1);
         mbar_init(&dq_empty[s], 4);
@@ -1089,8 +1091,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       tma_load_2d(sK, &P.tk, kv_full, col0, kv_row0);
       tma_load_2d(sV, &P.tv, kv_full, col0, kv_row0);
       for (int i = 0; i < P.n_q; ++i) {
-        const int st = i & 1;
-        mbar_wait(&qdo_empty[st], ((i >> 1) & 1) ^ 1);
+        const int st = i % ST;
+        mbar_wait(&qdo_empty[st], ((i / ST) & 1) ^ 1);
         mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
         tma_load_2d(sQ(st), &P.tq, &qdo_full[st], col0, q_row_base + i * kTile);
         tma_load_2d(sdO(st), &P.tdo, &qdo_full[st], col0, q_row_base + i * kTile);
@@ -1121,10 +1123,10 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
     }
     __syncwarp();
     for (int i = 0; i < P.n_q; ++i) {
-      const int st = i & 1;
+      const int st = i % ST, buf = i & 1;  // Q/dO ring stage; dS / dQ double-buffer parity
       const uint32_t ph = i & 1;
       const bool more = i + 1 < P.n_q;
-      const int st1 = st ^ 1;
+      const int st1 = (i + 1) % ST;
       mbar_wait(p_full, ph);
       BTP_STAMP64(8);
       tc_fence_after();
@@ -1137,7 +1139,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       }
       __syncwarp();
       if (more) {
-        mbar_wait(&qdo_full[st1], ((i + 1) >> 1) & 1);
+        mbar_wait(&qdo_full[st1], ((i + 1) / ST) & 1);
         tc_fence_after();
         if (elect_one()) {
           mma_ss(tmem + C::tS, k_base, smem_u32(sQ(st1)));  // [1]_{i+1}
@@ -1156,7 +1158,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       mbar_wait(ds_full, ph);
       BTP_STAMP64(10);
       tc_fence_after();
-      const uint32_t ds_base = smem_u32(sdS + st * C::kDsBytes);
+      const uint32_t ds_base = smem_u32(sdS + buf * C::kDsBytes);
       if (elect_one()) {
         // [4] dK += dS^T Q: A = dS^T K-major in shared memory (chunk g = queries [64g, +64), 128 B rows)
 #pragma unroll
@@ -1168,7 +1170,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       }
       __syncwarp();
       if (i >= 2) {
-        mbar_wait(&dq_empty[st], ((i >> 1) - 1) & 1);
+        mbar_wait(&dq_empty[buf], ((i >> 1) - 1) & 1);
         tc_fence_after();
       }
       BTP_STAMP64(11);
@@ -1176,10 +1178,10 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
         // [5] dQ_i = dS K: A = dS MN-major (the same tile), B = K MN-major
 #pragma unroll
         for (int k = 0; k < kTile / 16; ++k)
-          umma_bf16(tmem + C::tdQ + st * 64, make_sw128_desc(ds_base + k * 2048, kTile * 128, 1024),
+          umma_bf16(tmem + C::tdQ + buf * 64, make_sw128_desc(ds_base + k * 2048, kTile * 128, 1024),
                     make_sw128_desc(k_base + k * 2048, kTile * 128, 1024), idesc_dq, k > 0 ? 1u : 0u);
-        umma_commit(&dq_full[st]);
-        umma_commit(&sds_empty[st]);
+        umma_commit(&dq_full[buf]);
+        umma_commit(&sds_empty[buf]);
       }
       __syncwarp();
       BTP_STAMP64(12);
@@ -1194,10 +1196,10 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
     const uint32_t lane_addr = (q4 * 32) << 16;
     const float2 c2 = make_float2(P.c, P.c);
     for (int i = 0; i < P.n_q; ++i) {
-      const int st = i & 1;
+      const int st = i % ST, buf = i & 1;
       const uint32_t ph = i & 1;
       const uint32_t lse_a = smem_u32(sLse(st)) + g * 256, d_a = smem_u32(sD(st)) + g * 256;
-      mbar_wait(&qdo_full[st], (i >> 1) & 1);  // lse / D of this query tile are resident
+      mbar_wait(&qdo_full[st], (i / ST) & 1);  // lse / D of this query tile are resident
       mbar_wait(s_full, ph);
       if (q4 == 2) BTP_STAMP64(4 * g);
       tc_fence_after();
@@ -1239,9 +1241,9 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       if (q4 == 2) BTP_STAMP64(4 * g + 1);
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      if (i >= 2) mbar_wait(&sds_empty[st], ((i >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
+      if (i >= 2) mbar_wait(&sds_empty[buf], ((i >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
       if (q4 == 2) BTP_STAMP64(4 * g + 2);
-      const uint32_t ds_row = smem_u32(sdS + st * C::kDsBytes) + g * (kTile * 128) + row * 128;
+      const uint32_t ds_row = smem_u32(sdS + buf * C::kDsBytes) + g * (kTile * 128) + row * 128;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {  // 32 queries per half
         uint32_t dp[32];
@@ -1305,32 +1307,31 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
     const uint32_t lane_addr = (q4 * 32) << 16;
     const bool issuer = (warp == 10 && lane == 0);
     for (int i = 0; i < P.n_q; ++i) {
-      const int st = i & 1;
-      mbar_wait(&dq_full[st], (i >> 1) & 1);
+      const int buf = i & 1;
+      mbar_wait(&dq_full[buf], (i >> 1) & 1);
       if (q4 == 2) BTP_STAMP64(13);
       tc_fence_after();
       uint32_t o[64];
-      tmem_ld_32x32b_x64(tmem + C::tdQ + st * 64 + lane_addr, o);
+      tmem_ld_32x32b_x64(tmem + C::tdQ + buf * 64 + lane_addr, o);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_empty[st]);
-      if (issuer) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
-      named_bar_sync(1, 128);
+      if (lane == 0) mbar_arrive(&dq_empty[buf]);
 #pragma unroll
-      for (int bx = 0; bx < 2; ++bx) {  // box bx: columns [32 bx, 32 bx + 32) = 8 units of 16 B per row
-        const uint32_t base = smem_u32(sdQ) + bx * (kTile * 128) + row * 128;
+      for (int bx = 0; bx < 2; ++bx) {  // one 32-column box at a time through the 16 KB staging tile
+        if (issuer) bulk_wait_read<0>();  // the previous box's reduce has read the staging tile
+        named_bar_sync(1, 128);
+        const uint32_t base = smem_u32(sdQ) + row * 128;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           st_shared_v4(base + ((u ^ (row & 7)) << 4), o[bx * 32 + 4 * u], o[bx * 32 + 4 * u + 1],
                        o[bx * 32 + 4 * u + 2], o[bx * 32 + 4 * u + 3]);
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (issuer) {
-        tma_reduce_add_2d(&P.tdq, sdQ, col0, q_row_base + i * kTile);
-        tma_reduce_add_2d(&P.tdq, reinterpret_cast<uint8_t*>(sdQ) + kTile * 128, col0 + 32, q_row_base + i * kTile);
-        bulk_commit();
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (issuer) {
+          tma_reduce_add_2d(&P.tdq, sdQ, col0 + 32 * bx, q_row_base + i * kTile);
+          bulk_commit();
+        }
       }
     }
     if (issuer) bulk_wait<0>();
