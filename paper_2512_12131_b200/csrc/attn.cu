@@ -591,6 +591,311 @@ __global__ void __launch_bounds__(Fwd2Cfg<HD, ST, kSplit, kSBuf, kQT>::kThreads,
 #undef FSTAMP
 }
 
+// ---------------------------------------------------------------------------- forward, P apart from S
+// hd 64. In the kernels above P_j is written over S_j, so S_{j+1} of a query tile can only be issued
+// after PV_j has read P_j: per tile the chain S MMA -> softmax -> PV MMA -> next S MMA is serial, and
+// the traces show the softmax warps waiting on it (~1580 cycles per (query, key) tile against the
+// MUFU's 1024). Here each query tile has its own P columns, so the softmax releases S_j as soon as
+// it has pulled the row into registers and S_{j+1} runs on the tensor core underneath softmax j:
+//   TMEM (512 columns): S_u at 128 u, P_u (bf16 pairs) at 256 + 64 u, O_u at 384 + 64 u, u = 0, 1
+//   w0 TMA (Q_0, Q_1 once; K_j / V_j ring of ST stages), w1 MMA, w2..w9 softmax (query tile u =
+//   (w - 2) / 4; thread = query row = TMEM lane, all 128 keys of the tile in registers).
+// MMA issue order per key tile j and query tile u: PV_(u,j) once P_(u,j) is published, then
+// S_(u,j+2) once softmax (u, j+1) has released S_u (S_(u,0), S_(u,1) before the loop). The two query
+// tiles' softmax groups share every K / V tile and keep each scheduler's MUFU fed in turn.
+// Measured (profiles/attention/README.md): S never gates the softmax any more; the loop runs at the
+// exp2 rate two warps per scheduler reach (scripts/microbench/softmax_rate.cu), ~4 % ahead of the
+// two-query-tile kernel above at the bench shape; opt-in, btp_attn_tune(1, 5) / (1, 6) split rows.
+// kHalves = 2: every query row's 128 keys are split over two warps (64 each: 16 softmax warps, four
+// per scheduler, which is what keeps the MUFU busy - scripts/microbench/softmax_rate.cu); the pair
+// shares O_u and P_u (each writes its 32 P columns), exchanges its row maxima through shared memory
+// every key tile (so both halves take identical lazy-rescale decisions), and sums l in the epilogue.
+template <int ST, int kHalves>
+struct Fwd3Cfg {
+  static constexpr int kTileBytes = kTile * 64 * 2;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kXBytes = kHalves == 2 ? 2 * 2 * 2 * kTile * 4 : 0;  // [j & 1][u][half][row] maxima
+  static constexpr int kSmem = 1024 + kTileBytes * (2 + 2 * ST) + kXBytes + kBarBytes;
+  static constexpr int kSoftWarps = 8 * kHalves;
+  static constexpr int kThreads = 64 + 32 * kSoftWarps;
+  static constexpr int kKW = kTile / kHalves;  // keys per softmax warp
+  static constexpr uint32_t tP = 256, tO = 384;
+};
+
+template <int ST, int kPoly, int kHalves>
+__global__ void __launch_bounds__(Fwd3Cfg<ST, kHalves>::kThreads, 1)
+    attn_fwd3_kernel(const __grid_constant__ FwdParams P) {
+  using C = Fwd3Cfg<ST, kHalves>;
+  constexpr int kKW = C::kKW;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + 2 * C::kTileBytes;
+  uint8_t* sV = sK + ST * C::kTileBytes;
+  float* sX = reinterpret_cast<float*>(sV + ST * C::kTileBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * C::kTileBytes + C::kXBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + ST;
+  uint64_t* s_full = kv_empty + ST;  // [2]
+  uint64_t* s_free = s_full + 2;     // [2]
+  uint64_t* p_full = s_free + 2;     // [2]
+  uint64_t* o_bar = p_full + 2;      // [2], one phase per PV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+
+  const int qt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
+  const int row0 = bi * P.s + qt * 2 * kTile;
+  const int kv0 = bi * P.s;
+  const int col0 = head * 64;
+  const int n = P.n_kv;
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  long long* const tr = (qt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
+#define FSTAMP(jj, e)                                               \
+  do {                                                              \
+    if (tr != nullptr && lane == 0) tr[(jj) * 16 + (e)] = clock64(); \
+  } while (0)
+
+  if (warp == 1) FSTAMP(0, 12);  // CTA start
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&P.tq);
+    tma_prefetch_desc(&P.tk);
+    tma_prefetch_desc(&P.tv);
+  }
+  if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(q_full, 1);
+      for (int s = 0; s < ST; ++s) {
+        mbar_init(&kv_full[s], 1);
+        mbar_init(&kv_empty[s], 1);
+      }
+      for (int u = 0; u < 2; ++u) {
+        mbar_init(&s_full[u], 1);
+        mbar_init(&s_free[u], 4 * kHalves);
+        mbar_init(&p_full[u], 4 * kHalves);
+        mbar_init(&o_bar[u], 1);
+      }
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<512>(tmem_slot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 1) FSTAMP(0, 13);  // barriers + TMEM ready
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, 2 * C::kTileBytes);
+      tma_load_2d(sQ, &P.tq, q_full, col0, row0);
+      tma_load_2d(sQ + C::kTileBytes, &P.tq, q_full, col0, row0 + kTile);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % ST;
+        mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kTileBytes);
+        tma_load_2d(sK + st * C::kTileBytes, &P.tk, &kv_full[st], col0, kv0 + j * kTile);
+        tma_load_2d(sV + st * C::kTileBytes, &P.tv, &kv_full[st], col0, kv0 + j * kTile);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_bf16_f32(kTile, kTile, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16_f32(kTile, 64, false, true);
+    auto issue_s = [&](int u, int j) {  // S_(u,j) = Q_u K_j^T
+      const int st = j % ST;
+      mbar_wait(&kv_full[st], (j / ST) & 1);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sK + st * C::kTileBytes);
+      const uint32_t q_base = smem_u32(sQ + u * C::kTileBytes);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(tmem + u * 128, make_sw128_desc(q_base + k * 32, 16, 1024),
+                    make_sw128_desc(k_base + k * 32, 16, 1024), idesc_s, k > 0 ? 1u : 0u);
+        umma_commit(&s_full[u]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int u, int j) {  // O_u += P_(u,j) V_j
+      const int st = j % ST;
+      mbar_wait(&p_full[u], j & 1);
+      FSTAMP(j, 8 + 2 * u);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sV + st * C::kTileBytes);
+      if (elect_one()) {
+        // A = P_u (bf16 pairs, 8 columns per 16 keys), B = V (MN-major, 2 KB per 16 keys)
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + C::tO + u * 64, tmem + C::tP + u * 64 + k * 8,
+                       make_sw128_desc(v_base + k * 2048, kTile * 128, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        if (u == 1) umma_commit(&kv_empty[st]);
+        umma_commit(&o_bar[u]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    if (n > 1) {
+      for (int u = 0; u < 2; ++u) {
+        mbar_wait(&s_free[u], 0);
+        issue_s(u, 1);
+      }
+    }
+    for (int j = 0; j < n; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        issue_pv(u, j);
+        if (j + 2 < n) {
+          mbar_wait(&s_free[u], (j + 1) & 1);
+          issue_s(u, j + 2);
+          FSTAMP(j, 9 + 2 * u);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax warps 2 .. 2 + 8 kHalves
+    const uint32_t u = (warp - 2) / (4 * kHalves);
+    const uint32_t hf = ((warp - 2) >> 2) % kHalves;  // key half of the row
+    const uint32_t q4 = warp & 3;
+    const uint32_t row = q4 * 32 + lane;
+    const uint32_t lane_addr = (q4 * 32) << 16;
+    const uint32_t tS = tmem + u * 128 + hf * kKW + lane_addr;
+    const uint32_t tPu = tmem + C::tP + u * 64 + hf * (kKW / 2) + lane_addr;
+    const uint32_t tOu = tmem + C::tO + u * 64 + lane_addr;
+    constexpr int kOW = 64 / kHalves;  // O columns this warp rescales / writes: [hf kOW, (hf + 1) kOW)
+    // the two warps of a row pair (kHalves = 2) meet on named barrier 1 + 4 u + q4 (64 threads)
+    auto pair_max = [&](int j, float m) {
+      if (kHalves == 1) return m;
+      float* x = sX + (((j & 1) * 2 + u) * 2) * kTile;
+      x[hf * kTile + row] = m;
+      named_bar_sync(1 + 4 * u + q4, 64);
+      return fmaxf(m, x[(hf ^ 1) * kTile + row]);
+    };
+    const float c = P.c;
+    float m_used = 0.f, l = 0.f;
+    auto row_max = [&](const uint32_t* v, int cnt, float m) {
+      float mx[2] = {m, m};
+#pragma unroll
+      for (int i = 0; i < cnt; i += 4) {
+        mx[0] = fmax3(mx[0], __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        mx[1] = fmax3(mx[1], __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+      }
+      return fmaxf(mx[0], mx[1]);
+    };
+    // rescale O_u / l when the row max grew by > 2^8 (lazy): O_u must hold PV_(u,j-1) first
+    auto rescale = [&](int j, float m_new) {
+      if (j == 0) {
+        m_used = m_new;
+        return;
+      }
+      const bool need = m_new > m_used + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        mbar_wait(&o_bar[u], (j - 1) & 1);  // completed PVs: j - 1 or j
+        tc_fence_after();
+        const float alpha = need ? ex2_approx(m_used - m_new) : 1.f;
+#pragma unroll
+        for (int cc = 0; cc < kOW / 16; ++cc) {
+          uint32_t o[16];
+          tmem_ld_32x32b_x16(tOu + hf * kOW + cc * 16, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st_32x32b_x16(tOu + hf * kOW + cc * 16, o);
+        }
+        tmem_st_wait();
+        if (need) {
+          l *= alpha;
+          m_used = m_new;
+        }
+      }
+    };
+    const bool stamp = q4 == 2 && hf == 0;
+    uint32_t s[kKW];
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&s_full[u], j & 1);
+      tc_fence_after();
+      if (stamp) FSTAMP(j, 4 * u + 0);
+#pragma unroll
+      for (int cc = 0; cc < kKW / 64; ++cc)
+        tmem_ld_32x32b_x64(tS + cc * 64, *reinterpret_cast<uint32_t(*)[64]>(&s[cc * 64]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[u]);  // S_u may now take S_(u,j+1)
+      rescale(j, pair_max(j, row_max(s, kKW, -3.0e38f)) * c);
+      if (stamp) FSTAMP(j, 4 * u + 1);
+      float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
+      const float2 c2 = make_float2(c, c), nm = make_float2(-m_used, -m_used);
+#pragma unroll
+      for (int i = 0; i < kKW / 2; ++i) {  // P pair i packed into s[i] (s[2i], s[2i+1] are consumed by then)
+        const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nm);
+        float2 e;
+        if (kPoly > 0 && (i % (kPoly > 0 ? kPoly : 1)) == kPoly - 1) {
+          e = ex2_poly2(x);
+        } else {
+          e.x = ex2_approx(x.x);
+          e.y = ex2_approx(x.y);
+        }
+        if (i & 1) l2b = fadd2(l2b, e);
+        else l2a = fadd2(l2a, e);
+        s[i] = pack_bf16(e.x, e.y);
+      }
+      l += (l2a.x + l2a.y) + (l2b.x + l2b.y);
+      if (j > 0) {
+        mbar_wait(&o_bar[u], (j - 1) & 1);  // PV_(u,j-1) has read P_u
+        tc_fence_after();
+      }
+      if (stamp) FSTAMP(j, 4 * u + 3);
+#pragma unroll
+      for (int cc = 0; cc < kKW / 64; ++cc)
+        tmem_st_32x32b_x32(tPu + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[cc * 32]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[u]);
+      if (stamp) FSTAMP(j, 4 * u + 2);
+    }
+    if (kHalves == 2) {  // l of the whole row: the two halves' partial sums (same reference max)
+      float* x = sX + (((n & 1) * 2 + u) * 2) * kTile;
+      x[hf * kTile + row] = l;
+      named_bar_sync(1 + 4 * u + q4, 64);
+      l += x[(hf ^ 1) * kTile + row];
+    }
+    // ---------------------------------------------------------------- epilogue: O / l, lse
+    mbar_wait(&o_bar[u], (n - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = P.o + (long long)(row0 + u * kTile + row) * P.ldo + col0 + hf * kOW;
+#pragma unroll
+    for (int cc = 0; cc < kOW / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tOu + hf * kOW + cc * 32, o);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        st_global_v4(orow + cc * 32 + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+    }
+    if (hf == 0) P.lse[((long long)bi * P.h + head) * P.s + (qt * 2 + u) * kTile + row] = m_used + __log2f(l);
+    if (stamp && u == 0) FSTAMP(0, 14);  // epilogue stored
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+    FSTAMP(0, 15);  // CTA done
+  }
+#undef FSTAMP
+}
+
 // ============================================================================ backward
 //
 // One CTA per 128-row key/value tile of one (batch, head) (one CTA per SM: 512 TMEM columns);
@@ -1854,7 +2159,8 @@ int f32_tile_map(CUtensorMap* m, const void* ptr, int rows, int width, long long
 static int g_fwd_poly = 2;     // every n-th exp2 pair on the FMA pipe (0: all on the MUFU)
 static int g_fwd_dry = 0;      // diagnostics: handshake-only softmax in the split-row kernels (wrong results)
 static int g_fwd_variant = 4;  // 4: two query tiles per CTA (s % 256), 3: split rows single S, 2 / 1: split rows
-                               // double-buffered with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel
+                               // double-buffered with 4 / 2 key groups (hd 128: 2), 0: attn_fwd_kernel;
+                               // hd 64, s % 256: 5 two query tiles with P apart from S, 6 the same, split rows
 
 template <int HD, int ST, int kPoly>
 int launch_fwd_poly(const FwdParams& P, int b, cudaStream_t stream) {
@@ -1971,6 +2277,33 @@ int launch_fwd2(const FwdParams& P, int b, cudaStream_t stream) {
   }
 }
 
+template <int ST, int kPoly, int kHalves>
+int launch_fwd3_poly(const FwdParams& P, int b, cudaStream_t stream) {
+  using C = Fwd3Cfg<ST, kHalves>;
+  static_assert(C::kSmem <= 232448, "shared memory budget");
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd3_kernel<ST, kPoly, kHalves>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmem) != cudaSuccess)
+      return BTP_ERR_CUDA;
+    configured = true;
+  }
+  dim3 grid(P.s / (2 * kTile), P.h, b);
+  attn_fwd3_kernel<ST, kPoly, kHalves><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
+}
+
+template <int ST, int kHalves>
+int launch_fwd3(const FwdParams& P, int b, cudaStream_t stream) {
+  switch (g_fwd_poly) {
+    case 0: return launch_fwd3_poly<ST, 0, kHalves>(P, b, stream);
+    case 2: return launch_fwd3_poly<ST, 2, kHalves>(P, b, stream);
+    case 3: return launch_fwd3_poly<ST, 3, kHalves>(P, b, stream);
+    case 5: return launch_fwd3_poly<ST, 5, kHalves>(P, b, stream);
+    default: return launch_fwd3_poly<ST, 4, kHalves>(P, b, stream);
+  }
+}
+
 template <int HD, int ST>
 int launch_fwd(const FwdParams& P, int b, cudaStream_t stream) {
   switch (g_fwd_poly) {
@@ -2023,7 +2356,9 @@ int attn_fwd(const void* q, long long ldq, const void* k, long long ldk, const v
   P.n_kv = s / kTile;
   P.c = 1.4426950408889634f / sqrtf((float)hd);
   P.trace = trace;
-  if (g_fwd_variant == 4 && s % 256 == 0)
+  if (g_fwd_variant == 5 && s % 256 == 0 && hd == 64) return launch_fwd3<4, 1>(P, b, stream);
+  if (g_fwd_variant == 6 && s % 256 == 0 && hd == 64) return launch_fwd3<4, 2>(P, b, stream);
+  if (g_fwd_variant >= 4 && s % 256 == 0)
     return hd == 64 ? launch_fwd2<64, 3, 2, 1, 2>(P, b, stream) : launch_fwd2<128, 2, 1, 1, 2>(P, b, stream);
   if (g_fwd_variant == 3 && hd == 64) return launch_fwd2<64, 2, 2, 1>(P, b, stream);
   if (g_fwd_variant == 2 && hd == 64) return launch_fwd2<64, 3, 4>(P, b, stream);

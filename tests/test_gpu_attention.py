@@ -141,13 +141,13 @@ def test_native_attention_rejects_unsupported_shapes():
         Attention(1, 128, 2, 32, "native")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
-@pytest.mark.parametrize("poly", [0, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("poly", [0, 3, 4])
 @pytest.mark.parametrize("hd", [64, 128])
 def test_attn_fwd_kernel_variants(variant, poly, hd):
     """Every forward kernel variant behind btp_attn_tune (single S buffer / split rows double-buffered /
-    4 key groups / split rows single-buffered / two query tiles per CTA) and the polynomial exp2
-    share, against torch fp32."""
+    4 key groups / split rows single-buffered / two query tiles per CTA / two query tiles with P apart
+    from S, hd 64) and the polynomial exp2 share, against torch fp32."""
     from paper_2512_12131_b200 import _native
 
     lib = _native.load()
@@ -163,6 +163,33 @@ def test_attn_fwd_kernel_variants(variant, poly, hd):
         lib.btp_attn_tune(1, prev_v)
         lib.btp_attn_tune(0, prev_p)
     o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
+    assert _rel(o, o_ref) < 1e-2
+    assert torch.allclose(lse * math.log(2.0), lse_ref, atol=2e-3, rtol=1e-5)
+
+
+@pytest.mark.parametrize("variant", [4, 5, 6])
+def test_attn_fwd_growing_row_max(variant):
+    """Scores that grow along the keys (every key tile raises the row max) plus one dominant key in
+    the last tile (a late jump far above the 2^8 lazy-rescale threshold): the O / l rescale paths of
+    the two-query-tile kernels, against torch fp32."""
+    from paper_2512_12131_b200 import _native
+
+    lib = _native.load()
+    b, s, h, hd = 1, 1024, 2, 64
+    q, k, v = _inputs(b, s, h, hd, seed=11)
+    ramp = torch.linspace(0.2, 3.0, s, device="cuda").repeat(b).unsqueeze(1)
+    k = (k.float() * ramp).bfloat16()
+    k[s - 5] = (q[3].float() * 6.0).bfloat16()  # query row 3 (both heads) meets a huge score late
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    prev = lib.btp_attn_tune(1, variant)
+    try:
+        K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+        torch.cuda.synchronize()
+    finally:
+        lib.btp_attn_tune(1, prev)
+    o_ref, lse_ref = _ref(q, k, v, b, s, h, hd)
+    assert torch.isfinite(o.float()).all()
     assert _rel(o, o_ref) < 1e-2
     assert torch.allclose(lse * math.log(2.0), lse_ref, atol=2e-3, rtol=1e-5)
 
