@@ -75,6 +75,26 @@ def test_grouped_and_mixed_majors():
     assert rel(dW, dY.float().t() @ X.float()) < 1e-5
 
 
+@pytest.mark.parametrize(
+    "shapes",
+    [
+        [(16384, 2048, 512)] * 3,  # the q|k|v up-projection launch at the bench config
+        [(4096, 5472, 512)] * 2,  # gate|up widths (N tail: 5472 = 21.375 x 256)
+        [(1000, 640, 200), (296, 2048, 512), (2560, 136, 64)],  # M / N / K tails in one launch
+        [(300, 4096, 448)],  # fewer M blocks than CTA pairs
+    ],
+)
+def test_grouped_short_k_launches(shapes):
+    """Grouped K <= 512 launches (the forward up-projections) with ragged M / N / K, against torch fp32."""
+    A = [_mk(m, kd) for m, n, kd in shapes]
+    B = [_mk(n, kd) for m, n, kd in shapes]
+    C = [torch.empty(m, n, device="cuda", dtype=torch.bfloat16) for m, n, kd in shapes]
+    K.gemm(*[K.Gemm(a, b, c) for a, b, c in zip(A, B, C)])
+    torch.cuda.synchronize()
+    for a, b, c in zip(A, B, C):
+        assert rel(c, a.float() @ b.float().t()) < TOL
+
+
 @pytest.mark.parametrize("N", [640, 5472])
 def test_swiglu_bwd_epilogue(N):
     T, r = 1024, 512
