@@ -362,7 +362,9 @@ int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ld
  * and dS, default; 1 = split roles: P warps, alternating dS warp groups, dQ-reduce warps); keys 4 / 5:
  * diagnostics of the split-role kernel (WRONG results; 4: handshakes only, 5: bit 0 no dS stores, bit 1
  * no proxy fence, bit 2 no lse / D loads); key 6: forward diagnostics (split-row variants, WRONG results:
- * softmax warps only do the handshakes). value < 0 only queries. Returns the previous value (-1: unknown key). */
+ * softmax warps only do the handshakes); key 7: hd-64 backward grid (1 = persistent, one CTA per SM walking
+ * the key-tile work items, default; 0 = one CTA per key tile). value < 0 only queries. Returns the previous
+ * value (-1: unknown key). */
 int btp_attn_tune(int key, int value);
 
 /* *ctr += delta on the stream (device-side step counters). */

@@ -950,6 +950,7 @@ struct BwdParams {
   int dry;           // diagnostics (split-role kernel): 1 = P / dS / reduce warps only do the handshakes
   int diag;          // diagnostics (split-role kernel, wrong results): bit0 no dS st.shared, bit1 no proxy
                      // fence after them, bit2 no lse / D shared loads
+  int n_items;       // hd-64 kernel: key tiles x heads x batch (work items, walked persistently)
 };
 
 #define BTP_STAMP64(e)                                                                            \
@@ -1340,14 +1341,34 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
   uint64_t* dq_full = sds_empty + 2;   // [2]
   uint64_t* dq_empty = dq_full + 2;    // [2]
   uint64_t* acc_full = dq_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* acc_empty = acc_full + 1;  // persistent: the compute warps have read this item's dK / dV
+  uint64_t* kv_empty = acc_empty + 1;  // persistent: the item's last MMA reading K / V is done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + 1);
 
-  const int kt = blockIdx.x, head = blockIdx.y, bi = blockIdx.z;
-  const int kv_row0 = bi * P.s + kt * kTile;
-  const int q_row_base = bi * P.s;
-  const int col0 = head * HD;
-  const long long stat0 = ((long long)bi * P.h + head) * P.s;
-  long long* const tr = (kTrace && kt == 0 && head == 0 && bi == 0) ? P.trace : nullptr;
+  // Work items (key tile kt of head `head` of sequence bi) are walked persistently: CTA x takes items
+  // x, x + gridDim.x, ... (with gridDim.x == n_items every CTA has one). Per-tile barrier phases, the
+  // Q / dO ring and the dS / dQ double buffers run on the CTA's global tile counter g = it * n_q + i,
+  // so the next item's loads and first MMAs overlap this item's dQ-reduce tail and dK / dV stores.
+  struct Item {
+    int kv_row0, q_row_base, col0;
+    long long stat0;
+  };
+  auto item_of = [&](int it) {
+    const int item = (int)blockIdx.x + it * (int)gridDim.x;
+    const int kt = item % P.n_q, r = item / P.n_q;
+    const int head = r % P.h, bi = r / P.h;
+    return Item{bi * P.s + kt * kTile, bi * P.s, head * HD, ((long long)bi * P.h + head) * P.s};
+  };
+  const int n_it = ((int)blockIdx.x < P.n_items) ? (P.n_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // kTrace: every CTA's (SM id, start, walk done, end) clock64 stamps after the per-tile stamps
+  long long* const ct =
+      kTrace ? P.trace + (long long)P.n_q * 16 + 8ll * blockIdx.x : nullptr;
+  if (kTrace && threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    ct[0] = sm;
+    ct[1] = clock64();
+  }
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
   auto sQ = [&](int st) { return sStage + st * C::kStageBytes; };
@@ -1379,6 +1400,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       mbar_init(dp_read, 8);
       mbar_init(ds_full, 8);
       mbar_init(acc_full, 1);
+      mbar_init(acc_empty, 8);
+      mbar_init(kv_empty, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -1392,19 +1415,32 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (elect_one()) {
-      mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
-      tma_load_2d(sK, &P.tk, kv_full, col0, kv_row0);
-      tma_load_2d(sV, &P.tv, kv_full, col0, kv_row0);
-      for (int i = 0; i < P.n_q; ++i) {
-        const int st = i % ST;
-        mbar_wait(&qdo_empty[st], ((i / ST) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
-        tma_load_2d(sQ(st), &P.tq, &qdo_full[st], col0, q_row_base + i * kTile);
-        tma_load_2d(sdO(st), &P.tdo, &qdo_full[st], col0, q_row_base + i * kTile);
-        bulk_load_1d(sLse(st), P.lse + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
-        bulk_load_1d(sD(st), P.D + stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+      for (int it = 0; it < n_it; ++it) {
+        const Item w = item_of(it);
+        // K / V of item `it` once the previous item's last MMA has read them; issued after the first
+        // ring tiles of this item (whose slots free up earlier) so those loads are not held back
+        auto load_kv = [&]() {
+          if (it > 0) mbar_wait(kv_empty, (it - 1) & 1);
+          mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
+          tma_load_2d(sK, &P.tk, kv_full, w.col0, w.kv_row0);
+          tma_load_2d(sV, &P.tv, kv_full, w.col0, w.kv_row0);
+        };
+        const int kv_at = P.n_q < ST ? P.n_q : ST;
+        for (int i = 0; i < P.n_q; ++i) {
+          if (i == kv_at) load_kv();
+          const int g = it * P.n_q + i;
+          const int st = g % ST;
+          mbar_wait(&qdo_empty[st], ((g / ST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&qdo_full[st], C::kStageBytes);
+          tma_load_2d(sQ(st), &P.tq, &qdo_full[st], w.col0, w.q_row_base + i * kTile);
+          tma_load_2d(sdO(st), &P.tdo, &qdo_full[st], w.col0, w.q_row_base + i * kTile);
+          bulk_load_1d(sLse(st), P.lse + w.stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+          bulk_load_1d(sD(st), P.D + w.stat0 + i * kTile, kTile * 4, &qdo_full[st]);
+        }
+        if (kv_at == P.n_q) load_kv();
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_ss = make_idesc_bf16_f32(kTile, kTile, false, false);  // [1], [2]
@@ -1417,22 +1453,28 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
         umma_bf16(d, make_sw128_desc(a_base + k * 32, 16, 1024), make_sw128_desc(b_base + k * 32, 16, 1024), idesc_ss,
                   k > 0 ? 1u : 0u);
     };
-    mbar_wait(kv_full, 0);
-    mbar_wait(&qdo_full[0], 0);
+    for (int it = 0; it < n_it; ++it) {
+    long long* const tr = (kTrace && blockIdx.x == 0 && it == 0) ? P.trace : nullptr;
+    const int g0 = it * P.n_q;
+    mbar_wait(kv_full, it & 1);
+    mbar_wait(&qdo_full[g0 % ST], (g0 / ST) & 1);
+    if (it > 0) mbar_wait(dp_read, (g0 - 1) & 1);  // the previous item's last dP^T is in registers
     tc_fence_after();
     if (elect_one()) {
-      mma_ss(tmem + C::tS, k_base, smem_u32(sQ(0)));
+      mma_ss(tmem + C::tS, k_base, smem_u32(sQ(g0 % ST)));
       umma_commit(s_full);
-      mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(0)));
+      mma_ss(tmem + C::tdP, v_base, smem_u32(sdO(g0 % ST)));
       umma_commit(dp_full);
     }
     __syncwarp();
     for (int i = 0; i < P.n_q; ++i) {
-      const int st = i % ST, buf = i & 1;  // Q/dO ring stage; dS / dQ double-buffer parity
-      const uint32_t ph = i & 1;
+      const int g = g0 + i;
+      const int st = g % ST, buf = g & 1;  // Q/dO ring stage; dS / dQ double-buffer parity
+      const uint32_t ph = g & 1;
       const bool more = i + 1 < P.n_q;
-      const int st1 = (i + 1) % ST;
+      const int st1 = (g + 1) % ST;
       mbar_wait(p_full, ph);
+      if (i == 0 && it > 0) mbar_wait(acc_empty, (it - 1) & 1);  // dV / dK of the previous item are read
       BTP_STAMP64(8);
       tc_fence_after();
       if (elect_one()) {  // [3] dV += P^T dO: A = P^T pairs, queries [64g, +64) at TMEM columns [64g, +32)
@@ -1444,7 +1486,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       }
       __syncwarp();
       if (more) {
-        mbar_wait(&qdo_full[st1], ((i + 1) / ST) & 1);
+        mbar_wait(&qdo_full[st1], ((g + 1) / ST) & 1);
         tc_fence_after();
         if (elect_one()) {
           mma_ss(tmem + C::tS, k_base, smem_u32(sQ(st1)));  // [1]_{i+1}
@@ -1474,8 +1516,8 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
         umma_commit(&qdo_empty[st]);
       }
       __syncwarp();
-      if (i >= 2) {
-        mbar_wait(&dq_empty[buf], ((i >> 1) - 1) & 1);
+      if (g >= 2) {
+        mbar_wait(&dq_empty[buf], ((g >> 1) - 1) & 1);
         tc_fence_after();
       }
       BTP_STAMP64(11);
@@ -1487,12 +1529,15 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
                     make_sw128_desc(k_base + k * 2048, kTile * 128, 1024), idesc_dq, k > 0 ? 1u : 0u);
         umma_commit(&dq_full[buf]);
         umma_commit(&sds_empty[buf]);
+        if (!more) umma_commit(kv_empty);  // the item's last MMA on K / V
       }
       __syncwarp();
       BTP_STAMP64(12);
     }
     if (elect_one()) umma_commit(acc_full);
     __syncwarp();
+    if (kTrace && lane == 0) ct[2] = clock64();  // last MMA issued
+    }
   } else if (warp < 10) {
     // ---------------------------------------------------------------- compute warps 2..9
     const uint32_t g = (warp - 2) >> 2;
@@ -1500,11 +1545,15 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
     const uint32_t row = q4 * 32 + lane;  // key row within the tile == TMEM lane
     const uint32_t lane_addr = (q4 * 32) << 16;
     const float2 c2 = make_float2(P.c, P.c);
+    for (int it = 0; it < n_it; ++it) {
+    long long* const tr = (kTrace && blockIdx.x == 0 && it == 0) ? P.trace : nullptr;
+    const Item w = item_of(it);
     for (int i = 0; i < P.n_q; ++i) {
-      const int st = i % ST, buf = i & 1;
-      const uint32_t ph = i & 1;
+      const int gt = it * P.n_q + i;
+      const int st = gt % ST, buf = gt & 1;
+      const uint32_t ph = gt & 1;
       const uint32_t lse_a = smem_u32(sLse(st)) + g * 256, d_a = smem_u32(sD(st)) + g * 256;
-      mbar_wait(&qdo_full[st], (i / ST) & 1);  // lse / D of this query tile are resident
+      mbar_wait(&qdo_full[st], (gt / ST) & 1);  // lse / D of this query tile are resident
       mbar_wait(s_full, ph);
       if (q4 == 2) BTP_STAMP64(4 * g);
       tc_fence_after();
@@ -1546,7 +1595,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       if (q4 == 2) BTP_STAMP64(4 * g + 1);
       mbar_wait(dp_full, ph);
       tc_fence_after();
-      if (i >= 2) mbar_wait(&sds_empty[buf], ((i >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
+      if (gt >= 2) mbar_wait(&sds_empty[buf], ((gt >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
       if (q4 == 2) BTP_STAMP64(4 * g + 2);
       const uint32_t ds_row = smem_u32(sdS + buf * C::kDsBytes) + g * (kTile * 128) + row * 128;
 #pragma unroll
@@ -1585,23 +1634,30 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       if (q4 == 2) BTP_STAMP64(4 * g + 3);
     }
     // ---------------------------------------------------------------- dK / dV epilogue (group 0: dV, 1: dK)
-    mbar_wait(acc_full, 0);
+    if (kTrace && warp == 2 && lane == 0) ct[3] = clock64();  // compute walk done
+    mbar_wait(acc_full, it & 1);
     tc_fence_after();
     const uint32_t tcol = g == 0 ? C::tdV : C::tdK;
     const float sc = g == 0 ? 1.f : P.dk_scale;
-    __nv_bfloat16* out = g == 0 ? P.dv + (long long)(kv_row0 + row) * P.lddv + col0
-                                : P.dk + (long long)(kv_row0 + row) * P.lddk + col0;
+    __nv_bfloat16* out = g == 0 ? P.dv + (long long)(w.kv_row0 + row) * P.lddv + w.col0
+                                : P.dk + (long long)(w.kv_row0 + row) * P.lddk + w.col0;
+    uint32_t o[64];
+    tmem_ld_32x32b_x64(tmem + tcol + lane_addr, o);
+    tmem_ld_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);  // the next item's first dV / dK MMA may overwrite them
 #pragma unroll
     for (int cc = 0; cc < HD / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tmem + tcol + lane_addr + cc * 32, o);
-      tmem_ld_wait();
       uint32_t ok[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) ok[j] = pack_bf16(__uint_as_float(o[2 * j]) * sc, __uint_as_float(o[2 * j + 1]) * sc);
+      for (int j = 0; j < 16; ++j)
+        ok[j] = pack_bf16(__uint_as_float(o[cc * 32 + 2 * j]) * sc, __uint_as_float(o[cc * 32 + 2 * j + 1]) * sc);
 #pragma unroll
       for (int v = 0; v < 4; ++v)
         st_global_v4(out + cc * 32 + v * 8, make_uint4(ok[4 * v], ok[4 * v + 1], ok[4 * v + 2], ok[4 * v + 3]));
+    }
+    if (kTrace && warp == 2 && lane == 0) ct[7] = clock64();  // dK / dV stored
     }
   } else {
     // ---------------------------------------------------------------- dQ reduce warps 10..13
@@ -1611,9 +1667,13 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
     const uint32_t row = q4 * 32 + lane;  // query row within the tile
     const uint32_t lane_addr = (q4 * 32) << 16;
     const bool issuer = (warp == 10 && lane == 0);
+    for (int it = 0; it < n_it; ++it) {
+    long long* const tr = (kTrace && blockIdx.x == 0 && it == 0) ? P.trace : nullptr;
+    const Item w = item_of(it);
     for (int i = 0; i < P.n_q; ++i) {
-      const int buf = i & 1;
-      mbar_wait(&dq_full[buf], (i >> 1) & 1);
+      const int gt = it * P.n_q + i;
+      const int buf = gt & 1;
+      mbar_wait(&dq_full[buf], (gt >> 1) & 1);
       if (q4 == 2) BTP_STAMP64(13);
       tc_fence_after();
       uint32_t o[64];
@@ -1634,15 +1694,20 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (issuer) {
-          tma_reduce_add_2d(&P.tdq, sdQ, col0 + 32 * bx, q_row_base + i * kTile);
+          tma_reduce_add_2d(&P.tdq, sdQ, w.col0 + 32 * bx, w.q_row_base + i * kTile);
           bulk_commit();
         }
       }
     }
+    }
+    if (kTrace && issuer) ct[4] = clock64();
     if (issuer) bulk_wait<0>();
+    if (kTrace && issuer) ct[5] = clock64();
+    __syncwarp();  // the issuer lane rejoins its warp before the final barrier (bar.sync is per warp)
   }
   tc_fence_before();
   __syncthreads();
+  if (kTrace && threadIdx.x == 0) ct[6] = clock64();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -2195,6 +2260,9 @@ int launch_bwd(const BwdParams& P, int b, cudaStream_t stream) {
 
 static int g_bwd_poly = 0;  // every n-th group of 4 exp2s in the backward's P phase: 2 on the FMA pipe (0: none)
 
+static int g_bwd_persist = 1;  // 1 (default): persistent hd-64 backward (one CTA per SM walking the work items;
+                               // 1552 vs 1629 us at the bench shape, scripts/microbench/attn_bwd_variants.py 7)
+
 template <bool kTrace, int kPoly>
 int launch_bwd64_t(const BwdParams& P, int b, cudaStream_t stream) {
   using C = Bwd64Cfg;
@@ -2206,8 +2274,11 @@ int launch_bwd64_t(const BwdParams& P, int b, cudaStream_t stream) {
       return BTP_ERR_CUDA;
     configured = true;
   }
-  dim3 grid(P.s / kTile, P.h, b);
-  attn_bwd64_kernel<kTrace, kPoly><<<grid, C::kThreads, C::kSmem, stream>>>(P);
+  BwdParams Q = P;
+  Q.n_items = P.n_q * P.h * b;
+  const int nsm = num_sms_cached();
+  const int grid = g_bwd_persist && Q.n_items > nsm ? nsm : Q.n_items;
+  attn_bwd64_kernel<kTrace, kPoly><<<grid, C::kThreads, C::kSmem, stream>>>(Q);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
@@ -2325,6 +2396,7 @@ int attn_tune(int key, int value) {
               : key == 4 ? &g_bwd_dry
               : key == 5 ? &g_bwd_diag
               : key == 6 ? &g_fwd_dry
+              : key == 7 ? &g_bwd_persist
                          : nullptr;
   if (slot == nullptr) return -1;
   const int prev = *slot;

@@ -221,6 +221,36 @@ def test_attn_bwd_hd64_kernel_variants(variant, b, s, h):
     assert max(errs.values()) < 2e-2, errs
 
 
+@pytest.mark.parametrize("persist", [1, 0])
+@pytest.mark.parametrize("b,s,h", [(1, 128, 3), (2, 256, 5), (2, 1024, 80), (1, 4096, 2)])
+def test_attn_bwd_hd64_persistent_walk(persist, b, s, h):
+    """The hd-64 backward's persistent walk (btp_attn_tune(7, 1), default: one CTA per SM taking key-tile
+    items x, x + grid, ...) and the one-CTA-per-item grid, vs torch fp32: fewer query tiles than ring
+    stages (s = 128, 256), item counts that do not divide by the grid (2 x 8 x 80 = 1280 items), and
+    fewer items than SMs."""
+    from paper_2512_12131_b200 import _native
+
+    lib = _native.load()
+    hd = 64
+    q, k, v = _inputs(b, s, h, hd, seed=7 * s + h)
+    do = torch.randn(b * s, h * hd, device="cuda").bfloat16()
+    o = torch.empty(b * s, h * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, h, s, device="cuda")
+    K.attn_fwd(q, k, v, o, lse, b=b, s=s, heads=h, head_dim=hd)
+    D = torch.empty(b, h, s, device="cuda")
+    acc = torch.empty(b * s, h * hd, device="cuda")
+    dq, dk, dv = (torch.empty_like(o) for _ in range(3))
+    prev = lib.btp_attn_tune(7, persist)
+    try:
+        K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd)
+        torch.cuda.synchronize()
+    finally:
+        lib.btp_attn_tune(7, prev)
+    rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
+    errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
+    assert max(errs.values()) < 2e-2, errs
+
+
 def test_paper_7b_width_block_native_attention_vs_oracle():
     """CoLA-7B block widths (32 heads of hd 128: the hd-128 forward / backward kernels) with native
     attention inside the BTP block, fwd + bwd vs the float64 oracle."""
