@@ -151,9 +151,12 @@ class ClockSampler:
 def attention_label(attn: str, cfg, args) -> str:
     from paper_2512_12131_b200 import attention as A
 
-    native = attn == "native" or (attn == "auto" and A.AUTO_NATIVE and A.native_supported(args.s, cfg.d // cfg.heads))
-    if native:
+    if attn == "auto":
+        attn = A.auto_backend(args.s, cfg.d // cfg.heads)
+    if attn == "native":
         return "own tcgen05/TMEM flash kernels (btp_attn_fwd / btp_attn_bwd; not a changed subsystem)"
+    if attn == "hybrid":
+        return "cuDNN SDPA forward + own tcgen05/TMEM backward (btp_attn_bwd; not a changed subsystem)"
     return "cuDNN SDPA via torch (not a changed subsystem)"
 
 
@@ -209,7 +212,8 @@ def _attention_ab(b, s, h, hd, reps=10):
             "cudnn": {"fwd_ms": cud_f, "bwd_ms": cud_b, "fwd_tflops": flops / cud_f / 1e9,
                       "bwd_tflops": 2.5 * flops / cud_b / 1e9},
             "native_vs_cudnn_out_rel_err": err,
-            "note": "the step runs cuDNN (--attn native runs ours); profiles/attention/README.md"}
+            "note": "default step (--attn auto at hd 64): cuDNN forward + own backward ('hybrid'); --attn native / "
+                    "cudnn run one implementation both ways; profiles/attention/README.md"}
 
 
 def cpu_oracle_rate(cfg, s, seconds_budget=30.0, max_steps=None, lean=True, optimizer=True):
@@ -803,7 +807,7 @@ def main(argv=None):
                     help="CPU + gloo: launch path, rendezvous and JSON schema only (contract test; no measurement)")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
-    ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native"])
+    ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native", "hybrid"])
     ap.add_argument("--no-attention-ab", action="store_true",
                     help="skip the in-process attention A/B (own kernels vs cuDNN) in the bench line")
     ap.add_argument("--share-gpu", action="store_true",

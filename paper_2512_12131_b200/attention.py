@@ -10,11 +10,17 @@ unmasked softmax(q k^T / sqrt(hd)) v per head with heads as contiguous feature s
 * "cudnn" / "flash": torch's SDPA dispatcher (cuDNN's Blackwell kernels first), with q/k/v passed as
   strided [b, h, s, hd] views of the [T, d] buffers; the backward is one `torch.autograd.grad` over
   the recorded SDPA node.
-"auto" picks "native" where it applies (measured per shape in scripts/microbench/gpu_attn_bench.py),
-else cuDNN. "fp32" is the parity mode (fp32 q/k/v through the exact SDPA kernels).
+* "hybrid": cuDNN's forward (the aten cuDNN SDPA op called directly, with its log-sum-exp, converted to
+  the log2 domain) and this package's tcgen05 backward (faster than cuDNN's at hd 64:
+  profiles/attention/README.md); same shape limits as "native".
+"auto" picks "hybrid" at head_dim 64 (s % 128 == 0), where the own backward is the faster one (the
+bench step: 4.41-4.51 vs 4.57-4.59 ms with cuDNN for both directions on one box), else cuDNN.
+"fp32" is the parity mode (fp32 q/k/v through the exact SDPA kernels).
 """
 
 from __future__ import annotations
+
+import math
 
 import torch
 import torch.nn.functional as F
@@ -54,9 +60,19 @@ def native_supported(s: int, head_dim: int) -> bool:
     return s % 128 == 0 and head_dim in (64, 128)
 
 
-# "auto" resolution: the native kernels where they apply and are the faster choice (set from the
-# measured A/B; scripts/microbench/gpu_attn_bench.py, profiles/README.md)
+# "auto" resolution, from the measured A/B (scripts/microbench/gpu_attn_bench.py, bench.py's
+# attention_ab, profiles/attention/README.md): the native forward is behind cuDNN's, the native hd-64
+# backward ahead of it, the generic hd-128 backward behind it
 AUTO_NATIVE = False
+AUTO_HYBRID = True
+
+
+def auto_backend(s: int, head_dim: int) -> str:
+    if AUTO_NATIVE and native_supported(s, head_dim):
+        return "native"
+    if AUTO_HYBRID and native_supported(s, head_dim) and head_dim == 64:
+        return "hybrid"
+    return "auto"
 
 
 class Attention:
@@ -65,13 +81,14 @@ class Attention:
     def __init__(self, b: int, s: int, heads: int, head_dim: int, backend: str = "auto"):
         self.b, self.s, self.h, self.hd = b, s, heads, head_dim
         self.scale = 1.0 / head_dim**0.5
-        if backend == "auto" and AUTO_NATIVE and native_supported(s, head_dim):
-            backend = "native"
-        if backend == "native" and not native_supported(s, head_dim):
-            raise ValueError(f"native attention needs s % 128 == 0 and head_dim in (64, 128); got s={s}, "
+        if backend == "auto":
+            backend = auto_backend(s, head_dim)
+        if backend in ("native", "hybrid") and not native_supported(s, head_dim):
+            raise ValueError(f"{backend} attention needs s % 128 == 0 and head_dim in (64, 128); got s={s}, "
                              f"head_dim={head_dim}")
+        self.hybrid = backend == "hybrid"
         self.native = backend == "native"
-        self.backends = None if self.native else _BACKENDS[backend]
+        self.backends = None if (self.native or self.hybrid) else _BACKENDS[backend]
         self.stats = None  # the owning executor's ExecStats: native launches are counted there
 
     def _view4(self, t2d: torch.Tensor) -> torch.Tensor:
@@ -94,6 +111,14 @@ class Attention:
             if self.stats is not None:
                 self.stats.kernel_launches += 1
             return out, (q, k, v, out, lse)
+        if self.hybrid:
+            with _Timed(self.timer, "fwd"):
+                res = torch.ops.aten._scaled_dot_product_cudnn_attention(
+                    self._view4(q), self._view4(k), self._view4(v), None, True, 0.0, False, False, scale=self.scale)
+                # cuDNN's natural-log lse of the scaled scores -> the native backward's log2 domain
+                lse = (res[1].reshape(self.b, self.h, self.s) * (1.0 / math.log(2.0))).contiguous()
+                out = self._as2d(res[0])
+            return out, (q, k, v, out, lse)
         q4, k4, v4 = (self._view4(t).detach().requires_grad_(need_grad) for t in (q, k, v))
         with torch.enable_grad() if need_grad else torch.no_grad(), sdpa_kernel(self.backends, set_priority=True), \
                 _Timed(self.timer, "fwd"):
@@ -101,7 +126,7 @@ class Attention:
         return self._as2d(out.detach()), (q4, k4, v4, out)
 
     def backward(self, dout: torch.Tensor, ctx):
-        if self.native:
+        if self.native or self.hybrid:
             q, k, v, out, lse = ctx
             T, W = self.b * self.s, self.h * self.hd
             dq, dk, dv = (torch.empty(T, W, device=q.device, dtype=torch.bfloat16) for _ in range(3))

@@ -132,6 +132,48 @@ def test_block_step_native_attention_vs_oracle(grouping):
     assert errs[worst] < BF16_TOL, errs
 
 
+@pytest.mark.parametrize("grouping", [True])
+def test_block_step_hybrid_attention_vs_oracle(grouping):
+    """The same block with the "hybrid" attention (cuDNN forward + its log-sum-exp converted to log2,
+    then the native tcgen05 backward) against the float64 oracle."""
+    from paper_2512_12131_b200.api import train_step
+    from paper_2512_12131_b200.model import RunShape, Variant
+    from paper_2512_12131_b200.plan import Strategy, plan
+    from tests.gpu_util import BF16_TOL, C60M, inputs, oracle_step, rel
+
+    b, s = 2, 256
+    blk, x, G, oblk = inputs(C60M, Variant.COLA, b, s)
+    pl = plan(Strategy.BOTTLENECK, C60M, RunShape(b, s, 1), Variant.COLA, online_norm=True, grouping=grouping)
+    st = train_step(pl, blk, x, G, attn_backend="hybrid")
+    torch.cuda.synchronize()
+    assert st.executor.attn.hybrid
+    y_ref, g_ref, _, _ = oracle_step(oblk, x, G, C60M, b, s)
+    errs = {"y": rel(st.y.values, y_ref), "dx": rel(st.dx, g_ref["dx"])}
+    for n in g_ref["A"]:
+        errs[f"A_{n}"] = rel(st.grads["A"][n], g_ref["A"][n])
+        errs[f"B_{n}"] = rel(st.grads["B"][n], g_ref["B"][n])
+    worst = max(errs, key=errs.get)
+    assert errs[worst] < BF16_TOL, errs
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+@pytest.mark.parametrize("b,s,h", [(1, 256, 3), (2, 1024, 4)])
+def test_hybrid_attention_matches_fp32(b, s, h, hd):
+    """Attention(backend="hybrid") forward + backward against torch fp32 autograd."""
+    from paper_2512_12131_b200.attention import Attention
+
+    q, k, v = _inputs(b, s, h, hd, scale=1.5, seed=31 * s + h)
+    do = torch.randn(b * s, h * hd, device="cuda").bfloat16()
+    att = Attention(b, s, h, hd, "hybrid")
+    out, ctx = att.forward(q, k, v)
+    dq, dk, dv = att.backward(do, ctx)
+    torch.cuda.synchronize()
+    o_ref, _ = _ref(q, k, v, b, s, h, hd)
+    rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
+    errs = {"o": _rel(out, o_ref), "dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
+    assert max(errs.values()) < 2e-2, errs
+
+
 def test_native_attention_rejects_unsupported_shapes():
     from paper_2512_12131_b200.attention import Attention
 
@@ -139,6 +181,8 @@ def test_native_attention_rejects_unsupported_shapes():
         Attention(1, 100, 2, 64, "native")
     with pytest.raises(ValueError):
         Attention(1, 128, 2, 32, "native")
+    with pytest.raises(ValueError):
+        Attention(1, 100, 2, 64, "hybrid")
 
 
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])

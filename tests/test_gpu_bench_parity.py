@@ -21,7 +21,7 @@ from tests.gpu_util import BF16_TOL, inputs, rel
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("attn", ["auto", "native"])
+@pytest.mark.parametrize("attn", ["cudnn", "native", "hybrid"])
 @pytest.mark.parametrize("b,s", [(4, 4096)])
 def test_bench_config_block_vs_oracle(b, s, attn):
     cfg = preset("1b")

@@ -284,7 +284,7 @@ def test_btp_tp8_fp32_boundary_margin(cfg_name, bs):
     assert worst[top] < 1.7e-2, worst
 
 
-@pytest.mark.parametrize("attn", ["auto", "native"])
+@pytest.mark.parametrize("attn", ["cudnn", "native", "hybrid"])
 def test_btp_tp2_attention_backends_match_oracle(attn):
     """TP = 2 (two processes, gloo) at s = 128 with cuDNN ("auto") and with the native attention
     kernels on each rank's heads (2 of 4), fwd + bwd vs the float64 oracle sliced per rank. The loss
