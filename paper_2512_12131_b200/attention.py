@@ -87,6 +87,7 @@ class Attention:
             raise ValueError(f"{backend} attention needs s % 128 == 0 and head_dim in (64, 128); got s={s}, "
                              f"head_dim={head_dim}")
         self.hybrid = backend == "hybrid"
+        self._hybrid_fallback = False
         self.native = backend == "native"
         self.backends = None if (self.native or self.hybrid) else _BACKENDS[backend]
         self.stats = None  # the owning executor's ExecStats: native launches are counted there
@@ -111,13 +112,29 @@ class Attention:
             if self.stats is not None:
                 self.stats.kernel_launches += 1
             return out, (q, k, v, out, lse)
-        if self.hybrid:
+        if self.hybrid and not self._hybrid_fallback:
+            try:
+                with _Timed(self.timer, "fwd"):
+                    res = torch.ops.aten._scaled_dot_product_cudnn_attention(
+                        self._view4(q), self._view4(k), self._view4(v), None, True, 0.0, False, False,
+                        scale=self.scale)
+                    # cuDNN's natural-log lse of the scaled scores -> the native backward's log2 domain
+                    lse = (res[1].reshape(self.b, self.h, self.s) * (1.0 / math.log(2.0))).contiguous()
+                    out = self._as2d(res[0])
+                return out, (q, k, v, out, lse)
+            except RuntimeError as exc:  # no cuDNN SDPA for this build / device: our forward from now on
+                import warnings
+
+                warnings.warn(f"cuDNN SDPA forward unavailable ({exc}); hybrid attention uses btp_attn_fwd")
+                self._hybrid_fallback = True
+        if self.hybrid:  # fallback: the native forward (its lse is already in the backward's layout)
+            T = self.b * self.s
+            out = torch.empty(T, self.h * self.hd, device=q.device, dtype=torch.bfloat16)
+            lse = torch.empty(self.b, self.h, self.s, device=q.device, dtype=torch.float32)
             with _Timed(self.timer, "fwd"):
-                res = torch.ops.aten._scaled_dot_product_cudnn_attention(
-                    self._view4(q), self._view4(k), self._view4(v), None, True, 0.0, False, False, scale=self.scale)
-                # cuDNN's natural-log lse of the scaled scores -> the native backward's log2 domain
-                lse = (res[1].reshape(self.b, self.h, self.s) * (1.0 / math.log(2.0))).contiguous()
-                out = self._as2d(res[0])
+                K.attn_fwd(q, k, v, out, lse, b=self.b, s=self.s, heads=self.h, head_dim=self.hd)
+            if self.stats is not None:
+                self.stats.kernel_launches += 1
             return out, (q, k, v, out, lse)
         q4, k4, v4 = (self._view4(t).detach().requires_grad_(need_grad) for t in (q, k, v))
         with torch.enable_grad() if need_grad else torch.no_grad(), sdpa_kernel(self.backends, set_priority=True), \
