@@ -358,7 +358,7 @@ int btp_attn_fwd_trace(const void* q, long long ldq, const void* k, long long ld
  * s % 256 == 0; 3 = split rows, one S buffer, two CTAs per SM; 2 / 1 = split rows, double-buffered S, 4 / 2
  * key groups; 0 = single S buffer, two CTAs per SM; hd 64 and s % 256 == 0 only: 5 = two query tiles with P in
  * its own TMEM columns, 6 = the same with each row split over two warps); key 2: in the hd-64 backward's P phase, every n-th group of four exp2s has two
- * on the FMA pipe (n in {0 = none, 1, 2, 4}); key 3: hd-64 backward kernel (0 = the same 8 warps for P
+ * on the FMA pipe (n in {0 = none, 1, 2 = default, 4}); key 3: hd-64 backward kernel (0 = the same 8 warps for P
  * and dS, default; 1 = split roles: P warps, alternating dS warp groups, dQ-reduce warps); keys 4 / 5:
  * diagnostics of the split-role kernel (WRONG results; 4: handshakes only, 5: bit 0 no dS stores, bit 1
  * no proxy fence, bit 2 no lse / D loads); key 6: forward diagnostics (split-row variants, WRONG results:

@@ -2258,7 +2258,8 @@ int launch_bwd(const BwdParams& P, int b, cudaStream_t stream) {
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
-static int g_bwd_poly = 0;  // every n-th group of 4 exp2s in the backward's P phase: 2 on the FMA pipe (0: none)
+static int g_bwd_poly = 2;  // every n-th group of 4 exp2s in the backward's P phase: 2 on the FMA pipe (0: none);
+                            // 2 (default): 1748 vs 1819 us median under sustained load, same cold (r02_bwd_poly_ab.log)
 
 static int g_bwd_persist = 1;  // 1 (default): persistent hd-64 backward (one CTA per SM walking the work items;
                                // 1552 vs 1629 us at the bench shape, scripts/microbench/attn_bwd_variants.py 7)

@@ -265,11 +265,13 @@ def test_attn_bwd_hd64_kernel_variants(variant, b, s, h):
     assert max(errs.values()) < 2e-2, errs
 
 
+@pytest.mark.parametrize("poly", [2, 0])
 @pytest.mark.parametrize("persist", [1, 0])
 @pytest.mark.parametrize("b,s,h", [(1, 128, 3), (2, 256, 5), (2, 1024, 80), (1, 4096, 2)])
-def test_attn_bwd_hd64_persistent_walk(persist, b, s, h):
+def test_attn_bwd_hd64_persistent_walk(persist, b, s, h, poly):
     """The hd-64 backward's persistent walk (btp_attn_tune(7, 1), default: one CTA per SM taking key-tile
-    items x, x + grid, ...) and the one-CTA-per-item grid, vs torch fp32: fewer query tiles than ring
+    items x, x + grid, ...) and the one-CTA-per-item grid, with and without the polynomial exp2 share
+    (btp_attn_tune(2, 2), default), vs torch fp32: fewer query tiles than ring
     stages (s = 128, 256), item counts that do not divide by the grid (2 x 8 x 80 = 1280 items), and
     fewer items than SMs."""
     from paper_2512_12131_b200 import _native
@@ -284,12 +286,13 @@ def test_attn_bwd_hd64_persistent_walk(persist, b, s, h):
     D = torch.empty(b, h, s, device="cuda")
     acc = torch.empty(b * s, h * hd, device="cuda")
     dq, dk, dv = (torch.empty_like(o) for _ in range(3))
-    prev = lib.btp_attn_tune(7, persist)
+    prev, prev_p = lib.btp_attn_tune(7, persist), lib.btp_attn_tune(2, poly)
     try:
         K.attn_bwd(q, k, v, o, do, lse, D, acc, dq, dk, dv, b=b, s=s, heads=h, head_dim=hd)
         torch.cuda.synchronize()
     finally:
         lib.btp_attn_tune(7, prev)
+        lib.btp_attn_tune(2, prev_p)
     rq, rk, rv = _ref_bwd(q, k, v, do, b, s, h, hd)
     errs = {"dq": _rel(dq, rq), "dk": _rel(dk, rk), "dv": _rel(dv, rv)}
     assert max(errs.values()) < 2e-2, errs
