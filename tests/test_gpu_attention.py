@@ -157,7 +157,7 @@ def test_block_step_hybrid_attention_vs_oracle(grouping):
 
 
 @pytest.mark.parametrize("hd", [64, 128])
-@pytest.mark.parametrize("b,s,h", [(1, 256, 3), (2, 1024, 4)])
+@pytest.mark.parametrize("b,s,h", [(1, 256, 3), (2, 1024, 4), (3, 384, 5)])
 def test_hybrid_attention_matches_fp32(b, s, h, hd):
     """Attention(backend="hybrid") forward + backward against torch fp32 autograd."""
     from paper_2512_12131_b200.attention import Attention
@@ -267,13 +267,14 @@ def test_attn_bwd_hd64_kernel_variants(variant, b, s, h):
 
 @pytest.mark.parametrize("poly", [2, 0])
 @pytest.mark.parametrize("persist", [1, 0])
-@pytest.mark.parametrize("b,s,h", [(1, 128, 3), (2, 256, 5), (2, 1024, 80), (1, 4096, 2)])
+@pytest.mark.parametrize("b,s,h", [(1, 128, 3), (2, 256, 5), (3, 384, 7), (2, 640, 33), (2, 1024, 80), (1, 4096, 2)])
 def test_attn_bwd_hd64_persistent_walk(persist, b, s, h, poly):
     """The hd-64 backward's persistent walk (btp_attn_tune(7, 1), default: one CTA per SM taking key-tile
     items x, x + grid, ...) and the one-CTA-per-item grid, with and without the polynomial exp2 share
-    (btp_attn_tune(2, 2), default), vs torch fp32: fewer query tiles than ring
-    stages (s = 128, 256), item counts that do not divide by the grid (2 x 8 x 80 = 1280 items), and
-    fewer items than SMs."""
+    (btp_attn_tune(2, 2), default), vs torch fp32: fewer query tiles than ring stages (s = 128, 256),
+    an odd number of query tiles per item (s = 384, 640: the per-item phase parity alternates), item
+    counts that do not divide by the grid (2 x 8 x 80 = 1280, 2 x 5 x 33 = 330 items), and fewer items
+    than SMs."""
     from paper_2512_12131_b200 import _native
 
     lib = _native.load()
