@@ -657,6 +657,23 @@ def run_ours(args, cfg):
     gms = (gemm.get("back_to_back") or gemm)["ms"]
     breakdown = {"gemm_ms": gms, "attention_fwd_ms": att.get("fwd"), "attention_bwd_ms": att.get("bwd"),
                  "other_ms": ms - gms - sum(v for v in att.values() if v)}
+    # the attention backward, the step's other large kernel when it is ours (native / hybrid at hd 64):
+    # algorithmic FLOPs = its five GEMM-shaped products, 5 x 2 b h s^2 hd, over its in-step time
+    roof_att = None
+    hd_ = cfg.d // cfg.heads
+    from paper_2512_12131_b200.attention import auto_backend
+
+    att_backend = args.attn if args.attn != "auto" else auto_backend(s, hd_)
+    if att.get("bwd") and att_backend in ("native", "hybrid"):
+        fl_att = 10 * b * (cfg.heads // tp) * s * s * hd_
+        ach_att = fl_att / (att["bwd"] * 1e-3) / 1e12
+        roof_att = {"bound": "tensor", "kernel": "btp_attn_bwd (D / zero prep + persistent tcgen05 walk + dQ convert)",
+                    "achieved": ach_att, "peak": peak_sus, "unit": "TFLOP/s", "frac": ach_att / peak_sus,
+                    "algorithmic_flops_per_launch": fl_att, "ms_in_step": att["bwd"],
+                    "ceiling": ("hd 64: the N = 64 products (dV, dK, dQ) run at half the M128 tcgen05 rate, so the "
+                                "MMA issue floor is ~2160 cycles per (key, query) tile pair, ~0.97 ms at the bench "
+                                "shape (~1.4 PF/s, about this measured peak); the exp2 floor (MUFU 16/clk/SM) is "
+                                "~0.46 ms (profiles/attention/README.md)")}
     graphed = trainer.graphed
     del trainer, x_dev, g_dev, xh, xh2, gh
     if not args.dry_run:
@@ -721,6 +738,7 @@ def run_ours(args, cfg):
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": roof,
+        **({"roofline_attention_bwd": roof_att} if roof_att else {}),
         "algorithmic_tflops_per_gpu": flops / (ms / 1e3) / 1e12,
         "breakdown": breakdown,
     }
