@@ -284,6 +284,53 @@ def test_btp_tp8_fp32_boundary_margin(cfg_name, bs):
     assert worst[top] < 1.7e-2, worst
 
 
+@pytest.mark.parametrize("cfg_name,bs", [("C60M", (2, 128)), ("P7B", (1, 256))])
+@pytest.mark.parametrize("bdt", ["bf16", "fp32"])
+def test_btp_tp8_whole_tensor_margin(cfg_name, bs, bdt):
+    """TP = 8, errors of the WHOLE gradient tensors (the north_star's "within 2e-2 relative on
+    gradients"): the relative Frobenius error of the concatenated per-rank shards,
+    sqrt(sum_r |got_r - ref_r|^2) / sqrt(sum_r |ref_r|^2). The per-shard worst case (above) is a
+    stricter statistic: a TP=8 rank's d-shard of dgamma2 is only d/8 = 64 elements at C60M, so its
+    relative error is a noisy small-sample estimate of the same per-element error."""
+    from tests import gpu_util
+    from tests.gpu_util import inputs, oracle_step
+    from oracle import btp_oracle as O
+    from paper_2512_12131_b200.model import Variant
+
+    cfg = getattr(gpu_util, cfg_name)
+    b, s = bs
+    world = 8
+    res = _run_tp2("btp", True, True, False, world=world, cfg_name=cfg_name, bs=(b, s), bdt=bdt)
+    blk, x, G, oblk = inputs(cfg, Variant.COLA, b, s)
+    y_ref, g_ref, _, loss_ref = oracle_step(oblk, x, G, cfg, b, s, tp=world, sharded=False)
+    num, den, shard_worst = {}, {}, {}
+
+    def acc(key, got, want):
+        got = np.asarray(got, dtype=np.float64).reshape(np.shape(want))
+        want = np.asarray(want, dtype=np.float64)
+        e, w = float(np.sum((got - want) ** 2)), float(np.sum(want ** 2))
+        num[key] = num.get(key, 0.0) + e
+        den[key] = den.get(key, 0.0) + w
+        shard_worst[key] = max(shard_worst.get(key, 0.0), (e / max(w, 1e-300)) ** 0.5)
+
+    for rank, (_, y, loss, dx, grads, *_r) in res.items():
+        gr = O.grads_for_rank(g_ref, world, rank, cfg.d, cfg.d_ff)
+        if rank == 0:
+            acc("y", y.reshape(-1, cfg.d), y_ref)  # y is gathered on every rank
+        acc("dx", dx, gr["dx"])
+        acc("g1", grads["gamma1"], gr["dgamma1"])
+        acc("g2", grads["gamma2"], gr["dgamma2"])
+        for n in O.PROJECTIONS:
+            acc("A_" + n, grads["A"][n], gr["A"][n])
+            acc("B_" + n, grads["B"][n], gr["B"][n])
+    whole = {k: (num[k] / max(den[k], 1e-300)) ** 0.5 for k in num}
+    top, stop = max(whole, key=whole.get), max(shard_worst, key=shard_worst.get)
+    print(f"{cfg_name} TP=8 {bdt} boundaries: whole-tensor worst {top} = {whole[top]:.3e}; "
+          f"per-shard worst {stop} = {shard_worst[stop]:.3e}; whole g2 = {whole['g2']:.3e}")
+    assert whole[top] < 1.5e-2, whole
+    assert shard_worst[stop] < 2e-2, shard_worst
+
+
 @pytest.mark.parametrize("attn", ["cudnn", "native", "hybrid"])
 def test_btp_tp2_attention_backends_match_oracle(attn):
     """TP = 2 (two processes, gloo) at s = 128 with cuDNN ("auto") and with the native attention
