@@ -572,6 +572,10 @@ def run_ours(args, cfg):
             from paper_2512_12131_b200 import kernels as _K
 
             _K.set_res4(args.gemm_res)
+        if args.attn_bwd_variant >= 0:
+            from paper_2512_12131_b200 import _native as _N
+
+            _N.load().btp_attn_tune(3, args.attn_bwd_variant)
     from paper_2512_12131_b200.model import RunShape, Variant
     from paper_2512_12131_b200.plan import Strategy
 
@@ -826,6 +830,9 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--dump-gemms", default="", help="write per-launch GEMM timings (JSON) to this path")
     ap.add_argument("--attn", default="auto", choices=["auto", "cudnn", "flash", "native", "hybrid"])
+    ap.add_argument("--attn-bwd-variant", type=int, default=-1, choices=[-1, 0, 1, 2],
+                    help="hd-64 attention backward kernel (btp_attn_tune key 3): 0 shared warps, 1 split roles, "
+                         "2 shared warps with the packed-P dS phase (A/B)")
     ap.add_argument("--no-attention-ab", action="store_true",
                     help="skip the in-process attention A/B (own kernels vs cuDNN) in the bench line")
     ap.add_argument("--share-gpu", action="store_true",

@@ -1317,7 +1317,11 @@ struct Bwd64Cfg {
   static constexpr uint32_t tS = 0, tdP = 128, tdV = 256, tdK = 320, tdQ = 384;  // dQ: 384 / 448
 };
 
-template <bool kTrace, int kPoly>
+// kPk (btp_attn_tune(3, 2)): the dS phase computes P^T (dP^T - D) from the bf16 P^T pairs the P phase
+// already packed for the dV MMA (32 registers instead of 64 fp32), so the whole 64-column dP^T block
+// fits in registers at once: ONE x64 TMEM load, and dp_read (which gates the next tile's dP^T MMA)
+// arrives before any dS math instead of after the first 32-column half.
+template <bool kTrace, int kPoly, bool kPk = false>
 __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constant__ BwdParams P) {
   using C = Bwd64Cfg;
   constexpr int HD = 64, ST = C::ST;
@@ -1559,11 +1563,11 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       tc_fence_after();
       // P^T in fp32 registers for dS below; its bf16 pairs go to TMEM for the dV MMA
       float pv[64];
+      uint32_t pk[32];
       tmem_ld_32x32b_x64(tmem + C::tS + lane_addr + g * 64, *reinterpret_cast<uint32_t(*)[64]>(&pv[0]));
       tmem_ld_wait();
       if (q4 == 2 && g == 0) BTP_STAMP64(14);
       {
-        uint32_t pk[32];
 #pragma unroll
         for (int m = 0; m < 64; m += 4) {
           const float4 l4 = ld_shared_f4(lse_a + m * 4);
@@ -1598,6 +1602,33 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
       if (gt >= 2) mbar_wait(&sds_empty[buf], ((gt >> 1) - 1) & 1);  // dQ_{i-2} has read this dS buffer
       if (q4 == 2) BTP_STAMP64(4 * g + 2);
       const uint32_t ds_row = smem_u32(sdS + buf * C::kDsBytes) + g * (kTile * 128) + row * 128;
+      if constexpr (kPk) {
+        uint32_t dp[64];
+        tmem_ld_32x32b_x64(tmem + C::tdP + lane_addr + g * 64, dp);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_read);  // the next tile's dP^T MMA may overwrite the block now
+#pragma unroll
+        for (int unit = 0; unit < 8; ++unit) {  // 8 queries per 16-byte unit
+          uint32_t ds[4];
+#pragma unroll
+          for (int j = 0; j < 8; j += 4) {
+            const int m = unit * 8 + j;
+            const float4 d4 = ld_shared_f4(d_a + m * 4);
+            const float2 p01 = make_float2(__uint_as_float(pk[m / 2] << 16), __uint_as_float(pk[m / 2] & 0xffff0000u));
+            const float2 p23 =
+                make_float2(__uint_as_float(pk[m / 2 + 1] << 16), __uint_as_float(pk[m / 2 + 1] & 0xffff0000u));
+            const float2 a01 = fmul2(p01, fadd2(make_float2(__uint_as_float(dp[m]), __uint_as_float(dp[m + 1])),
+                                                make_float2(-d4.x, -d4.y)));
+            const float2 a23 = fmul2(p23, fadd2(make_float2(__uint_as_float(dp[m + 2]), __uint_as_float(dp[m + 3])),
+                                                make_float2(-d4.z, -d4.w)));
+            ds[j / 2] = pack_bf16(a01.x, a01.y);
+            ds[j / 2 + 1] = pack_bf16(a23.x, a23.y);
+          }
+          st_shared_v4(ds_row + ((unit ^ (row & 7)) << 4), ds[0], ds[1], ds[2], ds[3]);
+        }
+      } else {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {  // 32 queries per half
         uint32_t dp[32];
@@ -1627,6 +1658,7 @@ __global__ void __launch_bounds__(448, 1) attn_bwd64_kernel(const __grid_constan
           const uint32_t unit = hh * 4 + u;
           st_shared_v4(ds_row + ((unit ^ (row & 7)) << 4), ds[0], ds[1], ds[2], ds[3]);
         }
+      }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -2264,13 +2296,13 @@ static int g_bwd_poly = 2;  // every n-th group of 4 exp2s in the backward's P p
 static int g_bwd_persist = 1;  // 1 (default): persistent hd-64 backward (one CTA per SM walking the work items;
                                // 1552 vs 1629 us at the bench shape, scripts/microbench/attn_bwd_variants.py 7)
 
-template <bool kTrace, int kPoly>
+template <bool kTrace, int kPoly, bool kPk>
 int launch_bwd64_t(const BwdParams& P, int b, cudaStream_t stream) {
   using C = Bwd64Cfg;
   static_assert(C::kSmem <= 232448, "shared memory budget");
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attn_bwd64_kernel<kTrace, kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(attn_bwd64_kernel<kTrace, kPoly, kPk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmem) != cudaSuccess)
       return BTP_ERR_CUDA;
     configured = true;
@@ -2279,21 +2311,22 @@ int launch_bwd64_t(const BwdParams& P, int b, cudaStream_t stream) {
   Q.n_items = P.n_q * P.h * b;
   const int nsm = num_sms_cached();
   const int grid = g_bwd_persist && Q.n_items > nsm ? nsm : Q.n_items;
-  attn_bwd64_kernel<kTrace, kPoly><<<grid, C::kThreads, C::kSmem, stream>>>(Q);
+  attn_bwd64_kernel<kTrace, kPoly, kPk><<<grid, C::kThreads, C::kSmem, stream>>>(Q);
   return cudaGetLastError() == cudaSuccess ? BTP_OK : BTP_ERR_CUDA;
 }
 
-template <bool kTrace>
+template <bool kTrace, bool kPk>
 int launch_bwd64_p(const BwdParams& P, int b, cudaStream_t stream) {
   switch (g_bwd_poly) {
-    case 1: return launch_bwd64_t<kTrace, 1>(P, b, stream);
-    case 2: return launch_bwd64_t<kTrace, 2>(P, b, stream);
-    case 4: return launch_bwd64_t<kTrace, 4>(P, b, stream);
-    default: return launch_bwd64_t<kTrace, 0>(P, b, stream);
+    case 1: return launch_bwd64_t<kTrace, 1, kPk>(P, b, stream);
+    case 2: return launch_bwd64_t<kTrace, 2, kPk>(P, b, stream);
+    case 4: return launch_bwd64_t<kTrace, 4, kPk>(P, b, stream);
+    default: return launch_bwd64_t<kTrace, 0, kPk>(P, b, stream);
   }
 }
 
-static int g_bwd_variant = 0;  // 1: split-role hd-64 kernel (attn_bwd64s_kernel), 0: attn_bwd64_kernel (default)
+static int g_bwd_variant = 0;  // 1: split-role hd-64 kernel (attn_bwd64s_kernel), 0: attn_bwd64_kernel (default),
+                               // 2: attn_bwd64_kernel with the packed-P dS phase (kPk)
 static int g_bwd_dry = 0;      // diagnostics: handshakes only in the split-role kernel (wrong results)
 static int g_bwd_diag = 0;     // diagnostics: BwdParams::diag bits (wrong results)
 
@@ -2317,7 +2350,9 @@ int launch_bwd64s(const BwdParams& P, int b, cudaStream_t stream) {
 
 int launch_bwd64(const BwdParams& P, int b, cudaStream_t stream) {
   if (g_bwd_variant == 1) return launch_bwd64s(P, b, stream);
-  return P.trace != nullptr ? launch_bwd64_p<true>(P, b, stream) : launch_bwd64_p<false>(P, b, stream);
+  if (g_bwd_variant == 2)
+    return P.trace != nullptr ? launch_bwd64_p<true, true>(P, b, stream) : launch_bwd64_p<false, true>(P, b, stream);
+  return P.trace != nullptr ? launch_bwd64_p<true, false>(P, b, stream) : launch_bwd64_p<false, false>(P, b, stream);
 }
 
 template <int HD, int ST, int kPoly, int kSplit, int kSBuf = 2, int kQT = 1>
