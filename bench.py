@@ -560,6 +560,8 @@ def run_ours(args, cfg):
             _executor.FUSE_SIGMA = False
         if args.concurrent_wgrad:
             _executor.ExecutorBase.concurrent_wgrad = True
+        if args.no_merge_bwd_gemms:
+            _executor.ExecutorBase.merge_bwd_gemms = False
         if args.gemm_pair >= 0:
             from paper_2512_12131_b200 import kernels as _K
 
@@ -633,13 +635,17 @@ def run_ours(args, cfg):
     if args.model:  # L blocks (sharded) + the replicated head: 3 * 2 T d V on every rank
         flops = flops * trainer.ex.blocks.__len__() + 3 * 2 * b * s * cfg.d * args.vocab
     traffic, traffic_src = None, None
-    tfile = ROOT / "profiles" / "r02_gemm_traffic_summary.json"
-    if not tfile.exists():
-        tfile = ROOT / "profiles" / "r01_gemm_traffic_summary.json"
-    if tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model:
-        t = json.loads(tfile.read_text())
-        traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
     b2b = gemm.get("back_to_back") or gemm
+    # ncu DRAM bytes of the step's GEMM launches (one capture per launch structure; the newest whose
+    # launch count matches this step's, else none)
+    for name in ("r02m_gemm_traffic_summary.json", "r02_gemm_traffic_summary.json", "r01_gemm_traffic_summary.json"):
+        tfile = ROOT / "profiles" / name
+        if not (tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model):
+            continue
+        t = json.loads(tfile.read_text())
+        if t.get("launches") == b2b.get("launches"):
+            traffic, traffic_src = t["dram_bytes_per_launch_avg"], t["source"]
+            break
     g_ms = b2b["ms"] or float("nan")
     # achieved = the step's GEMM launches replayed back to back (one graph, two CUDA events): each
     # kernel's own device time plus the graph's inter-kernel gap; the per-launch event brackets
@@ -823,6 +829,8 @@ def main(argv=None):
                     help="residual-epilogue layout: 0 per-chunk, 1 whole tile, 2 producer-warp pipeline, "
                          "3 by width (default) (A/B)")
     ap.add_argument("--concurrent-wgrad", action="store_true", help="weight-gradient GEMMs on a side stream (A/B)")
+    ap.add_argument("--no-merge-bwd-gemms", action="store_true",
+                    help="launch each backward dgrad and its weight gradient separately (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true", help="skip the naive-TP / full-rank same-box arms")
     ap.add_argument("--dry-run", action="store_true",

@@ -99,6 +99,25 @@ def _pick_splits(tiles: int, k_blocks: int, units: int) -> int:
     return best
 
 
+def _pick_splits_behind(ahead_kb: list, w_tiles: int, k_blocks: int, units: int) -> int:
+    """Split-K factor for weight-gradient tiles launched BEHIND other tiles in the same persistent
+    launch (ahead_kb: k-blocks of each tile ahead, in launch order). Tiles go round-robin to the CTA
+    pairs; the launch takes the busiest pair's sum of (k-blocks + ~5) per tile (the _pick_splits
+    model, with heterogeneous tiles)."""
+    best, best_cost = 1, None
+    for s in range(1, 17):
+        kb = -(-k_blocks // s)
+        if s > 1 and kb < 4:
+            break
+        loads = [0] * units
+        for j, c in enumerate(list(ahead_kb) + [kb] * (w_tiles * s)):
+            loads[j % units] += c + 5
+        cost = max(loads)
+        if best_cost is None or cost < best_cost:
+            best, best_cost = s, cost
+    return best
+
+
 @dataclass
 class StepStats:
     gemm_launches: int = 0
@@ -304,6 +323,37 @@ class ExecutorBase:
         with torch.cuda.stream(side):
             self._wgrad_now(pairs, col_scale)
         self._side_pending = True
+
+    # With no collective to start between them and no side stream, a dgrad and its chunk's
+    # independent weight gradient(s) go out as ONE grouped launch (<= 4 problems): the weight-gradient
+    # split tiles fill the dgrad's last wave and one launch's prologue / pipeline fill / drain is
+    # saved. (_up_bwd merges only without live collectives: there the boundary all-reduce of the
+    # dgrad output starts before the weight gradient and overlaps it.) `merge_bwd_gemms = False`
+    # restores two launches (A/B).
+    merge_bwd_gemms = True
+
+    def _dgrad_wgrad(self, dgrad_probs, pairs, col_scale=None):
+        """dgrad problem(s) then the weight gradient(s) of `pairs` (see _wgrad_now), merged into one
+        launch when nothing needs the dgrad output early."""
+        if not self.merge_bwd_gemms or self.concurrent_wgrad or len(dgrad_probs) + len(pairs) > 4:
+            self._gemm(*dgrad_probs)
+            self._wgrad(pairs, col_scale)
+            return
+        units = max(self.sms // 2, 1)
+        ahead = []
+        for p in dgrad_probs:
+            M = p.a.shape[1] if p.a_mn else p.a.shape[0]
+            Kd = p.a.shape[0] if p.a_mn else p.a.shape[1]
+            N = p.b.shape[1] if p.b_mn else p.b.shape[0]
+            ahead += [(Kd + 63) // 64] * (math.ceil(M / 256) * math.ceil(N / 256))
+        T = pairs[0][0].shape[0]
+        w_tiles = sum(math.ceil(dy.shape[1] / 256) * math.ceil(x.shape[1] / 256) for dy, x, _ in pairs)
+        splits = _pick_splits_behind(ahead, w_tiles, (T + 63) // 64, units)
+        if splits > 1:
+            for _, _, o in pairs:
+                K.zero(o)
+        self._gemm(*dgrad_probs, *[K.Gemm(dy, x, o, a_mn=True, b_mn=True, splits=splits, col_scale=col_scale)
+                                   for dy, x, o in pairs])
 
     def _wgrad_now(self, pairs, col_scale=None):
         """pairs: list of (dY [T, M] (MN-major A), X [T, N] (MN-major B), out fp32 [M, N]).
@@ -906,7 +956,10 @@ class BTPBlockExecutor(ExecutorBase):
         zP is the stored z (= all-reduce buffer of the forward): [T, k*r] grouped, [k, T, r] not."""
         if self.peer is not None:
             return self._up_bwd_peer(names, dgrad_probs, wgrad_pairs, zP, s, dss_name)
-        if self.grouping or len(dgrad_probs) == 1:
+        if (self.grouping or len(dgrad_probs) == 1) and not self.comm.live:
+            self._dgrad_wgrad(dgrad_probs, wgrad_pairs)  # no-op collective below: one launch when it fits
+            wgrad_pairs = None
+        elif self.grouping or len(dgrad_probs) == 1:
             self._gemm(*dgrad_probs)
         else:
             for p in dgrad_probs:
@@ -916,7 +969,8 @@ class BTPBlockExecutor(ExecutorBase):
             handles = [self.comm.all_reduce_start(da_P, names[0] if k == 1 else self._gid(names))]
         else:
             handles = [self.comm.all_reduce_start(da_P[i], nm) for i, nm in enumerate(names)]
-        self._wgrad(wgrad_pairs)
+        if wgrad_pairs is not None:
+            self._wgrad(wgrad_pairs)
         for h in handles:
             self.comm.wait(h)
         return self._sigma_bwd(names, da_P, zP, s, dss_name)
@@ -1009,8 +1063,7 @@ class BTPBlockExecutor(ExecutorBase):
         T, dl, r, k = self.T, self.dl, self.r, len(names)
         dh = self.buf("dh", (T, dl))
         if self.grouping or k == 1:
-            self._gemm(K.Gemm(dP, W, dh, b_mn=True))
-            self._wgrad([(dP, x_res, self.grad[grad_key])], col_scale=gamma)
+            self._dgrad_wgrad([K.Gemm(dP, W, dh, b_mn=True)], [(dP, x_res, self.grad[grad_key])], col_scale=gamma)
         else:
             # dh = sum_i dP_i @ W_i, accumulated through the residual epilogue (one launch each,
             # like the reference's per-projection GEMMs)
@@ -1048,10 +1101,12 @@ class BTPBlockExecutor(ExecutorBase):
             self._gemm(K.Gemm(dP, W["d_d"], dgu[0], b_mn=True, swiglu_bwd=(gu[0], gu[1], dgu[1])))
         else:
             dact = self.buf("dact", (T, fl))
-            self._gemm(K.Gemm(dP, W["d_d"], dact, b_mn=True))                 # dact = dz_d @ Wd_d
+            self._dgrad_wgrad([K.Gemm(dP, W["d_d"], dact, b_mn=True)],         # dact = dz_d @ Wd_d
+                              [(dP, S["act"], G["d_d"])])                       # dWd_d = dz_d^T act
             K.swiglu_bwd(gu[0], gu[1], dact, dgu[0], dgu[1])
             self.stats.kernel_launches += 1
-        self._wgrad([(dP, S["act"], G["d_d"])])                                # dWd_d = dz_d^T act
+        if self.fuse_swiglu_bwd:
+            self._wgrad([(dP, S["act"], G["d_d"])])
         # ---------------- gate|up chunk
         names = ("gate", "up")
         da = self._da_buffer(names)
@@ -1070,8 +1125,7 @@ class BTPBlockExecutor(ExecutorBase):
         dP, _ = self._up_bwd(names, [K.Gemm(dx_mid, W["u_o"], da, b_mn=True)], [(dx_mid, S["a_o"][0], G["u_o"])],
                              da, S["P_o"], None, "dss_o")
         dattn = self.buf("dattn", (T, dl))
-        self._gemm(K.Gemm(dP, W["d_o"], dattn, b_mn=True))
-        self._wgrad([(dP, S["attn"], G["d_o"])])
+        self._dgrad_wgrad([K.Gemm(dP, W["d_o"], dattn, b_mn=True)], [(dP, S["attn"], G["d_o"])])
         dq, dk, dv = self.attn.backward(dattn, S["actx"])
         # ---------------- q|k|v chunk
         names = ("q", "k", "v")

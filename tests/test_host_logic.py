@@ -4,7 +4,7 @@ import math
 
 import pytest
 
-from paper_2512_12131_b200.executor import _pick_splits
+from paper_2512_12131_b200.executor import _pick_splits, _pick_splits_behind
 
 
 @pytest.mark.parametrize("shapes,best", [
@@ -27,6 +27,25 @@ def test_split_k_picker_limits():
     assert _pick_splits(1000, 256, 74) == 1        # plenty of tiles: no split
     assert _pick_splits(1, 8, 74) == 2             # >= 4 k-blocks per split
     assert _pick_splits(1, 2, 74) == 1
+
+
+@pytest.mark.parametrize("tiles,kb", [(8, 256), (32, 256), (44, 256), (128, 256), (1, 8), (1000, 256)])
+def test_split_k_picker_behind_nothing_equals_plain_picker(tiles, kb):
+    """With no tiles ahead, the round-robin makespan model is the waves model of _pick_splits."""
+    assert _pick_splits_behind([], tiles, kb, 74) == _pick_splits(tiles, kb, 74)
+
+
+def test_split_k_picker_behind_a_dgrad_fills_its_last_wave():
+    # o-chunk dgrad of the CoLA-1B step ([16384 x 512], K = 2048: 128 tiles of 32 k-blocks on 74 pairs,
+    # the second wave 54 pairs deep) followed by its weight gradient [512 x 2048] over 256 k-blocks
+    ahead = [32] * 128
+    s = _pick_splits_behind(ahead, 8, 256, 74)
+    loads = [0] * 74
+    for j, c in enumerate(ahead + [-(-256 // s)] * (8 * s)):
+        loads[j % 74] += c + 5
+    # the merged launch is no longer than the two launches' models added
+    alone = -(-128 // 74) * (32 + 5) + -(-8 * _pick_splits(8, 256, 74) // 74) * (-(-256 // _pick_splits(8, 256, 74)) + 5)
+    assert max(loads) <= alone
 
 
 def test_tensor_ops_errors_match_reference():
