@@ -259,13 +259,19 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
         G = self.grad
         dz = self.buf(f"dz_{'_'.join(names)}", (T, k * rl))
         probs = [K.Gemm(dout_list[i], Wu_list[i], dz[:, i * rl:(i + 1) * rl], b_mn=True) for i in range(k)]
-        self._gemm(*probs)
         z_all = zs[0] if len(zs) == 1 else None
+        pairs = []
         for i in range(k):
             a_i = (as_[0] if len(as_) == 1 else as_[i])
             a_i = a_i[:, i * rl:(i + 1) * rl] if len(as_) == 1 else a_i
             gu = G[gkey_u][i] if isinstance(G[gkey_u], list) else G[gkey_u]
-            self._wgrad([(dout_list[i], a_i, gu)])
+            pairs.append((dout_list[i], a_i, gu))
+        if 2 * k <= 4:  # the dgrad and the up-factor weight gradients in one launch
+            self._dgrad_wgrad(probs, pairs)
+        else:
+            self._gemm(*probs)
+            for pr in pairs:
+                self._wgrad([pr])
         if self.var == 1:
             if z_all is not None:
                 K.fixup_sigma_bwd(z_all, dz, dz, r=rl, nproj=k, variant=1)
@@ -279,8 +285,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
                 self.dh_prev = {}
             for i, n in enumerate(names):
                 self.dh_prev[n] = dz[:, i * rl:(i + 1) * rl]
-        self._wgrad([(dz, inp, G[gkey_d])])
-        self._gemm(K.Gemm(dz, Wd_all, din_full, b_mn=True))
+        self._dgrad_wgrad([K.Gemm(dz, Wd_all, din_full, b_mn=True)], [(dz, inp, G[gkey_d])])
         self.comm.all_reduce(din_full, chunk_ids[0])
 
     def backward(self, dy: torch.Tensor) -> torch.Tensor:
@@ -409,19 +414,18 @@ class FullRankExecutor(_ReplicatedNormMixin, ExecutorBase):
             self._gemm(K.Gemm(dy, W["down"], dgu[:, :fl], b_mn=True, swiglu_bwd=(g, u, dgu[:, fl:])))
         else:
             dact = self.buf("dact", (T, fl))
-            self._gemm(K.Gemm(dy, W["down"], dact, b_mn=True))
+            self._dgrad_wgrad([K.Gemm(dy, W["down"], dact, b_mn=True)], [(dy, S["act"], G["down"])])
             K.swiglu_bwd(g, u, dact, dgu[:, :fl], dgu[:, fl:])
             self.stats.kernel_launches += 1
-        self._wgrad([(dy, S["act"], G["down"])])
-        self._wgrad([(dgu, S["n2"], G["gu"])])
+        if self.fuse_swiglu_bwd:
+            self._wgrad([(dy, S["act"], G["down"])])
         dn2 = self.buf("dn2", (T, d))
-        self._gemm(K.Gemm(dgu, W["gu"], dn2, b_mn=True))
+        self._dgrad_wgrad([K.Gemm(dgu, W["gu"], dn2, b_mn=True)], [(dgu, S["n2"], G["gu"])])
         self.comm.all_reduce(dn2, "mlp")
         dx_mid = self.buf("dx_mid", (T, d))
         self._rnorm_bwd(dn2, S["x_mid"], self.gamma2, S["s2"], dy, dx_mid, "gamma2")
         dattn = self.buf("dattn", (T, dl))
-        self._gemm(K.Gemm(dx_mid, W["o"], dattn, b_mn=True))
-        self._wgrad([(dx_mid, S["attn"], G["o"])])
+        self._dgrad_wgrad([K.Gemm(dx_mid, W["o"], dattn, b_mn=True)], [(dx_mid, S["attn"], G["o"])])
         dq, dk, dv = self.attn.backward(dattn, S["actx"])
         gq = G["qkv"]
         self._wgrad([(dq, S["n1"], gq[:dl]), (dk, S["n1"], gq[dl:2 * dl]), (dv, S["n1"], gq[2 * dl:])])
