@@ -638,7 +638,8 @@ def run_ours(args, cfg):
     b2b = gemm.get("back_to_back") or gemm
     # ncu DRAM bytes of the step's GEMM launches (one capture per launch structure; the newest whose
     # launch count matches this step's, else none)
-    for name in ("r02m_gemm_traffic_summary.json", "r02_gemm_traffic_summary.json", "r01_gemm_traffic_summary.json"):
+    for name in ("r02o_gemm_traffic_summary.json", "r02m_gemm_traffic_summary.json", "r02_gemm_traffic_summary.json",
+                 "r01_gemm_traffic_summary.json"):
         tfile = ROOT / "profiles" / name
         if not (tfile.exists() and args.config == "1b" and tp == 1 and strategy.value == "btp" and not args.model):
             continue

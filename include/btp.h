@@ -76,7 +76,7 @@ typedef struct btp_gemm_problem {
   int sigma_half; /* epilogue 1: r/2 (half-width of the crossgate pairs) */
 } btp_gemm_problem;
 
-/* Grouped/batched tcgen05 GEMM: n (1..4) independent problems in ONE persistent launch.
+/* Grouped/batched tcgen05 GEMM: n (1..8) independent problems in ONE persistent launch.
  * All problems share (a_mn, b_mn). bn_hint: 0 = auto, 128 or 256 = N tile.
  * Replaces: simulator.py:208-218 `_gemm_ranks_batched`, tensor.py:97-112 `batched_matmul`
  * (grouped up-projections q|k|v and gate|up, simulator.py:655-668). */

@@ -266,7 +266,7 @@ class VanillaExecutor(_ReplicatedNormMixin, ExecutorBase):
             a_i = a_i[:, i * rl:(i + 1) * rl] if len(as_) == 1 else a_i
             gu = G[gkey_u][i] if isinstance(G[gkey_u], list) else G[gkey_u]
             pairs.append((dout_list[i], a_i, gu))
-        if 2 * k <= 4:  # the dgrad and the up-factor weight gradients in one launch
+        if 2 * k <= 8:  # the dgrad and the up-factor weight gradients in one launch
             self._dgrad_wgrad(probs, pairs)
         else:
             self._gemm(*probs)

@@ -34,7 +34,7 @@ namespace btp {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kMaxProblems = 4;
+constexpr int kMaxProblems = 8;  // DevParams (~8 KB with 8) travels as a >4 KB kernel parameter (CUDA >= 12.1)
 constexpr int kThreads = 256;
 constexpr int kEpiStageBytes = 32 * 128;              // one warp's 32 rows x 128 B chunk
 

@@ -325,7 +325,7 @@ class ExecutorBase:
         self._side_pending = True
 
     # With no collective to start between them and no side stream, a dgrad and its chunk's
-    # independent weight gradient(s) go out as ONE grouped launch (<= 4 problems): the weight-gradient
+    # independent weight gradient(s) go out as ONE grouped launch (<= 8 problems): the weight-gradient
     # split tiles fill the dgrad's last wave and one launch's prologue / pipeline fill / drain is
     # saved. (_up_bwd merges only without live collectives: there the boundary all-reduce of the
     # dgrad output starts before the weight gradient and overlaps it.) `merge_bwd_gemms = False`
@@ -335,7 +335,8 @@ class ExecutorBase:
     def _dgrad_wgrad(self, dgrad_probs, pairs, col_scale=None):
         """dgrad problem(s) then the weight gradient(s) of `pairs` (see _wgrad_now), merged into one
         launch when nothing needs the dgrad output early."""
-        if not self.merge_bwd_gemms or self.concurrent_wgrad or len(dgrad_probs) + len(pairs) > 4:
+        cap = 4 if dgrad_probs[0].a.dtype == F32 else 8  # problems per launch: fp32 SIMT GEMM / tcgen05 GEMM
+        if not self.merge_bwd_gemms or self.concurrent_wgrad or len(dgrad_probs) + len(pairs) > cap:
             self._gemm(*dgrad_probs)
             self._wgrad(pairs, col_scale)
             return

@@ -127,7 +127,7 @@ class Gemm:
 
 
 def gemm(*problems: Gemm, bn: int = 0) -> None:
-    """One launch of the persistent tcgen05 GEMM over 1..4 problems."""
+    """One launch of the persistent tcgen05 GEMM over 1..8 problems (the fp32 SIMT GEMM: 1..4)."""
     arr = (GemmProblem * len(problems))(*[p.to_c() for p in problems])
     if problems[0].a.dtype == F32:
         _native.call("btp_gemm_f32", arr, len(problems), _stream())
