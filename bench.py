@@ -204,7 +204,8 @@ def _attention_ab(b, s, h, hd, reps=10):
         ref = F.scaled_dot_product_attention(*v4, scale=1 / math.sqrt(hd))
         do4 = do.view(b, s, h, hd).transpose(1, 2)
         cud_b = timed(lambda: torch.autograd.grad(ref, v4, do4, retain_graph=True))
-    err = float((o.float() - ref.detach().transpose(1, 2).reshape(T, W).float()).norm() / ref.float().norm())
+    ref = ref.detach()
+    err = float((o.float() - ref.transpose(1, 2).reshape(T, W).float()).norm() / ref.float().norm())
     flops = 4 * b * h * s * s * hd
     return {"shape": {"b": b, "s": s, "heads": h, "head_dim": hd},
             "native": {"fwd_ms": nat_f, "bwd_ms": nat_b, "fwd_tflops": flops / nat_f / 1e9,
