@@ -368,6 +368,8 @@ class BlockTrainer:
         g_tail.replay()
         self._replays += 1
 
+    FIRST_COPY_STREAMS = 4  # copy streams for the first batch's (exposed) H2D in fit()
+
     def fit(self, x_hosts, G_host: torch.Tensor) -> list[float]:
         """Pipelined steps over pinned-host input shards; returns every step's loss.
 
@@ -380,13 +382,34 @@ class BlockTrainer:
             self._slots = [torch.empty(shape, dtype=dt, device=dev) for _ in range(2)]
             self._target = torch.empty(G_host.shape, dtype=G_host.dtype, device=dev)
             self._copy_stream = torch.cuda.Stream(device=dev)
+            self._first_streams = [torch.cuda.Stream(device=dev) for _ in range(self.FIRST_COPY_STREAMS - 1)]
         main, copy = torch.cuda.current_stream(), self._copy_stream
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
         g_copied = torch.cuda.Event()
         copy.wait_stream(main)
+        # the first batch's H2D is the one copy no step hides: it goes out in row slices on several
+        # copy streams at once (one 64 MiB pinned copy: 36 GB/s on one stream, 48 GB/s on four,
+        # scripts/probe_h2d.py); later batches copy on one stream under the previous step
+        n_sl = len(self._first_streams) + 1
+        rows = x_hosts[0].shape[0]
+        if n_sl > 1 and rows % n_sl == 0:
+            step = rows // n_sl
+            joins = []
+            for j, st in enumerate([copy] + self._first_streams):
+                st.wait_stream(main)
+                with torch.cuda.stream(st):
+                    self._slots[0][j * step:(j + 1) * step].copy_(x_hosts[0][j * step:(j + 1) * step], non_blocking=True)
+                    if j:
+                        ev = torch.cuda.Event()
+                        ev.record(st)
+                        joins.append(ev)
+            for ev in joins:
+                copy.wait_event(ev)
+        else:
+            with torch.cuda.stream(copy):
+                self._slots[0].copy_(x_hosts[0], non_blocking=True)
         with torch.cuda.stream(copy):
-            self._slots[0].copy_(x_hosts[0], non_blocking=True)
             copied[0].record(copy)
             # G (the loss projection) is needed only after step 0's forward: its copy runs under it
             self._target.copy_(G_host, non_blocking=True)
