@@ -269,3 +269,31 @@ def test_residual_layouts_and_store_paths(res_mode, st_global):
     finally:
         K.set_res4(prev_r)
         K.set_st_global(bool(prev_s))
+
+
+@pytest.mark.parametrize("n_probs", [5, 6, 8])
+def test_up_to_eight_problems_dgrad_and_split_wgrad(n_probs):
+    """The merged backward launches (executor._dgrad_wgrad): up to 8 problems in ONE launch, bf16
+    dgrads (B MN-major) ahead of fp32 split-K weight gradients (both operands MN-major, TMA
+    reduce-add into zeroed outputs, with and without a column scale), ragged shapes included."""
+    T = 1536
+    probs, checks = [], []
+    n_d = n_probs // 2
+    for i in range(n_d):  # dgrads: dA[T, r] = dY[T, w] @ W[r, w]^T... with W read MN-major
+        w, r = 384 + 64 * i, 128 + 32 * i
+        dY, W = _mk(T, w), _mk(w, r)
+        out = torch.empty(T, r, device="cuda", dtype=torch.bfloat16)
+        probs.append(K.Gemm(dY, W, out, b_mn=True))
+        checks.append((out, dY.float() @ W.float(), TOL))
+    for i in range(n_probs - n_d):  # weight gradients: dW[m, n] = dY^T X over the T tokens, split-K 3
+        m, n = 256 + 96 * i, 320 + 64 * i
+        dY, X = _mk(T, m), _mk(T, n)
+        dW = torch.empty(m, n, device="cuda")
+        K.zero(dW)
+        cs = (torch.rand(n, device="cuda") + 0.5) if i % 2 else None
+        probs.append(K.Gemm(dY, X, dW, a_mn=True, b_mn=True, splits=3, col_scale=cs))
+        ref = dY.float().t() @ X.float()
+        checks.append((dW, ref * cs[None, :] if cs is not None else ref, 1e-5))
+    K.gemm(*probs)
+    for got, want, tol in checks:
+        assert rel(got, want) < tol
