@@ -64,7 +64,12 @@ def _main(port, q):
             # weight gradients: split-K partials meet in an fp32 reduce-add whose order is not fixed
             for fam in ("A", "B"):
                 for n, g in ref.grads[fam].items():
-                    same[f"d{fam}_{n}"] = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g)) < 1e-4
+                    e = float(np.linalg.norm(g - got.grads[fam][n]) / np.linalg.norm(g))
+                    # the q factors also inherit dQ's run-to-run rounding: the attention backward
+                    # reduce-adds each key tile's fp32 dQ contribution in unfixed order before the bf16
+                    # rounding, so a few dq elements differ by one bf16 ulp between runs (measured
+                    # 1.1e-5 .. 1.2e-4 on dA_q / dB_q over 8 runs, every other factor <= 5e-7)
+                    same[f"d{fam}_{n}"] = e < (5e-4 if n == "q" else 1e-4)
             out[grouping] = (same, got.trace.record_tuples("forward") == ref.trace.record_tuples("forward"),
                              len(got.trace.record_tuples("backward")))
         # the trainer loop with live NCCL collectives: CUDA-graph captured (NCCL kernels inside the
