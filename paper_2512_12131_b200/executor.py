@@ -99,6 +99,9 @@ def _pick_splits(tiles: int, k_blocks: int, units: int) -> int:
     return best
 
 
+_BEHIND_TILE_OVERHEAD = 5  # k-block equivalents of per-tile epilogue / pipeline fill in the merged model
+
+
 def _pick_splits_behind(ahead_kb: list, w_tiles: int, k_blocks: int, units: int) -> int:
     """Split-K factor for weight-gradient tiles launched BEHIND other tiles in the same persistent
     launch (ahead_kb: k-blocks of each tile ahead, in launch order). Tiles go round-robin to the CTA
@@ -111,7 +114,7 @@ def _pick_splits_behind(ahead_kb: list, w_tiles: int, k_blocks: int, units: int)
             break
         loads = [0] * units
         for j, c in enumerate(list(ahead_kb) + [kb] * (w_tiles * s)):
-            loads[j % units] += c + 5
+            loads[j % units] += c + _BEHIND_TILE_OVERHEAD
         cost = max(loads)
         if best_cost is None or cost < best_cost:
             best, best_cost = s, cost
